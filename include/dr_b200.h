@@ -1,0 +1,119 @@
+/*
+ * dr_b200.h -- C-ABI of libdrb200.so, the B200 (sm_100a) masked-inpainting hot path of
+ * arXiv 2509.10466 (reference package `dimreal`, /root/reference/pkg).
+ *
+ * Plain C types only: device pointers, sizes, a cudaStream_t passed as void*.  Every
+ * device-pointer entry point is stream-ordered and never synchronises the host; results
+ * and the per-frame status flags are valid once the stream reaches the end of the call.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/dimreal):
+ *   dr_create          DsttEngine.__init__ + load_weights     inpaint/dstt.py:292-299, :331-342
+ *   dr_forward         DsttModel.forward + the engine composite
+ *                                                             inpaint/dstt.py:256-268,
+ *                                                             inpaint/base.py:52-89
+ *   dr_inpaint_u8_host InpaintEngine.inpaint / DsttEngine._fill on host u8 buffers
+ *                                                             inpaint/base.py:52-89,
+ *                                                             inpaint/dstt.py:313-326
+ *   dr_mask_stage      new: dilate (masks._CROSS, masks.py:17/:193), feather, token mask
+ *   dr_last_error      exception message of the failing call
+ * Error codes map onto the reference exceptions (errors.py:4-33):
+ *   DR_ERR_CONFIG -> ConfigError, DR_ERR_INPUT -> InputError,
+ *   DR_ERR_NUMERIC -> EngineNumericError, DR_ERR_CUDA -> RuntimeError.
+ */
+#ifndef DR_B200_H
+#define DR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DR_OK 0
+#define DR_ERR_CONFIG 1
+#define DR_ERR_INPUT 2
+#define DR_ERR_NUMERIC 3
+#define DR_ERR_CUDA 4
+
+/* per-frame status bits written to dr_frame_io.flags */
+#define DR_FLAG_NONFINITE 1    /* network output not finite  -> EngineNumericError */
+#define DR_FLAG_UNREDACTED 2   /* u8 input nonzero inside m0 -> InputError         */
+
+/* DsttConfig (inpaint/dstt.py:35-86) plus the mask-stage fields. */
+typedef struct dr_config {
+  int32_t width, height, patch, channels, kernel, heads, temporal_groups;
+  int32_t n_blocks;
+  char blocks[16];               /* 'S' / 'T', n_blocks of them */
+  int32_t mask_dilate;           /* r: 3x3-cross dilation iterations (0 = off)       */
+  float mask_feather_sigma;      /* Gaussian feather sigma (0 = binary alpha)        */
+  int32_t mask_aware_attention;  /* 1 = exclude fully masked tokens as keys (MAT)    */
+} dr_config;
+
+typedef struct dr_engine dr_engine;
+
+typedef struct dr_frame_io {
+  int32_t frames;                /* B                                                */
+  const float* rgb_f32;          /* [B][3][H][W] in [0,1], or NULL                   */
+  const uint8_t* rgb_u8;         /* [B][H][W][3], or NULL (exactly one rgb input)    */
+  const uint8_t* mask_m0;        /* [B][H][W], nonzero = private                     */
+  const float* slot0;            /* memory, oldest first: [B][T][C] or [T][C]        */
+  const float* slot1;
+  int32_t slot_batched;          /* 1: slots are [B][T][C]; 0: one [T][C] for all    */
+  float* new_slot;               /* [B][T][C] out: post-block tokens (required)      */
+  float* out_f32;                /* [B][3][H][W] composite (float API), or NULL      */
+  uint8_t* out_u8;               /* [B][H][W][3] composite (u8 API), or NULL         */
+  float* fill;                   /* [B][3][H][W] raw network output, or NULL         */
+  uint8_t* dilated;              /* [B][H][W] m1, or NULL                            */
+  float* alpha;                  /* [B][H][W] feathered alpha, or NULL               */
+  uint8_t* token_valid;          /* [B][T] token validity, or NULL                   */
+  int32_t* flags;                /* [B] DR_FLAG_* bits, or NULL (engine-internal)    */
+} dr_frame_io;
+
+/* Build an engine on `device` from the 72 DRWT tensors in state_dict order (host fp32
+ * pointers, element counts checked against cfg).  Weights are repacked once into
+ * fragment-major fp16 images; they are immutable afterwards. */
+int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* numels,
+              int32_t n_tensors, int32_t device, dr_engine** out);
+
+void dr_destroy(dr_engine* e);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* dr_last_error(void);
+
+int32_t dr_version(void);
+
+/* Full path on device buffers: mask stage -> forward -> composite.  Stream-ordered. */
+int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream);
+
+/* The mask stage alone, no engine needed: m0 [B][H][W] -> m1 (u8), alpha (f32) and token
+ * validity [B][(H/patch)*(W/patch)] (patch 4 or 8).  Any output may be NULL.  Scratch is
+ * stream-ordered (cudaMallocAsync).  radius <= 31, sigma <= 7.9. */
+int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, int32_t radius,
+                  float sigma, const uint8_t* m0, uint8_t* m1, float* alpha,
+                  uint8_t* token_valid, void* stream);
+
+/* One u8 frame through host buffers, like InpaintEngine.inpaint: copies rgb/mask in,
+ * runs the path with the engine-held 2-slot memory (FIFO advanced once per call), copies
+ * the composite out and synchronises.  Returns DR_ERR_INPUT if the frame is not
+ * redacted inside the mask, DR_ERR_NUMERIC on a non-finite network output. */
+int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                       uint8_t* out_hwc, void* stream);
+
+/* Reset the engine-held memory of dr_inpaint_u8_host to two zero slots. */
+int dr_reset_memory(dr_engine* e);
+
+/* Number of kernels one dr_forward launches for `frames` frames (for accounting). */
+int32_t dr_kernels_per_forward(dr_engine* e);
+
+/* Per-stage CUDA events on the launch stream (off by default).  After the stream has
+ * passed a dr_forward, dr_profile_read fills ms[i] / kinds[i] for each stage and returns
+ * the count (-1 on an event error).  Kinds: 0 mask stage, 1 slot K/V, 2 embed,
+ * 3 spatial attention, 4 temporal attention, 5 out-proj+FFN+QKV, 6 vec2patch,
+ * 7 decode.0, 8 decode.2+composite. */
+int dr_profile(dr_engine* e, int32_t on);
+int32_t dr_profile_read(dr_engine* e, float* ms, int32_t* kinds, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DR_B200_H */

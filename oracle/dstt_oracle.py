@@ -107,11 +107,16 @@ def _correlate1d_nearest(a: np.ndarray, w: np.ndarray, axis: int) -> np.ndarray:
     n = a.shape[axis]
     idx = np.clip(np.arange(-radius, n + radius), 0, n - 1)
     padded = np.take(a64, idx, axis=axis)
-    acc = np.zeros_like(a64)
-    for j in range(len(w)):
+
+    def tap(d):                       # input shifted by d along axis
         sl = [slice(None)] * a.ndim
-        sl[axis] = slice(j, j + n)
-        acc += w[j] * padded[tuple(sl)]
+        sl[axis] = slice(radius + d, radius + d + n)
+        return padded[tuple(sl)]
+    # scipy NI_Correlate1D, symmetric weights: x[0]*w[0], then the pairs from the
+    # outermost inward, (x[-j] + x[+j]) * w[j] -- same order, so float64-identical.
+    acc = tap(0) * w[radius]
+    for jj in range(-radius, 0):
+        acc = acc + (tap(jj) + tap(-jj)) * w[radius + jj]
     return acc.astype(F32)
 
 
@@ -210,6 +215,11 @@ def gelu(x):
 def attention(q, k, v, key_bias=None):
     """scaled_dot_product (dstt.py:89-99): softmax(q k^T / sqrt(dh)) v.
     q (..., Tq, dh), k/v (..., Tk, dh); key_bias broadcastable to (..., Tq, Tk)."""
+    tq = q.shape[-2]
+    step = 1024                        # query chunks: bounded memory at 1024^2
+    if tq > step:
+        return np.concatenate([attention(q[..., i:i + step, :], k, v, key_bias)
+                               for i in range(0, tq, step)], axis=-2)
     s = (q @ np.swapaxes(k, -1, -2)) * q.dtype.type(1.0 / math.sqrt(q.shape[-1]))
     if key_bias is not None:
         s = s + key_bias

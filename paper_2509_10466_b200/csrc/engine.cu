@@ -1,0 +1,599 @@
+// C-ABI of libdrb200.so: engine lifetime, weight repack, workspace, and the per-frame
+// launch sequence (mask stage -> slot K/V -> embed -> S/T blocks -> decoder tail).
+// See include/dr_b200.h for the contract and the reference interfaces replaced.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dr_b200.h"
+#include "kernels.h"
+
+using namespace dr;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(DR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+uint32_t h2(float lo, float hi) {
+  __half a = __float2half_rn(lo), b = __float2half_rn(hi);
+  uint16_t ua, ub;
+  std::memcpy(&ua, &a, 2);
+  std::memcpy(&ub, &b, 2);
+  return (uint32_t)ua | ((uint32_t)ub << 16);
+}
+
+// W is N x K row-major (W[n][k]); emits N/8 x K/16 fragments of 32 lanes (uint2 b0,b1)
+// in the m16n8k16 B layout: b0 = {W[n0+g][k0+2t], W[n0+g][k0+2t+1]}, b1 = k + 8.
+void pack_frags(const std::vector<float>& W, int N, int K, std::vector<uint2>& out) {
+  for (int nt = 0; nt < N / 8; ++nt)
+    for (int kt = 0; kt < K / 16; ++kt)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        const int n = nt * 8 + g, k = kt * 16 + 2 * t;
+        const float* r = &W[(size_t)n * K];
+        out.push_back(make_uint2(h2(r[k], r[k + 1]), h2(r[k + 8], r[k + 9])));
+      }
+}
+
+struct Blk {
+  size_t ln1_w, ln1_b, bqkv, bo, ln2_w, ln2_b, b1, b2;      // float offsets
+  size_t wqkv, wo, w1, w2;                                  // frag offsets
+  bool temporal;
+};
+
+// scipy.ndimage._filters._gaussian_kernel1d (order 0) in float64, radius int(4 sigma + 0.5)
+std::vector<double> feather_taps(double sigma) {
+  const int r = sigma > 0 ? (int)(4.0 * sigma + 0.5) : 0;
+  std::vector<double> fw(2 * r + 1, 1.0);
+  if (r == 0) return fw;
+  double sum = 0;
+  for (int i = -r; i <= r; ++i) {
+    fw[i + r] = std::exp(-0.5 / (sigma * sigma) * (double)i * (double)i);
+    sum += fw[i + r];
+  }
+  for (double& x : fw) x /= sum;
+  return fw;
+}
+
+}  // namespace
+
+struct dr_engine {
+  dr_config cfg{};
+  int device = 0;
+  int H = 0, W = 0, R = 0, Cc = 0, T = 0, nb = 0, n_temporal = 0, feather_r = 0;
+  std::vector<Blk> blk;
+  size_t we = 0, be = 0, wv2p = 0, bv2p = 0, wd0 = 0, bd0 = 0, wd2 = 0, bd2 = 0;
+  uint2* frags = nullptr;
+  float* fparams = nullptr;
+  double* feather_w = nullptr;
+  // workspace
+  int cap = 0;
+  void* ws = nullptr;
+  uint32_t *bits0 = nullptr, *bits1 = nullptr;
+  uint8_t *m1 = nullptr, *tv = nullptr;
+  float *alpha = nullptr, *resid[2] = {nullptr, nullptr};
+  __half *xin = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr,
+         *tok16 = nullptr, *raster = nullptr, *d0 = nullptr, *slotkv = nullptr;
+  int* flags = nullptr;
+  // host-buffer path (dr_inpaint_u8_host): device frame buffers + 3-slot ring
+  uint8_t *h_rgb = nullptr, *h_m0 = nullptr, *h_out = nullptr;   // device
+  float* ring[3] = {nullptr, nullptr, nullptr};
+  int mem0 = 0, mem1 = 0;                                        // ring index of slots
+  uint8_t* pin = nullptr;                                        // pinned staging
+  int* pin_flags = nullptr;
+  // optional per-stage CUDA events (dr_profile): ev[0] before the first stage
+  static constexpr int kMaxEv = 64;
+  int profiling = 0, n_ev = 0;
+  cudaEvent_t ev[kMaxEv] = {};
+  int ev_kind[kMaxEv] = {};
+
+  void mark(int kind, cudaStream_t s) {
+    if (!profiling || n_ev >= kMaxEv) return;
+    if (!ev[n_ev]) cudaEventCreate(&ev[n_ev]);
+    ev_kind[n_ev] = kind;
+    cudaEventRecord(ev[n_ev++], s);
+  }
+
+  BlockW block_w(int i) const {
+    const Blk& b = blk[i];
+    BlockW w;
+    w.ln1_w = fparams + b.ln1_w; w.ln1_b = fparams + b.ln1_b;
+    w.wqkv = frags + b.wqkv; w.bqkv = fparams + b.bqkv;
+    w.wo = frags + b.wo; w.bo = fparams + b.bo;
+    w.ln2_w = fparams + b.ln2_w; w.ln2_b = fparams + b.ln2_b;
+    w.w1 = frags + b.w1; w.b1 = fparams + b.b1;
+    w.w2 = frags + b.w2; w.b2 = fparams + b.b2;
+    return w;
+  }
+
+  size_t frame_px() const { return (size_t)H * W; }
+  size_t slotkv_stride() const { return (size_t)cap * T * C; }   // one K or V image
+
+  __half* skv(int ti, int slot, int which) const {              // which: 0 K, 1 V
+    return slotkv + ((size_t)(ti * 2 + slot) * 2 + which) * slotkv_stride();
+  }
+
+  void free_ws() {
+    if (ws) cudaFree(ws);
+    ws = nullptr;
+    cap = 0;
+  }
+
+  int ensure(int frames) {
+    if (frames <= cap) return DR_OK;
+    free_ws();
+    const int Ww = (W + 31) / 32;
+    const size_t px = frame_px() * frames, tok = (size_t)T * frames;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+    const size_t o_b0 = take((size_t)frames * H * Ww * 4), o_b1 = take((size_t)frames * H * Ww * 4);
+    const size_t o_m1 = take(px), o_tv = take(tok), o_alpha = take(px * 4);
+    const size_t o_r0 = take(tok * C * 4), o_r1 = take(tok * C * 4);
+    const size_t o_xin = take(tok * 4 * cfg.patch * cfg.patch * 2);
+    const size_t o_q = take(tok * C * 2), o_k = take(tok * C * 2), o_v = take(tok * C * 2);
+    const size_t o_at = take(tok * C * 2), o_t16 = take(tok * C * 2);
+    const size_t o_ras = take(px * C * 2), o_d0 = take(px * C * 2);
+    const size_t o_skv = take((size_t)std::max(n_temporal, 1) * 4 * tok * C * 2);
+    const size_t o_fl = take((size_t)frames * 4);
+    CUDA_TRY(cudaMalloc(&ws, off));
+    uint8_t* b = static_cast<uint8_t*>(ws);
+    bits0 = (uint32_t*)(b + o_b0); bits1 = (uint32_t*)(b + o_b1);
+    m1 = b + o_m1; tv = b + o_tv; alpha = (float*)(b + o_alpha);
+    resid[0] = (float*)(b + o_r0); resid[1] = (float*)(b + o_r1);
+    xin = (__half*)(b + o_xin);
+    q = (__half*)(b + o_q); k = (__half*)(b + o_k); v = (__half*)(b + o_v);
+    attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
+    raster = (__half*)(b + o_ras); d0 = (__half*)(b + o_d0);
+    slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
+    cap = frames;
+    return DR_OK;
+  }
+};
+
+namespace {
+
+int check_cfg(const dr_config* c) {
+  if (!c) return fail(DR_ERR_CONFIG, "null config");
+  if (c->width <= 0 || c->height <= 0 || c->patch <= 0)
+    return fail(DR_ERR_CONFIG, "width, height and patch must be positive");
+  if (c->width % c->patch || c->height % c->patch)
+    return fail(DR_ERR_CONFIG, "width and height must be divisible by patch size");
+  if (c->heads <= 0 || c->channels % c->heads)
+    return fail(DR_ERR_CONFIG, "channels must be divisible by head count");
+  if (c->kernel < c->patch) return fail(DR_ERR_CONFIG, "reconstruction kernel must be >= patch size");
+  if (c->temporal_groups <= 0 || (c->height / c->patch) % c->temporal_groups)
+    return fail(DR_ERR_CONFIG, "token rows must split evenly into temporal groups");
+  if (c->n_blocks <= 0 || c->n_blocks > 16)
+    return fail(DR_ERR_CONFIG, "block sequence must hold 1..16 blocks");
+  for (int i = 0; i < c->n_blocks; ++i)
+    if (c->blocks[i] != 'S' && c->blocks[i] != 'T')
+      return fail(DR_ERR_CONFIG, "block sequence must be a nonempty mix of 'S'/'T'");
+  if (c->mask_dilate < 0 || c->mask_dilate > 31)
+    return fail(DR_ERR_CONFIG, "mask_dilate must be in [0, 31]");
+  if (!(c->mask_feather_sigma >= 0.f) || (int)(4.0 * c->mask_feather_sigma + 0.5) > 32)
+    return fail(DR_ERR_CONFIG, "mask_feather_sigma must be in [0, 7.9]");
+  // Shapes the sm_100a kernels are specialised for (the reference default network).
+  if (c->channels != C || c->heads != HEADS || c->patch != 8 || c->kernel != 10)
+    return fail(DR_ERR_CONFIG,
+                "B200 kernels support channels=64, heads=4, patch=8, kernel=10 (got channels=" +
+                    std::to_string(c->channels) + ", heads=" + std::to_string(c->heads) +
+                    ", patch=" + std::to_string(c->patch) + ", kernel=" +
+                    std::to_string(c->kernel) + ")");
+  if ((c->width / c->patch) % 1 != 0) return fail(DR_ERR_CONFIG, "bad token grid");
+  return DR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dr_last_error(void) { return g_err.c_str(); }
+
+int32_t dr_version(void) { return 1; }
+
+int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* numels,
+              int32_t n_tensors, int32_t device, dr_engine** out) {
+  if (!out) return fail(DR_ERR_CONFIG, "null output pointer");
+  *out = nullptr;
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  const int nb = cfg->n_blocks;
+  const int expect = 2 + 16 * nb + 6;
+  if (n_tensors != expect)
+    return fail(DR_ERR_CONFIG, "weights file has " + std::to_string(n_tensors) +
+                                   " tensors, model needs " + std::to_string(expect));
+  const int c = cfg->channels, p = cfg->patch, kk = cfg->kernel;
+  std::vector<int64_t> want = {(int64_t)c * 4 * p * p, c};
+  for (int i = 0; i < nb; ++i) {
+    const int64_t blockn[16] = {c, c, c * c, c, c * c, c, c * c, c, c * c, c, c, c,
+                                2 * c * c, 2 * c, 2 * c * c, c};
+    want.insert(want.end(), blockn, blockn + 16);
+  }
+  const int64_t tail[6] = {(int64_t)c * c * kk * kk, c, (int64_t)c * c * 9, c, 3 * c * 9, 3};
+  want.insert(want.end(), tail, tail + 6);
+  for (int i = 0; i < expect; ++i) {
+    if (!weights[i]) return fail(DR_ERR_CONFIG, "null weight tensor " + std::to_string(i));
+    if (numels[i] != want[i])
+      return fail(DR_ERR_CONFIG, "tensor " + std::to_string(i) + ": " + std::to_string(numels[i]) +
+                                     " elements, model needs " + std::to_string(want[i]));
+  }
+  CUDA_TRY(cudaSetDevice(device));
+
+  dr_engine* e = new dr_engine();
+  e->cfg = *cfg;
+  e->device = device;
+  e->H = cfg->height; e->W = cfg->width;
+  e->R = e->H / p; e->Cc = e->W / p; e->T = e->R * e->Cc;
+  e->nb = nb;
+
+  std::vector<uint2> fr;
+  std::vector<float> fp;
+  auto vec = [&](int idx) { return std::vector<float>(weights[idx], weights[idx] + numels[idx]); };
+  auto addf = [&](int idx) { size_t o = fp.size(); fp.insert(fp.end(), weights[idx], weights[idx] + numels[idx]); return o; };
+
+  // embed Conv2d(4, C, p, p): W[co][ci*p*p + ky*p + kx] is already the flatten order.
+  e->we = fr.size(); pack_frags(vec(0), c, 4 * p * p, fr);
+  e->be = addf(1);
+  for (int i = 0; i < nb; ++i) {
+    const int base = 2 + 16 * i;
+    Blk b;
+    b.temporal = cfg->blocks[i] == 'T';
+    b.ln1_w = addf(base + 0); b.ln1_b = addf(base + 1);
+    std::vector<float> wqkv = vec(base + 2);
+    std::vector<float> wk = vec(base + 4), wv = vec(base + 6);
+    wqkv.insert(wqkv.end(), wk.begin(), wk.end());
+    wqkv.insert(wqkv.end(), wv.begin(), wv.end());
+    b.wqkv = fr.size(); pack_frags(wqkv, 3 * c, c, fr);
+    b.bqkv = addf(base + 3); addf(base + 5); addf(base + 7);       // contiguous q|k|v bias
+    b.wo = fr.size(); pack_frags(vec(base + 8), c, c, fr);
+    b.bo = addf(base + 9);
+    b.ln2_w = addf(base + 10); b.ln2_b = addf(base + 11);
+    b.w1 = fr.size(); pack_frags(vec(base + 12), 2 * c, c, fr);
+    b.b1 = addf(base + 13);
+    b.w2 = fr.size(); pack_frags(vec(base + 14), c, 2 * c, fr);
+    b.b2 = addf(base + 15);
+    if (b.temporal) e->n_temporal++;
+    e->blk.push_back(b);
+  }
+  const int tb = 2 + 16 * nb;
+  {  // ConvTranspose2d weight (C_in, C_out, k, k): per tap, B[k=ci][n=co]
+    const float* wt = weights[tb];
+    e->wv2p = fr.size();
+    std::vector<float> m((size_t)c * c);
+    for (int a = 0; a < kk; ++a)
+      for (int bb = 0; bb < kk; ++bb) {
+        for (int co = 0; co < c; ++co)
+          for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = wt[(((size_t)ci * c + co) * kk + a) * kk + bb];
+        pack_frags(m, c, c, fr);
+      }
+    e->bv2p = addf(tb + 1);
+  }
+  {  // decode.0 Conv2d(C, C, 3): per tap W[co][ci]
+    const float* w0 = weights[tb + 2];
+    e->wd0 = fr.size();
+    std::vector<float> m((size_t)c * c);
+    for (int tap = 0; tap < 9; ++tap) {
+      for (int co = 0; co < c; ++co)
+        for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = w0[((size_t)co * c + ci) * 9 + tap];
+      pack_frags(m, c, c, fr);
+    }
+    e->bd0 = addf(tb + 3);
+  }
+  {  // decode.2 Conv2d(C, 3, 3): N padded 3 -> 8 with zeros
+    const float* w2 = weights[tb + 4];
+    e->wd2 = fr.size();
+    std::vector<float> m((size_t)8 * c, 0.f);
+    for (int tap = 0; tap < 9; ++tap) {
+      std::fill(m.begin(), m.end(), 0.f);
+      for (int co = 0; co < 3; ++co)
+        for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = w2[((size_t)co * c + ci) * 9 + tap];
+      pack_frags(m, 8, c, fr);
+    }
+    e->bd2 = addf(tb + 5);
+  }
+  // Feather taps: scipy _gaussian_kernel1d (float64), radius int(4 sigma + 0.5).
+  std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
+  e->feather_r = (int)(fw.size() / 2);
+
+  auto cleanup = [&](int code) { dr_destroy(e); return code; };
+  if (cudaMalloc(&e->frags, fr.size() * sizeof(uint2)) != cudaSuccess ||
+      cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&e->feather_w, fw.size() * sizeof(double)) != cudaSuccess)
+    return cleanup(fail(DR_ERR_CUDA, "cudaMalloc of weights failed"));
+  if (cudaMemcpy(e->frags, fr.data(), fr.size() * sizeof(uint2), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(e->fparams, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(e->feather_w, fw.data(), fw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return cleanup(fail(DR_ERR_CUDA, "weight upload failed"));
+  *out = e;
+  return DR_OK;
+}
+
+void dr_destroy(dr_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  e->free_ws();
+  cudaFree(e->frags);
+  cudaFree(e->fparams);
+  cudaFree(e->feather_w);
+  cudaFree(e->h_rgb);
+  cudaFree(e->h_m0);
+  cudaFree(e->h_out);
+  for (auto* r : e->ring) cudaFree(r);
+  for (auto& ev : e->ev) if (ev) cudaEventDestroy(ev);
+  if (e->pin) cudaFreeHost(e->pin);
+  if (e->pin_flags) cudaFreeHost(e->pin_flags);
+  delete e;
+}
+
+int32_t dr_kernels_per_forward(dr_engine* e) {
+  if (!e) return 0;
+  const int mask = 3 + (e->feather_r > 0 ? 1 : 0);
+  return mask + 2 * e->n_temporal + 1 + 2 * e->nb + 3;
+}
+
+static void fill_mask_args(dr_engine* e, MaskArgs& m, int frames, const uint8_t* m0,
+                           uint8_t* m1, float* alpha, uint8_t* tv, int* flags) {
+  m.frames = frames; m.H = e->H; m.W = e->W; m.patch = e->cfg.patch;
+  m.radius = e->cfg.mask_dilate;
+  m.feather_radius = e->feather_r;
+  m.feather_w = e->feather_w;
+  m.m0 = m0;
+  m.bits0 = e->bits0; m.bits1 = e->bits1;
+  m.m1 = m1; m.alpha = alpha; m.token_valid = tv;
+  m.gtmp = nullptr;
+  m.flags = flags;
+}
+
+int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, int32_t radius,
+                  float sigma, const uint8_t* m0, uint8_t* m1, float* alpha,
+                  uint8_t* token_valid, void* stream) {
+  if (frames <= 0 || height <= 0 || width <= 0 || !m0)
+    return fail(DR_ERR_INPUT, "need frames, height, width > 0 and a mask");
+  if (radius < 0 || radius > 31) return fail(DR_ERR_CONFIG, "radius must be in [0, 31]");
+  if (!(sigma >= 0.f) || (int)(4.0 * sigma + 0.5) > 32)
+    return fail(DR_ERR_CONFIG, "sigma must be in [0, 7.9]");
+  if (token_valid && (patch != 4 && patch != 8))
+    return fail(DR_ERR_CONFIG, "token mask supports patch 4 or 8");
+  if (token_valid && (height % patch || width % patch))
+    return fail(DR_ERR_CONFIG, "width and height must be divisible by patch size");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int Ww = (width + 31) / 32;
+  const size_t words = (size_t)frames * height * Ww * 4;
+  std::vector<double> fw = feather_taps(sigma);
+  const int fr = (int)(fw.size() / 2);
+  uint8_t* scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&scratch, 2 * words + fw.size() * sizeof(double) + 256, s));
+  double* dfw = reinterpret_cast<double*>(scratch + ((2 * words + 255) & ~(size_t)255));
+  CUDA_TRY(cudaMemcpyAsync(dfw, fw.data(), fw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  MaskArgs m{};
+  m.frames = frames; m.H = height; m.W = width; m.patch = patch;
+  m.radius = radius; m.feather_radius = fr; m.feather_w = dfw;
+  m.m0 = m0;
+  m.bits0 = reinterpret_cast<uint32_t*>(scratch);
+  m.bits1 = reinterpret_cast<uint32_t*>(scratch + words);
+  m.m1 = m1; m.alpha = alpha; m.token_valid = token_valid;
+  launch_mask_stage(m, s);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(scratch, s));
+  return DR_OK;
+}
+
+int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
+  if (!e || !io) return fail(DR_ERR_CONFIG, "null engine or io");
+  const int B = io->frames;
+  if (B <= 0) return fail(DR_ERR_INPUT, "frames must be positive");
+  if ((io->rgb_f32 == nullptr) == (io->rgb_u8 == nullptr))
+    return fail(DR_ERR_INPUT, "exactly one of rgb_f32 / rgb_u8 is required");
+  if (!io->mask_m0 || !io->slot0 || !io->slot1 || !io->new_slot)
+    return fail(DR_ERR_INPUT, "mask, both memory slots and new_slot are required");
+  if (io->out_u8 && !io->rgb_u8) return fail(DR_ERR_INPUT, "out_u8 needs the u8 input");
+  if (io->out_f32 && !io->rgb_f32) return fail(DR_ERR_INPUT, "out_f32 needs the f32 input");
+  CUDA_TRY(cudaSetDevice(e->device));
+  int rc = e->ensure(B);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int T = e->T;
+  int* flags = io->flags ? io->flags : e->flags;
+  e->n_ev = 0;
+  e->mark(-1, s);
+  CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * B, s));
+
+  // 1. mask stage + packed network input
+  MaskArgs m{};
+  uint8_t* tv = io->token_valid ? io->token_valid : e->tv;
+  float* alpha = io->alpha ? io->alpha : e->alpha;
+  fill_mask_args(e, m, B, io->mask_m0, io->dilated, alpha, tv, flags);
+  m.rgb_f32 = io->rgb_f32; m.rgb_u8 = io->rgb_u8; m.xin = e->xin;
+  launch_mask_stage(m, s);
+  e->mark(0, s);
+
+  // 2. memory-slot K/V of every temporal block (LN1 + k/v projection of each slot)
+  const int fs = io->slot_batched ? B : 1;
+  const bool same_slot = io->slot0 == io->slot1;
+  {
+    int ti = 0;
+    for (int i = 0; i < e->nb; ++i) {
+      if (!e->blk[i].temporal) continue;
+      for (int sl = 0; sl < (same_slot ? 1 : 2); ++sl) {
+        TokenArgs a{};
+        a.n_tok = fs * T; a.T = T;
+        a.resid_in = sl == 0 ? io->slot0 : io->slot1;
+        a.next = e->block_w(i);
+        a.k = e->skv(ti, sl, 0); a.v = e->skv(ti, sl, 1);
+        launch_token(TOK_SLOTKV, a, s);
+        e->mark(1, s);
+      }
+      ++ti;
+    }
+  }
+
+  // 3. patch embed (+ LN1/QKV of block 0)
+  {
+    TokenArgs a{};
+    a.n_tok = B * T; a.T = T;
+    a.xin = e->xin; a.we = e->frags + e->we; a.be = e->fparams + e->be;
+    a.kin = 4 * e->cfg.patch * e->cfg.patch;
+    a.resid_out = e->resid[0];
+    a.has_next = 1; a.next = e->block_w(0);
+    a.q = e->q; a.k = e->k; a.v = e->v;
+    launch_token(TOK_EMBED, a, s);
+    e->mark(2, s);
+  }
+
+  // 4. blocks; mask-aware validity (MAT update) resolved into a per-block mode
+  bool seen_t = false;
+  int cur = 0, ti = 0;
+  for (int i = 0; i < e->nb; ++i) {
+    const bool temporal = e->blk[i].temporal;
+    int mode = 0;
+    if (e->cfg.mask_aware_attention && !seen_t) {
+      if (i == 0) mode = temporal ? 2 : 1;
+      else mode = temporal ? 3 : 0;
+    }
+    AttnArgs at{};
+    at.q = e->q; at.T = T; at.frames = B; at.out = e->attn;
+    at.k[0] = e->k; at.v[0] = e->v; at.seg_frame_stride[0] = 1;
+    at.key_valid = tv; at.mask_mode = mode;
+    if (temporal) {
+      const int sl1 = same_slot ? 0 : 1;
+      at.n_seg = 3; at.groups = e->cfg.temporal_groups; at.band = T / at.groups;
+      at.k[1] = e->skv(ti, 0, 0); at.v[1] = e->skv(ti, 0, 1);
+      at.k[2] = e->skv(ti, sl1, 0); at.v[2] = e->skv(ti, sl1, 1);
+      at.seg_frame_stride[1] = at.seg_frame_stride[2] = io->slot_batched ? 1 : 0;
+      ++ti;
+      seen_t = true;
+    } else {
+      at.n_seg = 1; at.groups = 1; at.band = T;
+    }
+    launch_attention(at, s);
+    e->mark(temporal ? 4 : 3, s);
+
+    const bool last = i == e->nb - 1;
+    TokenArgs a{};
+    a.n_tok = B * T; a.T = T;
+    a.attn = e->attn; a.resid_in = e->resid[cur]; a.cur = e->block_w(i);
+    a.resid_out = last ? io->new_slot : e->resid[cur ^ 1];
+    a.has_next = !last;
+    if (!last) a.next = e->block_w(i + 1);
+    a.q = e->q; a.k = e->k; a.v = e->v;
+    a.tok16 = e->tok16;
+    launch_token(TOK_POST, a, s);
+    e->mark(5, s);
+    cur ^= 1;
+  }
+
+  // 5. decoder tail
+  DecodeArgs d{};
+  d.frames = B; d.H = e->H; d.W = e->W; d.R = e->R; d.Cc = e->Cc;
+  d.tok16 = e->tok16;
+  d.wv2p = e->frags + e->wv2p; d.bv2p = e->fparams + e->bv2p;
+  d.wd0 = e->frags + e->wd0; d.bd0 = e->fparams + e->bd0;
+  d.wd2 = e->frags + e->wd2; d.bd2 = e->fparams + e->bd2;
+  d.raster = e->raster; d.d0 = e->d0;
+  d.alpha = alpha; d.rgb_f32 = io->rgb_f32; d.rgb_u8 = io->rgb_u8;
+  d.fill = io->fill; d.out_f32 = io->out_f32; d.out_u8 = io->out_u8; d.flags = flags;
+  launch_vec2patch(d, s);
+  e->mark(6, s);
+  launch_decode0(d, s);
+  e->mark(7, s);
+  launch_decode2(d, s);
+  e->mark(8, s);
+  CUDA_TRY(cudaGetLastError());
+  return DR_OK;
+}
+
+int dr_profile(dr_engine* e, int32_t on) {
+  if (!e) return fail(DR_ERR_CONFIG, "null engine");
+  e->profiling = on;
+  e->n_ev = 0;
+  return DR_OK;
+}
+
+int32_t dr_profile_read(dr_engine* e, float* ms, int32_t* kinds, int32_t cap) {
+  if (!e || !e->profiling || e->n_ev < 2) return 0;
+  int n = 0;
+  for (int i = 1; i < e->n_ev && n < cap; ++i, ++n) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, e->ev[i - 1], e->ev[i]) != cudaSuccess) return -1;
+    ms[n] = t;
+    kinds[n] = e->ev_kind[i];
+  }
+  return n;
+}
+
+int dr_reset_memory(dr_engine* e) {
+  if (!e) return fail(DR_ERR_CONFIG, "null engine");
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t slot = (size_t)e->T * C * sizeof(float);
+  for (auto*& r : e->ring) {
+    if (!r) CUDA_TRY(cudaMalloc(&r, slot));
+    CUDA_TRY(cudaMemset(r, 0, slot));
+  }
+  e->mem0 = 0;
+  e->mem1 = 0;                       // cold start: both slots are the same zero tensor
+  return DR_OK;
+}
+
+int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                       uint8_t* out_hwc, void* stream) {
+  if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t px = e->frame_px();
+  if (!e->h_rgb) {
+    CUDA_TRY(cudaMalloc(&e->h_rgb, px * 3));
+    CUDA_TRY(cudaMalloc(&e->h_m0, px));
+    CUDA_TRY(cudaMalloc(&e->h_out, px * 3));
+    CUDA_TRY(cudaMallocHost(&e->pin, px * 7));
+    CUDA_TRY(cudaMallocHost(&e->pin_flags, sizeof(int)));
+    int rc = dr_reset_memory(e);
+    if (rc) return rc;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* p_rgb = e->pin;
+  uint8_t* p_m0 = e->pin + px * 3;
+  uint8_t* p_out = e->pin + px * 4;
+  std::memcpy(p_rgb, rgb_hwc, px * 3);
+  std::memcpy(p_m0, mask_hw, px);
+  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, px, cudaMemcpyHostToDevice, s));
+  int fresh = 0;
+  while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
+  dr_frame_io io{};
+  io.frames = 1;
+  io.rgb_u8 = e->h_rgb; io.mask_m0 = e->h_m0;
+  io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
+  io.new_slot = e->ring[fresh];
+  io.out_u8 = e->h_out;
+  int rc = dr_forward(e, &io, stream);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(p_out, e->h_out, px * 3, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(e->pin_flags, e->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const int fl = *e->pin_flags;
+  if (fl & DR_FLAG_UNREDACTED)
+    return fail(DR_ERR_INPUT, "input is not redacted: nonzero pixels inside mask");
+  if (fl & DR_FLAG_NONFINITE) return fail(DR_ERR_NUMERIC, "model produced non-finite output");
+  std::memcpy(out_hwc, p_out, px * 3);
+  e->mem0 = e->mem1;
+  e->mem1 = fresh;
+  return DR_OK;
+}
+
+}  // extern "C"

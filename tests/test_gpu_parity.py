@@ -1,0 +1,268 @@
+"""GPU parity of the sm_100a path (through the C-ABI) against the CPU oracle and the
+reference golden fixtures.
+
+Tolerances (BASELINE.json north_star): dilated and token masks bit-exact; feathered alpha
+within 1e-6 (it is bit-identical to scipy by construction); inpainted frames within
+max-abs 2e-2 on [0,1] pixels and PSNR >= 40 dB against the fp32 CPU output.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cfg_from, golden, perturb_1d
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import dstt_oracle as O  # noqa: E402
+from paper_2509_10466_b200 import (BinaryMask, DsttConfig, DsttEngine, EngineNumericError,  # noqa: E402
+                                   InputError, dilate_mask, feather_mask, token_mask)
+from paper_2509_10466_b200 import synth  # noqa: E402
+from paper_2509_10466_b200.weights import seed_parameters  # noqa: E402
+
+MAX_ABS = 2e-2
+MIN_PSNR = 40.0
+
+
+def psnr(a, b):
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10 * np.log10(1.0 / mse)
+
+
+def assert_close_img(got, ref, what=""):
+    err = float(np.max(np.abs(got - ref)))
+    p = psnr(got, ref)
+    assert err <= MAX_ABS, f"{what} max-abs {err:.3e}"
+    assert p >= MIN_PSNR, f"{what} PSNR {p:.1f} dB"
+    return err, p
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+# ------------------------------------------------------------------ mask stage
+@pytest.mark.parametrize("r", [0, 1, 3, 5])
+def test_dilate_bit_exact_vs_reference(r):
+    g = golden("masks.npz")
+    m1 = dilate_mask(cuda(g["m0"].astype(np.uint8)), r).cpu().numpy().astype(bool)
+    assert np.array_equal(m1, g[f"dilate_r{r}"])
+
+
+@pytest.mark.parametrize("sigma", [1.5, 3.0])
+def test_feather_vs_reference_scipy(sigma):
+    g = golden("masks.npz")
+    a = feather_mask(cuda(g["dilate_r3"].astype(np.uint8)), sigma).cpu().numpy()
+    ref = g[f"feather_r3_s{sigma}"]
+    assert np.max(np.abs(a - ref)) <= 1e-6
+    # scipy's float64 summation order is replicated: expect bit-identical output
+    assert np.mean(a == ref) > 0.999
+
+
+def test_token_mask_bit_exact_random(rng):
+    m = rng.random((3, 64, 96)) > 0.3
+    m[0, :32, :32] = True
+    m[2] = True
+    got = token_mask(cuda(m.astype(np.uint8)), 8).cpu().numpy().astype(bool)
+    assert np.array_equal(got, O.token_mask(m, 8))
+
+
+def test_mask_stage_large_radius_borders(rng):
+    m0 = rng.random((2, 128, 160)) > 0.995
+    m0[1, 0, :] = True
+    for r in (7, 12, 31):
+        got = dilate_mask(cuda(m0.astype(np.uint8)), r).cpu().numpy().astype(bool)
+        assert np.array_equal(got, O.dilate_mask(m0, r)), r
+
+
+# ------------------------------------------------------------------ forward vs goldens
+def _engine_b64(g, **kw):
+    cfg = cfg_from(g["cfg"], **kw)
+    w = perturb_1d(seed_parameters(cfg, int(g["weight_seed"])), int(g["perturb_seed"]))
+    return cfg, w, DsttEngine.from_arrays(cfg, w)
+
+
+def test_forward_cold_and_warm_vs_reference_golden():
+    """Reference DsttModel.forward outputs (perturbed biases/LN), B=2, cold + warm."""
+    g = golden("forward_b64.npz")
+    cfg, w, eng = _engine_b64(g)
+    zero = torch.zeros(cfg.tokens, cfg.channels)
+    fill, slot = eng.model_forward(cuda(g["rgb"]), cuda(g["mask"]), (zero, zero))
+    assert_close_img(fill.cpu().numpy(), g["out_cold"], "cold")
+    assert np.max(np.abs(slot.cpu().numpy() - g["slot_cold"])) < 5e-2
+    fill, slot = eng.model_forward(cuda(g["rgb"]), cuda(g["mask"]),
+                                   (cuda(g["warm0"]), cuda(g["warm1"])))
+    assert_close_img(fill.cpu().numpy(), g["out_warm"], "warm")
+    assert np.max(np.abs(slot.cpu().numpy() - g["slot_warm"])) < 5e-2
+
+
+def test_mask_aware_vs_reference_shim_golden():
+    g = golden("mask_aware_b64.npz")
+    cfg, w, eng = _engine_b64(g, mask_aware_attention=True)
+    res = eng.run(cuda(g["rgb"]), cuda(g["m"]), (cuda(g["warm0"]), cuda(g["warm1"])),
+                  want_fill=True, want_masks=True)
+    assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), g["valid"])
+    assert_close_img(res["fill"].cpu().numpy(), g["out"], "mask-aware")
+    assert np.max(np.abs(res["slot"].cpu().numpy() - g["slot"])) < 5e-2
+
+
+def test_c1_full_path_vs_reference_golden():
+    """BASELINE configs[0]: 256^2, r=5, sigma=3, seeded weights, cold memory."""
+    g = golden("c1_256.npz")
+    cfg = DsttConfig.baseline(256, mask_dilate=5, mask_feather_sigma=3.0)
+    eng = DsttEngine(cfg, seed=0)
+    img, m0 = synth.c1_frame(0, 256)
+    res = eng.run(cuda(img[None]), cuda(m0[None]), None, want_fill=True, want_masks=True)
+    assert np.array_equal(np.packbits(res["m1"][0].cpu().numpy().astype(bool)), g["m1"])
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    ref = O.inpaint_path(cfg, seed_parameters(cfg, 0), img[None], m0[None], (zero, zero))
+    assert np.max(np.abs(res["alpha"].cpu().numpy() - ref["alpha"])) <= 1e-6
+    assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), ref["token_valid"])
+    assert_close_img(res["fill"].cpu().numpy(), ref["fill"], "C1 fill vs oracle")
+    assert_close_img(res["out"].cpu().numpy(), ref["out"], "C1 composite vs oracle")
+    assert_close_img(res["fill"].cpu().numpy()[0], g["out_f16"].astype(np.float32),
+                     "C1 fill vs reference")
+
+
+def test_c2_sequence_512_vs_oracle():
+    """BASELINE configs[1] shapes: 512^2 frames, memory carried across 3 frames."""
+    cfg = DsttConfig.baseline(512, mask_dilate=5, mask_feather_sigma=3.0)
+    eng = DsttEngine(cfg, seed=0)
+    w = seed_parameters(cfg, 0)
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    ref_slots = (zero, zero)
+    mem = eng.zero_memory()
+    for seed in range(3):
+        img, m0 = synth.c2_frame(seed)
+        res = eng.run(cuda(img[None]), cuda(m0[None]), mem.slots, want_fill=True,
+                      want_masks=True)
+        mem = mem.push(res["slot"][0])
+        ref = O.inpaint_path(cfg, w, img[None], m0[None], ref_slots)
+        ref_slots = (ref_slots[1], ref["slot"][0])
+        assert np.array_equal(res["m1"].cpu().numpy().astype(bool), ref["m1"])
+        assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool),
+                              ref["token_valid"])
+        assert np.max(np.abs(res["alpha"].cpu().numpy() - ref["alpha"])) <= 1e-6
+        assert_close_img(res["out"].cpu().numpy(), ref["out"], f"C2 frame {seed}")
+
+
+# ------------------------------------------------------------------ reference u8 API
+def _redacted(rng, h, w, frac):
+    rgb = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    bits = rng.random((h, w)) < frac
+    rgb[bits] = 0
+    return rgb, bits
+
+
+def test_u8_inpaint_matches_oracle_and_composite_guarantee(rng):
+    cfg = DsttConfig.baseline(64)
+    eng = DsttEngine(cfg, seed=1)
+    w = seed_parameters(cfg, 1)
+    mem = eng.zero_memory()
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    slots = (zero, zero)
+    for t in range(6):
+        rgb, bits = _redacted(rng, 64, 64, float(rng.uniform(0.05, 0.5)))
+        if t == 3:
+            bits[:] = False
+        res = eng.inpaint(rgb, BinaryMask(bits), mem)
+        mem = res.memory
+        assert mem.pushes == t + 1
+        assert np.array_equal(res.rgb[~bits], rgb[~bits]), "leaked outside the mask"
+        fill, slot = O.model_forward(cfg, w, O.u8_to_unit(rgb),
+                                     bits[None, None].astype(np.float32), slots)
+        slots = (slots[1], slot[0])
+        ref = O.composite_u8(O.to_u8(fill)[0], rgb, bits.astype(np.float32))
+        diff = np.abs(res.rgb.astype(int) - ref.astype(int))
+        assert diff.max() <= 6 and psnr(res.rgb / 255.0, ref / 255.0) >= MIN_PSNR
+
+
+def test_u8_inpaint_errors():
+    cfg = DsttConfig.baseline(64)
+    eng = DsttEngine(cfg, seed=0)
+    rgb = np.full((64, 64, 3), 7, np.uint8)
+    bits = np.zeros((64, 64), bool)
+    bits[10:20, 10:20] = True
+    with pytest.raises(InputError):
+        eng.inpaint(rgb, BinaryMask(bits))                  # not redacted
+    with pytest.raises(InputError):
+        eng.inpaint(rgb.astype(np.float32), BinaryMask(bits))
+    from paper_2509_10466_b200 import ConfigError
+    with pytest.raises(ConfigError):
+        eng.inpaint(np.zeros((32, 64, 3), np.uint8), BinaryMask(np.zeros((32, 64), bool)))
+    w = seed_parameters(cfg, 0)
+    w[-4] = np.full_like(w[-4], np.nan)                     # decode.0 weight (test_dstt.py:216)
+    bad = DsttEngine.from_arrays(cfg, w)
+    with pytest.raises(EngineNumericError):
+        bad.inpaint(np.zeros((64, 64, 3), np.uint8), BinaryMask.empty(64, 64))
+
+
+def test_memory_fifo_and_memory_changes_output(rng):
+    cfg = DsttConfig.baseline(64)
+    eng = DsttEngine(cfg, seed=2)
+    rgb, bits = _redacted(rng, 64, 64, 0.3)
+    mask = BinaryMask(bits)
+    mem = eng.zero_memory()
+    seen = []
+    for _ in range(3):
+        r = eng.inpaint(rgb, BinaryMask.empty(64, 64), mem)
+        mem = r.memory
+        seen.append(mem.slots[-1])
+    assert torch.equal(mem.slots[0], seen[1]) and torch.equal(mem.slots[1], seen[2])
+    cold = eng.inpaint(rgb, mask, eng.zero_memory())
+    warm = eng.inpaint(rgb, mask, eng.zero_memory().push(torch.randn(cfg.tokens, 64))
+                       .push(torch.randn(cfg.tokens, 64)))
+    assert not np.array_equal(cold.rgb, warm.rgb)
+
+
+def test_host_buffer_path_equals_device_path(rng):
+    """dr_inpaint_u8_host (engine-held memory) == engine.inpaint with carried memory."""
+    cfg = DsttConfig.baseline(64, mask_dilate=2, mask_feather_sigma=1.5)
+    eng = DsttEngine(cfg, seed=4)
+    mem = eng.zero_memory()
+    for _ in range(4):
+        rgb, bits = _redacted(rng, 64, 64, 0.2)
+        a = eng.inpaint(rgb, BinaryMask(bits), mem)
+        mem = a.memory
+        b = eng.inpaint_host(rgb, bits)
+        assert np.array_equal(a.rgb, b)
+
+
+# ------------------------------------------------------------------ full-size properties
+def test_batch_invariance_and_determinism_512():
+    cfg = DsttConfig.baseline(512, mask_dilate=5, mask_feather_sigma=3.0)
+    eng = DsttEngine(cfg, seed=0)
+    imgs, masks = synth.frame_pool("C5", 3)
+    rng = np.random.default_rng(0)
+    slots = [cuda(rng.normal(0, 1, (3, cfg.tokens, 64)).astype(np.float32)) for _ in range(2)]
+    out_b, slot_b = eng.forward(cuda(imgs), cuda(masks), slots)
+    out_b2, _ = eng.forward(cuda(imgs), cuda(masks), slots)
+    assert torch.equal(out_b, out_b2), "non-deterministic"
+    for i in range(3):
+        o, s = eng.forward(cuda(imgs[i:i + 1]), cuda(masks[i:i + 1]),
+                           [sl[i:i + 1] for sl in slots])
+        assert torch.equal(o[0], out_b[i]) and torch.equal(s[0], slot_b[i])
+    # composite guarantee: alpha == 0 pixels are the input frame bit-exactly
+    res = eng.run(cuda(imgs), cuda(masks), slots, want_masks=True)
+    a = res["alpha"].cpu().numpy()
+    out = res["out"].cpu().numpy()
+    keep = np.broadcast_to((a == 0)[:, None], out.shape)
+    assert np.array_equal(out[keep], imgs[keep])
+    assert (a[masks] == 1.0).all()
+
+
+def test_c4_1024_mask_aware_vs_oracle():
+    """BASELINE configs[3]: 1024^2, 30-45% occlusion, mask-aware attention on."""
+    cfg = DsttConfig.baseline(1024, mask_dilate=5, mask_feather_sigma=3.0,
+                              mask_aware_attention=True)
+    eng = DsttEngine(cfg, seed=0)
+    img, m0 = synth.c4_frame(0)
+    res = eng.run(cuda(img[None]), cuda(m0[None]), None, want_masks=True)
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    ref = O.inpaint_path(cfg, seed_parameters(cfg, 0), img[None], m0[None], (zero, zero))
+    assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), ref["token_valid"])
+    assert (~ref["token_valid"]).any()
+    assert_close_img(res["out"].cpu().numpy(), ref["out"], "C4 composite")
