@@ -105,6 +105,13 @@ int dr_reset_memory(dr_engine* e);
 /* Number of kernels one dr_forward launches for `frames` frames (for accounting). */
 int32_t dr_kernels_per_forward(dr_engine* e);
 
+/* Op-level entry for parity tests of the tcgen05 implicit-GEMM convolution
+ * (decode.0 form, dstt.py:241-242): out = LeakyReLU_0.2(conv3x3(in) + bias), NHWC fp16
+ * rasters [frames][H][W][64], weight [64][64][3][3] fp32 host, bias [64] fp32 host. */
+int dr_op_conv3x3(int32_t frames, int32_t height, int32_t width, const void* in_nhwc_f16,
+                  const float* weight_host, const float* bias_host, void* out_nhwc_f16,
+                  void* stream);
+
 /* Per-stage CUDA events on the launch stream (off by default).  After the stream has
  * passed a dr_forward, dr_profile_read fills ms[i] / kinds[i] for each stage and returns
  * the count (-1 on an event error).  Kinds: 0 mask stage, 1 slot K/V, 2 embed,

@@ -57,6 +57,9 @@ SIGNATURES = {
                                           ctypes.c_void_p, ctypes.c_void_p]),
     "dr_reset_memory": (ctypes.c_int, [ctypes.c_void_p]),
     "dr_kernels_per_forward": (ctypes.c_int32, [ctypes.c_void_p]),
+    "dr_op_conv3x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p]),
     "dr_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "dr_profile_read": (ctypes.c_int32, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
                                          ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]),

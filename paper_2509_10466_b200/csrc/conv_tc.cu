@@ -1,0 +1,227 @@
+// 3x3 convolutions of the decoder on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+//   decode.0  Conv2d(64, 64, 3, pad 1) + LeakyReLU(0.2)          dstt.py:241-242
+//   decode.2  Conv2d(64, 3, 3, pad 1), (tanh+1)/2, u8 conversion, non-finite guard and
+//             the alpha composite                               dstt.py:243, :267, :322-325;
+//                                                               base.py:87-88
+//
+// Implicit GEMM, M = 128 pixels of one output row, N = output channels (64, or 16 with
+// 3 real for decode.2), K = 9 taps x 64 input channels.  A persistent CTA owns the whole
+// fp16 weight image in smem (one bulk copy) and walks 2-row x 128-pixel tiles:
+//   warp 0      TMA: the 4 x 130-pixel x 64-channel input halo of the next tile, as 8
+//               planes of 8 channels (K-major, no swizzle: core matrix = 8 px x 16 B);
+//               off-image rows/columns are zero-filled by TMA = the conv's zero padding
+//   warp 1      one thread issues 2 x 9 x 4 tcgen05.mma (128 x N x 16) per tile into a
+//               double-buffered TMEM accumulator; tap (dy,dx) is just a descriptor offset
+//   warps 2-5   epilogue: tcgen05.ld (lane = pixel), bias + activation, stores
+// Double-buffered halo (2 x 65 KB) and TMEM let TMA, MMA and the epilogue overlap.
+#include <cuda.h>
+#include <math.h>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace dr {
+
+namespace {
+
+constexpr int TX = 128;                     // pixels per MMA (M)
+constexpr int TR = 2;                       // output rows per tile
+constexpr int HX = TX + 2, HR = TR + 2;     // halo
+constexpr int HALO_BYTES = HR * HX * 128;   // [row][px][64 ch] fp16, 128B-swizzled rows
+constexpr int THREADS = 192;
+static_assert(HALO_BYTES % 1024 == 0, "halo buffers must stay 1024-byte aligned");
+// The tap (dy,dx) A operand starts (r+dy)*130+dx pixel rows into a 1024-byte aligned
+// swizzled halo.  Measured on B200: the MMA unit applies the 128B XOR swizzle on absolute
+// smem address bits (like TMA), so such row-shifted descriptors need base_offset 0
+// (tests/test_gpu_ops.py pins this; base_offset = row & 7 produces garbage).
+
+template <int N>
+struct __align__(128) ConvSmem {
+  uint8_t halo[2][HALO_BYTES];
+  uint8_t w[9 * 8 * N * 16];                 // [tap][k-chunk][co][8 ci] fp16
+  uint64_t halo_full[2], halo_empty[2], tmem_full[2], tmem_empty[2], w_full;
+  uint32_t tmem_base;
+};
+
+template <int N>
+constexpr uint32_t tmem_cols() { return 2 * TR * N <= 32 ? 32 : (2 * TR * N <= 64 ? 64 : (2 * TR * N <= 128 ? 128 : 256)); }
+
+template <int N, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  ConvSmem<N>& sm = *reinterpret_cast<ConvSmem<N>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t COLS = tmem_cols<N>();
+  constexpr uint32_t WBYTES = 9 * 8 * N * 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_x = (a.W + TX - 1) / TX, tiles_y = (a.H + TR - 1) / TR;
+  const int n_tiles = a.frames * tiles_y * tiles_x;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&sm.halo_full[b], 1);
+      tc::mbar_init(&sm.halo_empty[b], 1);
+      tc::mbar_init(&sm.tmem_full[b], 1);
+      tc::mbar_init(&sm.tmem_empty[b], 4);
+    }
+    tc::mbar_init(&sm.w_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<COLS>(&sm.tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {                                     // ---------------- TMA producer
+      tc::tma_prefetch(&tin);
+      tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES);
+      for (uint32_t off = 0; off < WBYTES; off += 16384) {
+        const uint32_t n = WBYTES - off < 16384 ? WBYTES - off : 16384;
+        tc::bulk_load(sm.w + off, reinterpret_cast<const uint8_t*>(a.w) + off, n, &sm.w_full);
+      }
+      int i = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        const int tx = t % tiles_x, rest = t / tiles_x;
+        const int ty = rest % tiles_y, f = rest / tiles_y;
+        tc::mbar_wait(&sm.halo_empty[buf], ph ^ 1);
+        tc::mbar_arrive_expect_tx(&sm.halo_full[buf], HALO_BYTES);
+        tc::tma_load_4d(sm.halo[buf], &tin, &sm.halo_full[buf], 0, tx * TX - 1, ty * TR - 1, f);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                     // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_f16(128, N);
+      tc::mbar_wait(&sm.w_full, 0);
+      const uint32_t w_s = tc::smem_u32(sm.w);
+      int i = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        tc::mbar_wait(&sm.halo_full[buf], ph);
+        tc::mbar_wait(&sm.tmem_empty[buf], ph ^ 1);
+        tc::fence_after();
+        const uint32_t h_s = tc::smem_u32(sm.halo[buf]);
+#pragma unroll 1
+        for (int r = 0; r < TR; ++r) {
+          const uint32_t d = tbase + (uint32_t)(buf * TR * N + r * N);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint32_t row = (uint32_t)((r + dy) * HX + dx);      // first pixel row
+              const uint32_t aa = h_s + row * 128 + ks * 32;
+              const uint64_t ad = tc::sdesc_sw128(aa, 0);
+              const uint64_t bd = tc::sdesc(w_s + (tap * 8 + 2 * ks) * N * 16, N * 16, 128);
+              tc::mma_f16(d, ad, bd, idesc, (tap | ks) != 0);
+            }
+          }
+        }
+        tc::mma_commit(&sm.halo_empty[buf]);
+        tc::mma_commit(&sm.tmem_full[buf]);
+      }
+    }
+  } else {                                               // ---------------- epilogue
+    const int q = warp & 3;                              // TMEM lanes 32q..32q+31
+    const size_t plane = (size_t)a.H * a.W;
+    int i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int buf = i & 1;
+      const uint32_t ph = (i >> 1) & 1;
+      const int tx = t % tiles_x, rest = t / tiles_x;
+      const int ty = rest % tiles_y, f = rest / tiles_y;
+      const int x = tx * TX + 32 * q + lane;
+      tc::mbar_wait(&sm.tmem_full[buf], ph);
+      tc::fence_after();
+#pragma unroll 1
+      for (int r = 0; r < TR; ++r) {
+        const int y = ty * TR + r;
+        uint32_t v[N];
+        const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * TR * N + r * N);
+#pragma unroll
+        for (int j = 0; j < N / 16; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
+        tc::tmem_wait_ld();
+        if (y >= a.H || x >= a.W) continue;
+        const size_t pix = (size_t)y * a.W + x;
+        if constexpr (EPI == 0) {
+          uint4* dst = reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + pix) * 64);
+#pragma unroll
+          for (int c8 = 0; c8 < N / 8; ++c8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = c8 * 8 + 2 * e;
+              float u0 = __uint_as_float(v[c]) + __ldg(a.bias + c);
+              float u1 = __uint_as_float(v[c + 1]) + __ldg(a.bias + c + 1);
+              u0 = u0 >= 0.f ? u0 : 0.2f * u0;
+              u1 = u1 >= 0.f ? u1 : 0.2f * u1;
+              pk[e] = pack_half2(u0, u1);
+            }
+            dst[c8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        } else {
+          const float al = a.alpha ? a.alpha[(size_t)f * plane + pix] : 1.f;
+          bool bad = false;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float raw = __uint_as_float(v[ch]) + __ldg(a.bias + ch);
+            const float out01 = (tanhf(raw) + 1.0f) * 0.5f;
+            bad |= !isfinite(out01);
+            const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
+            if (a.fill) a.fill[pl] = out01;
+            if (a.out_f32) {
+              const float fr = a.rgb_f32[pl];
+              a.out_f32[pl] = __fadd_rn(__fmul_rn(al, out01), __fmul_rn(__fsub_rn(1.0f, al), fr));
+            }
+            if (a.out_u8) {
+              const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
+              const size_t pu = ((size_t)f * plane + pix) * 3 + ch;
+              const uint8_t src8 = a.rgb_u8[pu];
+              uint8_t o;
+              if (al == 0.f) o = src8;
+              else if (al == 1.f) o = fill8;
+              else o = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(al, (float)fill8),
+                                                             __fmul_rn(__fsub_rn(1.0f, al), (float)src8))), 0.f), 255.f);
+              a.out_u8[pu] = o;
+            }
+          }
+          if (bad) atomicOr(a.flags + f, 1);
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<COLS>(tbase);
+}
+
+template <int N, int EPI>
+void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
+  static int sms = 0;
+  const int smem = (int)sizeof(ConvSmem<N>) + 1024;
+  if (!sms) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
+  const int grid = tiles < sms ? tiles : sms;
+  conv3x3_tc_kernel<N, EPI><<<grid, THREADS, smem, s>>>(tin, a);
+}
+
+}  // namespace
+
+size_t conv_tc_weight_bytes(int n) { return (size_t)9 * 8 * n * 16; }
+void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
+  if (n == 64) launch<64, 0>(tin, a, s);
+  else launch<16, 1>(tin, a, s);
+}
+
+}  // namespace dr

@@ -1,9 +1,12 @@
 // C-ABI of libdrb200.so: engine lifetime, weight repack, workspace, and the per-frame
 // launch sequence (mask stage -> slot K/V -> embed -> S/T blocks -> decoder tail).
 // See include/dr_b200.h for the contract and the reference interfaces replaced.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -72,6 +75,51 @@ std::vector<double> feather_taps(double sigma) {
   return fw;
 }
 
+// TMA view of an NHWC fp16 raster [frames][H][W][64]: box = 8 channels x 130 px x 4 rows
+// (one K-chunk plane of the conv halo; coordinates may be negative / past the edge, the
+// out-of-bounds elements are zero-filled = the conv's zero padding).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && fn)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  return encode;
+}
+
+int make_nhwc_map(CUtensorMap* map, void* base, int frames, int H, int W) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)frames};
+  const cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
+  const cuuint32_t box[4] = {64, 130, 4, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return DR_OK;
+}
+
+// tcgen05 conv weight image, K-major no-swizzle core matrices: [tap][k-chunk][co][8 ci]
+// fp16, from a PyTorch Conv2d weight [co_real][c][3][3]; rows co >= co_real are zero.
+void pack_conv_tc(const float* w, int c, int co_real, int co_pad, std::vector<uint16_t>& out) {
+  for (int tap = 0; tap < 9; ++tap)
+    for (int ch = 0; ch < c / 8; ++ch)
+      for (int co = 0; co < co_pad; ++co)
+        for (int j = 0; j < 8; ++j) {
+          const float v = co < co_real ? w[((size_t)co * c + ch * 8 + j) * 9 + tap] : 0.f;
+          const __half h = __float2half_rn(v);
+          uint16_t u;
+          std::memcpy(&u, &h, 2);
+          out.push_back(u);
+        }
+}
+
 }  // namespace
 
 struct dr_engine {
@@ -79,10 +127,13 @@ struct dr_engine {
   int device = 0;
   int H = 0, W = 0, R = 0, Cc = 0, T = 0, nb = 0, n_temporal = 0, feather_r = 0;
   std::vector<Blk> blk;
-  size_t we = 0, be = 0, wv2p = 0, bv2p = 0, wd0 = 0, bd0 = 0, wd2 = 0, bd2 = 0;
+  size_t we = 0, be = 0, bv2p = 0, bd0 = 0, bd2 = 0;
   uint2* frags = nullptr;
   float* fparams = nullptr;
   double* feather_w = nullptr;
+  uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
+  size_t wtc_d2 = 0, wtc_v2p = 0;    // byte offsets of the decode.2 / Vec2Patch images
+  CUtensorMap map_raster{}, map_d0{}, map_tok{};
   // workspace
   int cap = 0;
   void* ws = nullptr;
@@ -148,7 +199,8 @@ struct dr_engine {
     const size_t o_r0 = take(tok * C * 4), o_r1 = take(tok * C * 4);
     const size_t o_xin = take(tok * 4 * cfg.patch * cfg.patch * 2);
     const size_t o_q = take(tok * C * 2), o_k = take(tok * C * 2), o_v = take(tok * C * 2);
-    const size_t o_at = take(tok * C * 2), o_t16 = take(tok * C * 2);
+    const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
+    const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
     const size_t o_ras = take(px * C * 2), o_d0 = take(px * C * 2);
     const size_t o_skv = take((size_t)std::max(n_temporal, 1) * 4 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
@@ -163,6 +215,31 @@ struct dr_engine {
     raster = (__half*)(b + o_ras); d0 = (__half*)(b + o_d0);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
     cap = frames;
+    CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
+    int rc = make_raster_map(&map_raster, raster, frames);
+    if (rc) return rc;
+    rc = make_raster_map(&map_d0, d0, frames);
+    if (rc) return rc;
+    return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
+  }
+
+  int make_raster_map(CUtensorMap* map, void* base, int frames) {
+    return make_nhwc_map(map, base, frames, H, W);
+  }
+
+  // TMA view of the padded fp16 token grid [frames][np][64]: box 64 ch x 128 positions.
+  int make_token_map(CUtensorMap* map, void* base, int frames, int np) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {64, (cuuint64_t)np, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)np * 128};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled (tokens) failed: " + std::to_string((int)r));
     return DR_OK;
   }
 };
@@ -273,50 +350,43 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
     e->blk.push_back(b);
   }
   const int tb = 2 + 16 * nb;
-  {  // ConvTranspose2d weight (C_in, C_out, k, k): per tap, B[k=ci][n=co]
+  e->bv2p = addf(tb + 1);
+  e->bd0 = addf(tb + 3);
+  e->bd2 = addf(tb + 5);
+  // tcgen05 weight images, K-major no-swizzle core matrices [tap][k-chunk][co][8 ci] fp16:
+  // decode.0 (N=64), decode.2 (N=16, 3 real), then Vec2Patch (100 taps a*10+b, B[n=co][k=ci]
+  // = ConvTranspose2d weight[ci][co][a][b]).
+  std::vector<uint16_t> tcimg;
+  pack_conv_tc(weights[tb + 2], c, c, 64, tcimg);
+  e->wtc_d2 = tcimg.size() * 2;
+  pack_conv_tc(weights[tb + 4], c, 3, 16, tcimg);
+  e->wtc_v2p = tcimg.size() * 2;
+  {
     const float* wt = weights[tb];
-    e->wv2p = fr.size();
-    std::vector<float> m((size_t)c * c);
     for (int a = 0; a < kk; ++a)
-      for (int bb = 0; bb < kk; ++bb) {
-        for (int co = 0; co < c; ++co)
-          for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = wt[(((size_t)ci * c + co) * kk + a) * kk + bb];
-        pack_frags(m, c, c, fr);
-      }
-    e->bv2p = addf(tb + 1);
+      for (int bb = 0; bb < kk; ++bb)
+        for (int ch = 0; ch < c / 8; ++ch)
+          for (int co = 0; co < c; ++co)
+            for (int j = 0; j < 8; ++j) {
+              const int ci = ch * 8 + j;
+              const __half h = __float2half_rn(wt[(((size_t)ci * c + co) * kk + a) * kk + bb]);
+              uint16_t u;
+              std::memcpy(&u, &h, 2);
+              tcimg.push_back(u);
+            }
   }
-  {  // decode.0 Conv2d(C, C, 3): per tap W[co][ci]
-    const float* w0 = weights[tb + 2];
-    e->wd0 = fr.size();
-    std::vector<float> m((size_t)c * c);
-    for (int tap = 0; tap < 9; ++tap) {
-      for (int co = 0; co < c; ++co)
-        for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = w0[((size_t)co * c + ci) * 9 + tap];
-      pack_frags(m, c, c, fr);
-    }
-    e->bd0 = addf(tb + 3);
-  }
-  {  // decode.2 Conv2d(C, 3, 3): N padded 3 -> 8 with zeros
-    const float* w2 = weights[tb + 4];
-    e->wd2 = fr.size();
-    std::vector<float> m((size_t)8 * c, 0.f);
-    for (int tap = 0; tap < 9; ++tap) {
-      std::fill(m.begin(), m.end(), 0.f);
-      for (int co = 0; co < 3; ++co)
-        for (int ci = 0; ci < c; ++ci) m[(size_t)co * c + ci] = w2[((size_t)co * c + ci) * 9 + tap];
-      pack_frags(m, 8, c, fr);
-    }
-    e->bd2 = addf(tb + 5);
-  }
-  // Feather taps: scipy _gaussian_kernel1d (float64), radius int(4 sigma + 0.5).
+
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
   e->feather_r = (int)(fw.size() / 2);
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
   if (cudaMalloc(&e->frags, fr.size() * sizeof(uint2)) != cudaSuccess ||
       cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
-      cudaMalloc(&e->feather_w, fw.size() * sizeof(double)) != cudaSuccess)
+      cudaMalloc(&e->feather_w, fw.size() * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&e->wtc, tcimg.size() * 2) != cudaSuccess)
     return cleanup(fail(DR_ERR_CUDA, "cudaMalloc of weights failed"));
+  if (cudaMemcpy(e->wtc, tcimg.data(), tcimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
+    return cleanup(fail(DR_ERR_CUDA, "weight upload failed"));
   if (cudaMemcpy(e->frags, fr.data(), fr.size() * sizeof(uint2), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(e->fparams, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(e->feather_w, fw.data(), fw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -332,6 +402,7 @@ void dr_destroy(dr_engine* e) {
   cudaFree(e->frags);
   cudaFree(e->fparams);
   cudaFree(e->feather_w);
+  cudaFree(e->wtc);
   cudaFree(e->h_rgb);
   cudaFree(e->h_m0);
   cudaFree(e->h_out);
@@ -494,28 +565,58 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     if (!last) a.next = e->block_w(i + 1);
     a.q = e->q; a.k = e->k; a.v = e->v;
     a.tok16 = e->tok16;
+    a.R = e->R; a.Cc = e->Cc;
     launch_token(TOK_POST, a, s);
     e->mark(5, s);
     cur ^= 1;
   }
 
   // 5. decoder tail
-  DecodeArgs d{};
-  d.frames = B; d.H = e->H; d.W = e->W; d.R = e->R; d.Cc = e->Cc;
-  d.tok16 = e->tok16;
-  d.wv2p = e->frags + e->wv2p; d.bv2p = e->fparams + e->bv2p;
-  d.wd0 = e->frags + e->wd0; d.bd0 = e->fparams + e->bd0;
-  d.wd2 = e->frags + e->wd2; d.bd2 = e->fparams + e->bd2;
-  d.raster = e->raster; d.d0 = e->d0;
-  d.alpha = alpha; d.rgb_f32 = io->rgb_f32; d.rgb_u8 = io->rgb_u8;
-  d.fill = io->fill; d.out_f32 = io->out_f32; d.out_u8 = io->out_u8; d.flags = flags;
-  launch_vec2patch(d, s);
+  V2pArgs vp{};
+  vp.frames = B; vp.H = e->H; vp.W = e->W; vp.R = e->R; vp.Cc = e->Cc;
+  vp.w = e->wtc + e->wtc_v2p; vp.bias = e->fparams + e->bv2p; vp.raster = e->raster;
+  launch_v2p_tc(e->map_tok, vp, s);
   e->mark(6, s);
-  launch_decode0(d, s);
+  ConvTcArgs cv{};
+  cv.frames = B; cv.H = e->H; cv.W = e->W;
+  cv.w = e->wtc; cv.bias = e->fparams + e->bd0; cv.out16 = e->d0;
+  launch_conv3x3_tc(64, e->map_raster, cv, s);
   e->mark(7, s);
-  launch_decode2(d, s);
+  ConvTcArgs c2{};
+  c2.frames = B; c2.H = e->H; c2.W = e->W;
+  c2.w = e->wtc + e->wtc_d2; c2.bias = e->fparams + e->bd2;
+  c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
+  c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
+  launch_conv3x3_tc(16, e->map_d0, c2, s);
   e->mark(8, s);
   CUDA_TRY(cudaGetLastError());
+  return DR_OK;
+}
+
+int dr_op_conv3x3(int32_t frames, int32_t height, int32_t width, const void* in_nhwc_f16,
+                  const float* weight_host, const float* bias_host, void* out_nhwc_f16,
+                  void* stream) {
+  if (frames <= 0 || height <= 0 || width <= 0 || !in_nhwc_f16 || !weight_host ||
+      !bias_host || !out_nhwc_f16)
+    return fail(DR_ERR_INPUT, "bad conv arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<uint16_t> img;
+  pack_conv_tc(weight_host, 64, 64, 64, img);
+  CUtensorMap map;
+  int rc = make_nhwc_map(&map, const_cast<void*>(in_nhwc_f16), frames, height, width);
+  if (rc) return rc;
+  uint8_t* dev = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&dev, img.size() * 2 + 256, s));
+  CUDA_TRY(cudaMemcpyAsync(dev, img.data(), img.size() * 2, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(dev + img.size() * 2, bias_host, 256, cudaMemcpyHostToDevice, s));
+  ConvTcArgs cv{};
+  cv.frames = frames; cv.H = height; cv.W = width;
+  cv.w = dev; cv.bias = reinterpret_cast<const float*>(dev + img.size() * 2);
+  cv.out16 = static_cast<__half*>(out_nhwc_f16);
+  launch_conv3x3_tc(64, map, cv, s);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(dev, s));
+  CUDA_TRY(cudaStreamSynchronize(s));      // host vectors above are pageable staging
   return DR_OK;
 }
 

@@ -36,7 +36,9 @@ struct TokenArgs {
   int has_next;
   BlockW next;            // LN1 + QKV of the following block
   __half* q; __half* k; __half* v;   // [frames][HEADS][T][DH]
-  __half* tok16;          // [n_tok][64] fp16 copy when there is no next block
+  __half* tok16;          // fp16 copy when there is no next block, on the zero-padded
+                          // [frames][(R+2)(Cc+2)][64] grid that Vec2Patch reads
+  int R, Cc;              // token grid
 };
 
 enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
@@ -84,25 +86,40 @@ struct MaskArgs {
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- decoder
-struct DecodeArgs {
-  int frames, H, W, R, Cc;   // image and token grid
-  const __half* tok16;       // [frames][T][64]
-  const uint2* wv2p; const float* bv2p;   // [100][8][4][32] frags
-  const uint2* wd0; const float* bd0;     // [9][8][4][32]
-  const uint2* wd2; const float* bd2;     // [9][1][4][32] (N padded 3->8)
-  __half* raster;            // [frames][H][W][64]
-  __half* d0;                // [frames][H][W][64]
-  // tail
-  const float* alpha;        // [frames][H][W]
-  const float* rgb_f32;      // [frames][3][H][W] (float API) or null
-  const uint8_t* rgb_u8;     // [frames][H][W][3] (u8 API) or null
-  float* fill;               // [frames][3][H][W] raw network output (optional)
-  float* out_f32;            // [frames][3][H][W] composite (float API)
-  uint8_t* out_u8;           // [frames][H][W][3] composite (u8 API)
-  int* flags;                // bit0 = non-finite network output
+// tcgen05 3x3 convolution (conv_tc.cu).  Input = TMA tensor map over an NHWC fp16
+// raster [frames][H][W][64] (box 64 ch x 130 px x 4 rows, 128B swizzle).  Weights: fp16
+// image [tap 9][k-chunk 8][co N][8 ci], N = 64 (decode.0) or 16 (decode.2, 3 real).
+struct ConvTcArgs {
+  int frames, H, W;
+  const void* w;             // weight image, conv_tc_weight_bytes(N)
+  const float* bias;         // [N real]
+  __half* out16;             // decode.0: [frames][H][W][64]
+  // decode.2 tail: alpha [frames][H][W]; rgb/out f32 [frames][3][H][W] (float API) or
+  // u8 [frames][H][W][3] (u8 API); fill = raw network output; flags bit0 = non-finite
+  const float* alpha;
+  const float* rgb_f32;
+  const uint8_t* rgb_u8;
+  float* fill;
+  float* out_f32;
+  uint8_t* out_u8;
+  int* flags;
 };
-void launch_vec2patch(const DecodeArgs& a, cudaStream_t s);
-void launch_decode0(const DecodeArgs& a, cudaStream_t s);
-void launch_decode2(const DecodeArgs& a, cudaStream_t s);
+}  // namespace dr
+#include <cuda.h>
+namespace dr {
+size_t conv_tc_weight_bytes(int n);
+
+// tcgen05 Vec2Patch (v2p_tc.cu).  Tokens: fp16 [frames][(R+2)(Cc+2)][64], zero-padded grid
+// (token (i,j) at padded (i+1, j+1)), TMA box 64 ch x 128 positions, 128B swizzle.
+// Weights: [tap a*10+b][k-chunk 8][co 64][8 ci] fp16.
+struct V2pArgs {
+  int frames, H, W, R, Cc;
+  const void* w;
+  const float* bias;
+  __half* raster;            // [frames][H][W][64]
+};
+size_t v2p_tc_weight_bytes();
+void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s);
+void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
 
 }  // namespace dr

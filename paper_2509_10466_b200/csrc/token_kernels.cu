@@ -48,15 +48,23 @@ DR_DEV void store_rows_f32(const Frag16x64& x, float* dst, int n0, int n_tok, in
   }
 }
 
-DR_DEV void store_rows_f16(const Frag16x64& x, __half* dst, int n0, int n_tok, int lane) {
+// fp16 tokens onto the zero-padded (R+2) x (Cc+2) grid of Vec2Patch.
+DR_DEV size_t padded_pos(int n, int T, int R, int Cc) {
+  const int f = n / T, t = n - f * T;
+  const int i = t / Cc, j = t - i * Cc;
+  return ((size_t)f * (R + 2) + i + 1) * (Cc + 2) + j + 1;
+}
+
+DR_DEV void store_rows_padded_f16(const Frag16x64& x, __half* dst, int n0, int n_tok, int T,
+                                  int R, int Cc, int lane) {
   const int g = lane >> 2, t = lane & 3;
   const bool v0 = n0 + g < n_tok, v1 = n0 + g + 8 < n_tok;
+  __half* r0 = dst + (v0 ? padded_pos(n0 + g, T, R, Cc) : 0) * C;
+  __half* r1 = dst + (v1 ? padded_pos(n0 + g + 8, T, R, Cc) : 0) * C;
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
-    if (v0) *reinterpret_cast<uint32_t*>(dst + (size_t)(n0 + g) * C + nt * 8 + 2 * t) =
-        pack_half2(x.v[nt][0], x.v[nt][1]);
-    if (v1) *reinterpret_cast<uint32_t*>(dst + (size_t)(n0 + g + 8) * C + nt * 8 + 2 * t) =
-        pack_half2(x.v[nt][2], x.v[nt][3]);
+    if (v0) *reinterpret_cast<uint32_t*>(r0 + nt * 8 + 2 * t) = pack_half2(x.v[nt][0], x.v[nt][1]);
+    if (v1) *reinterpret_cast<uint32_t*>(r1 + nt * 8 + 2 * t) = pack_half2(x.v[nt][2], x.v[nt][3]);
   }
 }
 
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(WARPS * 32) token_kernel(TokenArgs a) {
   if (a.has_next) {
     qkv_out(x, a.next, a.q, a.k, a.v, n0, a.n_tok, a.T, 0, lane);
   } else if (a.tok16) {
-    store_rows_f16(x, a.tok16, n0, a.n_tok, lane);
+    store_rows_padded_f16(x, a.tok16, n0, a.n_tok, a.T, a.R, a.Cc, lane);
   }
 }
 

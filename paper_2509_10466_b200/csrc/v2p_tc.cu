@@ -1,0 +1,160 @@
+// Vec2Patch on the 5th-gen tensor cores: ConvTranspose2d(64, 64, k=10, stride=8) over the
+// token grid + crop offset 1 (reference dstt.py:198-221), written as an NHWC fp16 raster.
+//
+// Output-stationary phase GEMM.  Canvas pixel (8i+py, 8j+px) (raster pixel (y,x) = canvas
+// - 1) is the sum over the 1, 2 or 4 tokens whose 10x10 kernel covers it:
+//   token (i,j)     through tap (py,   px)
+//   token (i,j-1)   through tap (py,   px+8)   if px < 2
+//   token (i-1,j)   through tap (py+8, px)     if py < 2
+//   token (i-1,j-1) through tap (py+8, px+8)   if both
+// Tokens are stored on a zero-padded (R+2) x (Cc+2) grid (position (i+1, j+1)), so for a
+// run of 128 consecutive padded positions the four neighbour sets are the same run shifted
+// by 0, -1, -(Cc+2), -(Cc+3) rows: one TMA window (128B-swizzled, 128 B = one token per
+// row) serves every term as a descriptor offset.  A CTA = (128 positions, one py, frame):
+// 8 output phases px accumulate in 8 x 64 TMEM columns (the whole TMEM), 10 or 20 taps
+// of 8 KB weights sit in smem.  Warp 0 TMA, warp 1 MMA issue, warps 2-5 epilogue (bias,
+// fp16, 128-byte pixel stores), with a TMEM barrier per phase so stores overlap MMAs.
+#include <cuda.h>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace dr {
+
+namespace {
+
+constexpr int M = 128;
+constexpr int THREADS = 192;
+constexpr int TAP_BYTES = 64 * 64 * 2;                 // [k-chunk 8][co 64][8 ci] fp16
+constexpr int WIN_CHUNKS = 3;                          // window <= 384 rows (Cc <= 253)
+
+struct __align__(1024) V2pSmem {
+  uint8_t win[WIN_CHUNKS][M * 128];                    // token window, 128B-swizzled rows
+  uint8_t w[20][TAP_BYTES];
+  uint64_t win_full, w_full, tmem_full[8];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  V2pSmem& sm = *reinterpret_cast<V2pSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P0 = blockIdx.x * M, py = blockIdx.y, f = blockIdx.z;
+  const int PC = a.Cc + 2;                              // padded row length
+  const int NP = (a.R + 2) * PC;
+  const int win_rows = M + PC + 1;
+  const int n_chunks = (win_rows + M - 1) / M;
+  const int n_taps = py < 2 ? 20 : 10;
+
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sm.win_full, 1);
+    tc::mbar_init(&sm.w_full, 1);
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&sm.tmem_full[i], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&sm.tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {                                   // ------------------- loads
+      tc::tma_prefetch(&tok);
+      tc::mbar_arrive_expect_tx(&sm.win_full, n_chunks * M * 128);
+      for (int c = 0; c < n_chunks; ++c)
+        tc::tma_load_3d(sm.win[c], &tok, &sm.win_full, 0, P0 - (PC + 1) + c * M, f);
+      tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);
+      const uint8_t* w0 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)(py * 10) * TAP_BYTES;
+      for (int t = 0; t < 10; ++t) tc::bulk_load(sm.w[t], w0 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
+      if (py < 2) {
+        const uint8_t* w1 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)((py + 8) * 10) * TAP_BYTES;
+        for (int t = 0; t < 10; ++t)
+          tc::bulk_load(sm.w[10 + t], w1 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                   // ------------------- MMA issue
+      constexpr uint32_t idesc = tc::idesc_f16(128, 64);
+      tc::mbar_wait(&sm.win_full, 0);
+      tc::mbar_wait(&sm.w_full, 0);
+      tc::fence_after();
+      const uint32_t a_s = tc::smem_u32(sm.win[0]), w_s = tc::smem_u32(sm.w[0]);
+#pragma unroll 1
+      for (int px = 0; px < 8; ++px) {
+        // (tap slot in smem, window row offset of the token set)
+        int taps[4], offs[4], n = 0;
+        taps[n] = px;      offs[n++] = PC + 1;          // (i, j)
+        if (px < 2) { taps[n] = px + 8; offs[n++] = PC; }          // (i, j-1)
+        if (py < 2) { taps[n] = 10 + px; offs[n++] = 1; }          // (i-1, j)
+        if (py < 2 && px < 2) { taps[n] = 18 + px; offs[n++] = 0; } // (i-1, j-1)
+        const uint32_t d = tbase + (uint32_t)(px * 64);
+        for (int u = 0; u < n; ++u)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ad = tc::sdesc_sw128(a_s + (uint32_t)offs[u] * 128 + ks * 32, 0);
+            const uint64_t bd = tc::sdesc(w_s + (uint32_t)taps[u] * TAP_BYTES + 2 * ks * 1024, 1024, 128);
+            tc::mma_f16(d, ad, bd, idesc, (u | ks) != 0);
+          }
+        tc::mma_commit(&sm.tmem_full[px]);
+      }
+    }
+  } else {                                             // ------------------- epilogue
+    const int q = warp & 3;
+    const int m = 32 * q + lane;
+    const int P = P0 + m;
+    const int ii = P / PC, jj = P - ii * PC;
+    const int y = 8 * (ii - 1) + py - 1;
+    const bool row_ok = P < NP && y >= 0 && y < a.H && jj >= 1;
+    float bias[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) bias[c] = __ldg(a.bias + c);
+#pragma unroll 1
+    for (int px = 0; px < 8; ++px) {
+      tc::mbar_wait(&sm.tmem_full[px], 0);
+      tc::fence_after();
+      uint32_t v[64];
+      const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(px * 64);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
+      tc::tmem_wait_ld();
+      const int x = 8 * (jj - 1) + px - 1;
+      if (row_ok && x >= 0 && x < a.W) {
+        uint4* dst = reinterpret_cast<uint4*>(a.raster + (((size_t)f * a.H + y) * a.W + x) * 64);
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = c8 * 8 + 2 * e;
+            pk[e] = pack_half2(__uint_as_float(v[c]) + bias[c], __uint_as_float(v[c + 1]) + bias[c + 1]);
+          }
+          dst[c8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace
+
+size_t v2p_tc_weight_bytes() { return (size_t)100 * TAP_BYTES; }
+
+void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s) {
+  static bool init = false;
+  const int smem = (int)sizeof(V2pSmem) + 1024;
+  if (!init) {
+    cudaFuncSetAttribute(v2p_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  const int NP = (a.R + 2) * (a.Cc + 2);
+  dim3 grid((NP + M - 1) / M, 8, a.frames);
+  v2p_tc_kernel<<<grid, THREADS, smem, s>>>(tok, a);
+}
+
+}  // namespace dr
