@@ -5,11 +5,18 @@
 // band of queries to cat[band(cur), band(slot0), band(slot1)] (:166-191).  The reference
 // materialises the T x T weights; here scores live only in registers: online softmax in
 // the log2 domain (one FFMA + one MUFU ex2 per score), P packed to fp16 in registers and
-// fed straight back into the P*V HMMA.  With dh=16 the kernel is bound by MUFU ex2
-// (16/clk/SM) and by issue, not by the tensor pipe (64 MMA flops per score), so the
-// design goal is latency hiding: a CTA = 4 query tiles x 2 key halves = 8 warps that
-// share the cp.async-staged K/V blocks; the two halves' (max, sum, O) are merged through
-// smem at the end.  Accumulator chains are split (two O / l partials) for ILP.
+// fed straight back into the P*V HMMA.
+//
+// With dh = 16 the floor is MUFU ex2 (measured 16/clk/SM on B200, profiles/r01/
+// pipe_microbench_b200.txt), so everything else per score must stay small:
+//  * K/V arrive as 128-key blocks by cp.async.bulk (one thread, mbarrier completion);
+//    the producer (token_kernels.cu) already stored them with the 16-byte chunk swizzle
+//    that makes ldmatrix conflict-free, so no per-key index math runs on the SMs;
+//  * row sums come out of the P*V HMMA through a constant ones column (no FADD chain);
+//  * the running max is rescaled lazily (only when a row max grows by > 2^8, exact
+//    because numerator and denominator share the stale max);
+//  * a CTA = 4 query tiles x 2 key halves = 8 warps sharing the smem K/V stages; the two
+//    halves' (max, sum, O) are merged through smem at the end.
 //
 // Mask-aware mode (NEW): keys of fully-masked tokens of the current frame get
 // -inf; memory-slot keys are always valid; a spatial block whose frame has no valid key
@@ -19,6 +26,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc.cuh"
 
 namespace dr {
 
@@ -27,23 +35,28 @@ namespace {
 constexpr int QT = 4;                 // query tiles of 16 per CTA
 constexpr int KS = 2;                 // key splits per CTA
 constexpr int WARPS = QT * KS;
-constexpr int KB = 64;                // keys per block
+constexpr int KB = 128;               // keys per block
 constexpr int STAGES = 3;
+constexpr float RESCALE_SLACK = 8.f;  // log2 units: p <= 2^8 between rescales
 
 struct __align__(128) Smem {
   __half k[STAGES][KS][KB][DH];
   __half v[STAGES][KS][KB][DH];
-  float bias[STAGES][KS][KB];
+  float bias[STAGES][KS][KB];         // mask-aware mode only
   float ml[QT][32][4];                // key-half 1 partials: m0, m1, l0, l1 per lane
   float o[QT][32][8];
+  uint64_t full[STAGES];
 };
 
 // Swizzled 16-byte chunk position inside a 32-byte key row (conflict-free ldmatrix).
 DR_DEV int swz(int key, int chunk) { return chunk ^ ((key >> 2) & 1); }
 
+DR_DEV float max3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
+
 template <bool MASKED>
 __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
-  __shared__ Smem sm;
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qt = warp & (QT - 1), kh = warp / QT;
   const int g = lane >> 2, t = lane & 3;
@@ -54,6 +67,16 @@ __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
   const int n_kb = (n_keys + KB - 1) / KB;
   const int nkb_h = (n_kb + 1) / 2;            // blocks per key half
 
+  // zero the K/V ring once: tails of partial blocks must hold finite values
+  {
+    uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0][0][0]);
+    constexpr int n16 = (int)(2 * sizeof(sm.k) / 16);
+    for (int i = tid; i < n16; i += WARPS * 32) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) tc::mbar_init(&sm.full[s], 1);
+    tc::fence_barrier_init();
+  }
   int any_valid = 1;
   if constexpr (MASKED) {
     if (a.mask_mode == 1 || a.mask_mode == 3) {
@@ -63,43 +86,58 @@ __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
       any_valid = __syncthreads_or(mine);
     }
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
 
-  auto load_stage = [&](int kb, int st) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int idx = tid + c * WARPS * 32;            // 0..511
-      const int half = idx >> 8, rem = idx & 255;
-      const int which = rem >> 7, key = (rem & 127) >> 1, chunk = rem & 1;
+  // One thread: bulk-copy the key blocks of both halves for pipeline step kb.
+  auto issue = [&](int kb, int st) {
+    uint32_t bytes = 0;
+    int piece_kk[KS][3], piece_n[KS][3], n_pieces[KS] = {0, 0};   // <= 3 segments
+    for (int half = 0; half < KS; ++half) {
       const int blk = half * nkb_h + kb;
-      const int kk = blk * KB + key;
-      const bool valid = kb < nkb_h && blk < n_kb && kk < n_keys;
-      const int seg = valid ? kk / a.band : 0;
-      const int tok = band0 + (valid ? kk - seg * a.band : 0);
-      const int stride = seg == 0 ? a.seg_frame_stride[0]
-                       : (seg == 1 ? a.seg_frame_stride[1] : a.seg_frame_stride[2]);
-      const int fr = stride ? frame : 0;
-      const __half* kb_ = seg == 0 ? a.k[0] : (seg == 1 ? a.k[1] : a.k[2]);
-      const __half* vb_ = seg == 0 ? a.v[0] : (seg == 1 ? a.v[1] : a.v[2]);
-      const __half* src = (which ? vb_ : kb_) + ((size_t)(fr * HEADS + h) * a.T + tok) * DH + chunk * 8;
-      __half* dst = which ? &sm.v[st][half][key][swz(key, chunk) * 8]
-                          : &sm.k[st][half][key][swz(key, chunk) * 8];
-      cp_async16_zfill(dst, src, valid);
+      if (kb >= nkb_h || blk >= n_kb) continue;
+      const int kk0 = blk * KB, kk1 = min(kk0 + KB, n_keys);
+      int kk = kk0;
+      while (kk < kk1) {
+        const int seg = kk >= a.band ? (kk >= 2 * a.band ? 2 : 1) : 0;
+        const int end = min(kk1, (seg + 1) * a.band);
+        piece_kk[half][n_pieces[half]] = kk;
+        piece_n[half][n_pieces[half]++] = end - kk;
+        bytes += 2u * (uint32_t)(end - kk) * (DH * 2);
+        kk = end;
+      }
     }
-    if (tid < KS * KB) {                               // key bias: 0 valid, -inf masked
+    tc::mbar_arrive_expect_tx(&sm.full[st], bytes);
+    for (int half = 0; half < KS; ++half) {
+      const int kk0 = (half * nkb_h + kb) * KB;
+      for (int p = 0; p < n_pieces[half]; ++p) {
+        const int kk = piece_kk[half][p], n = piece_n[half][p];
+        const int seg = kk >= a.band ? (kk >= 2 * a.band ? 2 : 1) : 0;
+        const int stride = seg == 0 ? a.seg_frame_stride[0]
+                         : (seg == 1 ? a.seg_frame_stride[1] : a.seg_frame_stride[2]);
+        const int fr = stride ? frame : 0;
+        const size_t off = ((size_t)(fr * HEADS + h) * a.T + band0 + kk - seg * a.band) * DH;
+        const __half* ks = (seg == 0 ? a.k[0] : (seg == 1 ? a.k[1] : a.k[2])) + off;
+        const __half* vs = (seg == 0 ? a.v[0] : (seg == 1 ? a.v[1] : a.v[2])) + off;
+        tc::bulk_load(&sm.k[st][half][kk - kk0][0], ks, (uint32_t)n * DH * 2, &sm.full[st]);
+        tc::bulk_load(&sm.v[st][half][kk - kk0][0], vs, (uint32_t)n * DH * 2, &sm.full[st]);
+      }
+    }
+  };
+  // Mask-aware key bias for step kb (all threads, one key each).
+  auto write_bias = [&](int kb, int st) {
+    if constexpr (MASKED) {
       const int half = tid / KB, key = tid - half * KB;
       const int blk = half * nkb_h + kb;
       const int kk = blk * KB + key;
       float bias = -INFINITY;
       if (kb < nkb_h && blk < n_kb && kk < n_keys) {
         bool ok = true;
-        if constexpr (MASKED) {
-          const int seg = kk / a.band;
-          if (seg == 0 && a.mask_mode != 0) {
-            const bool kv = a.key_valid[(size_t)frame * a.T + band0 + kk] != 0;
-            if (a.mask_mode == 1) ok = kv || !any_valid;
-            else if (a.mask_mode == 2) ok = kv;
-            else ok = any_valid;
-          }
+        if (kk < a.band && a.mask_mode != 0) {        // current-frame keys only
+          const bool kv = a.key_valid[(size_t)frame * a.T + band0 + kk] != 0;
+          if (a.mask_mode == 1) ok = kv || !any_valid;
+          else if (a.mask_mode == 2) ok = kv;
+          else ok = any_valid;
         }
         bias = ok ? 0.f : -INFINITY;
       }
@@ -121,30 +159,34 @@ __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
     qa[3] = qv1 ? __ldg(r1 + 4 + t) : 0u;
   }
 
-#pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nkb_h) load_stage(s, s);
-    cp_async_commit();
+    if (tid == 0) issue(s, s);
+    write_bias(s, s);
   }
 
   const float sl2 = 0.25f * 1.4426950408889634f;   // 1/sqrt(16) * log2(e)
+  const uint32_t ones = g == 0 ? 0x3C003C00u : 0u;  // B column 0 = 1: P * ones = row sum
   float m0 = -INFINITY, m1 = -INFINITY;
-  float l0a = 0.f, l0b = 0.f, l1a = 0.f, l1b = 0.f;
-  float oe[2][4] = {}, oo[2][4] = {};               // even / odd key sub-tile partials
+  float oe[3][4] = {}, oo[3][4] = {};               // [dims 0-7, dims 8-15, row sum]
 
   for (int kb = 0; kb < nkb_h; ++kb) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    const int st = kb % STAGES;
+    tc::mbar_wait(&sm.full[st], (uint32_t)(kb / STAGES) & 1u);
+    __syncthreads();                                 // bias visible; slot kb-1 released
     {
       const int nk = kb + STAGES - 1;
-      if (nk < nkb_h) load_stage(nk, nk % STAGES);
-      cp_async_commit();
+      if (nk < nkb_h) {
+        if (tid == 0) issue(nk, nk % STAGES);
+        write_bias(nk, nk % STAGES);
+      }
     }
-    const int st = kb % STAGES;
+    const int blk = kh * nkb_h + kb;
+    if (blk >= n_kb) continue;                       // warp-uniform: odd block count
+    const int n_valid = min(KB, n_keys - blk * KB);
 
-    float s[8][4];
+    float s[16][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
       uint32_t kf[4];
       const int key = 16 * j + (lane & 7) + ((lane >> 4) & 1) * 8;
       const int chunk = (lane >> 3) & 1;
@@ -154,70 +196,72 @@ __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
       mma16816(s[2 * j], qa, kf[0], kf[1]);
       mma16816(s[2 * j + 1], qa, kf[2], kf[3]);
     }
-    // key bias: always in mask-aware mode, else only on a partial / empty last block
-    if (MASKED || (kh * nkb_h + kb + 1) * KB > n_keys) {
+    if constexpr (MASKED) {
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
+      for (int nt = 0; nt < 16; ++nt) {
         const float2 b = *reinterpret_cast<const float2*>(&sm.bias[st][kh][nt * 8 + 2 * t]);
         s[nt][0] += b.x; s[nt][1] += b.y; s[nt][2] += b.x; s[nt][3] += b.y;
       }
-    }
-    float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-    float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-    float mx0b = fmaxf(fmaxf(s[2][0], s[2][1]), fmaxf(s[3][0], s[3][1]));
-    float mx1b = fmaxf(fmaxf(s[2][2], s[2][3]), fmaxf(s[3][2], s[3][3]));
+    } else if (n_valid < KB) {
 #pragma unroll
-    for (int nt = 4; nt < 8; nt += 2) {
-      mx0 = fmaxf(mx0, fmaxf(fmaxf(s[nt][0], s[nt][1]), fmaxf(s[nt + 1][0], s[nt + 1][1])));
-      mx1 = fmaxf(mx1, fmaxf(fmaxf(s[nt][2], s[nt][3]), fmaxf(s[nt + 1][2], s[nt + 1][3])));
+      for (int nt = 0; nt < 16; ++nt) {
+        const int col = nt * 8 + 2 * t;
+        if (col >= n_valid) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
+        if (col + 1 >= n_valid) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
+      }
     }
-    mx0 = quad_max(fmaxf(mx0, mx0b)) * sl2;
-    mx1 = quad_max(fmaxf(mx1, mx1b)) * sl2;
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float base0 = mn0 == -INFINITY ? 0.f : mn0;
-    const float base1 = mn1 == -INFINITY ? 0.f : mn1;
-    const float c0 = ex2(m0 - base0), c1 = ex2(m1 - base1);
-    m0 = mn0; m1 = mn1;
-    uint32_t pa[4][4];
-    float ps0a = 0.f, ps0b = 0.f, ps1a = 0.f, ps1b = 0.f;
+    float mx0 = max3(s[0][0], s[0][1], s[1][0]), mx1 = max3(s[0][2], s[0][3], s[1][2]);
+    float nx0 = max3(s[1][1], s[2][0], s[2][1]), nx1 = max3(s[1][3], s[2][2], s[2][3]);
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      const float p0 = ex2(fmaf(s[nt][0], sl2, -base0));
-      const float p1 = ex2(fmaf(s[nt][1], sl2, -base0));
-      const float p2 = ex2(fmaf(s[nt][2], sl2, -base1));
-      const float p3 = ex2(fmaf(s[nt][3], sl2, -base1));
-      if (nt & 1) { ps0b += p0 + p1; ps1b += p2 + p3; }
-      else { ps0a += p0 + p1; ps1a += p2 + p3; }
-      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_half2(p0, p1);
-      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_half2(p2, p3);
+    for (int nt = 3; nt < 15; nt += 2) {
+      mx0 = max3(mx0, s[nt][0], s[nt][1]);
+      mx1 = max3(mx1, s[nt][2], s[nt][3]);
+      nx0 = max3(nx0, s[nt + 1][0], s[nt + 1][1]);
+      nx1 = max3(nx1, s[nt + 1][2], s[nt + 1][3]);
     }
-    l0a = l0a * c0 + ps0a; l0b = l0b * c0 + ps0b;
-    l1a = l1a * c1 + ps1a; l1b = l1b * c1 + ps1b;
+    mx0 = max3(mx0, nx0, fmaxf(s[15][0], s[15][1]));
+    mx1 = max3(mx1, nx1, fmaxf(s[15][2], s[15][3]));
+    mx0 = quad_max(mx0) * sl2;
+    mx1 = quad_max(mx1) * sl2;
+    if (__any_sync(0xffffffffu, mx0 > m0 + RESCALE_SLACK || mx1 > m1 + RESCALE_SLACK)) {
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float c0 = ex2(m0 - (mn0 == -INFINITY ? 0.f : mn0));
+      const float c1 = ex2(m1 - (mn1 == -INFINITY ? 0.f : mn1));
+      m0 = mn0; m1 = mn1;
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      oe[nt][0] *= c0; oe[nt][1] *= c0; oe[nt][2] *= c1; oe[nt][3] *= c1;
-      oo[nt][0] *= c0; oo[nt][1] *= c0; oo[nt][2] *= c1; oo[nt][3] *= c1;
+      for (int nt = 0; nt < 3; ++nt) {
+        oe[nt][0] *= c0; oe[nt][1] *= c0; oe[nt][2] *= c1; oe[nt][3] *= c1;
+        oo[nt][0] *= c0; oo[nt][1] *= c0; oo[nt][2] *= c1; oo[nt][3] *= c1;
+      }
     }
+    const float base0 = m0 == -INFINITY ? 0.f : m0;
+    const float base1 = m1 == -INFINITY ? 0.f : m1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
+      uint32_t pa[4];
+      pa[0] = pack_half2(ex2(fmaf(s[2 * j][0], sl2, -base0)), ex2(fmaf(s[2 * j][1], sl2, -base0)));
+      pa[1] = pack_half2(ex2(fmaf(s[2 * j][2], sl2, -base1)), ex2(fmaf(s[2 * j][3], sl2, -base1)));
+      pa[2] = pack_half2(ex2(fmaf(s[2 * j + 1][0], sl2, -base0)), ex2(fmaf(s[2 * j + 1][1], sl2, -base0)));
+      pa[3] = pack_half2(ex2(fmaf(s[2 * j + 1][2], sl2, -base1)), ex2(fmaf(s[2 * j + 1][3], sl2, -base1)));
       uint32_t vf[4];
       const int mi = lane >> 3;
       const int key = 16 * j + (lane & 7) + (mi & 1) * 8;
       const int chunk = mi >> 1;
       ldmatrix_x4_trans(vf, &sm.v[st][kh][key][swz(key, chunk) * 8]);
       float (*o)[4] = (j & 1) ? oo : oe;
-      mma16816(o[0], pa[j], vf[0], vf[1]);
-      mma16816(o[1], pa[j], vf[2], vf[3]);
+      mma16816(o[0], pa, vf[0], vf[1]);
+      mma16816(o[1], pa, vf[2], vf[3]);
+      mma16816(o[2], pa, ones, ones);
     }
   }
-  cp_async_wait<0>();
 
-  float l0 = quad_sum(l0a + l0b), l1 = quad_sum(l1a + l1b);
-  float o[2][4];
+  float o[3][4];
 #pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
+  for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) o[nt][e] = oe[nt][e] + oo[nt][e];
+  float l0 = __shfl_sync(0xffffffffu, o[2][0], lane & ~3);   // row sums live in column 0
+  float l1 = __shfl_sync(0xffffffffu, o[2][2], lane & ~3);
 
   // merge the two key halves (log2-domain running max / sum / O)
   if (kh == 1) {
@@ -265,11 +309,18 @@ __global__ void __launch_bounds__(WARPS * 32) attn_kernel(AttnArgs a) {
 }  // namespace
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
+  static bool init = false;
+  const int smem = (int)sizeof(Smem) + 128;
+  if (!init) {
+    cudaFuncSetAttribute(attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
   dim3 grid((a.band + QT * 16 - 1) / (QT * 16), HEADS, a.frames * a.groups);
   if (a.mask_mode != 0 && a.key_valid)
-    attn_kernel<true><<<grid, WARPS * 32, 0, s>>>(a);
+    attn_kernel<true><<<grid, WARPS * 32, smem, s>>>(a);
   else
-    attn_kernel<false><<<grid, WARPS * 32, 0, s>>>(a);
+    attn_kernel<false><<<grid, WARPS * 32, smem, s>>>(a);
 }
 
 }  // namespace dr

@@ -273,7 +273,9 @@ int check_cfg(const dr_config* c) {
                     std::to_string(c->channels) + ", heads=" + std::to_string(c->heads) +
                     ", patch=" + std::to_string(c->patch) + ", kernel=" +
                     std::to_string(c->kernel) + ")");
-  if ((c->width / c->patch) % 1 != 0) return fail(DR_ERR_CONFIG, "bad token grid");
+  // attention K/V rows are swizzled in 8-token groups: every band must start on one
+  if (((c->height / c->patch) / c->temporal_groups * (c->width / c->patch)) % 8 != 0)
+    return fail(DR_ERR_CONFIG, "B200 kernels need a multiple of 8 tokens per temporal band");
   return DR_OK;
 }
 

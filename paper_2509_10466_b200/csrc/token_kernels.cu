@@ -173,15 +173,18 @@ DR_DEV void qkv_groups(const Slice& x, const BlockW& w, __half* q, __half* k, __
     gemm<2, 4>(acc, a, w.wqkv, 2 * p, lane);
     const int which = p >> 2, h = p & 3;
     __half* dst = which == 0 ? q : (which == 1 ? k : v);
+    // K and V rows are stored with the attention kernel's smem swizzle (16-byte chunk c
+    // of token t at c ^ ((t >> 2) & 1)) so its bulk copies land conflict-free.
+    const int sa = which ? ((ta >> 2) & 1) * 4 : 0, sb = which ? ((tb >> 2) & 1) * 4 : 0;
     if (na < n_tok) {
       uint32_t* r = reinterpret_cast<uint32_t*>(dst + ((size_t)(fa * HEADS + h) * T + ta) * DH);
-      r[t] = pack_half2(acc[0][0], acc[0][1]);
-      r[4 + t] = pack_half2(acc[1][0], acc[1][1]);
+      r[sa + t] = pack_half2(acc[0][0], acc[0][1]);
+      r[(4 ^ sa) + t] = pack_half2(acc[1][0], acc[1][1]);
     }
     if (nb < n_tok) {
       uint32_t* r = reinterpret_cast<uint32_t*>(dst + ((size_t)(fb * HEADS + h) * T + tb) * DH);
-      r[t] = pack_half2(acc[0][2], acc[0][3]);
-      r[4 + t] = pack_half2(acc[1][2], acc[1][3]);
+      r[sb + t] = pack_half2(acc[0][2], acc[0][3]);
+      r[(4 ^ sb) + t] = pack_half2(acc[1][2], acc[1][3]);
     }
   }
 }
