@@ -87,7 +87,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream);
 
 /* The mask stage alone, no engine needed: m0 [B][H][W] -> m1 (u8), alpha (f32) and token
  * validity [B][(H/patch)*(W/patch)] (patch 4 or 8).  Any output may be NULL.  Scratch is
- * stream-ordered (cudaMallocAsync).  radius <= 31, sigma <= 7.9. */
+ * stream-ordered (cudaMallocAsync).  radius <= 31, sigma <= 7.8. */
 int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, int32_t radius,
                   float sigma, const uint8_t* m0, uint8_t* m1, float* alpha,
                   uint8_t* token_valid, void* stream);

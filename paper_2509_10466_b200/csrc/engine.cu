@@ -264,8 +264,8 @@ int check_cfg(const dr_config* c) {
       return fail(DR_ERR_CONFIG, "block sequence must be a nonempty mix of 'S'/'T'");
   if (c->mask_dilate < 0 || c->mask_dilate > 31)
     return fail(DR_ERR_CONFIG, "mask_dilate must be in [0, 31]");
-  if (!(c->mask_feather_sigma >= 0.f) || (int)(4.0 * c->mask_feather_sigma + 0.5) > 32)
-    return fail(DR_ERR_CONFIG, "mask_feather_sigma must be in [0, 7.9]");
+  if (!(c->mask_feather_sigma >= 0.f) || (int)(4.0 * c->mask_feather_sigma + 0.5) > 31)
+    return fail(DR_ERR_CONFIG, "mask_feather_sigma must be in [0, 7.8] (feather radius <= 31)");
   // Shapes the sm_100a kernels are specialised for (the reference default network).
   if (c->channels != C || c->heads != HEADS || c->patch != 8 || c->kernel != 10)
     return fail(DR_ERR_CONFIG,
@@ -440,8 +440,8 @@ int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, 
   if (frames <= 0 || height <= 0 || width <= 0 || !m0)
     return fail(DR_ERR_INPUT, "need frames, height, width > 0 and a mask");
   if (radius < 0 || radius > 31) return fail(DR_ERR_CONFIG, "radius must be in [0, 31]");
-  if (!(sigma >= 0.f) || (int)(4.0 * sigma + 0.5) > 32)
-    return fail(DR_ERR_CONFIG, "sigma must be in [0, 7.9]");
+  if (!(sigma >= 0.f) || (int)(4.0 * sigma + 0.5) > 31)
+    return fail(DR_ERR_CONFIG, "sigma must be in [0, 7.8] (feather radius <= 31)");
   if (token_valid && (patch != 4 && patch != 8))
     return fail(DR_ERR_CONFIG, "token mask supports patch 4 or 8");
   if (token_valid && (height % patch || width % patch))

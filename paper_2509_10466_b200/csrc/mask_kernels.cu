@@ -1,18 +1,22 @@
 // Mask stage: privacy mask m0 -> dilated m1 -> feathered alpha, token validity, and the
-// packed fp16 network input.  HBM-bound integer/byte work; no tensor cores.
+// packed fp16 network input, fused in ONE kernel over 16 x 64-pixel tiles.  HBM-bound
+// integer/byte work; no tensor cores.  Per tile (256 threads):
 //
-//  pack_bits   m0 u8 rows -> 32-pixel bit words (warp ballot, coalesced byte reads)
-//  dilate      m1 = m0 (+) L1-ball(r) == r-fold 3x3-cross dilation (masks.py:17, :193;
-//              SURVEY A2): OR over rows dy of the row dilated horizontally by r-|dy|,
-//              on bit words (shift/or), bit-exact by construction; off-frame = 0
-//  token_pack  token valid = any pixel of the patch outside m1; network
-//              input cat[rgb zeroed in m1, m1] as fp16 in conv-weight (c,ky,kx) order
-//              (dstt.py:253, :314-316; u8 -> f32 is an IEEE divide by 255); redaction
-//              check of the u8 API (base.py:76-79) -> flags bit 1
-//  feather     alpha = max(m1, G_sigma(m1)) with scipy.ndimage.gaussian_filter semantics
-//              (mode 'nearest', truncate 4): vertical then horizontal pass, each in
-//              float64 in scipy's symmetric-filter summation order, rounded to float32
-//              between passes, so alpha is bit-identical to scipy
+//  1. m0 bytes of the tile plus a halo of r + R pixels -> 32-pixel bit words in smem
+//     (warp ballots over coalesced byte loads; off-frame = 0)
+//  2. m1 = m0 (+) L1-ball(r) == the r-fold 3x3-cross dilation (masks.py:17, :193; SURVEY
+//     A2): per row, OR over dy of the row dilated horizontally by r-|dy| (shift/or on bit
+//     words) -- bit-exact by construction; computed on the tile plus a halo of R
+//  3. feather: alpha = max(m1, G_sigma(m1)), scipy.ndimage.gaussian_filter
+//     semantics (mode 'nearest', truncate 4): vertical then horizontal pass, each in
+//     float64 in scipy's symmetric-filter order (x[0]*w[0], then (x[-j]+x[+j])*w[j] from
+//     the outermost pair inward) and rounded to float32 between passes, so alpha is
+//     bit-identical to scipy.  Exact fast paths: alpha = 1 on m1 (the vertical/horizontal
+//     sums of a binary image never exceed 1.0f); an all-zero / all-one 25-pixel window
+//     gives 0 / the precomputed all-ones sum
+//  4. token validity (any pixel of the patch outside m1) and the network input
+//     cat[rgb zeroed in m1, m1] in conv-weight (c, ky, kx) order (dstt.py:253, :314-316;
+//     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79)
 #include "common.cuh"
 #include "kernels.h"
 
@@ -20,189 +24,314 @@ namespace dr {
 
 namespace {
 
-__global__ void pack_bits_kernel(const uint8_t* __restrict__ m0, uint32_t* __restrict__ bits,
-                                 int frames, int H, int W, int Ww) {
-  const int lane = threadIdx.x & 31;
-  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long total = (long)frames * H * Ww;
-  if (warp >= total) return;
-  const int w = (int)(warp % Ww);
-  const long row = warp / Ww;                       // frame * H + y
-  const int x = w * 32 + lane;
-  const bool set = x < W && m0[row * W + x] != 0;
-  const uint32_t word = __ballot_sync(0xffffffffu, set);
-  if (lane == 0) bits[row * Ww + w] = word;
+constexpr int TH = 16, TW = 64;            // tile
+constexpr int MAXH = 62;                   // max halo r + R (r <= 31, R <= 31)
+constexpr int MAXR = 31;                   // 2R+1 <= 63: a column window fits a uint64
+constexpr int NW_MAX = 2 + 2 * (MAXH / 32);
+constexpr int NR_MAX = TH + 2 * MAXH;
+
+struct Smem {
+  uint8_t m0[NR_MAX][NW_MAX * 32];         // m0 bytes of tile + halo (cp.async)
+  float rgb[3][TH][TW];                    // f32 input tile, or u8 HWC bytes (aliased)
+  uint32_t b0[NR_MAX][NW_MAX];             // m0 bits, rows y0-H.., words from xs
+  uint32_t b1[TH + 2 * MAXR][NW_MAX];      // m1 bits, rows y0-R..
+  float vs[TH][TW + 2 * MAXR + 2];         // vertical feather pass
+  uint32_t vor[TH][NW_MAX], vand[TH][NW_MAX];
+  uint32_t nzm[TH][5];                     // nonzero columns of vs (+1 zero word)
+  double w[2 * MAXR + 1];
+  double all_ones;
+  int dirty;
+};
+
+DR_DEV void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  int n = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(s), "l"(gmem), "r"(n));
 }
 
-__global__ void dilate_kernel(const uint32_t* __restrict__ b0, uint32_t* __restrict__ b1,
-                              uint8_t* __restrict__ m1, float* __restrict__ alpha, int frames,
-                              int H, int W, int Ww, int r) {
-  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long total = (long)frames * H * Ww;
-  if (idx >= total) return;
-  const int w = (int)(idx % Ww);
-  const long row = idx / Ww;
-  const int y = (int)(row % H);
-  const long f = row / H;
-  const uint32_t* fb = b0 + f * (long)H * Ww;
-  uint32_t acc = 0;
-  for (int dy = -r; dy <= r; ++dy) {
-    const int yy = y + dy;
-    if (yy < 0 || yy >= H) continue;
-    const int k = r - (dy < 0 ? -dy : dy);
-    const uint32_t cur = fb[(long)yy * Ww + w];
-    const uint32_t lf = w > 0 ? fb[(long)yy * Ww + w - 1] : 0u;
-    const uint32_t rt = w + 1 < Ww ? fb[(long)yy * Ww + w + 1] : 0u;
-    uint32_t hd = cur;
-    for (int s = 1; s <= k; ++s)
-      hd |= (cur << s) | (lf >> (32 - s)) | (cur >> s) | (rt << (32 - s));
-    acc |= hd;
-  }
-  const int valid_bits = W - w * 32;
-  if (valid_bits < 32) acc &= (1u << valid_bits) - 1u;
-  b1[idx] = acc;
-  const long px = row * W + (long)w * 32;
-  if (m1) {
-    for (int i = 0; i < 32 && i < valid_bits; ++i) m1[px + i] = (acc >> i) & 1u;
-  }
-  if (alpha) {
-    for (int i = 0; i < 32 && i < valid_bits; ++i) alpha[px + i] = (float)((acc >> i) & 1u);
-  }
+DR_DEV uint32_t hdilate(uint32_t cur, uint32_t lf, uint32_t rt, int k) {
+  uint32_t hd = cur;
+  for (int s = 1; s <= k; ++s)
+    hd |= (cur << s) | (lf >> (32 - s)) | (cur >> s) | (rt << (32 - s));
+  return hd;
 }
 
-// One warp per token.  P = patch size (8: 4 ch x 8 rows lanes, 4: 4 ch x 4 rows).
 template <int P>
-__global__ void token_pack_kernel(MaskArgs a) {
-  const int lane = threadIdx.x & 31;
-  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int R = a.H / P, Cc = a.W / P, T = R * Cc;
-  if (warp >= (long)a.frames * T) return;
-  const int f = (int)(warp / T), tok = (int)(warp - (long)f * T);
-  const int i = tok / Cc, j = tok - i * Cc;
-  const int Ww = (a.W + 31) / 32;
-  constexpr int ROWS = P;                 // lanes: c = lane / ROWS, ky = lane % ROWS
-  const bool active = lane < 4 * ROWS;
-  const int c = lane / ROWS, ky = lane % ROWS;
-  const int y = i * P + ky, x0 = j * P;
-  uint32_t mbits = 0, m0bits = 0;
-  if (active) {
-    const long wrow = ((long)f * a.H + y) * Ww + (x0 >> 5);
-    mbits = (a.bits1[wrow] >> (x0 & 31)) & ((1u << P) - 1u);
-    m0bits = (a.bits0[wrow] >> (x0 & 31)) & ((1u << P) - 1u);
-  }
-  const bool any_unmasked = __any_sync(0xffffffffu, active && mbits != ((1u << P) - 1u));
-  if (lane == 0) a.token_valid[warp] = any_unmasked ? 1 : 0;
-  if (a.xin == nullptr) return;
-  float v[P];
-  bool dirty = false;
-  if (!active) {
-#pragma unroll
-    for (int kx = 0; kx < P; ++kx) v[kx] = 0.f;
-  } else if (c == 3) {
-#pragma unroll
-    for (int kx = 0; kx < P; ++kx) v[kx] = (float)((mbits >> kx) & 1u);
-  } else if (a.rgb_f32) {
-    const float* src = a.rgb_f32 + (((long)f * 3 + c) * a.H + y) * a.W + x0;
-#pragma unroll
-    for (int kx = 0; kx < P; kx += 4) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(src + kx));
-      v[kx] = q.x; v[kx + 1] = q.y; v[kx + 2] = q.z; v[kx + 3] = q.w;
-    }
-#pragma unroll
-    for (int kx = 0; kx < P; ++kx) if ((mbits >> kx) & 1u) v[kx] = 0.f;
-  } else {
-    const uint8_t* src = a.rgb_u8 + (((long)f * a.H + y) * a.W + x0) * 3 + c;
-#pragma unroll
-    for (int kx = 0; kx < P; ++kx) {
-      const uint8_t u = __ldg(src + 3 * kx);
-      dirty |= ((m0bits >> kx) & 1u) && u != 0;
-      v[kx] = ((mbits >> kx) & 1u) ? 0.f : __fdiv_rn((float)u, 255.0f);
-    }
-  }
-  const bool any_dirty = __any_sync(0xffffffffu, dirty);
-  if (a.flags && any_dirty && lane == 0) atomicOr(a.flags + f, 2);
-  if (!active) return;
-  __half* dst = a.xin + ((long)f * T + tok) * (4 * P * P) + c * P * P + ky * P;
-  uint32_t packed[P / 2];
-#pragma unroll
-  for (int kx = 0; kx < P; kx += 2) packed[kx / 2] = pack_half2(v[kx], v[kx + 1]);
-  if constexpr (P == 8) {
-    *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-  } else {
-    *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
-  }
-}
+__global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];   // keep the shared address space:
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);        // no integer round trip (LDS, not LD)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, f = blockIdx.z;
+  const int r = a.radius, R = a.feather_radius;
+  const int Hd = r + R;
+  const int wh = (Hd + 31) / 32;                  // halo words each side
+  const int NW = 2 + 2 * wh;
+  const int xs = x0 - 32 * wh;                    // pixel of bit 0 of word 0
+  const int NR0 = TH + 2 * Hd, NR1 = TH + 2 * R;
+  const size_t plane = (size_t)a.H * a.W;
 
-// Fused separable feather on a TILE_H x TILE_W tile; vertical pass into smem (float32),
-// horizontal pass out.  The summation order replicates scipy's NI_Correlate1D for
-// symmetric weights: out = x[0]*w[0]; for jj=-R..-1: out += (x[jj] + x[-jj]) * w[jj].
-constexpr int FT_H = 16, FT_W = 64, FT_MAXR = 32;
+  if (tid == 0) sm.dirty = 0;
+  for (int i = tid; i < 2 * R + 1; i += 256) sm.w[i] = a.feather_w[i];
 
-__global__ void __launch_bounds__(256) feather_kernel(MaskArgs a) {
-  __shared__ float vs[FT_H][FT_W + 2 * FT_MAXR];
-  __shared__ double wsm[2 * FT_MAXR + 1];
-  const int R = a.feather_radius;
-  const int Ww = (a.W + 31) / 32;
-  const int x0 = blockIdx.x * FT_W, y0 = blockIdx.y * FT_H, f = blockIdx.z;
-  for (int i = threadIdx.x; i < 2 * R + 1; i += blockDim.x) wsm[i] = a.feather_w[i];
-  __syncthreads();
-  const uint32_t* fb = a.bits1 + (long)f * a.H * Ww;
-  const double* wc = wsm + R;                       // centre tap
-  const int span = FT_W + 2 * R;
-  for (int e = threadIdx.x; e < FT_H * span; e += blockDim.x) {
-    const int ty = e / span, tx = e - ty * span;
-    const int y = y0 + ty;
-    int x = x0 + tx - R;
-    x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);     // 'nearest' in x (input to pass 2)
-    if (y >= a.H) { vs[ty][tx] = 0.f; continue; }
-    auto bit = [&](int yy) -> double {
-      yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
-      return (double)((fb[(long)yy * Ww + (x >> 5)] >> (x & 31)) & 1u);
-    };
-    double acc = __dmul_rn(bit(y), wc[0]);
-    for (int jj = -R; jj < 0; ++jj)
-      acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(bit(y + jj), bit(y - jj)), wc[jj]));
-    vs[ty][tx] = (float)acc;
+  // 0. one async round trip for every input of the tile: m0 bytes (+halo, 4-byte
+  //    pieces, zero-filled off-frame; W % 8 == 0 keeps pieces inside a row) and rgb
+  {
+    const uint8_t* m0f = a.m0 + (size_t)f * plane;
+    if ((a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0) {
+      const int pieces = NR0 * NW * 8;
+      for (int e = tid; e < pieces; e += 256) {
+        const int row = e / (NW * 8), pc = e - row * (NW * 8);
+        const int y = y0 - Hd + row, x = xs + 4 * pc;
+        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
+        cp_async4_zfill(&sm.m0[row][4 * pc], v ? m0f + (size_t)y * a.W + x : m0f, v);
+      }
+    } else {                                      // odd widths (standalone mask stage)
+      for (int e = tid; e < NR0 * NW * 32; e += 256) {
+        const int row = e / (NW * 32), px = e - row * (NW * 32);
+        const int y = y0 - Hd + row, x = xs + px;
+        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
+        sm.m0[row][px] = v ? m0f[(size_t)y * a.W + x] : 0;
+      }
+    }
+    if (a.xin != nullptr && a.rgb_f32) {
+      for (int e = tid; e < 3 * TH * (TW / 4); e += 256) {
+        const int c = e / (TH * TW / 4), rem = e - c * (TH * TW / 4);
+        const int ty = rem / (TW / 4), q = rem - ty * (TW / 4);
+        const int y = y0 + ty, x = x0 + 4 * q;
+        const bool v = y < a.H && x < a.W;
+        const float* src = a.rgb_f32 + ((size_t)f * 3 + c) * plane + (size_t)y * a.W + x;
+        cp_async16_zfill(&sm.rgb[c][ty][4 * q], v ? src : a.rgb_f32, v);
+      }
+    } else if (a.xin != nullptr && a.rgb_u8) {
+      uint8_t* dst = reinterpret_cast<uint8_t*>(&sm.rgb[0][0][0]);  // [TH][TW][3] bytes
+      for (int e = tid; e < TH * TW * 3 / 4; e += 256) {
+        const int ty = e / (TW * 3 / 4), q = e - ty * (TW * 3 / 4);
+        const int y = y0 + ty;
+        const bool v = y < a.H && x0 + (4 * q) / 3 < a.W;
+        const uint8_t* src = a.rgb_u8 + ((size_t)f * plane + (size_t)y * a.W + x0) * 3 + 4 * q;
+        cp_async4_zfill(dst + ty * TW * 3 + 4 * q, v ? src : a.rgb_u8, v);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+
+  // 1. m0 -> bits (one warp per 32-pixel word, bytes from smem)
+  for (int e = warp; e < NR0 * NW; e += 8) {
+    const int row = e / NW, w = e - row * NW;
+    const uint32_t word = __ballot_sync(0xffffffffu, sm.m0[row][32 * w + lane] != 0);
+    if (lane == 0) sm.b0[row][w] = word;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < FT_H * FT_W; e += blockDim.x) {
-    const int ty = e / FT_W, tx = e - ty * FT_W;
+
+  // 2. m1 on rows y0-R .. y0+TH+R
+  for (int e = tid; e < NR1 * NW; e += 256) {
+    const int row = e / NW, w = e - row * NW;
+    const int y = y0 - R + row;
+    uint32_t acc = 0;
+    if (y >= 0 && y < a.H) {
+      const int r0 = row + (Hd - R);              // this row in b0
+      for (int dy = -r; dy <= r; ++dy) {
+        const int yy = y + dy;
+        if (yy < 0 || yy >= a.H) continue;
+        const int k = r - (dy < 0 ? -dy : dy);
+        const uint32_t* br = sm.b0[r0 + dy];
+        acc |= hdilate(br[w], w > 0 ? br[w - 1] : 0u, w + 1 < NW ? br[w + 1] : 0u, k);
+      }
+      // clear bits of pixels outside the frame
+      const int xw = xs + 32 * w;
+      if (xw < 0) acc &= xw + 32 <= 0 ? 0u : (0xffffffffu << (-xw));
+      if (xw + 32 > a.W) acc &= xw >= a.W ? 0u : (0xffffffffu >> (xw + 32 - a.W));
+    }
+    sm.b1[row][w] = acc;
+  }
+  if (tid == 0 && R > 0) {                        // scipy-order sum of an all-ones window
+    const double* wc = sm.w + R;
+    double s = wc[0];
+    for (int jj = -R; jj < 0; ++jj) s = __dadd_rn(s, __dmul_rn(2.0, wc[jj]));
+    sm.all_ones = s;
+  }
+  __syncthreads();
+
+  // m1 bit at frame pixel (y, x) with 'nearest' clamping (pixel must map into b1)
+  auto m1bit = [&](int y, int x) -> uint32_t {
+    y = y < 0 ? 0 : (y >= a.H ? a.H - 1 : y);
+    x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
+    const int row = y - (y0 - R), px = x - xs;
+    return (sm.b1[row][px >> 5] >> (px & 31)) & 1u;
+  };
+
+  // outputs: m1 bytes (+ binary alpha)
+  for (int e = tid; e < TH * TW; e += 256) {
+    const int ty = e / TW, tx = e - ty * TW;
     const int y = y0 + ty, x = x0 + tx;
     if (y >= a.H || x >= a.W) continue;
-    // pass-2 input at column x+d: smem column tx + R + d, clamped to the frame
-    auto g = [&](int d) -> double {
-      int xx = x + d;
-      xx = xx < 0 ? 0 : (xx >= a.W ? a.W - 1 : xx);
-      return (double)vs[ty][xx - x0 + R];
-    };
-    double acc = __dmul_rn(g(0), wc[0]);
-    for (int jj = -R; jj < 0; ++jj)
-      acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(g(jj), g(-jj)), wc[jj]));
-    const float m = (float)((fb[(long)y * Ww + (x >> 5)] >> (x & 31)) & 1u);
-    a.alpha[((long)f * a.H + y) * a.W + x] = fmaxf(m, (float)acc);
+    const uint32_t b = m1bit(y, x);
+    if (a.m1) a.m1[(size_t)f * plane + (size_t)y * a.W + x] = (uint8_t)b;
+    if (R == 0 && a.alpha) a.alpha[(size_t)f * plane + (size_t)y * a.W + x] = (float)b;
   }
+
+  // 3. feather
+  if (R > 0 && a.alpha) {
+    const double* wc = sm.w + R;
+    const int span = TW + 2 * R;
+    // 3a. per (tile row, b1 word): OR / AND of the 2R+1 clamped rows -> which columns
+    //     have an all-zero / all-one vertical window (exact fast paths)
+    for (int e = tid; e < TH * NW; e += 256) {
+      const int ty = e / NW, w = e - ty * NW;
+      uint32_t o = 0u, n = 0xffffffffu;
+      for (int j = -R; j <= R; ++j) {
+        int yy = y0 + ty + j;
+        yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
+        const uint32_t b = sm.b1[yy - (y0 - R)][w];
+        o |= b;
+        n &= b;
+      }
+      sm.vor[ty][w] = o;
+      sm.vand[ty][w] = n;
+    }
+    __syncthreads();
+    // 3b. vertical pass (float64, scipy order) for columns x0-R .. x0+TW+R (clamped)
+    for (int e = tid; e < TH * span; e += 256) {
+      const int ty = e / span, tx = e - ty * span;
+      const int y = y0 + ty;
+      int x = x0 + tx - R;
+      x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
+      const int px = x - xs;
+      double acc;
+      if (y >= a.H || !((sm.vor[ty][px >> 5] >> (px & 31)) & 1u)) acc = 0.0;
+      else if ((sm.vand[ty][px >> 5] >> (px & 31)) & 1u) acc = sm.all_ones;
+      else {
+        uint64_t pat = 0;                          // bit j <-> row y - R + j
+        for (int j = 0; j <= 2 * R; ++j) {
+          int yy = y - R + j;
+          yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
+          pat |= (uint64_t)((sm.b1[yy - (y0 - R)][px >> 5] >> (px & 31)) & 1u) << j;
+        }
+        acc = __dmul_rn((double)((pat >> R) & 1u), wc[0]);
+        for (int jj = -R; jj < 0; ++jj) {
+          const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
+          acc = __dadd_rn(acc, __dmul_rn(pr, wc[jj]));
+        }
+      }
+      sm.vs[ty][tx] = (float)acc;
+    }
+    __syncthreads();
+    // 3c. nonzero mask of every vertical-pass row (one ballot per 32 columns)
+    for (int e = warp; e < TH * 4; e += 8) {
+      const int ty = e >> 2, c = e & 3, tx = 32 * c + lane;
+      const bool nz = tx < span && sm.vs[ty][tx] != 0.f;
+      const uint32_t m = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) sm.nzm[ty][c] = m;
+    }
+    __syncthreads();
+    // 3d. horizontal pass: alpha = 1 on m1, 0 where the whole window is zero, else sum.
+    //     Off-frame columns of sm.vs already hold their clamped ('nearest') values.
+    for (int e = tid; e < TH * TW; e += 256) {
+      const int ty = e / TW, tx = e - ty * TW;
+      const int y = y0 + ty, x = x0 + tx;
+      if (y >= a.H || x >= a.W) continue;
+      float out;
+      const int bx = x - xs;
+      if ((sm.b1[y - (y0 - R)][bx >> 5] >> (bx & 31)) & 1u) out = 1.0f;
+      else {
+        // window = vertical columns tx .. tx + 2R
+        const uint64_t lo = (uint64_t)sm.nzm[ty][tx >> 5] | ((uint64_t)sm.nzm[ty][(tx >> 5) + 1] << 32);
+        const uint64_t hi = (uint64_t)sm.nzm[ty][(tx >> 5) + 2];
+        const int sh = tx & 31;
+        const uint64_t win = (lo >> sh) | (sh ? (hi << (64 - sh)) : 0ull);
+        const uint64_t need = (1ull << (2 * R + 1)) - 1ull;
+        if (!(win & need)) out = 0.f;
+        else {
+          const float* v = &sm.vs[ty][tx + R];
+          double acc = __dmul_rn((double)v[0], wc[0]);
+          for (int jj = -R; jj < 0; ++jj)
+            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn((double)v[jj], (double)v[-jj]), wc[jj]));
+          out = fmaxf(0.f, (float)acc);
+        }
+      }
+      a.alpha[(size_t)f * plane + (size_t)y * a.W + x] = out;
+    }
+  }
+
+  // 4. tokens of this tile: one warp per token (lanes = 4 channels x P rows)
+  if (a.token_valid) {
+    const int Cc = a.W / P, T = (a.H / P) * Cc;
+    const int tr = TH / P, tcn = TW / P;
+    for (int tk = warp; tk < tr * tcn; tk += 8) {
+      const int ti = tk / tcn, tj = tk - ti * tcn;
+      const int i = y0 / P + ti, j = x0 / P + tj;
+      if (i * P >= a.H || j * P >= a.W) continue;
+      const int tok = i * Cc + j;
+      const bool active = lane < 4 * P;
+      const int c = lane / P, ky = lane % P;
+      const int y = i * P + ky, xl = j * P;
+      uint32_t mb = 0, m0b = 0;
+      if (active) {
+        for (int kx = 0; kx < P; ++kx) {
+          mb |= m1bit(y, xl + kx) << kx;
+          const int px = xl + kx - xs, row = y - (y0 - Hd);
+          m0b |= ((sm.b0[row][px >> 5] >> (px & 31)) & 1u) << kx;
+        }
+      }
+      const bool any_unmasked = __any_sync(0xffffffffu, active && mb != ((1u << P) - 1u));
+      if (lane == 0) a.token_valid[(size_t)f * T + tok] = any_unmasked ? 1 : 0;
+      if (a.xin == nullptr) continue;
+      float v[P];
+      bool dirty = false;
+      if (!active) {
+#pragma unroll
+        for (int kx = 0; kx < P; ++kx) v[kx] = 0.f;
+      } else if (c == 3) {
+#pragma unroll
+        for (int kx = 0; kx < P; ++kx) v[kx] = (float)((mb >> kx) & 1u);
+      } else if (a.rgb_f32) {
+        const float* src = &sm.rgb[c][y - y0][xl - x0];
+#pragma unroll
+        for (int kx = 0; kx < P; ++kx) v[kx] = ((mb >> kx) & 1u) ? 0.f : src[kx];
+      } else {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(&sm.rgb[0][0][0]) +
+                             ((y - y0) * TW + (xl - x0)) * 3 + c;
+#pragma unroll
+        for (int kx = 0; kx < P; ++kx) {
+          const uint8_t u = src[3 * kx];
+          dirty |= ((m0b >> kx) & 1u) && u != 0;
+          v[kx] = ((mb >> kx) & 1u) ? 0.f : __fdiv_rn((float)u, 255.0f);
+        }
+      }
+      if (__any_sync(0xffffffffu, dirty) && lane == 0) sm.dirty = 1;
+      if (!active) continue;
+      __half* dst = a.xin + ((size_t)f * T + tok) * (4 * P * P) + c * P * P + ky * P;
+      uint32_t packed[P / 2];
+#pragma unroll
+      for (int kx = 0; kx < P; kx += 2) packed[kx / 2] = pack_half2(v[kx], v[kx + 1]);
+      if constexpr (P == 8) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && sm.dirty && a.flags) atomicOr(a.flags + f, 2);
 }
 
 }  // namespace
 
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
-  const int Ww = (a.W + 31) / 32;
-  const long words = (long)a.frames * a.H * Ww;
-  pack_bits_kernel<<<(unsigned)((words + 7) / 8), 256, 0, s>>>(a.m0, a.bits0, a.frames, a.H, a.W, Ww);
-  dilate_kernel<<<(unsigned)((words + 127) / 128), 128, 0, s>>>(
-      a.bits0, a.bits1, a.m1, a.feather_radius == 0 ? a.alpha : nullptr, a.frames, a.H, a.W,
-      Ww, a.radius);
-  if (a.token_valid) {
-    const long toks = (long)a.frames * (a.H / a.patch) * (a.W / a.patch);
-    if (a.patch == 8)
-      token_pack_kernel<8><<<(unsigned)((toks + 7) / 8), 256, 0, s>>>(a);
-    else if (a.patch == 4)
-      token_pack_kernel<4><<<(unsigned)((toks + 7) / 8), 256, 0, s>>>(a);
+  static bool init = false;
+  const int smem = (int)sizeof(Smem) + 16;
+  if (!init) {
+    cudaFuncSetAttribute(mask_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mask_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
   }
-  if (a.feather_radius > 0 && a.alpha) {
-    dim3 grid((a.W + FT_W - 1) / FT_W, (a.H + FT_H - 1) / FT_H, a.frames);
-    feather_kernel<<<grid, 256, 0, s>>>(a);
-  }
+  dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, a.frames);
+  if (a.patch == 4)
+    mask_fused_kernel<4><<<grid, 256, smem, s>>>(a);
+  else
+    mask_fused_kernel<8><<<grid, 256, smem, s>>>(a);
 }
 
 }  // namespace dr
