@@ -7,14 +7,17 @@
 //
 // Implicit GEMM, M = 128 pixels of one output row, N = output channels (64, or 16 with
 // 3 real for decode.2), K = 9 taps x 64 input channels.  A persistent CTA owns the whole
-// fp16 weight image in smem (one bulk copy) and walks 2-row x 128-pixel tiles:
-//   warp 0      TMA: the 4 x 130-pixel x 64-channel input halo of the next tile, as 8
-//               planes of 8 channels (K-major, no swizzle: core matrix = 8 px x 16 B);
-//               off-image rows/columns are zero-filled by TMA = the conv's zero padding
-//   warp 1      one thread issues 2 x 9 x 4 tcgen05.mma (128 x N x 16) per tile into a
+// fp16 weight image in smem (one bulk copy) and walks TR-row x 128-pixel tiles:
+//   warp 0      TMA: the (TR+2) x 130-pixel x 64-channel input halo of the next tile, one
+//               box, 128B-swizzled K-major rows (128 B = one pixel); off-image rows and
+//               columns are zero-filled by TMA = the conv's zero padding
+//   warp 1      one thread issues TR x 9 x 4 tcgen05.mma (128 x N x 16) per tile into a
 //               double-buffered TMEM accumulator; tap (dy,dx) is just a descriptor offset
-//   warps 2-5   epilogue: tcgen05.ld (lane = pixel), bias + activation, stores
-// Double-buffered halo (2 x 65 KB) and TMEM let TMA, MMA and the epilogue overlap.
+//   warps 2-9   epilogue (two warps per TMEM lane quarter, alternate rows): tcgen05.ld
+//               (lane = pixel), bias (registers) + activation, stores; decode.2
+//               prefetches alpha / rgb of the next tile before waiting on the accumulator
+// Double-buffered halo and TMEM let TMA, MMA and the epilogue overlap.  decode.0 uses
+// 2-row tiles (74 KB of weights + 2 x 65 KB halo), decode.2 4-row tiles (1.5x halo reuse).
 #include <cuda.h>
 #include <math.h>
 
@@ -26,35 +29,37 @@ namespace dr {
 namespace {
 
 constexpr int TX = 128;                     // pixels per MMA (M)
-constexpr int TR = 2;                       // output rows per tile
-constexpr int HX = TX + 2, HR = TR + 2;     // halo
-constexpr int HALO_BYTES = HR * HX * 128;   // [row][px][64 ch] fp16, 128B-swizzled rows
-constexpr int THREADS = 192;
-static_assert(HALO_BYTES % 1024 == 0, "halo buffers must stay 1024-byte aligned");
+constexpr int HX = TX + 2;                  // halo width
+constexpr int THREADS = 320;                // TMA warp, MMA warp, 8 epilogue warps
 // The tap (dy,dx) A operand starts (r+dy)*130+dx pixel rows into a 1024-byte aligned
 // swizzled halo.  Measured on B200: the MMA unit applies the 128B XOR swizzle on absolute
 // smem address bits (like TMA), so such row-shifted descriptors need base_offset 0
 // (tests/test_gpu_ops.py pins this; base_offset = row & 7 produces garbage).
 
-template <int N>
-struct __align__(128) ConvSmem {
-  uint8_t halo[2][HALO_BYTES];
+template <int N, int TR>
+struct __align__(1024) ConvSmem {
+  static constexpr int HALO_BYTES = (TR + 2) * HX * 128;    // [row][px][64 ch] fp16
+  static constexpr int HALO_STRIDE = (HALO_BYTES + 1023) & ~1023;   // keep 1024 alignment
+  uint8_t halo[2][HALO_STRIDE];
   uint8_t w[9 * 8 * N * 16];                 // [tap][k-chunk][co][8 ci] fp16
   uint64_t halo_full[2], halo_empty[2], tmem_full[2], tmem_empty[2], w_full;
   uint32_t tmem_base;
 };
 
-template <int N>
-constexpr uint32_t tmem_cols() { return 2 * TR * N <= 32 ? 32 : (2 * TR * N <= 64 ? 64 : (2 * TR * N <= 128 ? 128 : 256)); }
+template <int N, int TR>
+constexpr uint32_t tmem_cols() {
+  return 2 * TR * N <= 32 ? 32 : (2 * TR * N <= 64 ? 64 : (2 * TR * N <= 128 ? 128 : (2 * TR * N <= 256 ? 256 : 512)));
+}
 
-template <int N, int EPI>
+template <int N, int EPI, int TR>
 __global__ void __launch_bounds__(THREADS, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  ConvSmem<N>& sm = *reinterpret_cast<ConvSmem<N>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t COLS = tmem_cols<N>();
+  using Smem = ConvSmem<N, TR>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  constexpr uint32_t COLS = tmem_cols<N, TR>();
   constexpr uint32_t WBYTES = 9 * 8 * N * 16;
+  constexpr int HALO_BYTES = Smem::HALO_BYTES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_x = (a.W + TX - 1) / TX, tiles_y = (a.H + TR - 1) / TR;
   const int n_tiles = a.frames * tiles_y * tiles_x;
@@ -64,7 +69,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       tc::mbar_init(&sm.halo_full[b], 1);
       tc::mbar_init(&sm.halo_empty[b], 1);
       tc::mbar_init(&sm.tmem_full[b], 1);
-      tc::mbar_init(&sm.tmem_empty[b], 4);
+      tc::mbar_init(&sm.tmem_empty[b], 8);
     }
     tc::mbar_init(&sm.w_full, 1);
     tc::fence_barrier_init();
@@ -95,10 +100,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                     // ---------------- MMA issuer
-      constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    {                                                    // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_f16(128, N);   // (whole warp, elected lane issues)
       tc::mbar_wait(&sm.w_full, 0);
-      const uint32_t w_s = tc::smem_u32(sm.w);
+      const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w), N * 16, 128);
       int i = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int buf = i & 1;
@@ -106,8 +111,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
         tc::mbar_wait(&sm.halo_full[buf], ph);
         tc::mbar_wait(&sm.tmem_empty[buf], ph ^ 1);
         tc::fence_after();
-        const uint32_t h_s = tc::smem_u32(sm.halo[buf]);
-#pragma unroll 1
+        // Base descriptors once per tile; each MMA adds a compile-time offset to the
+        // 16-byte-unit address field (never carries: smem < 256 KB).
+        const uint64_t a0 = tc::sdesc_sw128(tc::smem_u32(sm.halo[buf]), 0);
+#pragma unroll
         for (int r = 0; r < TR; ++r) {
           const uint32_t d = tbase + (uint32_t)(buf * TR * N + r * N);
 #pragma unroll
@@ -116,20 +123,22 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const uint32_t row = (uint32_t)((r + dy) * HX + dx);      // first pixel row
-              const uint32_t aa = h_s + row * 128 + ks * 32;
-              const uint64_t ad = tc::sdesc_sw128(aa, 0);
-              const uint64_t bd = tc::sdesc(w_s + (tap * 8 + 2 * ks) * N * 16, N * 16, 128);
-              tc::mma_f16(d, ad, bd, idesc, (tap | ks) != 0);
+              tc::mma_f16_warp(d, a0 + (row * 8 + ks * 2), b0 + (uint64_t)((tap * 8 + 2 * ks) * N),
+                               idesc, (tap | ks) != 0);
             }
           }
         }
-        tc::mma_commit(&sm.halo_empty[buf]);
-        tc::mma_commit(&sm.tmem_full[buf]);
+        tc::mma_commit_warp(&sm.halo_empty[buf]);
+        tc::mma_commit_warp(&sm.tmem_full[buf]);
       }
     }
   } else {                                               // ---------------- epilogue
-    const int q = warp & 3;                              // TMEM lanes 32q..32q+31
+    const int q = warp & 3;              // TMEM lanes 32q..32q+31 (fixed by warp id % 4)
+    const int rh = (warp - 2) >> 2;      // warps 2-5 rows 0,2,..; warps 6-9 rows 1,3,..
     const size_t plane = (size_t)a.H * a.W;
+    float bias[EPI == 0 ? N : 3];
+#pragma unroll
+    for (int c = 0; c < (EPI == 0 ? N : 3); ++c) bias[c] = __ldg(a.bias + c);
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int buf = i & 1;
@@ -137,10 +146,29 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       const int tx = t % tiles_x, rest = t / tiles_x;
       const int ty = rest % tiles_y, f = rest / tiles_y;
       const int x = tx * TX + 32 * q + lane;
+      // decode.2: fetch alpha / frame pixels while the MMAs of this tile run
+      float al[TR / 2], fr[TR / 2][3];
+      uint8_t fr8[TR / 2][3];
+      if constexpr (EPI == 1) {
+#pragma unroll
+        for (int k = 0; k < TR / 2; ++k) {
+          const int y = ty * TR + rh + 2 * k;
+          const bool ok = y < a.H && x < a.W;
+          const size_t pix = (size_t)(ok ? y : 0) * a.W + (ok ? x : 0);
+          al[k] = ok && a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            fr[k][ch] = ok && a.out_f32 ? __ldg(a.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix) : 0.f;
+            fr8[k][ch] = ok && a.out_u8 ? __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch) : 0;
+          }
+        }
+      }
       tc::mbar_wait(&sm.tmem_full[buf], ph);
       tc::fence_after();
-#pragma unroll 1
-      for (int r = 0; r < TR; ++r) {
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < TR / 2; ++k) {
+        const int r = rh + 2 * k;
         const int y = ty * TR + r;
         uint32_t v[N];
         const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * TR * N + r * N);
@@ -157,8 +185,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c = c8 * 8 + 2 * e;
-              float u0 = __uint_as_float(v[c]) + __ldg(a.bias + c);
-              float u1 = __uint_as_float(v[c + 1]) + __ldg(a.bias + c + 1);
+              float u0 = __uint_as_float(v[c]) + bias[c];
+              float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
               u0 = u0 >= 0.f ? u0 : 0.2f * u0;
               u1 = u1 >= 0.f ? u1 : 0.2f * u1;
               pk[e] = pack_half2(u0, u1);
@@ -166,62 +194,64 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
             dst[c8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         } else {
-          const float al = a.alpha ? a.alpha[(size_t)f * plane + pix] : 1.f;
-          bool bad = false;
+          const float alr = al[k];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float raw = __uint_as_float(v[ch]) + __ldg(a.bias + ch);
+            const float raw = __uint_as_float(v[ch]) + bias[ch];
             const float out01 = (tanhf(raw) + 1.0f) * 0.5f;
             bad |= !isfinite(out01);
             const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
             if (a.fill) a.fill[pl] = out01;
-            if (a.out_f32) {
-              const float fr = a.rgb_f32[pl];
-              a.out_f32[pl] = __fadd_rn(__fmul_rn(al, out01), __fmul_rn(__fsub_rn(1.0f, al), fr));
-            }
+            if (a.out_f32)
+              a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), fr[k][ch]));
             if (a.out_u8) {
               const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
-              const size_t pu = ((size_t)f * plane + pix) * 3 + ch;
-              const uint8_t src8 = a.rgb_u8[pu];
+              const uint8_t src8 = fr8[k][ch];
               uint8_t o;
-              if (al == 0.f) o = src8;
-              else if (al == 1.f) o = fill8;
-              else o = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(al, (float)fill8),
-                                                             __fmul_rn(__fsub_rn(1.0f, al), (float)src8))), 0.f), 255.f);
-              a.out_u8[pu] = o;
+              if (alr == 0.f) o = src8;
+              else if (alr == 1.f) o = fill8;
+              else o = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
+                                                             __fmul_rn(__fsub_rn(1.0f, alr), (float)src8))), 0.f), 255.f);
+              a.out_u8[((size_t)f * plane + pix) * 3 + ch] = o;
             }
           }
-          if (bad) atomicOr(a.flags + f, 1);
         }
+      }
+      if constexpr (EPI == 1) {
+        if (bad) atomicOr(a.flags + f, 1);
       }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);
     }
   }
+  tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<COLS>(tbase);
 }
 
-template <int N, int EPI>
+template <int N, int EPI, int TR>
 void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   static int sms = 0;
-  const int smem = (int)sizeof(ConvSmem<N>) + 1024;
+  const int smem = (int)sizeof(ConvSmem<N, TR>);
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<N, EPI, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
-  conv3x3_tc_kernel<N, EPI><<<grid, THREADS, smem, s>>>(tin, a);
+  conv3x3_tc_kernel<N, EPI, TR><<<grid, THREADS, smem, s>>>(tin, a);
 }
 
 }  // namespace
 
 size_t conv_tc_weight_bytes(int n) { return (size_t)9 * 8 * n * 16; }
+
+int conv_tc_rows(int n) { return n == 64 ? 2 : 4; }
+
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
-  if (n == 64) launch<64, 0>(tin, a, s);
-  else launch<16, 1>(tin, a, s);
+  if (n == 64) launch<64, 0, 2>(tin, a, s);
+  else launch<16, 1, 4>(tin, a, s);
 }
 
 }  // namespace dr

@@ -90,12 +90,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return encode;
 }
 
-int make_nhwc_map(CUtensorMap* map, void* base, int frames, int H, int W) {
+int make_nhwc_map(CUtensorMap* map, void* base, int frames, int H, int W, int box_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)frames};
   const cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
-  const cuuint32_t box[4] = {64, 130, 4, 1};
+  const cuuint32_t box[4] = {64, 130, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -216,16 +216,13 @@ struct dr_engine {
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
     cap = frames;
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
-    int rc = make_raster_map(&map_raster, raster, frames);
+    int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
     if (rc) return rc;
-    rc = make_raster_map(&map_d0, d0, frames);
+    rc = make_nhwc_map(&map_d0, d0, frames, H, W, conv_tc_rows(16) + 2);
     if (rc) return rc;
     return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
   }
 
-  int make_raster_map(CUtensorMap* map, void* base, int frames) {
-    return make_nhwc_map(map, base, frames, H, W);
-  }
 
   // TMA view of the padded fp16 token grid [frames][np][64]: box 64 ch x 128 positions.
   int make_token_map(CUtensorMap* map, void* base, int frames, int np) {
@@ -605,7 +602,8 @@ int dr_op_conv3x3(int32_t frames, int32_t height, int32_t width, const void* in_
   std::vector<uint16_t> img;
   pack_conv_tc(weight_host, 64, 64, 64, img);
   CUtensorMap map;
-  int rc = make_nhwc_map(&map, const_cast<void*>(in_nhwc_f16), frames, height, width);
+  int rc = make_nhwc_map(&map, const_cast<void*>(in_nhwc_f16), frames, height, width,
+                         conv_tc_rows(64) + 2);
   if (rc) return rc;
   uint8_t* dev = nullptr;
   CUDA_TRY(cudaMallocAsync((void**)&dev, img.size() * 2 + 256, s));

@@ -108,6 +108,7 @@ struct ConvTcArgs {
 #include <cuda.h>
 namespace dr {
 size_t conv_tc_weight_bytes(int n);
+int conv_tc_rows(int n);   // output rows per tile; the input TMA box is rows + 2 tall
 
 // tcgen05 Vec2Patch (v2p_tc.cu).  Tokens: fp16 [frames][(R+2)(Cc+2)][64], zero-padded grid
 // (token (i,j) at padded (i+1, j+1)), TMA box 64 ch x 128 positions, 128B swizzle.

@@ -76,29 +76,29 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                   // ------------------- MMA issue
-      constexpr uint32_t idesc = tc::idesc_f16(128, 64);
+    {                                                  // ------------------- MMA issue
+      constexpr uint32_t idesc = tc::idesc_f16(128, 64);   // (whole warp, elected lane)
       tc::mbar_wait(&sm.win_full, 0);
       tc::mbar_wait(&sm.w_full, 0);
       tc::fence_after();
-      const uint32_t a_s = tc::smem_u32(sm.win[0]), w_s = tc::smem_u32(sm.w[0]);
+      // base descriptors; per-MMA offsets in 16-byte units (row = 8, k-step = 2)
+      const uint64_t a0 = tc::sdesc_sw128(tc::smem_u32(sm.win[0]), 0);
+      const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 1024, 128);
+      auto term = [&](uint32_t d, int tap, int off, bool first) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_f16_warp(d, a0 + (uint64_t)(off * 8 + ks * 2),
+                           b0 + (uint64_t)(tap * (TAP_BYTES / 16) + ks * 128), idesc,
+                           !(first && ks == 0));
+      };
 #pragma unroll 1
       for (int px = 0; px < 8; ++px) {
-        // (tap slot in smem, window row offset of the token set)
-        int taps[4], offs[4], n = 0;
-        taps[n] = px;      offs[n++] = PC + 1;          // (i, j)
-        if (px < 2) { taps[n] = px + 8; offs[n++] = PC; }          // (i, j-1)
-        if (py < 2) { taps[n] = 10 + px; offs[n++] = 1; }          // (i-1, j)
-        if (py < 2 && px < 2) { taps[n] = 18 + px; offs[n++] = 0; } // (i-1, j-1)
         const uint32_t d = tbase + (uint32_t)(px * 64);
-        for (int u = 0; u < n; ++u)
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad = tc::sdesc_sw128(a_s + (uint32_t)offs[u] * 128 + ks * 32, 0);
-            const uint64_t bd = tc::sdesc(w_s + (uint32_t)taps[u] * TAP_BYTES + 2 * ks * 1024, 1024, 128);
-            tc::mma_f16(d, ad, bd, idesc, (u | ks) != 0);
-          }
-        tc::mma_commit(&sm.tmem_full[px]);
+        term(d, px, PC + 1, true);                                  // (i, j)
+        if (px < 2) term(d, px + 8, PC, false);                     // (i, j-1)
+        if (py < 2) term(d, 10 + px, 1, false);                     // (i-1, j)
+        if (py < 2 && px < 2) term(d, 18 + px, 0, false);           // (i-1, j-1)
+        tc::mma_commit_warp(&sm.tmem_full[px]);
       }
     }
   } else {                                             // ------------------- epilogue
