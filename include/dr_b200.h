@@ -67,6 +67,11 @@ typedef struct dr_frame_io {
   float* alpha;                  /* [B][H][W] feathered alpha, or NULL               */
   uint8_t* token_valid;          /* [B][T] token validity, or NULL                   */
   int32_t* flags;                /* [B] DR_FLAG_* bits, or NULL (engine-internal)    */
+  /* Slot K/V cache (bit0: slot0, bit1: slot1).  Set a bit only when that slot is the
+   * unmodified new_slot output of an earlier dr_forward of this engine: its per-temporal-
+   * block K/V, produced by that call, are then reused instead of re-projected.  0 always
+   * computes them (correct for any slot contents). */
+  int32_t slot_kv_reuse;
 } dr_frame_io;
 
 /* Build an engine on `device` from the 72 DRWT tensors in state_dict order (host fp32

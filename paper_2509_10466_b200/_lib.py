@@ -37,7 +37,7 @@ class DrFrameIO(ctypes.Structure):
                 ("out_f32", ctypes.c_void_p), ("out_u8", ctypes.c_void_p),
                 ("fill", ctypes.c_void_p), ("dilated", ctypes.c_void_p),
                 ("alpha", ctypes.c_void_p), ("token_valid", ctypes.c_void_p),
-                ("flags", ctypes.c_void_p)]
+                ("flags", ctypes.c_void_p), ("slot_kv_reuse", ctypes.c_int32)]
 
 
 # symbol -> (restype, argtypes); the export test checks this against include/dr_b200.h

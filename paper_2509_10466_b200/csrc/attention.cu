@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(THREADS, 2) attn_kernel(AttnArgs a) {
   const int n_kb = (n_keys + KB - 1) / KB;
   const int nkb_h = (n_kb + 1) / 2;            // blocks per key half
 
+  pdl_trigger();
   // zero the K/V ring once: tails of partial blocks must hold finite values
   {
     uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0][0][0]);
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, 2) attn_kernel(AttnArgs a) {
     }
     tc::fence_barrier_init();
   }
+  pdl_wait();                                     // q / k / v / key_valid of the predecessor
   int any_valid = 1;
   if constexpr (MASKED) {
     if (a.mask_mode == 1 || a.mask_mode == 3) {
@@ -348,9 +350,9 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
   }
   dim3 grid((a.band + QT * 16 - 1) / (QT * 16), HEADS, a.frames * a.groups);
   if (a.mask_mode != 0 && a.key_valid)
-    attn_kernel<true><<<grid, THREADS, smem, s>>>(a);
+    launch_pdl(attn_kernel<true>, grid, dim3(THREADS), smem, s, a);
   else
-    attn_kernel<false><<<grid, THREADS, smem, s>>>(a);
+    launch_pdl(attn_kernel<false>, grid, dim3(THREADS), smem, s, a);
 }
 
 }  // namespace dr

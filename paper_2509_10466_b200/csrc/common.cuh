@@ -82,4 +82,35 @@ DR_DEV uint2 ld_frag(const uint2* __restrict__ base, int frag, int lane) {
   return __ldg(base + frag * 32 + lane);
 }
 
+// ---------------------------------------------------------------- programmatic launch
+// Every kernel of the frame is launched with programmatic stream serialization: it lets
+// its dependent launch as soon as all of its CTAs are running (pdl_trigger at entry), does
+// its input-independent prologue (barriers, TMEM, weights), then pdl_wait()s for the
+// predecessor grid to complete and flush before touching any activation buffer.
+#ifndef DR_PDL_EARLY_TRIGGER
+#define DR_PDL_EARLY_TRIGGER 0
+#endif
+DR_DEV void pdl_trigger() {
+#if DR_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+DR_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 }  // namespace dr

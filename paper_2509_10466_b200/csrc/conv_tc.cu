@@ -64,6 +64,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
   const int tiles_x = (a.W + TX - 1) / TX, tiles_y = (a.H + TR - 1) / TR;
   const int n_tiles = a.frames * tiles_y * tiles_x;
 
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&sm.halo_full[b], 1);
@@ -84,10 +85,11 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     if (lane == 0) {                                     // ---------------- TMA producer
       tc::tma_prefetch(&tin);
       tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES);
-      for (uint32_t off = 0; off < WBYTES; off += 16384) {
+      for (uint32_t off = 0; off < WBYTES; off += 16384) {   // constant: before the wait
         const uint32_t n = WBYTES - off < 16384 ? WBYTES - off : 16384;
         tc::bulk_load(sm.w + off, reinterpret_cast<const uint8_t*>(a.w) + off, n, &sm.w_full);
       }
+      pdl_wait();                                        // input raster of the predecessor
       int i = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int buf = i & 1;
@@ -139,6 +141,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     float bias[EPI == 0 ? N : 3];
 #pragma unroll
     for (int c = 0; c < (EPI == 0 ? N : 3); ++c) bias[c] = __ldg(a.bias + c);
+    pdl_wait();                          // alpha / frame inputs, output buffers
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int buf = i & 1;
@@ -240,7 +243,7 @@ void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   }
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
-  conv3x3_tc_kernel<N, EPI, TR><<<grid, THREADS, smem, s>>>(tin, a);
+  launch_pdl(conv3x3_tc_kernel<N, EPI, TR>, dim3(grid), dim3(THREADS), smem, s, tin, a);
 }
 
 }  // namespace

@@ -147,6 +147,8 @@ struct dr_engine {
   uint8_t *h_rgb = nullptr, *h_m0 = nullptr, *h_out = nullptr;   // device
   float* ring[3] = {nullptr, nullptr, nullptr};
   int mem0 = 0, mem1 = 0;                                        // ring index of slots
+  bool ring_own[3] = {false, false, false};                      // written by dr_forward
+  int last_launches = 0;                                         // kernels of the last call
   uint8_t* pin = nullptr;                                        // pinned staging
   int* pin_flags = nullptr;
   // optional per-stage CUDA events (dr_profile): ev[0] before the first stage
@@ -175,16 +177,50 @@ struct dr_engine {
   }
 
   size_t frame_px() const { return (size_t)H * W; }
-  size_t slotkv_stride() const { return (size_t)cap * T * C; }   // one K or V image
 
-  __half* skv(int ti, int slot, int which) const {              // which: 0 K, 1 V
-    return slotkv + ((size_t)(ti * 2 + slot) * 2 + which) * slotkv_stride();
+  // Slot K/V cache: KV_ENTRIES entries (3 per memory stream: slot0, slot1, new slot),
+  // each n_temporal x {K, V} images of [cap][HEADS][T][DH] fp16, keyed by the slot
+  // tensor's device pointer, LRU replacement.
+  static constexpr int KV_ENTRIES = 6;
+  struct KvEntry {
+    const float* ptr;
+    int frames;
+    bool batched;
+    uint64_t used;
+  };
+  KvEntry kvc[KV_ENTRIES] = {};
+  uint64_t kv_tick = 0;
+
+  __half* kv_ptr(int entry, int ti, int which) const {         // which: 0 K, 1 V
+    return slotkv + ((size_t)(entry * MAX_TEMPORAL + ti) * 2 + which) * ((size_t)cap * T * C);
+  }
+  void kv_set(int i, const float* p, int frames, bool batched) {
+    kvc[i] = {p, frames, batched, ++kv_tick};
+  }
+  int kv_find(const float* p, int frames, int batched) {
+    for (int i = 0; i < KV_ENTRIES; ++i)  // one frame: [1][T][C] and [T][C] are the same
+      if (kvc[i].ptr == p && kvc[i].frames == frames &&
+          (frames == 1 || kvc[i].batched == (batched != 0))) {
+        kvc[i].used = ++kv_tick;
+        return i;
+      }
+    return -1;
+  }
+  // An entry for pointer p that is not `x0` / `x1`: the one already keyed by p, else LRU.
+  int kv_pick(int x0, int x1, const float* p) const {
+    for (int i = 0; i < KV_ENTRIES; ++i)
+      if (i != x0 && i != x1 && kvc[i].ptr == p) return i;
+    int best = -1;
+    for (int i = 0; i < KV_ENTRIES; ++i)
+      if (i != x0 && i != x1 && (best < 0 || kvc[i].used < kvc[best].used)) best = i;
+    return best;
   }
 
   void free_ws() {
     if (ws) cudaFree(ws);
     ws = nullptr;
     cap = 0;
+    for (auto& k : kvc) k = {nullptr, 0, false, 0};
   }
 
   int ensure(int frames) {
@@ -202,7 +238,7 @@ struct dr_engine {
     const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
     const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
     const size_t o_ras = take(px * C * 2), o_d0 = take(px * C * 2);
-    const size_t o_skv = take((size_t)std::max(n_temporal, 1) * 4 * tok * C * 2);
+    const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
     CUDA_TRY(cudaMalloc(&ws, off));
     uint8_t* b = static_cast<uint8_t*>(ws);
@@ -346,6 +382,10 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
     b.w2 = fr.size(); pack_frags(vec(base + 14), c, 2 * c, fr);
     b.b2 = addf(base + 15);
     if (b.temporal) e->n_temporal++;
+    if (e->n_temporal > MAX_TEMPORAL) {
+      dr_destroy(e);
+      return fail(DR_ERR_CONFIG, "B200 engine supports at most 4 temporal blocks");
+    }
     e->blk.push_back(b);
   }
   const int tb = 2 + 16 * nb;
@@ -414,8 +454,7 @@ void dr_destroy(dr_engine* e) {
 
 int32_t dr_kernels_per_forward(dr_engine* e) {
   if (!e) return 0;
-  const int mask = 3 + (e->feather_r > 0 ? 1 : 0);
-  return mask + 2 * e->n_temporal + 1 + 2 * e->nb + 3;
+  return e->last_launches;
 }
 
 static void fill_mask_args(dr_engine* e, MaskArgs& m, int frames, const uint8_t* m0,
@@ -494,23 +533,35 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   launch_mask_stage(m, s);
   e->mark(0, s);
 
-  // 2. memory-slot K/V of every temporal block (LN1 + k/v projection of each slot)
+  // 2. memory-slot K/V of every temporal block (LN1 + k/v projection of each slot,
+  //    dstt.py:188-190).  An LRU cache keyed by slot pointer holds them: the last block
+  //    of every forward writes the new slot's K/V, so in steady state (caller passes the
+  //    engine's own outputs back, slot_kv_reuse bits set) nothing is recomputed here.
   const int fs = io->slot_batched ? B : 1;
-  const bool same_slot = io->slot0 == io->slot1;
-  {
-    int ti = 0;
-    for (int i = 0; i < e->nb; ++i) {
-      if (!e->blk[i].temporal) continue;
-      for (int sl = 0; sl < (same_slot ? 1 : 2); ++sl) {
+  int ent[2] = {0, 0};
+  int n_slotkv = 0;
+  if (e->n_temporal > 0) {
+    const float* sp[2] = {io->slot0, io->slot1};
+    for (int sl = 0; sl < 2; ++sl) {
+      ent[sl] = -1;
+      if (sl == 1 && sp[1] == sp[0]) { ent[1] = ent[0]; continue; }
+      if ((io->slot_kv_reuse >> sl) & 1) ent[sl] = e->kv_find(sp[sl], fs, io->slot_batched);
+      if (ent[sl] >= 0) continue;
+      ent[sl] = e->kv_pick(sl == 1 ? ent[0] : -1, -1, sp[sl]);
+      e->kv_set(ent[sl], sp[sl], fs, io->slot_batched != 0);
+      int ti = 0;
+      for (int i = 0; i < e->nb; ++i) {
+        if (!e->blk[i].temporal) continue;
         TokenArgs a{};
         a.n_tok = fs * T; a.T = T;
-        a.resid_in = sl == 0 ? io->slot0 : io->slot1;
+        a.resid_in = sp[sl];
         a.next = e->block_w(i);
-        a.k = e->skv(ti, sl, 0); a.v = e->skv(ti, sl, 1);
+        a.k = e->kv_ptr(ent[sl], ti, 0); a.v = e->kv_ptr(ent[sl], ti, 1);
         launch_token(TOK_SLOTKV, a, s);
+        ++n_slotkv;
         e->mark(1, s);
+        ++ti;
       }
-      ++ti;
     }
   }
 
@@ -542,10 +593,9 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     at.k[0] = e->k; at.v[0] = e->v; at.seg_frame_stride[0] = 1;
     at.key_valid = tv; at.mask_mode = mode;
     if (temporal) {
-      const int sl1 = same_slot ? 0 : 1;
       at.n_seg = 3; at.groups = e->cfg.temporal_groups; at.band = T / at.groups;
-      at.k[1] = e->skv(ti, 0, 0); at.v[1] = e->skv(ti, 0, 1);
-      at.k[2] = e->skv(ti, sl1, 0); at.v[2] = e->skv(ti, sl1, 1);
+      at.k[1] = e->kv_ptr(ent[0], ti, 0); at.v[1] = e->kv_ptr(ent[0], ti, 1);
+      at.k[2] = e->kv_ptr(ent[1], ti, 0); at.v[2] = e->kv_ptr(ent[1], ti, 1);
       at.seg_frame_stride[1] = at.seg_frame_stride[2] = io->slot_batched ? 1 : 0;
       ++ti;
       seen_t = true;
@@ -565,7 +615,24 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     a.q = e->q; a.k = e->k; a.v = e->v;
     a.tok16 = e->tok16;
     a.R = e->R; a.Cc = e->Cc;
+    int en = -1;
+    if (last && e->n_temporal > 0) {                  // fill the cache for io->new_slot
+      en = e->kv_pick(ent[0], ent[1], io->new_slot);
+      int tj = 0;
+      for (int j = 0; j < e->nb; ++j) {
+        if (!e->blk[j].temporal) continue;
+        a.kv_w[tj] = e->block_w(j);
+        a.kv_k[tj] = e->kv_ptr(en, tj, 0);
+        a.kv_v[tj] = e->kv_ptr(en, tj, 1);
+        ++tj;
+      }
+      a.n_kv = tj;
+    }
     launch_token(TOK_POST, a, s);
+    if (en >= 0) {
+      for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // alias
+      e->kv_set(en, io->new_slot, B, true);
+    }
     e->mark(5, s);
     cur ^= 1;
   }
@@ -587,6 +654,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
   launch_conv3x3_tc(16, e->map_d0, c2, s);
+  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
   e->mark(8, s);
   CUDA_TRY(cudaGetLastError());
   return DR_OK;
@@ -649,6 +717,7 @@ int dr_reset_memory(dr_engine* e) {
   }
   e->mem0 = 0;
   e->mem1 = 0;                       // cold start: both slots are the same zero tensor
+  for (bool& o : e->ring_own) o = false;
   return DR_OK;
 }
 
@@ -682,8 +751,10 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
   io.new_slot = e->ring[fresh];
   io.out_u8 = e->h_out;
+  io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
   int rc = dr_forward(e, &io, stream);
   if (rc) return rc;
+  e->ring_own[fresh] = true;         // contents and slot K/V cache entry now agree
   CUDA_TRY(cudaMemcpyAsync(p_out, e->h_out, px * 3, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(e->pin_flags, e->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));

@@ -39,7 +39,13 @@ struct TokenArgs {
   __half* tok16;          // fp16 copy when there is no next block, on the zero-padded
                           // [frames][(R+2)(Cc+2)][64] grid that Vec2Patch reads
   int R, Cc;              // token grid
+  // last block only: K/V of the new memory slot for every temporal block (slot K/V cache)
+  int n_kv;
+  BlockW kv_w[4];
+  __half* kv_k[4];
+  __half* kv_v[4];
 };
+constexpr int MAX_TEMPORAL = 4;
 
 enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
 

@@ -70,8 +70,10 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
   const int NR0 = TH + 2 * Hd, NR1 = TH + 2 * R;
   const size_t plane = (size_t)a.H * a.W;
 
+  pdl_trigger();
   if (tid == 0) sm.dirty = 0;
-  for (int i = tid; i < 2 * R + 1; i += 256) sm.w[i] = a.feather_w[i];
+  for (int i = tid; i < 2 * R + 1; i += 256) sm.w[i] = a.feather_w[i];   // constant
+  pdl_wait();
 
   // 0. one async round trip for every input of the tile: m0 bytes (+halo, 4-byte
   //    pieces, zero-filled off-frame; W % 8 == 0 keeps pieces inside a row) and rgb
@@ -329,9 +331,9 @@ void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
   }
   dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, a.frames);
   if (a.patch == 4)
-    mask_fused_kernel<4><<<grid, 256, smem, s>>>(a);
+    launch_pdl(mask_fused_kernel<4>, grid, dim3(256), smem, s, a);
   else
-    mask_fused_kernel<8><<<grid, 256, smem, s>>>(a);
+    launch_pdl(mask_fused_kernel<8>, grid, dim3(256), smem, s, a);
 }
 
 }  // namespace dr

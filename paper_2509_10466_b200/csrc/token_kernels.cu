@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(WARPS * 32) token_kernel(TokenArgs a) {
   const int n0 = blockIdx.x * 16;
   const int col0 = 16 * warp;                          // this warp's 16 of the 64 channels
   Slice x;
+  pdl_trigger();
+  pdl_wait();
 
   if constexpr (MODE == TOK_SLOTKV) {
     load_slice_f32(x, a.resid_in, n0, a.n_tok, col0, lane);
@@ -277,8 +279,15 @@ __global__ void __launch_bounds__(WARPS * 32) token_kernel(TokenArgs a) {
   if (a.has_next) {
     __syncthreads();                                   // sm.y / sm.h reads are done
     qkv_groups(x, a.next, a.q, a.k, a.v, n0, a.n_tok, a.T, 3 * warp, 3, sm, col0, warp, lane);
-  } else if (a.tok16) {
-    store_slice_padded_f16(x, a.tok16, n0, a.n_tok, a.T, a.R, a.Cc, col0, lane);
+  } else {
+    if (a.tok16) store_slice_padded_f16(x, a.tok16, n0, a.n_tok, a.T, a.R, a.Cc, col0, lane);
+    // K/V of the new memory slot for every temporal block: the next frames read them
+    // from the slot K/V cache instead of re-projecting the slot (dstt.py:188-190).
+    for (int i = 0; i < a.n_kv; ++i) {
+      __syncthreads();                                 // sm.y / sm.h reads are done
+      qkv_groups(x, a.kv_w[i], nullptr, a.kv_k[i], a.kv_v[i], n0, a.n_tok, a.T, 4 + 2 * warp, 2,
+                 sm, col0, warp, lane);
+    }
   }
 }
 
@@ -287,9 +296,9 @@ __global__ void __launch_bounds__(WARPS * 32) token_kernel(TokenArgs a) {
 void launch_token(int mode, const TokenArgs& a, cudaStream_t s) {
   dim3 grid((a.n_tok + 15) / 16), block(WARPS * 32);
   switch (mode) {
-    case TOK_EMBED: token_kernel<TOK_EMBED><<<grid, block, 0, s>>>(a); break;
-    case TOK_POST: token_kernel<TOK_POST><<<grid, block, 0, s>>>(a); break;
-    default: token_kernel<TOK_SLOTKV><<<grid, block, 0, s>>>(a); break;
+    case TOK_EMBED: launch_pdl(token_kernel<TOK_EMBED>, grid, block, 0, s, a); break;
+    case TOK_POST: launch_pdl(token_kernel<TOK_POST>, grid, block, 0, s, a); break;
+    default: launch_pdl(token_kernel<TOK_SLOTKV>, grid, block, 0, s, a); break;
   }
 }
 

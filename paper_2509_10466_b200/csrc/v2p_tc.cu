@@ -48,6 +48,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   const int n_chunks = (win_rows + M - 1) / M;
   const int n_taps = py < 2 ? 20 : 10;
 
+  pdl_trigger();
   if (threadIdx.x == 0) {
     tc::mbar_init(&sm.win_full, 1);
     tc::mbar_init(&sm.w_full, 1);
@@ -63,10 +64,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   if (warp == 0) {
     if (lane == 0) {                                   // ------------------- loads
       tc::tma_prefetch(&tok);
-      tc::mbar_arrive_expect_tx(&sm.win_full, n_chunks * M * 128);
-      for (int c = 0; c < n_chunks; ++c)
-        tc::tma_load_3d(sm.win[c], &tok, &sm.win_full, 0, P0 - (PC + 1) + c * M, f);
-      tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);
+      tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);   // constant: pre-wait
       const uint8_t* w0 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)(py * 10) * TAP_BYTES;
       for (int t = 0; t < 10; ++t) tc::bulk_load(sm.w[t], w0 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
       if (py < 2) {
@@ -74,6 +72,10 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
         for (int t = 0; t < 10; ++t)
           tc::bulk_load(sm.w[10 + t], w1 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
       }
+      pdl_wait();                                      // tokens of the predecessor
+      tc::mbar_arrive_expect_tx(&sm.win_full, n_chunks * M * 128);
+      for (int c = 0; c < n_chunks; ++c)
+        tc::tma_load_3d(sm.win[c], &tok, &sm.win_full, 0, P0 - (PC + 1) + c * M, f);
     }
   } else if (warp == 1) {
     {                                                  // ------------------- MMA issue
@@ -102,6 +104,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       }
     }
   } else {                                             // ------------------- epilogue
+    pdl_wait();                                        // raster is written below
     const int q = warp & 3;
     const int m = 32 * q + lane;
     const int P = P0 + m;
@@ -154,7 +157,7 @@ void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s) {
   }
   const int NP = (a.R + 2) * (a.Cc + 2);
   dim3 grid((NP + M - 1) / M, 8, a.frames);
-  v2p_tc_kernel<<<grid, THREADS, smem, s>>>(tok, a);
+  launch_pdl(v2p_tc_kernel, grid, dim3(THREADS), smem, s, tok, a);
 }
 
 }  // namespace dr

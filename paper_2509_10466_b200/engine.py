@@ -158,6 +158,28 @@ class DsttEngine(InpaintEngine):
     def kernels_per_forward(self) -> int:
         return int(_lib.load().dr_kernels_per_forward(self.handle))
 
+    # Slot K/V cache bookkeeping (dr_frame_io.slot_kv_reuse): a memory slot may reuse the
+    # K/V the engine computed when it produced that slot only if it is the very tensor the
+    # engine wrote (same storage pointer, version counter unchanged = no in-place edits).
+    def _register_slot(self, t) -> None:
+        import weakref
+        rec = (weakref.ref(t), t.data_ptr(), t._version, tuple(t.shape))
+        self._produced = [r for r in getattr(self, "_produced", []) if r[0]() is not None][-5:]
+        self._produced.append(rec)
+
+    def _is_own_slot(self, s) -> bool:
+        import torch
+        if not isinstance(s, torch.Tensor) or not s.is_cuda or s.dtype != torch.float32:
+            return False
+        for ref, ptr, ver, shape in getattr(self, "_produced", []):
+            t = ref()
+            if t is None or ptr != s.data_ptr() or t._version != ver or s._version != ver:
+                continue
+            if tuple(s.shape) == shape or (len(shape) == 3 and shape[0] == 1
+                                           and tuple(s.shape) == shape[1:]):
+                return True
+        return False
+
     def _slot(self, s):
         import torch
         if not isinstance(s, torch.Tensor):
@@ -231,6 +253,7 @@ class DsttEngine(InpaintEngine):
         mask = (mask != 0).to(torch.uint8) if mask.dtype != torch.uint8 else mask.contiguous()
         if memory is None:
             memory = self.zero_memory().slots
+        reuse = sum(1 << i for i, s in enumerate(memory) if self._is_own_slot(s))
         slots = [self._slot(s) for s in memory]
         T, C = cfg.tokens, cfg.channels
         shapes = {tuple(s.shape) for s in slots}
@@ -283,6 +306,7 @@ class DsttEngine(InpaintEngine):
         if self._flags.numel() < B:
             self._flags = torch.zeros(B, dtype=torch.int32, device=dev)
         io.flags = self._flags.data_ptr()
+        io.slot_kv_reuse = reuse
         stream = torch.cuda.current_stream(dev)
         if sync:
             t0 = torch.cuda.Event(enable_timing=True)
@@ -290,6 +314,7 @@ class DsttEngine(InpaintEngine):
             t0.record(stream)
         _lib.check(self._native.lib.dr_forward(self.handle, ctypes.byref(io),
                                                stream.cuda_stream))
+        self._register_slot(new_slot)
         # keep inputs alive until the launch is enqueued (ctypes holds raw pointers)
         res["_keep"] = (rgb, mask, slots)
         if sync:

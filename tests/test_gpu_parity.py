@@ -231,6 +231,35 @@ def test_host_buffer_path_equals_device_path(rng):
         assert np.array_equal(a.rgb, b)
 
 
+def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
+    """Carried engine outputs reuse their cached K/V; clones recompute; bit-identical."""
+    cfg = DsttConfig.baseline(128, mask_dilate=2, mask_feather_sigma=1.0)
+    eng = DsttEngine(cfg, seed=3)
+    imgs, masks = synth.frame_pool("C1", 5, size=128)
+    mem_a = eng.zero_memory()
+    outs_a, launches = [], []
+    for t in range(5):                           # stream A: carried outputs, cache hits
+        ra = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]), mem_a.slots)
+        launches.append(eng.kernels_per_forward())
+        outs_a.append((ra["out"], ra["slot"]))
+        mem_a = mem_a.push(ra["slot"][0])
+    # cold: one zero slot (2 temporal blocks) re-projected; then the zero slot0 only;
+    # steady state: both slots cached -> 1 mask + 1 embed + 2 x 4 blocks + 3 decoder
+    assert launches == [15, 15, 13, 13, 13]
+    mem_b = eng.zero_memory()
+    for t in range(5):                           # stream B: clones, always recomputed
+        rb = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]),
+                     [s.clone() for s in mem_b.slots])
+        assert torch.equal(outs_a[t][0], rb["out"]) and torch.equal(outs_a[t][1], rb["slot"])
+        mem_b = mem_b.push(rb["slot"][0])
+    # an in-place edit of a carried slot must not reuse stale K/V
+    s0, s1 = mem_a.slots
+    s1.mul_(0.5)
+    ra = eng.run(cuda(imgs[:1]), cuda(masks[:1]), (s0, s1))
+    rb = eng.run(cuda(imgs[:1]), cuda(masks[:1]), (s0.clone(), s1.clone()))
+    assert torch.equal(ra["out"], rb["out"])
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_batch_invariance_and_determinism_512():
     cfg = DsttConfig.baseline(512, mask_dilate=5, mask_feather_sigma=3.0)
