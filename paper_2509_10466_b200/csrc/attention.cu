@@ -125,11 +125,14 @@ DR_DEV void attend_64(SoftmaxState& st, const uint32_t* qa, const __half (*ks)[D
   const uint32_t ones = (lane >> 2) == 0 ? 0x3C003C00u : 0u;   // B column 0 = 1 -> row sum
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
+    // (Offloading a quarter of these to ex2_poly on the FMA pipe measured slower at batch
+    //  1: the kernel is issue/latency-bound there, not MUFU-bound.)
+    auto e2 = [](float x) { return ex2(x); };
     uint32_t pa[4];
-    pa[0] = pack_half2(ex2(fmaf(s[2 * j][0], sl2, -base0)), ex2(fmaf(s[2 * j][1], sl2, -base0)));
-    pa[1] = pack_half2(ex2(fmaf(s[2 * j][2], sl2, -base1)), ex2(fmaf(s[2 * j][3], sl2, -base1)));
-    pa[2] = pack_half2(ex2(fmaf(s[2 * j + 1][0], sl2, -base0)), ex2(fmaf(s[2 * j + 1][1], sl2, -base0)));
-    pa[3] = pack_half2(ex2(fmaf(s[2 * j + 1][2], sl2, -base1)), ex2(fmaf(s[2 * j + 1][3], sl2, -base1)));
+    pa[0] = pack_half2(e2(fmaf(s[2 * j][0], sl2, -base0)), e2(fmaf(s[2 * j][1], sl2, -base0)));
+    pa[1] = pack_half2(e2(fmaf(s[2 * j][2], sl2, -base1)), e2(fmaf(s[2 * j][3], sl2, -base1)));
+    pa[2] = pack_half2(e2(fmaf(s[2 * j + 1][0], sl2, -base0)), e2(fmaf(s[2 * j + 1][1], sl2, -base0)));
+    pa[3] = pack_half2(e2(fmaf(s[2 * j + 1][2], sl2, -base1)), e2(fmaf(s[2 * j + 1][3], sl2, -base1)));
     uint32_t vf[4];
     const int mi = lane >> 3;
     const int key = 16 * j + (lane & 7) + (mi & 1) * 8;

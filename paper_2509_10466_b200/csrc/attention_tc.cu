@@ -1,0 +1,426 @@
+// Fused attention on the 5th-gen tensor cores (tcgen05 + TMEM), head_dim 16.
+//
+// Reference: scaled_dot_product (dstt.py:89-99) inside MultiHeadAttention (:111-120);
+// spatial blocks attend over the whole frame (:146-150), temporal blocks attend a row band
+// of queries to cat[band(cur), band(slot0), band(slot1)] (:166-191).
+//
+// One CTA = 128 queries x one head x half of the keys; a 2-CTA cluster covers all keys and
+// merges the two halves through distributed shared memory.  Per 128-key block:
+//   MMA warp      S = Q K^T         tcgen05.mma M=128 N=128 K=16, smem x smem -> TMEM
+//                 O += P [V | 1]    8 x tcgen05.mma M=128 N=32 K=16, A = P from TMEM, B = V
+//                                   (MN-major) plus a constant ones block at the LBO offset,
+//                                   so column 16 of O accumulates the softmax row sum
+//   4 softmax warps (thread = query row = TMEM lane): ONE tcgen05.ld sweep of its 128
+//                 scores (TMEM read bandwidth, not MUFU, bounds a two-pass softmax here):
+//                 one FFMA + one MUFU ex2 per score (log2 domain) against the running
+//                 base, row max tracked on the side, fp16 pack, tcgen05.st P;
+//                 no shuffles, no HMMA, no per-key index math on the math warps
+//   producer warp cp.async.bulk of the 128-key K and V blocks into a 3-stage ring
+// The QKV producer (token_kernels.cu) stores q/k/v rows with the 16-byte chunk swizzle of
+// the UMMA 32-byte swizzle mode, so bulk copies land as valid SWIZZLE_32B operands.
+// The running max is rescaled lazily (only when a row max grows by > 2^8; exact because
+// numerator and denominator share the stale max); a rescale reads, scales and writes the
+// warp's O rows in TMEM between P*V MMAs.
+//
+// Mask-aware mode (NEW): keys of fully-masked tokens of the current frame get
+// -inf; memory-slot keys are always valid; a spatial block whose frame has no valid key
+// falls back to unmasked attention (per-block mode resolved on the host, engine.cu).
+#include <math.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace dr {
+
+namespace {
+
+constexpr int QROWS = 128;
+constexpr int KB = 64;                        // keys per block
+constexpr int STAGES = 4;
+constexpr int THREADS = 192;                  // warp 0 loads, warp 1 MMA, warps 2-5 softmax
+// TMEM (double-buffered S and P so that S(j+1) is ready when softmax(j) ends):
+//   S[b] fp32 64 cols at 64b, P[b] fp16 pairs 32 cols at 128 + 32b, O 32 cols (16 + row sum)
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 192, TM_COLS = 256;
+constexpr float RESCALE_SLACK = 8.f;          // log2 units: p <= 2^8 between rescales
+constexpr int ROW_BYTES = DH * 2;             // 32 B per token row
+
+struct __align__(1024) Smem {
+  __half q[QROWS][DH];                        // 4 KB, SW32 K-major A operand
+  __half k[STAGES][KB][DH];                   // SW32 K-major B operand of S
+  __half v[STAGES][2][KB][DH];                // [0] V block, [1] constant ones block (+4 KB)
+  float bias[STAGES][KB];                     // mask-aware mode only
+  float mrg[QROWS][18];                       // cluster merge: m, l, o[16] of key half 1
+  uint64_t q_full, kv_full[STAGES], kv_empty[STAGES], s_full[2], p_full[2], pv_done, o_done;
+  uint32_t tmem_base;
+};
+
+// SWIZZLE_32B shared-memory descriptors (layout type 6), version 1.
+DR_DEV uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (6ull << 61);
+}
+
+// A operand in TMEM (P), B in smem.
+DR_DEV void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+#define DR_TMEM_LD32(taddr, r)                                                               \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"   \
+               "%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29," \
+               "%30,%31}, [%32];\n"                                                          \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),     \
+                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),   \
+                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),            \
+                 "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),            \
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]),            \
+                 "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
+               : "r"(taddr))
+#define DR_TMEM_ST32(taddr, r)                                                               \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,"   \
+               "%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,"    \
+               "%28,%29,%30,%31,%32};\n"                                                     \
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),         \
+                  "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),         \
+                  "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),    \
+                  "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),    \
+                  "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),    \
+                  "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory")
+#define DR_TMEM_ST16(taddr, r)                                                               \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,"   \
+               "%10,%11,%12,%13,%14,%15,%16};\n"                                             \
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),         \
+                  "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),         \
+                  "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory")
+DR_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+DR_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+DR_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n"
+               ::: "memory");
+}
+DR_DEV void st_cluster_f32(uint32_t local_saddr, uint32_t cta, float v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_saddr), "r"(cta));
+  asm volatile("st.shared::cluster.f32 [%0], %1;\n" :: "r"(remote), "f"(v) : "memory");
+}
+
+DR_DEV int seg_of(int kk, int band) { return kk >= band ? (kk >= 2 * band ? 2 : 1) : 0; }
+
+template <bool MASKED>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 2)
+attn_tc_kernel(AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();                 // key half
+  const int qtile = blockIdx.x >> 1, h = blockIdx.y;
+  const int frame = blockIdx.z / a.groups, grp = blockIdx.z - frame * a.groups;
+  const int band0 = grp * a.band;
+  const int q0 = qtile * QROWS;
+  const int n_keys = a.n_seg * a.band;
+  const int n_kb = (n_keys + KB - 1) / KB;
+  const int nkb_h = (n_kb + 1) / 2;
+  const int kb0 = crank * nkb_h;
+  const int nb = max(0, min(n_kb, kb0 + nkb_h) - kb0);   // this CTA's blocks
+
+  pdl_trigger();
+  // constant smem: zero Q / K / V rings (finite stale tails), ones blocks for row sums
+  {
+    uint4* z = reinterpret_cast<uint4*>(&sm.q[0][0]);
+    const int n16 = (int)((sizeof(sm.q) + sizeof(sm.k) + sizeof(sm.v)) / 16);
+    for (int i = threadIdx.x; i < n16; i += THREADS) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < STAGES * KB; i += THREADS) {
+    const int st = i / KB, key = i - st * KB;
+    // element (dim 0, key) of the ones block: chunk 0 sits at chunk (key >> 2) & 1
+    sm.v[st][1][key][((key >> 2) & 1) * 8] = __float2half(1.0f);
+  }
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&sm.kv_full[s], 1);
+      tc::mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&sm.s_full[b], 1);
+      tc::mbar_init(&sm.p_full[b], 4);
+    }
+    tc::mbar_init(&sm.pv_done, 1);
+    tc::mbar_init(&sm.o_done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  pdl_wait();
+
+  int any_valid = 1;
+  if constexpr (MASKED) {
+    if (a.mask_mode == 1 || a.mask_mode == 3) {
+      const uint8_t* kv = a.key_valid + (size_t)frame * a.T;
+      int mine = 0;
+      for (int i = threadIdx.x; i < a.T; i += THREADS) mine |= kv[i];
+      any_valid = __syncthreads_or(mine);
+    }
+  }
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      const int nq = max(0, min(QROWS, a.band - q0));
+      tc::mbar_arrive_expect_tx(&sm.q_full, (uint32_t)nq * ROW_BYTES);
+      if (nq > 0)
+        tc::bulk_load(&sm.q[0][0], a.q + ((size_t)(frame * HEADS + h) * a.T + band0 + q0) * DH,
+                      (uint32_t)nq * ROW_BYTES, &sm.q_full);
+    }
+    for (int j = 0; j < nb; ++j) {
+      const int st = j % STAGES;
+      if (j >= STAGES) tc::mbar_wait(&sm.kv_empty[st], (uint32_t)(j / STAGES - 1) & 1u);
+      const int kk0 = (kb0 + j) * KB, kk1 = min(kk0 + KB, n_keys);
+      if constexpr (MASKED) {
+        for (int key = lane; key < KB; key += 32) {
+          const int kk = kk0 + key;
+          float bias = -INFINITY;
+          if (kk < kk1) {
+            bool ok = true;
+            if (kk < a.band && a.mask_mode != 0) {          // current-frame keys only
+              const bool kv = a.key_valid[(size_t)frame * a.T + band0 + kk] != 0;
+              if (a.mask_mode == 1) ok = kv || !any_valid;
+              else if (a.mask_mode == 2) ok = kv;
+              else ok = any_valid;
+            }
+            bias = ok ? 0.f : -INFINITY;
+          }
+          sm.bias[st][key] = bias;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        tc::mbar_arrive_expect_tx(&sm.kv_full[st], 2u * (uint32_t)(kk1 - kk0) * ROW_BYTES);
+        int kk = kk0;
+        while (kk < kk1) {                                  // split at segment boundaries
+          const int seg = seg_of(kk, a.band);
+          const int end = min(kk1, (seg + 1) * a.band);
+          const int stride = seg == 0 ? a.seg_frame_stride[0]
+                           : (seg == 1 ? a.seg_frame_stride[1] : a.seg_frame_stride[2]);
+          const size_t off = ((size_t)((stride ? frame : 0) * HEADS + h) * a.T + band0 + kk - seg * a.band) * DH;
+          const __half* ks = (seg == 0 ? a.k[0] : (seg == 1 ? a.k[1] : a.k[2])) + off;
+          const __half* vs = (seg == 0 ? a.v[0] : (seg == 1 ? a.v[1] : a.v[2])) + off;
+          const uint32_t n = (uint32_t)(end - kk) * ROW_BYTES;
+          tc::bulk_load(&sm.k[st][kk - kk0][0], ks, n, &sm.kv_full[st]);
+          tc::bulk_load(&sm.v[st][0][kk - kk0][0], vs, n, &sm.kv_full[st]);
+          kk = end;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = tc::idesc_f16(128, KB);                   // K-major B
+    constexpr uint32_t idesc_pv = tc::idesc_f16(128, 32) | (1u << 16);     // MN-major B
+    // Issue order: S(0), S(1), then per block j: [p_full(j): softmax has read S(j) and
+    // written P(j)] O += P(j) V_j -> kv_empty, pv_done; S(j+2) into the freed S buffer.
+    // tcgen05 ops complete in issue order, so the commit of S(j+1) (issued after P(j-1)V)
+    // certifies that P(j-1)V has read P buffer (j+1)&1 before softmax(j+1) overwrites it;
+    // O itself may still be accumulating P(j)V during softmax(j+1), which therefore waits on
+    // pv_done(j) before it rescales O (the rare path).
+    const uint64_t qd = sdesc_sw32(tc::smem_u32(&sm.q[0][0]), 16, 256);
+    tc::mbar_wait(&sm.q_full, 0);
+    auto s_mma = [&](int jj) {
+      const int st = jj % STAGES;
+      tc::mbar_wait(&sm.kv_full[st], (uint32_t)(jj / STAGES) & 1u);
+      tc::fence_after();
+      const uint64_t kd = sdesc_sw32(tc::smem_u32(&sm.k[st][0][0]), 16, 256);
+      tc::mma_f16_warp(tbase + TM_S + KB * (jj & 1), qd, kd, idesc_s, 0);
+      tc::mma_commit_warp(&sm.s_full[jj & 1]);
+    };
+    if (nb > 0) s_mma(0);
+    if (nb > 1) s_mma(1);
+    for (int j = 0; j < nb; ++j) {
+      const int st = j % STAGES, b = j & 1;
+      tc::mbar_wait(&sm.p_full[b], (uint32_t)(j >> 1) & 1u);
+      tc::fence_after();
+      const uint64_t vd = sdesc_sw32(tc::smem_u32(&sm.v[st][0][0][0]), KB * ROW_BYTES, 256);
+      const uint32_t pcol = tbase + TM_P + (KB / 2) * b;
+#pragma unroll
+      for (int kk = 0; kk < KB / 16; ++kk)
+        mma_ts_warp(tbase + TM_O, pcol + 8 * kk, vd + (uint64_t)(kk * 16 * ROW_BYTES / 16),
+                    idesc_pv, (j | kk) != 0);
+      tc::mma_commit_warp(&sm.kv_empty[st]);
+      tc::mma_commit_warp(&sm.pv_done);
+      if (j + 2 < nb) s_mma(j + 2);
+    }
+    // pv_done may trail the softmax by two phases at the end (parity aliasing), so the
+    // final O read has its own single-phase barrier
+    if (nb > 0) tc::mma_commit_warp(&sm.o_done);
+  } else {
+    // ---------------------------------------------------------------- softmax warps
+    const int q = warp & 3;                            // TMEM lanes 32q.. (warp id % 4)
+    const int row = 32 * q + lane;
+    const uint32_t lane_base = tbase + ((uint32_t)(32 * q) << 16);
+    const float sl2 = 0.25f * 1.4426950408889634f;     // 1/sqrt(16) * log2(e)
+    float m = -INFINITY;
+    uint32_t r[KB];                                    // this row's scores of S(j)
+    // wait for S(jj) (its commit also says P(jj-2)*V has released P buffer jj&1) and start
+    // the TMEM loads; the registers are scoreboarded, the consumer waits on first use
+    auto load_s = [&](int jj) {
+      tc::mbar_wait(&sm.s_full[jj & 1], (uint32_t)(jj >> 1) & 1u);
+      tc::fence_after();
+      const uint32_t s_col = lane_base + TM_S + KB * (jj & 1);
+#pragma unroll
+      for (int ch = 0; ch < KB / 32; ++ch) DR_TMEM_LD32(s_col + 32 * ch, (r + 32 * ch));
+    };
+    if (nb > 0) load_s(0);
+    for (int j = 0; j < nb; ++j) {
+      const int st = j % STAGES, b = j & 1;
+      const int n_valid = min(KB, n_keys - (kb0 + j) * KB);
+      const uint32_t p_col = lane_base + TM_P + (KB / 2) * b;
+      tc::tmem_wait_ld();
+      // key bias / tail mask for score column c of this block
+      auto adjust = [&](float v, int c) -> float {
+        if constexpr (MASKED) return v + sm.bias[st][c];
+        return c < n_valid ? v : -INFINITY;
+      };
+      const bool full = MASKED ? false : n_valid == KB;
+      // One pass over S (each score is read from TMEM once): p = 2^(s*scale - base) as fp16
+      // pairs into P buffer b while tracking the block's row max; returns the scaled max.
+      // (FULL is compile-time so the tail/bias masking is never if-converted into the
+      // common full-block sweep)
+      auto sweep = [&](float base, auto track, auto full_tag) -> float {
+        constexpr bool FULL = decltype(full_tag)::value;
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int ch = 0; ch < KB / 32; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int k0 = 32 * ch + 2 * c;
+            float s0 = __uint_as_float(r[k0]), s1 = __uint_as_float(r[k0 + 1]);
+            if constexpr (!FULL) {
+              s0 = adjust(s0, k0);
+              s1 = adjust(s1, k0 + 1);
+            }
+            if constexpr (decltype(track)::value) mx[c & 3] = fmaxf(mx[c & 3], fmaxf(s0, s1));
+            pk[c] = pack_half2(ex2(fmaf(s0, sl2, -base)), ex2(fmaf(s1, sl2, -base)));
+          }
+          DR_TMEM_ST16(p_col + 16 * ch, pk);
+        }
+        return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
+      };
+      const float base0 = m == -INFINITY ? 0.f : m;
+      const float rmax = full ? sweep(base0, std::true_type{}, std::true_type{})
+                              : sweep(base0, std::true_type{}, std::false_type{});
+      // The running base m may lag the true max by RESCALE_SLACK (p <= 2^8, exact since
+      // numerator and denominator share it); past that, rescale O and redo the sweep (rare
+      // after the first block).  S(j) is still intact: P lives in its own columns.
+      const bool need = rmax > m + RESCALE_SLACK;
+      if (__any_sync(0xffffffffu, need)) {
+        const float mn = need ? rmax : m;
+        if (j > 0) {                                   // rescale this warp's O rows
+          // P(j-1)*V has landed in O.  Unambiguous: S(j) ready implies P(j-2)*V complete,
+          // and P(j)*V is not issued before this warp arrives, so pv_done is in phase j-1 or j.
+          tc::mbar_wait(&sm.pv_done, (uint32_t)(j - 1) & 1u);
+          tc::fence_after();
+          const float cfac = (need && m != -INFINITY) ? ex2(m - mn) : (need ? 0.f : 1.f);
+          uint32_t o[32];
+          DR_TMEM_LD32(lane_base + TM_O, o);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * cfac);
+          DR_TMEM_ST32(lane_base + TM_O, o);
+        }
+        m = mn;
+        tmem_wait_st();                                // P stores of the optimistic sweep
+        sweep(m == -INFINITY ? 0.f : m, std::false_type{}, std::false_type{});  // any block
+      }
+      // prefetch S(j+1) (normally complete already: S is double-buffered) so its TMEM load
+      // latency overlaps the completion of the P(j) stores and the hand-off
+      if (j + 1 < nb) load_s(j + 1);
+      tmem_wait_st();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.p_full[b]);
+    }
+    float o[16], l = 0.f;
+    if (nb > 0) {
+      tc::mbar_wait(&sm.o_done, 0);                   // committed once, after the last P*V
+      tc::fence_after();
+      uint32_t orr[32];
+      DR_TMEM_LD32(lane_base + TM_O, orr);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int d = 0; d < 16; ++d) o[d] = __uint_as_float(orr[d]);
+      l = __uint_as_float(orr[16]);
+    } else {
+#pragma unroll
+      for (int d = 0; d < 16; ++d) o[d] = 0.f;
+    }
+    // ---- merge the key halves: rank 1 ships (m, l, o) rows to rank 0 through DSMEM
+    if (crank == 1) {
+      const uint32_t base_addr = tc::smem_u32(&sm.mrg[row][0]);
+      st_cluster_f32(base_addr, 0, m);
+      st_cluster_f32(base_addr + 4, 0, l);
+#pragma unroll
+      for (int d = 0; d < 16; ++d) st_cluster_f32(base_addr + 8 + 4 * d, 0, o[d]);
+    }
+    cluster_sync();
+    if (crank == 0 && q0 + row < a.band) {
+      const float m1 = sm.mrg[row][0], l1 = sm.mrg[row][1];
+      const float M = fmaxf(m, m1);
+      const float b = M == -INFINITY ? 0.f : M;
+      const float a0 = ex2(m - b), a1 = ex2(m1 - b);
+      const float lt = l * a0 + l1 * a1;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      uint32_t outp[8];
+#pragma unroll
+      for (int d = 0; d < 8; ++d)
+        outp[d] = pack_half2((o[2 * d] * a0 + sm.mrg[row][2 + 2 * d] * a1) * inv,
+                             (o[2 * d + 1] * a0 + sm.mrg[row][3 + 2 * d] * a1) * inv);
+      uint4* dst = reinterpret_cast<uint4*>(a.out + ((size_t)frame * a.T + band0 + q0 + row) * C + h * DH);
+      dst[0] = make_uint4(outp[0], outp[1], outp[2], outp[3]);
+      dst[1] = make_uint4(outp[4], outp[5], outp[6], outp[7]);
+    }
+  }
+  if (warp < 2) cluster_sync();                        // every thread joins the merge barrier
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<TM_COLS>(tbase);
+}
+
+}  // namespace
+
+void launch_attention(const AttnArgs& a, cudaStream_t s) {
+  static bool init = false;
+  // TMEM holds exactly two CTAs (2 x 256 columns): pad shared memory so that a third CTA
+  // is never co-resident (it would spin in tcgen05.alloc and stall its cluster partner).
+  constexpr int SMEM_2PER_SM = 80 * 1024;
+  static_assert(sizeof(Smem) <= SMEM_2PER_SM, "attention smem exceeds the 2-per-SM pad");
+  const int smem = SMEM_2PER_SM;
+  if (!init) {
+    cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  dim3 grid(2 * ((a.band + QROWS - 1) / QROWS), HEADS, a.frames * a.groups);
+  if (a.mask_mode != 0 && a.key_valid)
+    launch_pdl(attn_tc_kernel<true>, grid, dim3(THREADS), smem, s, a);
+  else
+    launch_pdl(attn_tc_kernel<false>, grid, dim3(THREADS), smem, s, a);
+}
+
+}  // namespace dr

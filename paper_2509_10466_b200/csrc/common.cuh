@@ -63,6 +63,21 @@ DR_DEV float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes (no MUFU), for x <= ~16: x clamped at -125 (-> ~0; the
+// exponent-field add must not underflow, 2^f < 1 has biased exponent 126), split as
+// x = j + f with j = round(x) via the 1.5*2^23 magic add, f in [-0.5, 0.5]; 2^f by a
+// degree-3 minimax polynomial (rel. error < 1e-4, below the fp16 rounding of P), then j is
+// added to the exponent field (the FA4 MUFU-offload trick).
+DR_DEV float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float r = __fadd_rn(x, 12582912.f);            // 1.5 * 2^23: round to integer
+  const float j = __fadd_rn(r, -12582912.f);
+  const float f = __fsub_rn(x, j);                     // [-0.5, 0.5]
+  float p = fmaf(f, 0.05517161f, 0.24261111f);         // max rel. error 7.5e-5
+  p = fmaf(f, p, 0.69326097f);
+  p = fmaf(f, p, 0.99992806f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+}
 DR_DEV float quad_sum(float v) {
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);

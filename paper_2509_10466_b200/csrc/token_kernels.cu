@@ -173,9 +173,9 @@ DR_DEV void qkv_groups(const Slice& x, const BlockW& w, __half* q, __half* k, __
     gemm<2, 4>(acc, a, w.wqkv, 2 * p, lane);
     const int which = p >> 2, h = p & 3;
     __half* dst = which == 0 ? q : (which == 1 ? k : v);
-    // K and V rows are stored with the attention kernel's smem swizzle (16-byte chunk c
-    // of token t at c ^ ((t >> 2) & 1)) so its bulk copies land conflict-free.
-    const int sa = which ? ((ta >> 2) & 1) * 4 : 0, sb = which ? ((tb >> 2) & 1) * 4 : 0;
+    // q, k, v rows are stored with the UMMA 32-byte swizzle (16-byte chunk c of token t at
+    // c ^ ((t >> 2) & 1)): the attention kernel's bulk copies land as SWIZZLE_32B operands.
+    const int sa = ((ta >> 2) & 1) * 4, sb = ((tb >> 2) & 1) * 4;
     if (na < n_tok) {
       uint32_t* r = reinterpret_cast<uint32_t*>(dst + ((size_t)(fa * HEADS + h) * T + ta) * DH);
       r[sa + t] = pack_half2(acc[0][0], acc[0][1]);
