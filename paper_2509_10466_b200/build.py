@@ -31,26 +31,32 @@ def _stale(obj: Path, src: Path) -> bool:
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """trace=True builds a separate diagnostic library (_build_trace/, -DDR_TRACE: per-CTA
+    global-timer stamps in the attention kernel, scripts/attn_trace.py) — never the product."""
+    out_dir = PKG / "_build_trace" if trace else OUT_DIR
+    lib_path = out_dir / LIB.name
+    flags = FLAGS + (["-DDR_TRACE"] if trace else [])
+    out_dir.mkdir(exist_ok=True)
     objs = []
     for name in SOURCES:
         src = CSRC / name
-        obj = OUT_DIR / (name + ".o")
+        obj = out_dir / (name + ".o")
         objs.append(obj)
         if force or _stale(obj, src):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *ARCH, *flags, "-c", str(src), "-o", str(obj)]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             print("[build]", " ".join(cmd[-3:]), flush=True)
             subprocess.run(cmd, check=True)
-    if force or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+    if force or not lib_path.exists() or any(o.stat().st_mtime > lib_path.stat().st_mtime
+                                             for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(lib_path), *map(str, objs), "-lcudart_static",
                "-lrt", "-ldl", "-lpthread"]
-        print("[build] link", LIB.name, flush=True)
+        print("[build] link", lib_path.relative_to(PKG), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv)

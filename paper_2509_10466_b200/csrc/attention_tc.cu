@@ -45,6 +45,10 @@ constexpr int THREADS = 192;                  // warp 0 loads, warp 1 MMA, warps
 //   S[b] fp32 64 cols at 64b, P[b] fp16 pairs 32 cols at 128 + 32b, O 32 cols (16 + row sum)
 constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 192, TM_COLS = 256;
 constexpr float RESCALE_SLACK = 8.f;          // log2 units: p <= 2^8 between rescales
+#ifndef DR_POLY_EVERY
+#define DR_POLY_EVERY 4
+#endif
+constexpr int POLY_EVERY = DR_POLY_EVERY;     // 1 pair in POLY_EVERY via ex2_poly (0 = none)
 constexpr int ROW_BYTES = DH * 2;             // 32 B per token row
 
 struct __align__(1024) Smem {
@@ -52,8 +56,9 @@ struct __align__(1024) Smem {
   __half k[STAGES][KB][DH];                   // SW32 K-major B operand of S
   __half v[STAGES][2][KB][DH];                // [0] V block, [1] constant ones block (+4 KB)
   float bias[STAGES][KB];                     // mask-aware mode only
-  float mrg[QROWS][18];                       // cluster merge: m, l, o[16] of key half 1
+  float mrg[QROWS][20];                       // cluster merge: m, l, o[16] of key half 1 (+pad)
   uint64_t q_full, kv_full[STAGES], kv_empty[STAGES], s_full[2], p_full[2], pv_done, o_done;
+  uint64_t mrg_full;                          // rank 0: 128 remote arrivals of rank 1's rows
   uint32_t tmem_base;
 };
 
@@ -110,13 +115,59 @@ DR_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n"
                ::: "memory");
 }
-DR_DEV void st_cluster_f32(uint32_t local_saddr, uint32_t cta, float v) {
+DR_DEV uint32_t map_cluster(uint32_t local_saddr, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_saddr), "r"(cta));
-  asm volatile("st.shared::cluster.f32 [%0], %1;\n" :: "r"(remote), "f"(v) : "memory");
+  return remote;
+}
+DR_DEV void st_cluster_v4(uint32_t remote, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};\n"
+               :: "r"(remote), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+// arrive on an mbarrier in another CTA of the cluster, releasing this thread's prior
+// shared::cluster stores to whoever acquires the phase
+DR_DEV void mbar_arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n"
+               :: "r"(remote_bar) : "memory");
+}
+DR_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = tc::smem_u32(bar);
+  const long long t0 = clock64();
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1ll << 32)) __trap();        // protocol bug: fail loudly
+  }
 }
 
 DR_DEV int seg_of(int kk, int band) { return kk >= band ? (kk >= 2 * band ? 2 : 1) : 0; }
+
+// Diagnostic build only (-DDR_TRACE, build.py --trace): global-timer stamps per CTA taken by
+// softmax warp 2, read back by scripts/attn_trace.py.  Slots: 0 entry, 1 after pdl_wait,
+// 2 S(0) in registers, 3 softmax loop done, 4 merge done, 5 exit, 6 SM id, 7 blocks,
+// 8 O in registers, 9 DSMEM stores issued, 10 cluster rank.
+#ifdef DR_TRACE
+constexpr int TRACE_CTAS = 8192;
+__device__ unsigned long long g_trace[TRACE_CTAS * 16];
+DR_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DR_TRACE_AT(slot, value)                                                             \
+  do {                                                                                       \
+    const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);        \
+    if (warp == 2 && lane == 0 && cta_ < TRACE_CTAS) g_trace[cta_ * 16 + (slot)] = (value);   \
+  } while (0)
+#define DR_TRACE_T(slot) DR_TRACE_AT(slot, gtimer())
+#else
+#define DR_TRACE_AT(slot, value) do {} while (0)
+#define DR_TRACE_T(slot) do {} while (0)
+#endif
 
 template <bool MASKED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 2)
@@ -135,6 +186,7 @@ attn_tc_kernel(AttnArgs a) {
   const int kb0 = crank * nkb_h;
   const int nb = max(0, min(n_kb, kb0 + nkb_h) - kb0);   // this CTA's blocks
 
+  DR_TRACE_T(0);
   pdl_trigger();
   // constant smem: zero Q / K / V rings (finite stale tails), ones blocks for row sums
   {
@@ -160,15 +212,27 @@ attn_tc_kernel(AttnArgs a) {
     }
     tc::mbar_init(&sm.pv_done, 1);
     tc::mbar_init(&sm.o_done, 1);
+    tc::mbar_init(&sm.mrg_full, QROWS);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc::fence_before();
-  __syncthreads();
+  // cluster-wide: both CTAs' barriers are initialised before any remote arrive (this is the
+  // only cluster barrier; it runs before pdl_wait, overlapping the predecessor kernel)
+  cluster_sync();
   tc::fence_after();
   const uint32_t tbase = sm.tmem_base;
   pdl_wait();
+  DR_TRACE_T(1);
+#ifdef DR_TRACE
+  {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    DR_TRACE_AT(6, smid);
+    DR_TRACE_AT(7, nb);
+  }
+#endif
 
   int any_valid = 1;
   if constexpr (MASKED) {
@@ -291,6 +355,7 @@ attn_tc_kernel(AttnArgs a) {
       const int n_valid = min(KB, n_keys - (kb0 + j) * KB);
       const uint32_t p_col = lane_base + TM_P + (KB / 2) * b;
       tc::tmem_wait_ld();
+      if (j == 0) DR_TRACE_T(2);
       // key bias / tail mask for score column c of this block
       auto adjust = [&](float v, int c) -> float {
         if constexpr (MASKED) return v + sm.bias[st][c];
@@ -316,7 +381,12 @@ attn_tc_kernel(AttnArgs a) {
               s1 = adjust(s1, k0 + 1);
             }
             if constexpr (decltype(track)::value) mx[c & 3] = fmaxf(mx[c & 3], fmaxf(s0, s1));
-            pk[c] = pack_half2(ex2(fmaf(s0, sl2, -base)), ex2(fmaf(s1, sl2, -base)));
+            // FULL sweeps evaluate POLY_SHARE of the exponentials on the FMA pipe (MUFU
+            // offload; the polynomial's 7.5e-5 relative error is below P's fp16 rounding)
+            if (FULL && POLY_EVERY > 0 && c % POLY_EVERY == POLY_EVERY - 1)
+              pk[c] = pack_half2(ex2_poly(fmaf(s0, sl2, -base)), ex2_poly(fmaf(s1, sl2, -base)));
+            else
+              pk[c] = pack_half2(ex2(fmaf(s0, sl2, -base)), ex2(fmaf(s1, sl2, -base)));
           }
           DR_TMEM_ST16(p_col + 16 * ch, pk);
         }
@@ -356,6 +426,7 @@ attn_tc_kernel(AttnArgs a) {
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.p_full[b]);
     }
+    DR_TRACE_T(3);
     float o[16], l = 0.f;
     if (nb > 0) {
       tc::mbar_wait(&sm.o_done, 0);                   // committed once, after the last P*V
@@ -370,39 +441,55 @@ attn_tc_kernel(AttnArgs a) {
 #pragma unroll
       for (int d = 0; d < 16; ++d) o[d] = 0.f;
     }
-    // ---- merge the key halves: rank 1 ships (m, l, o) rows to rank 0 through DSMEM
+    DR_TRACE_T(8);
+    DR_TRACE_AT(10, crank);
+    // ---- merge the key halves: rank 1 ships its (m, l, o) row into rank 0's shared memory
+    // (5 vector DSMEM stores) and arrives on rank 0's mrg_full with release semantics; rank
+    // 0 acquires it.  No end-of-kernel cluster barrier: rank 1 may retire at once, rank 0
+    // (the only CTA whose shared memory is accessed remotely) outlives the stores it waits on.
     if (crank == 1) {
-      const uint32_t base_addr = tc::smem_u32(&sm.mrg[row][0]);
-      st_cluster_f32(base_addr, 0, m);
-      st_cluster_f32(base_addr + 4, 0, l);
+      const uint32_t dst = map_cluster(tc::smem_u32(&sm.mrg[row][0]), 0);
+      st_cluster_v4(dst, m, l, 0.f, 0.f);
 #pragma unroll
-      for (int d = 0; d < 16; ++d) st_cluster_f32(base_addr + 8 + 4 * d, 0, o[d]);
+      for (int d = 0; d < 16; d += 4) st_cluster_v4(dst + 16 + 4 * d, o[d], o[d + 1], o[d + 2], o[d + 3]);
+      mbar_arrive_remote(map_cluster(tc::smem_u32(&sm.mrg_full), 0));
+      DR_TRACE_T(9);
+    } else {
+      DR_TRACE_T(9);
+      mbar_wait_cluster(&sm.mrg_full, 0);
     }
-    cluster_sync();
+    DR_TRACE_T(4);
     if (crank == 0 && q0 + row < a.band) {
-      const float m1 = sm.mrg[row][0], l1 = sm.mrg[row][1];
-      const float M = fmaxf(m, m1);
+      const float4* mr = reinterpret_cast<const float4*>(&sm.mrg[row][0]);
+      const float4 ml = mr[0];
+      const float M = fmaxf(m, ml.x);
       const float b = M == -INFINITY ? 0.f : M;
-      const float a0 = ex2(m - b), a1 = ex2(m1 - b);
-      const float lt = l * a0 + l1 * a1;
+      const float a0 = ex2(m - b), a1 = ex2(ml.x - b);
+      const float lt = l * a0 + ml.y * a1;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
       uint32_t outp[8];
 #pragma unroll
-      for (int d = 0; d < 8; ++d)
-        outp[d] = pack_half2((o[2 * d] * a0 + sm.mrg[row][2 + 2 * d] * a1) * inv,
-                             (o[2 * d + 1] * a0 + sm.mrg[row][3 + 2 * d] * a1) * inv);
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const float4 o1 = mr[1 + q4];
+        outp[2 * q4] = pack_half2((o[4 * q4] * a0 + o1.x * a1) * inv, (o[4 * q4 + 1] * a0 + o1.y * a1) * inv);
+        outp[2 * q4 + 1] = pack_half2((o[4 * q4 + 2] * a0 + o1.z * a1) * inv, (o[4 * q4 + 3] * a0 + o1.w * a1) * inv);
+      }
       uint4* dst = reinterpret_cast<uint4*>(a.out + ((size_t)frame * a.T + band0 + q0 + row) * C + h * DH);
       dst[0] = make_uint4(outp[0], outp[1], outp[2], outp[3]);
       dst[1] = make_uint4(outp[4], outp[5], outp[6], outp[7]);
     }
   }
-  if (warp < 2) cluster_sync();                        // every thread joins the merge barrier
   tc::fence_before();
   __syncthreads();
+  DR_TRACE_T(5);
   if (warp == 1) tc::tmem_dealloc<TM_COLS>(tbase);
 }
 
 }  // namespace
+
+#ifdef DR_TRACE
+void trace_snapshot(cudaStream_t s, int n_cta);
+#endif
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
   static bool init = false;
@@ -421,6 +508,35 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     launch_pdl(attn_tc_kernel<true>, grid, dim3(THREADS), smem, s, a);
   else
     launch_pdl(attn_tc_kernel<false>, grid, dim3(THREADS), smem, s, a);
+#ifdef DR_TRACE
+  trace_snapshot(s, (int)(grid.x * grid.y * grid.z));
+#endif
 }
 
 }  // namespace dr
+
+#ifdef DR_TRACE
+// Diagnostic build only: launch_attention() snapshots g_trace after each of the first 16
+// launches (synchronising the stream); this returns launch `idx`'s per-CTA stamps.
+#include <vector>
+namespace dr {
+std::vector<std::vector<unsigned long long>>& trace_store() {
+  static std::vector<std::vector<unsigned long long>> v;
+  return v;
+}
+void trace_snapshot(cudaStream_t s, int n_cta) {
+  if (trace_store().size() >= 16) return;
+  cudaStreamSynchronize(s);
+  std::vector<unsigned long long> h((size_t)std::min(n_cta, TRACE_CTAS) * 16);
+  cudaMemcpyFromSymbol(h.data(), g_trace, h.size() * sizeof(unsigned long long));
+  trace_store().push_back(std::move(h));
+}
+}  // namespace dr
+extern "C" int dr_debug_attn_trace(int idx, unsigned long long* host, int n) {
+  auto& v = dr::trace_store();
+  if (idx < 0 || idx >= (int)v.size()) return -1;
+  const int k = std::min(n, (int)v[idx].size());
+  for (int i = 0; i < k; ++i) host[i] = v[idx][i];
+  return k;
+}
+#endif
