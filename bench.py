@@ -33,7 +33,6 @@ import os
 import statistics
 import subprocess
 import sys
-import tempfile
 import time
 from pathlib import Path
 
@@ -97,6 +96,13 @@ def stage_flops(cfg):
     }
 
 
+def stage_exps(cfg):
+    """Softmax exponentials per frame per attention launch (dense, all keys)."""
+    T, g = cfg.tokens, cfg.temporal_groups
+    tg = T // g
+    return {"attn_spatial": cfg.heads * T * T, "attn_temporal": cfg.heads * g * tg * 3 * tg}
+
+
 def frame_flops_reference(cfg):
     """Reference FlopCounterMode count per frame: the forward's dense
     contractions; attention counts QK^T and PV, linear layers once."""
@@ -133,43 +139,62 @@ def peaks():
 
 # ---------------------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle-reason sampler running DURING the timed region: an NVML thread
+    polling every ~2 ms (the batch-1 timed region is tens of ms, too short for the
+    100 ms floor of `nvidia-smi -lms`); falls back to one nvidia-smi query."""
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
-    def __init__(self, index):
-        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    def __init__(self, index, period_s=0.002):
+        import threading
+        self.rows, self.max_mhz, self.nvml = [], None, None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=self.file, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.nvml = (pynvml, h)
         except Exception:
-            self.proc = None
+            self.nvml = None
+        self.index = index
+        self.stop_ev = threading.Event()
+        self.thread = threading.Thread(target=self._run, args=(period_s,), daemon=True)
+        self.thread.start()
+
+    def _run(self, period_s):
+        if self.nvml is None:
+            return
+        pynvml, h = self.nvml
+        bits = {k: getattr(pynvml, v, 0) for k, v in self.REASONS.items()}
+        while not self.stop_ev.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), {k for k, b in bits.items() if rs & b}))
+            except Exception:
+                pass
+            self.stop_ev.wait(period_s)
 
     def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.file.flush()
-        rows = []
-        for line in Path(self.file.name).read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                rows.append(parts)
-        os.unlink(self.file.name)
-        if not rows:
-            return None
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "samples": len(rows), "reasons": reasons}
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
+        if not self.rows:
+            try:
+                q = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                    "--query-gpu=clocks.sm,clocks.max.sm",
+                                    "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=10).stdout.split(",")
+                return {"sm_mhz": float(q[0]), "sm_max_mhz": float(q[1]), "samples": 1,
+                        "reasons": [], "source": "nvidia-smi after the timed region"}
+            except Exception:
+                return None
+        sm = [r[0] for r in self.rows]
+        reasons = sorted(set().union(*(r[1] for r in self.rows)))
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm),
+                "sm_max_mhz": self.max_mhz, "samples": len(self.rows), "reasons": reasons,
+                "source": "NVML every 2 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------- CPU arm
@@ -340,13 +365,13 @@ def run_ours(args):
         return graphs[(k2 % P, k2 % 3) if carried else k2 % P]
 
     kernels = eng.kernels_per_forward()
-    clocks = Clocks(local)
     with torch.cuda.stream(stream):
         for k in range(args.warmup):
             graph_for(k).replay()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         barrier()
+        clocks = Clocks(local)
         w0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
@@ -355,8 +380,8 @@ def run_ours(args):
             ev[k][1].record(stream)
         barrier()
         wall = time.perf_counter() - w0
+        clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    clk = clocks.stop()
     total_ms = allmax(sum(step_ms))
     value = world * args.steps * B / (total_ms / 1e3)
     p50 = statistics.median(step_ms)
@@ -402,6 +427,16 @@ def run_ours(args):
                     "frac": round(ach / pk["bf16_tflops"], 4), "traffic": None,
                     "peak_source": f"{pk_src} dense bf16 burst (MEASURED_PEAKS.json)",
                     "mean_launch_ms": round(mean_ms, 5)}
+            if dom.startswith("attn_"):
+                # head_dim 16: the binding unit is MUFU ex2 (16/clk/SM measured,
+                # profiles/r01/pipe_microbench_b200.txt), not the tensor pipe
+                exps = stage_exps(cfg)[dom] * B
+                clk_hz = 1e6 * (clk["sm_mhz"] if clk and clk.get("sm_mhz") else pk.get("sm_max_mhz", 1965.0))
+                mufu_peak = 16 * 148 * clk_hz
+                roof["mufu"] = {"exps_per_launch": exps, "achieved_gexp_s": round(exps / (mean_ms * 1e-3) / 1e9, 1),
+                                "peak_gexp_s": round(mufu_peak / 1e9, 1),
+                                "frac": round(exps / (mean_ms * 1e-3) / mufu_peak, 4),
+                                "note": "exponentials executed on MUFU + FMA-polynomial pipes"}
     path_tflops = frame_flops_reference(cfg) * B * args.steps / (sum(step_ms) * 1e-3) / 1e12
 
     # e2e through the reference-facing C-ABI call with host buffers (u8 API)
