@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,9 +56,32 @@ void pack_frags(const std::vector<float>& W, int N, int K, std::vector<uint2>& o
       }
 }
 
+// tcgen05 operand image of W (N x K row-major): K-atoms of 64 halves; atom kb = N rows of
+// 128 B, 16-byte chunk c of row n stored at chunk c ^ (n & 7) (the UMMA / TMA 128-byte
+// swizzle on a 1024-byte aligned base).
+void pack_sw128(const float* W, int N, int K, std::vector<uint8_t>& out) {
+  const size_t base = out.size();
+  out.resize(base + (size_t)N * K * 2);
+  for (int kb = 0; kb < K / 64; ++kb)
+    for (int n = 0; n < N; ++n)
+      for (int c = 0; c < 8; ++c)
+        for (int j = 0; j < 8; ++j) {
+          const __half h = __float2half_rn(W[(size_t)n * K + kb * 64 + c * 8 + j]);
+          const size_t off = base + ((size_t)kb * N + n) * 128 + ((c ^ (n & 7)) * 16) + j * 2;
+          std::memcpy(&out[off], &h, 2);
+        }
+}
+
+void append_f32(const float* v, int64_t n, std::vector<uint8_t>& out) {
+  const size_t o = out.size();
+  out.resize(o + (size_t)n * 4);
+  std::memcpy(&out[o], v, (size_t)n * 4);
+}
+
 struct Blk {
   size_t ln1_w, ln1_b, bqkv, bo, ln2_w, ln2_b, b1, b2;      // float offsets
   size_t wqkv, wo, w1, w2;                                  // frag offsets
+  size_t img;                                               // tcgen05 image byte offset
   bool temporal;
 };
 
@@ -130,6 +154,8 @@ struct dr_engine {
   size_t we = 0, be = 0, bv2p = 0, bd0 = 0, bd2 = 0;
   uint2* frags = nullptr;
   float* fparams = nullptr;
+  uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We, then 64 KB per block
+  bool token_hmma = false;           // DR_TOKEN_HMMA=1: mma.sync token chains (A/B only)
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
   size_t wtc_d2 = 0, wtc_v2p = 0;    // byte offsets of the decode.2 / Vec2Patch images
@@ -173,10 +199,16 @@ struct dr_engine {
     w.ln2_w = fparams + b.ln2_w; w.ln2_b = fparams + b.ln2_b;
     w.w1 = frags + b.w1; w.b1 = fparams + b.b1;
     w.w2 = frags + b.w2; w.b2 = fparams + b.b2;
+    w.img = timg + b.img;
     return w;
   }
 
   size_t frame_px() const { return (size_t)H * W; }
+
+  void launch_tok(int mode, const TokenArgs& a, cudaStream_t s) const {
+    if (token_hmma) launch_token(mode, a, s);
+    else launch_token_tc(mode, a, s);
+  }
 
   // Slot K/V cache: KV_ENTRIES entries (3 per memory stream: slot0, slot1, new slot),
   // each n_temporal x {K, V} images of [cap][HEADS][T][DH] fp16, keyed by the slot
@@ -357,6 +389,9 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
 
   std::vector<uint2> fr;
   std::vector<float> fp;
+  std::vector<uint8_t> ti;
+  pack_sw128(weights[0], c, 4 * p * p, ti);                    // We: 64 x 256
+  append_f32(weights[1], numels[1], ti);                       // be
   auto vec = [&](int idx) { return std::vector<float>(weights[idx], weights[idx] + numels[idx]); };
   auto addf = [&](int idx) { size_t o = fp.size(); fp.insert(fp.end(), weights[idx], weights[idx] + numels[idx]); return o; };
 
@@ -381,6 +416,19 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
     b.b1 = addf(base + 13);
     b.w2 = fr.size(); pack_frags(vec(base + 14), c, 2 * c, fr);
     b.b2 = addf(base + 15);
+    b.img = ti.size();
+    pack_sw128(wqkv.data(), 3 * c, c, ti);
+    pack_sw128(weights[base + 8], c, c, ti);
+    pack_sw128(weights[base + 12], 2 * c, c, ti);
+    pack_sw128(weights[base + 14], c, 2 * c, ti);
+    {   // fp32 params: ln1_w ln1_b bq bk bv bo ln2_w ln2_b b1 b2 (token_tc.cu Prm)
+      const int order[10] = {0, 1, 3, 5, 7, 9, 10, 11, 13, 15};
+      for (int oi : order) append_f32(weights[base + oi], numels[base + oi], ti);
+    }
+    if (ti.size() - b.img != token_tc_block_image_bytes()) {
+      dr_destroy(e);
+      return fail(DR_ERR_CONFIG, "internal: token image size mismatch");
+    }
     if (b.temporal) e->n_temporal++;
     if (e->n_temporal > MAX_TEMPORAL) {
       dr_destroy(e);
@@ -417,14 +465,20 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
 
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
   e->feather_r = (int)(fw.size() / 2);
+  {
+    const char* ev = std::getenv("DR_TOKEN_HMMA");
+    e->token_hmma = ev && ev[0] == '1';
+  }
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
   if (cudaMalloc(&e->frags, fr.size() * sizeof(uint2)) != cudaSuccess ||
       cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&e->feather_w, fw.size() * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&e->wtc, tcimg.size() * 2) != cudaSuccess)
+      cudaMalloc(&e->wtc, tcimg.size() * 2) != cudaSuccess ||
+      cudaMalloc(&e->timg, ti.size()) != cudaSuccess)
     return cleanup(fail(DR_ERR_CUDA, "cudaMalloc of weights failed"));
-  if (cudaMemcpy(e->wtc, tcimg.data(), tcimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
+  if (cudaMemcpy(e->wtc, tcimg.data(), tcimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(e->timg, ti.data(), ti.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return cleanup(fail(DR_ERR_CUDA, "weight upload failed"));
   if (cudaMemcpy(e->frags, fr.data(), fr.size() * sizeof(uint2), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(e->fparams, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -442,6 +496,7 @@ void dr_destroy(dr_engine* e) {
   cudaFree(e->fparams);
   cudaFree(e->feather_w);
   cudaFree(e->wtc);
+  cudaFree(e->timg);
   cudaFree(e->h_rgb);
   cudaFree(e->h_m0);
   cudaFree(e->h_out);
@@ -557,7 +612,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
         a.resid_in = sp[sl];
         a.next = e->block_w(i);
         a.k = e->kv_ptr(ent[sl], ti, 0); a.v = e->kv_ptr(ent[sl], ti, 1);
-        launch_token(TOK_SLOTKV, a, s);
+        e->launch_tok(TOK_SLOTKV, a, s);
         ++n_slotkv;
         e->mark(1, s);
         ++ti;
@@ -569,12 +624,12 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   {
     TokenArgs a{};
     a.n_tok = B * T; a.T = T;
-    a.xin = e->xin; a.we = e->frags + e->we; a.be = e->fparams + e->be;
+    a.xin = e->xin; a.we = e->frags + e->we; a.be = e->fparams + e->be; a.we_img = e->timg;
     a.kin = 4 * e->cfg.patch * e->cfg.patch;
     a.resid_out = e->resid[0];
     a.has_next = 1; a.next = e->block_w(0);
     a.q = e->q; a.k = e->k; a.v = e->v;
-    launch_token(TOK_EMBED, a, s);
+    e->launch_tok(TOK_EMBED, a, s);
     e->mark(2, s);
   }
 
@@ -628,7 +683,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
       }
       a.n_kv = tj;
     }
-    launch_token(TOK_POST, a, s);
+    e->launch_tok(TOK_POST, a, s);
     if (en >= 0) {
       for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // alias
       e->kv_set(en, io->new_slot, B, true);

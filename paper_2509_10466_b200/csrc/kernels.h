@@ -19,14 +19,19 @@ struct BlockW {
   const float* ln2_w; const float* ln2_b;
   const uint2* w1;   const float* b1;     // N=128, K=64  : [16][4][32]
   const uint2* w2;   const float* b2;     // N=64,  K=128 : [8][8][32]
+  // tcgen05 image (token_tc.cu): K-major 128B-swizzled fp16, [Wqkv 192][Wo 64][W1 128]
+  // [W2 2 K-atoms x 64] rows of 128 B, 64 KB per block
+  const uint8_t* img;
 };
 
 struct TokenArgs {
   int n_tok;              // tokens in this launch (frames * T)
+  int tile_rows;          // tcgen05 path: tokens per CTA (32/64/128; 0 = pick by n_tok)
   int T;                  // tokens per frame
   // mode EMBED
   const __half* xin;      // [n_tok][kin] fp16 patch-major network input
   const uint2* we; const float* be; int kin;
+  const uint8_t* we_img;  // tcgen05 image of We: 4 K-atoms x 64 rows x 128 B
   // mode POST (out-proj + residual + LN2 + FFN + residual)
   const __half* attn;     // [n_tok][64] fp16 attention output (heads concatenated)
   const float* resid_in;  // [n_tok][64] fp32 residual stream (also SLOTKV input)
@@ -49,7 +54,10 @@ constexpr int MAX_TEMPORAL = 4;
 
 enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
 
-void launch_token(int mode, const TokenArgs& a, cudaStream_t s);
+void launch_token(int mode, const TokenArgs& a, cudaStream_t s);      // HMMA (mma.sync)
+void launch_token_tc(int mode, const TokenArgs& a, cudaStream_t s);   // tcgen05 + TMEM
+size_t token_tc_block_image_bytes();   // per block: weights + 704 fp32 params
+size_t token_tc_embed_image_bytes();   // We + be
 
 // ---------------------------------------------------------------- attention
 struct AttnArgs {

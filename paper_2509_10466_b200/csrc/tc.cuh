@@ -151,6 +151,12 @@ DR_DEV uint64_t sdesc_sw128(uint32_t saddr, uint32_t base_offset) {
                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                         \
                : "r"(taddr))
 DR_DEV void tmem_ld16(uint32_t taddr, uint32_t* r) { DR_TMEM_LD16(taddr, r); }
+DR_DEV void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 DR_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 DR_DEV bool elect_one() {

@@ -1,0 +1,446 @@
+// Token-wise GEMM chains of the DSTT blocks on the 5th-gen tensor cores (tcgen05 + TMEM),
+// reference dstt.py:102-150 (MultiHeadAttention projections, _FeedForward, pre-norm
+// residual blocks), :185-195 (temporal block), :246-254 (patch embed).
+//
+// Every GEMM is D[128 x N] (TMEM, fp32) = A[128 x K] (smem, fp16, K-major 128B-swizzled)
+// x W^T (smem, fp16, pre-swizzled K-major image bulk-copied once with the block's fp32
+// biases / LayerNorm affine), issued by one elected lane of warp 0.  The chain between
+// GEMMs never leaves the SM:
+//   TOK_EMBED : x = xin We^T + be                                         (dstt.py:246-254)
+//   TOK_POST  : x = r + attn Wo^T + bo ; x += W2 gelu(W1 LN2(x) + b1) + b2  (:146-149)
+//   then, next block:  [q|k|v] = LN1'(x) Wqkv'^T + b                      (:141-142, :106-117)
+//   last block:        tok16 = fp16(x) on the padded Vec2Patch grid, and for every
+//                      temporal block j: [k|v]_j = LN1_j(x) Wkv_j^T + b    (:188-190, slot K/V)
+//   TOK_SLOTKV: [k|v] = LN1(slot) Wkv^T + b for a memory slot             (:188-190)
+//
+// Thread layout: 32 warps; warp w reads TMEM lane quarter w % 4 (token row 32*(w%4) + lane,
+// the tcgen05.ld restriction) and column group w / 4 (8 of the 64 channels, 16 of the 128
+// FFN columns, 24 of the 192 q|k|v columns), so the fp32 epilogues (bias, residual,
+// LayerNorm, GELU) run 8 threads per token row.  A CTA owns `tile_rows` = 128, 64 or 32
+// tokens (MMA M is always 128; rows past the tile are never read): at batch 1 a 512^2 frame
+// (4096 tokens) runs as 128 CTAs of 32 tokens, the idle lane quarters exit after the
+// prologue and the active warps synchronise on a named barrier.  The path is latency-bound
+// at batch 1 (a chain of 4 dependent GEMMs per tile) and tensor/L2-bound at batch 64.
+// TMEM: 256 columns (D1 @0 N=64, D2 @64 N=128, D3 @0 N=64, D4 @64 N=192).
+#include <cuda.h>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+#define DR_DEV_HOST_INLINE __host__ __device__ __forceinline__
+
+namespace dr {
+
+namespace {
+
+constexpr int M = 128;
+constexpr int CG = 8;                        // column groups per token row
+constexpr int THREADS = 32 * 4 * CG;         // 1024
+constexpr int ATOM_A = M * 128;              // one 128-row x 64-half swizzled K-atom (16 KB)
+constexpr int TM_COLS = 256;
+constexpr int PRM_BYTES = 704 * 4;           // fp32 params of one block (Prm)
+
+// Smem offsets (bytes, from a 1024-aligned base).  `big` holds the 128 x 256 xin tile
+// (EMBED) or the 128 x 128 GELU output (POST).
+constexpr int OFF_A = 0;
+constexpr int OFF_BIG = ATOM_A;
+
+struct Ctl {
+  float red[2][CG][M];                       // LayerNorm partial sums per column group
+  uint64_t w_bar, mma_bar;
+  uint32_t tmem_base;
+};
+
+struct Prm {                                 // float offsets inside a params block
+  static constexpr int ln1_w = 0, ln1_b = 64, bqkv = 128, bo = 320, ln2_w = 384, ln2_b = 448,
+                       b1 = 512, b2 = 640;
+};
+
+// Weight image of one block (bytes): [Wqkv 192 rows][Wo 64][W1 128][W2 2 atoms x 64]
+// [fp32 params, PRM_BYTES].
+constexpr int IMG_QKV = 0, IMG_O = 192 * 128, IMG_1 = IMG_O + 64 * 128, IMG_2 = IMG_1 + 128 * 128;
+constexpr int IMG_PRM = IMG_2 + 2 * 64 * 128;
+constexpr int IMG_BYTES = IMG_PRM + PRM_BYTES;
+constexpr int IMG_KV = IMG_QKV + 64 * 128;   // k|v rows of Wqkv (128 rows)
+constexpr int WE_BYTES = 4 * 64 * 128;       // embed image: We, then be (64 fp32)
+
+DR_DEV uint32_t sw128(int row, int chunk) {  // byte offset of 16-B chunk in a K-atom
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+// D[tmem col] (+)= A (atoms of 128 rows) x B (atoms of N rows)^T over `atoms` x 64 K.
+DR_DEV void gemm_issue(uint32_t d, uint32_t a_addr, uint32_t b_addr, int n, int atoms,
+                       uint64_t* bar) {
+  const uint32_t idesc = tc::idesc_f16(M, n);
+  const uint64_t ad = tc::sdesc_sw128(a_addr, 0), bd = tc::sdesc_sw128(b_addr, 0);
+  for (int kb = 0; kb < atoms; ++kb)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+      tc::mma_f16_warp(d, ad + (uint64_t)(kb * (ATOM_A >> 4) + 2 * ks),
+                       bd + (uint64_t)(kb * (n * 128 >> 4) + 2 * ks), idesc, (kb | ks) != 0);
+  tc::mma_commit_warp(bar);
+}
+
+struct Thr {
+  int warp, row, cg, n;                      // token row in tile, column group, token index
+  int f, tk;                                 // frame, token within frame
+  int nact;                                  // threads of the active warps (CG x tile rows)
+  uint32_t lane_base;                        // TMEM lane field of this warp's quarter
+  bool valid;
+};
+
+// Barrier over the active warps only (named barrier 1); the idle lane quarters of a small
+// tile exit after the prologue.
+DR_DEV void sync_act(const Thr& t) { asm volatile("bar.sync 1, %0;\n" :: "r"(t.nact) : "memory"); }
+
+// Generic-proxy smem writes -> visible to the tensor core; TMEM reads ordered before the
+// next MMA; then one barrier.
+DR_DEV void publish(const Thr& t) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc::fence_before();
+  sync_act(t);
+  tc::fence_after();
+}
+
+DR_DEV void wait_mma(Ctl& ctl, uint32_t& phase) {
+  tc::mbar_wait(&ctl.mma_bar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+}
+
+template <int N>
+DR_DEV void tmem_row(uint32_t tbase, const Thr& t, int col, float (&v)[N]) {
+  static_assert(N == 8 || N == 16, "");
+  uint32_t r[N];
+  if constexpr (N == 16) tc::tmem_ld16(tbase + t.lane_base + (uint32_t)col, r);
+  else tc::tmem_ld8(tbase + t.lane_base + (uint32_t)col, r);
+  tc::tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+DR_DEV uint4 pack8(const float* v, const float* bias) {
+  return make_uint4(pack_half2(v[0] + bias[0], v[1] + bias[1]), pack_half2(v[2] + bias[2], v[3] + bias[3]),
+                    pack_half2(v[4] + bias[4], v[5] + bias[5]), pack_half2(v[6] + bias[6], v[7] + bias[7]));
+}
+
+// Row LayerNorm (eps 1e-5, biased variance) over 64 channels split in CG groups of 8.
+// Writes this thread's 8 normalised values (one fp16 chunk) into the A atom.
+DR_DEV void layer_norm_to_a(const float (&x)[8], const float* w, const float* b, uint8_t* sa,
+                            Ctl& ctl, const Thr& t) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  ctl.red[0][t.cg][t.row] = s;
+  sync_act(t);
+  float mu = 0.f;
+#pragma unroll
+  for (int g = 0; g < CG; ++g) mu += ctl.red[0][g][t.row];
+  mu *= 1.f / 64.f;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float d = x[i] - mu;
+    q += d * d;
+  }
+  ctl.red[1][t.cg][t.row] = q;
+  sync_act(t);
+  float var = 0.f;
+#pragma unroll
+  for (int g = 0; g < CG; ++g) var += ctl.red[1][g][t.row];
+  const float rs = rsqrtf(var * (1.f / 64.f) + 1e-5f);
+  const int c = 8 * t.cg;
+  float y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) y[i] = (x[i] - mu) * rs * w[c + i];
+  *reinterpret_cast<uint4*>(sa + sw128(t.row, t.cg)) = pack8(y, b + c);
+}
+
+// One 8-column chunk (half a head of q, k or v) + bias -> fp16 head-major
+// [frame][head][T][16] with the UMMA 32-byte swizzle the attention kernel's bulk copies
+// expect (chunk c of token t at c ^ ((t >> 2) & 1)).
+DR_DEV void store_chunk(const float (&v)[8], const float* bias, __half* dst, int T, const Thr& t,
+                        int h, int c) {
+  if (!t.valid) return;
+  uint4* r = reinterpret_cast<uint4*>(dst + ((size_t)(t.f * HEADS + h) * T + t.tk) * DH);
+  r[c ^ ((t.tk >> 2) & 1)] = pack8(v, bias);
+}
+
+// Smem layout after the activation tiles: weight images (1024-aligned), then the fp32
+// params blocks (current block, then next block or one per slot-K/V block).
+struct WLayout {
+  int w_bytes;      // weight images
+  int n_nx;         // params blocks after the current one
+  DR_DEV_HOST_INLINE int total() const { return w_bytes + (1 + n_nx) * PRM_BYTES; }
+};
+template <int MODE>
+DR_DEV_HOST_INLINE WLayout wlayout(const TokenArgs& a) {
+  WLayout l;
+  if (MODE == TOK_EMBED) { l.w_bytes = WE_BYTES + 192 * 128; l.n_nx = 1; }
+  else if (MODE == TOK_POST) {
+    l.w_bytes = (IMG_PRM - IMG_O) + (a.has_next ? 192 * 128 : a.n_kv * 128 * 128);
+    l.n_nx = a.has_next ? 1 : a.n_kv;
+  } else { l.w_bytes = 128 * 128; l.n_nx = 1; }
+  return l;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31;
+  Thr t;
+  t.warp = threadIdx.x >> 5;
+  t.row = 32 * (t.warp & 3) + lane;
+  t.cg = t.warp >> 2;
+  t.lane_base = (uint32_t)(32 * (t.warp & 3)) << 16;
+  const int rows = a.tile_rows;                           // 32, 64 or 128 tokens per CTA
+  t.n = blockIdx.x * rows + t.row;
+  t.nact = CG * rows;
+  t.valid = t.row < rows && t.n < a.n_tok;
+  t.f = t.n / a.T;
+  t.tk = t.n - t.f * a.T;
+  uint8_t* sa = sm + OFF_A;
+  uint8_t* big = sm + OFF_BIG;
+  constexpr int big_bytes = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
+  uint8_t* sw = big + big_bytes;                          // weight images
+  const WLayout L = wlayout<MODE>(a);
+  // params: EMBED keeps `be` (64 floats) in the current-params slot
+  const float* prm = reinterpret_cast<const float*>(sw + L.w_bytes);
+  auto prm_nx = [&](int j) { return prm + (1 + j) * (PRM_BYTES / 4); };
+  Ctl& ctl = *reinterpret_cast<Ctl*>(sw + L.total());
+
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&ctl.w_bar, 1);
+    tc::mbar_init(&ctl.mma_bar, 1);
+    tc::fence_barrier_init();
+  }
+  if (t.warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = ctl.tmem_base;
+  if (t.row >= rows) return;                               // idle lane quarter (small tiles)
+
+  if (threadIdx.x == 0) {                                  // constant weights: before pdl_wait
+    uint8_t* pc = sw + L.w_bytes;
+    if constexpr (MODE == TOK_EMBED) {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + 256 + PRM_BYTES));
+      tc::bulk_load(sw, a.we_img, WE_BYTES, &ctl.w_bar);
+      tc::bulk_load(sw + WE_BYTES, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
+      tc::bulk_load(pc, a.we_img + WE_BYTES, 256, &ctl.w_bar);
+      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+    } else if constexpr (MODE == TOK_POST) {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)L.total());
+      tc::bulk_load(sw, a.cur.img + IMG_O, IMG_PRM - IMG_O, &ctl.w_bar);
+      tc::bulk_load(pc, a.cur.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+      uint8_t* d = sw + (IMG_PRM - IMG_O);
+      if (a.has_next) {
+        tc::bulk_load(d, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
+        tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+      } else {
+        for (int j = 0; j < a.n_kv; ++j) {
+          tc::bulk_load(d + j * 128 * 128, a.kv_w[j].img + IMG_KV, 128 * 128, &ctl.w_bar);
+          tc::bulk_load(pc + (1 + j) * PRM_BYTES, a.kv_w[j].img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+        }
+      }
+    } else {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + PRM_BYTES));
+      tc::bulk_load(sw, a.next.img + IMG_KV, 128 * 128, &ctl.w_bar);
+      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+    }
+  }
+  pdl_wait();
+
+  uint32_t phase = 0;
+  float x[8];                                              // residual: 8 of 64 channels
+  const int c0 = 8 * t.cg;
+  auto store_resid = [&]() {
+    if (!t.valid) return;
+    float4* dst = reinterpret_cast<float4*>(a.resid_out + (size_t)t.n * C + c0);
+    dst[0] = make_float4(x[0], x[1], x[2], x[3]);
+    dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+  };
+  auto add_d64 = [&](int col, const float* bias) {        // x += D[:, col + c0 .. +8] + bias
+    float v[8];
+    tmem_row<8>(tbase, t, col + c0, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += v[i] + bias[c0 + i];
+  };
+
+  // ------------------------------------------------------------ stage 0: first GEMM input
+  if constexpr (MODE == TOK_EMBED) {
+    // xin row: 256 halves = 4 K-atoms of 8 chunks; this thread copies chunks 4cg..4cg+3
+    const uint4* src = reinterpret_cast<const uint4*>(a.xin + (size_t)t.n * a.kin) + 4 * t.cg;
+    uint4 r[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) r[c] = t.valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ch = 4 * t.cg + c;
+      *reinterpret_cast<uint4*>(big + (ch >> 3) * ATOM_A + sw128(t.row, ch & 7)) = r[c];
+    }
+    publish(t);
+    tc::mbar_wait(&ctl.w_bar, 0);
+    tc::fence_after();
+    if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(big), tc::smem_u32(sw), 64, 4, &ctl.mma_bar);
+    wait_mma(ctl, phase);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    add_d64(0, prm);
+    store_resid();
+  } else {
+    const float4* src = reinterpret_cast<const float4*>(a.resid_in + (size_t)t.n * C + c0);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 f0 = t.valid ? __ldg(src) : z, f1 = t.valid ? __ldg(src + 1) : z;
+    x[0] = f0.x; x[1] = f0.y; x[2] = f0.z; x[3] = f0.w;
+    x[4] = f1.x; x[5] = f1.y; x[6] = f1.z; x[7] = f1.w;
+  }
+
+  if constexpr (MODE == TOK_POST) {
+    // ---------------------------------------------------------- out-proj + residual
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(a.attn + (size_t)t.n * C) + t.cg;
+      const uint4 r0 = t.valid ? __ldg(src) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(sa + sw128(t.row, t.cg)) = r0;
+    }
+    publish(t);
+    tc::mbar_wait(&ctl.w_bar, 0);
+    tc::fence_after();
+    const uint32_t wo = tc::smem_u32(sw), w1 = wo + (IMG_1 - IMG_O), w2 = wo + (IMG_2 - IMG_O);
+    if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(sa), wo, 64, 1, &ctl.mma_bar);
+    wait_mma(ctl, phase);
+    add_d64(0, prm + Prm::bo);
+    // ---------------------------------------------------------- LN2 -> FFN1 -> GELU
+    layer_norm_to_a(x, prm + Prm::ln2_w, prm + Prm::ln2_b, sa, ctl, t);
+    publish(t);
+    if (t.warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), w1, 128, 1, &ctl.mma_bar);
+    wait_mma(ctl, phase);
+    {
+      const int col = 16 * t.cg;                           // FFN columns [16cg, 16cg+16)
+      float v[16];
+      tmem_row<16>(tbase, t, 64 + col, v);
+      const float* b1 = prm + Prm::b1 + col;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = gelu_erf(v[i] + b1[i]);
+      const float zero[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint8_t* atom = big + (col >> 6) * ATOM_A;
+      const int ch = (col & 63) >> 3;
+      *reinterpret_cast<uint4*>(atom + sw128(t.row, ch)) = pack8(v, zero);
+      *reinterpret_cast<uint4*>(atom + sw128(t.row, ch + 1)) = pack8(v + 8, zero);
+    }
+    publish(t);
+    // ---------------------------------------------------------- FFN2 + residual
+    if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(big), w2, 64, 2, &ctl.mma_bar);
+    wait_mma(ctl, phase);
+    add_d64(0, prm + Prm::b2);
+    store_resid();
+  }
+
+  // ------------------------------------------------------------ LN1' + projections
+  const uint32_t wnext = tc::smem_u32(sw) + (MODE == TOK_EMBED ? WE_BYTES
+                                            : (MODE == TOK_POST ? IMG_PRM - IMG_O : 0));
+  if constexpr (MODE == TOK_SLOTKV) {
+    tc::mbar_wait(&ctl.w_bar, 0);
+    tc::fence_after();
+  }
+  const bool qkv = MODE == TOK_EMBED || (MODE == TOK_POST && a.has_next);
+  if (qkv) {
+    const float* pn = prm_nx(0);
+    layer_norm_to_a(x, pn + Prm::ln1_w, pn + Prm::ln1_b, sa, ctl, t);
+    publish(t);
+    if (t.warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), wnext, 192, 1, &ctl.mma_bar);
+    wait_mma(ctl, phase);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {                          // 8-column chunks u = 3cg + i of 24
+      const int u = 3 * t.cg + i, p = u >> 1, which = p >> 2, h = p & 3;
+      float v[8];
+      tmem_row<8>(tbase, t, 64 + 8 * u, v);
+      __half* dst = which == 0 ? a.q : (which == 1 ? a.k : a.v);
+      store_chunk(v, pn + Prm::bqkv + 8 * u, dst, a.T, t, h, u & 1);
+    }
+  } else {
+    // k|v only: SLOTKV (one block) or the last block's slot K/V for every temporal block
+    const int n_kv = MODE == TOK_SLOTKV ? 1 : a.n_kv;
+    if constexpr (MODE == TOK_POST) {
+      if (a.tok16 && t.valid) {                            // fp16 tokens for Vec2Patch
+        const int i = t.tk / a.Cc, j = t.tk - i * a.Cc;
+        const size_t pos = ((size_t)t.f * (a.R + 2) + i + 1) * (a.Cc + 2) + j + 1;
+        const float zero[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        *reinterpret_cast<uint4*>(a.tok16 + pos * C + c0) = pack8(x, zero);
+      }
+    }
+    for (int j = 0; j < n_kv; ++j) {
+      const float* pn = prm_nx(j);
+      __half* kd = MODE == TOK_SLOTKV ? a.k : a.kv_k[j];
+      __half* vd = MODE == TOK_SLOTKV ? a.v : a.kv_v[j];
+      layer_norm_to_a(x, pn + Prm::ln1_w, pn + Prm::ln1_b, sa, ctl, t);
+      publish(t);
+      if (t.warp == 0)
+        gemm_issue(tbase + 64, tc::smem_u32(sa), wnext + j * 128 * 128, 128, 1, &ctl.mma_bar);
+      wait_mma(ctl, phase);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {                        // chunks u = 2cg + i of 16 (k|v)
+        const int u = 2 * t.cg + i, p = 4 + (u >> 1), h = p & 3;
+        float v[8];
+        tmem_row<8>(tbase, t, 64 + 8 * u, v);
+        store_chunk(v, pn + Prm::bqkv + 64 + 8 * u, p < 8 ? kd : vd, a.T, t, h, u & 1);
+      }
+    }
+  }
+  tc::fence_before();
+  sync_act(t);
+  if (t.warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
+}
+
+template <int MODE>
+int smem_bytes(const TokenArgs& a) {
+  constexpr int big = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
+  return ATOM_A + big + wlayout<MODE>(a).total() + (int)sizeof(Ctl) + 1024;
+}
+
+}  // namespace
+
+size_t token_tc_block_image_bytes() { return IMG_BYTES; }
+size_t token_tc_embed_image_bytes() { return WE_BYTES + 256; }
+
+// Tokens per CTA: the largest of 128 / 64 / 32 that still gives >= one CTA per SM.
+int token_tc_tile_rows(int n_tok, int sms) {
+  for (int r = 128; r > 32; r >>= 1)
+    if ((n_tok + r - 1) / r >= sms) return r;
+  return 32;
+}
+
+void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
+  static int sms = 0;
+  static bool init = false;
+  if (!init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int mx = 227 * 1024;
+    cudaFuncSetAttribute(token_tc_kernel<TOK_EMBED>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_tc_kernel<TOK_POST>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_tc_kernel<TOK_SLOTKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    init = true;
+  }
+  TokenArgs a = a_in;
+  if (a.tile_rows != 32 && a.tile_rows != 64 && a.tile_rows != 128)
+    a.tile_rows = token_tc_tile_rows(a.n_tok, sms);
+  dim3 grid((a.n_tok + a.tile_rows - 1) / a.tile_rows), block(THREADS);
+  switch (mode) {
+    case TOK_EMBED:
+      launch_pdl(token_tc_kernel<TOK_EMBED>, grid, block, smem_bytes<TOK_EMBED>(a), s, a);
+      break;
+    case TOK_POST:
+      launch_pdl(token_tc_kernel<TOK_POST>, grid, block, smem_bytes<TOK_POST>(a), s, a);
+      break;
+    default:
+      launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid, block, smem_bytes<TOK_SLOTKV>(a), s, a);
+      break;
+  }
+}
+
+}  // namespace dr
