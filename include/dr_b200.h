@@ -15,6 +15,11 @@
  *                                                             inpaint/base.py:52-89,
  *                                                             inpaint/dstt.py:313-326
  *   dr_mask_stage      new: dilate (masks._CROSS, masks.py:17/:193), feather, token mask
+ *   dr_display_composite  upscale2x + _composite_upscaled      pipeline.py:120-131, :203-222,
+ *                                                             _kernels.py:13-46
+ *   dr_merge_redact    merge_private_masks + redact            masks.py:128-154
+ *   dr_pack_pointcloud transplant_pointcloud / pack_pointcloud pipeline.py:147-157,
+ *                                                             _kernels.py:49-93
  *   dr_last_error      exception message of the failing call
  * Error codes map onto the reference exceptions (errors.py:4-33):
  *   DR_ERR_CONFIG -> ConfigError, DR_ERR_INPUT -> InputError,
@@ -124,6 +129,37 @@ int dr_op_conv3x3(int32_t frames, int32_t height, int32_t width, const void* in_
  * 7 decode.0, 8 decode.2+composite. */
 int dr_profile(dr_engine* e, int32_t on);
 int32_t dr_profile_read(dr_engine* e, float* ms, int32_t* kinds, int32_t cap);
+
+/* ---------------------------------------------------------------------------------------
+ * Frame byte kernels either side of the network (all device pointers, stream-ordered).
+ * ------------------------------------------------------------------------------------- */
+
+/* Display path of Pipeline.step (pipeline.py:307-314) in one pass: out (2H x 2W x C) =
+ * upscale2x(original) (pipeline.py:120-131, _kernels.py:13-46), and inside the
+ * nearest-upscaled mask either upscale2x(inpainted) (_composite_upscaled,
+ * pipeline.py:203-222) or 0 when engine_failed (fail-closed, pipeline.py:309-311).
+ * mask / inpainted may be NULL (plain upscale2x, pipeline.upscale2x).  C = 1 or 3. */
+int dr_display_composite(int32_t height, int32_t width, int32_t channels,
+                         const uint8_t* original_hwc, const uint8_t* inpainted_hwc,
+                         const uint8_t* mask_hw, int32_t engine_failed, uint8_t* out_hwc,
+                         void* stream);
+
+/* merge_private_masks + redact (masks.py:128-154): merged = OR of masks[k] over the k
+ * with private_flags[k] != 0 (device u8 [n]); redacted = rgb with the merged pixels
+ * zeroed.  merged / (rgb, redacted) may be NULL. */
+int dr_merge_redact(int32_t n_masks, int32_t height, int32_t width, const uint8_t* masks,
+                    const uint8_t* private_flags, const uint8_t* rgb_hwc, uint8_t* merged_hw,
+                    uint8_t* redacted_hwc, void* stream);
+
+/* pack_pointcloud / transplant_pointcloud (_kernels.py:49-93, pipeline.py:147-157):
+ * back-project every depth > 0 pixel in row-major order; xyz [count][3] f32, colors
+ * [count][3] u8 (capacity H*W), *count (device int) = number of points.  row_counts is
+ * device scratch of H ints.  Bit-identical to the numba kernel (float64 arithmetic,
+ * float32 store). */
+int dr_pack_pointcloud(int32_t height, int32_t width, const float* depth_hw,
+                       const uint8_t* rgb_hwc, double fx, double fy, double cx, double cy,
+                       int32_t* row_counts, float* xyz, uint8_t* colors, int32_t* count,
+                       void* stream);
 
 #ifdef __cplusplus
 }

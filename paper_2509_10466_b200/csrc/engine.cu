@@ -823,4 +823,64 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   return DR_OK;
 }
 
+// ------------------------------------------------------------------ frame byte kernels
+int dr_display_composite(int32_t height, int32_t width, int32_t channels,
+                         const uint8_t* original_hwc, const uint8_t* inpainted_hwc,
+                         const uint8_t* mask_hw, int32_t engine_failed, uint8_t* out_hwc,
+                         void* stream) {
+  if (height <= 0 || width <= 0 || !original_hwc || !out_hwc)
+    return fail(DR_ERR_INPUT, "display composite needs a non-empty raster and an output");
+  if (channels != 1 && channels != 3) return fail(DR_ERR_INPUT, "channels must be 1 or 3");
+  if (engine_failed && !mask_hw) return fail(DR_ERR_INPUT, "engine_failed needs the mask");
+  DisplayArgs a{};
+  a.height = height; a.width = width; a.channels = channels;
+  a.original = original_hwc; a.inpainted = inpainted_hwc; a.mask = mask_hw;
+  a.engine_failed = engine_failed ? 1 : 0; a.out = out_hwc;
+  launch_display(a, static_cast<cudaStream_t>(stream));
+  CUDA_TRY(cudaGetLastError());
+  return DR_OK;
+}
+
+int dr_merge_redact(int32_t n_masks, int32_t height, int32_t width, const uint8_t* masks,
+                    const uint8_t* private_flags, const uint8_t* rgb_hwc, uint8_t* merged_hw,
+                    uint8_t* redacted_hwc, void* stream) {
+  if (n_masks < 0 || height <= 0 || width <= 0)
+    return fail(DR_ERR_INPUT, "merge/redact needs n_masks >= 0 and a non-empty raster");
+  if (n_masks > 0 && (!masks || !private_flags))
+    return fail(DR_ERR_INPUT, "masks and private flags are required");
+  if ((rgb_hwc == nullptr) != (redacted_hwc == nullptr))
+    return fail(DR_ERR_INPUT, "redaction needs both the input and the output raster");
+  MergeRedactArgs a{};
+  a.n_masks = n_masks; a.height = height; a.width = width;
+  a.masks = masks; a.private_flags = private_flags;
+  a.rgb_in = rgb_hwc; a.merged = merged_hw; a.rgb_out = redacted_hwc;
+  launch_merge_redact(a, static_cast<cudaStream_t>(stream));
+  CUDA_TRY(cudaGetLastError());
+  return DR_OK;
+}
+
+int dr_pack_pointcloud(int32_t height, int32_t width, const float* depth_hw,
+                       const uint8_t* rgb_hwc, double fx, double fy, double cx, double cy,
+                       int32_t* row_counts, float* xyz, uint8_t* colors, int32_t* count,
+                       void* stream) {
+  if (height < 0 || width < 0 || !count)
+    return fail(DR_ERR_INPUT, "point cloud needs height, width >= 0 and a count");
+  if (!(fx != 0.0) || !(fy != 0.0)) return fail(DR_ERR_INPUT, "focal lengths must be nonzero");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (height == 0 || width == 0) {
+    CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
+    return DR_OK;
+  }
+  if (!depth_hw || !rgb_hwc || !row_counts || !xyz || !colors)
+    return fail(DR_ERR_INPUT, "depth, rgb, scratch and outputs are required");
+  PointCloudArgs a{};
+  a.height = height; a.width = width; a.depth = depth_hw; a.rgb = rgb_hwc;
+  a.inv_fx = 1.0 / fx; a.inv_fy = 1.0 / fy; a.cx = cx; a.cy = cy;
+  a.row_counts = row_counts; a.xyz = xyz; a.colors = colors; a.count = count;
+  launch_pointcloud(a, s);
+  CUDA_TRY(cudaGetLastError());
+  return DR_OK;
+}
+
 }  // extern "C"
+

@@ -137,4 +137,38 @@ size_t v2p_tc_weight_bytes();
 void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s);
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- frame byte kernels
+// (frame_ops.cu): display composite / upscale2x, merge + redact, point-cloud pack.
+struct DisplayArgs {
+  int height, width, channels;     // source raster; channels 1 or 3 (HWC u8)
+  const uint8_t* original;         // captured frame
+  const uint8_t* inpainted;        // engine output (or null: plain upscale)
+  const uint8_t* mask;             // [H][W] privacy mask (or null)
+  int engine_failed;               // 1: zero inside the upscaled mask
+  uint8_t* out;                    // [2H][2W][channels]
+};
+void launch_display(const DisplayArgs& a, cudaStream_t s);
+
+struct MergeRedactArgs {
+  int n_masks, height, width;
+  const uint8_t* masks;            // [n][H][W]
+  const uint8_t* private_flags;    // [n] device
+  const uint8_t* rgb_in;           // [H][W][3] or null
+  uint8_t* merged;                 // [H][W] or null
+  uint8_t* rgb_out;                // [H][W][3] or null
+};
+void launch_merge_redact(const MergeRedactArgs& a, cudaStream_t s);
+
+struct PointCloudArgs {
+  int height, width;
+  const float* depth;              // [H][W]
+  const uint8_t* rgb;              // [H][W][3]
+  double inv_fx, inv_fy, cx, cy;
+  int* row_counts;                 // [H] scratch
+  float* xyz;                      // [<= H*W][3]
+  uint8_t* colors;                 // [<= H*W][3]
+  int* count;                      // [1]
+};
+void launch_pointcloud(const PointCloudArgs& a, cudaStream_t s);
+
 }  // namespace dr

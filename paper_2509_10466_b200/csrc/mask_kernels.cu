@@ -1,19 +1,21 @@
 // Mask stage: privacy mask m0 -> dilated m1 -> feathered alpha, token validity, and the
 // packed fp16 network input, fused in ONE kernel over 16 x 64-pixel tiles.  HBM-bound
-// integer/byte work; no tensor cores.  Per tile (256 threads):
+// integer/byte work; no tensor cores.  Per tile (NT = 512 threads):
 //
 //  1. m0 bytes of the tile plus a halo of r + R pixels -> 32-pixel bit words in smem
 //     (warp ballots over coalesced byte loads; off-frame = 0)
 //  2. m1 = m0 (+) L1-ball(r) == the r-fold 3x3-cross dilation (masks.py:17, :193; SURVEY
-//     A2): per row, OR over dy of the row dilated horizontally by r-|dy| (shift/or on bit
-//     words) -- bit-exact by construction; computed on the tile plus a halo of R
+//     A2): r cross iterations on the bit words of the tile + halo (shift/or, ping-pong in
+//     smem) -- bit-exact by construction; kept on the tile plus a halo of R
 //  3. feather: alpha = max(m1, G_sigma(m1)), scipy.ndimage.gaussian_filter
 //     semantics (mode 'nearest', truncate 4): vertical then horizontal pass, each in
 //     float64 in scipy's symmetric-filter order (x[0]*w[0], then (x[-j]+x[+j])*w[j] from
 //     the outermost pair inward) and rounded to float32 between passes, so alpha is
-//     bit-identical to scipy.  Exact fast paths: alpha = 1 on m1 (the vertical/horizontal
-//     sums of a binary image never exceed 1.0f); an all-zero / all-one 25-pixel window
-//     gives 0 / the precomputed all-ones sum
+//     bit-identical to scipy.  The vertical pass reads each column's m1 bits as one
+//     bit-transposed column word (built once per column, rows clamped 'nearest'), so the
+//     (2R+1)-row window of any pixel is a funnel shift.  Exact fast paths: alpha = 1 on
+//     m1 (the vertical/horizontal sums of a binary image never exceed 1.0f); an all-zero /
+//     all-one window gives 0 / the precomputed all-ones sum
 //  4. token validity (any pixel of the patch outside m1) and the network input
 //     cat[rgb zeroed in m1, m1] in conv-weight (c, ky, kx) order (dstt.py:253, :314-316;
 //     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79)
@@ -25,18 +27,24 @@ namespace dr {
 namespace {
 
 constexpr int TH = 16, TW = 64;            // tile
+constexpr int NT = 512, NWARP = NT / 32;   // threads / warps per tile
 constexpr int MAXH = 62;                   // max halo r + R (r <= 31, R <= 31)
 constexpr int MAXR = 31;                   // 2R+1 <= 63: a column window fits a uint64
 constexpr int NW_MAX = 2 + 2 * (MAXH / 32);
 constexpr int NR_MAX = TH + 2 * MAXH;
+
+constexpr int SPAN_MAX = TW + 2 * MAXR;   // columns of the vertical pass
+constexpr int CW = 3;                      // column words: TH + 2R <= 78 rows < 96
 
 struct Smem {
   uint8_t m0[NR_MAX][NW_MAX * 32];         // m0 bytes of tile + halo (cp.async)
   float rgb[3][TH][TW];                    // f32 input tile, or u8 HWC bytes (aliased)
   uint32_t b0[NR_MAX][NW_MAX];             // m0 bits, rows y0-H.., words from xs
   uint32_t b1[TH + 2 * MAXR][NW_MAX];      // m1 bits, rows y0-R..
-  float vs[TH][TW + 2 * MAXR + 2];         // vertical feather pass
-  uint32_t vor[TH][NW_MAX], vand[TH][NW_MAX];
+  uint32_t bt[NR_MAX][NW_MAX];             // dilation ping-pong buffer
+  uint32_t col[CW][NW_MAX * 32];           // m1 column words of window pixel px: bit j =
+                                           // row y0-R+j (clamped 'nearest')
+  float vs[TH][SPAN_MAX + 2];              // vertical feather pass
   uint32_t nzm[TH][5];                     // nonzero columns of vs (+1 zero word)
   double w[2 * MAXR + 1];
   double all_ones;
@@ -49,30 +57,24 @@ DR_DEV void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(s), "l"(gmem), "r"(n));
 }
 
-DR_DEV uint32_t hdilate(uint32_t cur, uint32_t lf, uint32_t rt, int k) {
-  uint32_t hd = cur;
-  for (int s = 1; s <= k; ++s)
-    hd |= (cur << s) | (lf >> (32 - s)) | (cur >> s) | (rt << (32 - s));
-  return hd;
-}
-
-template <int P>
-__global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
+// WH = halo words per side (compile time: every word loop is shift/mask, no division)
+template <int P, int WH>
+__global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];   // keep the shared address space:
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);        // no integer round trip (LDS, not LD)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, f = blockIdx.z;
   const int r = a.radius, R = a.feather_radius;
   const int Hd = r + R;
-  const int wh = (Hd + 31) / 32;                  // halo words each side
-  const int NW = 2 + 2 * wh;
+  constexpr int wh = WH;                          // halo words each side
+  constexpr int NW = 2 + 2 * wh;
   const int xs = x0 - 32 * wh;                    // pixel of bit 0 of word 0
   const int NR0 = TH + 2 * Hd, NR1 = TH + 2 * R;
   const size_t plane = (size_t)a.H * a.W;
 
   pdl_trigger();
   if (tid == 0) sm.dirty = 0;
-  for (int i = tid; i < 2 * R + 1; i += 256) sm.w[i] = a.feather_w[i];   // constant
+  for (int i = tid; i < 2 * R + 1; i += NT) sm.w[i] = a.feather_w[i];   // constant
   pdl_wait();
 
   // 0. one async round trip for every input of the tile: m0 bytes (+halo, 4-byte
@@ -81,14 +83,14 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
     const uint8_t* m0f = a.m0 + (size_t)f * plane;
     if ((a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0) {
       const int pieces = NR0 * NW * 8;
-      for (int e = tid; e < pieces; e += 256) {
+      for (int e = tid; e < pieces; e += NT) {
         const int row = e / (NW * 8), pc = e - row * (NW * 8);
         const int y = y0 - Hd + row, x = xs + 4 * pc;
         const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
         cp_async4_zfill(&sm.m0[row][4 * pc], v ? m0f + (size_t)y * a.W + x : m0f, v);
       }
     } else {                                      // odd widths (standalone mask stage)
-      for (int e = tid; e < NR0 * NW * 32; e += 256) {
+      for (int e = tid; e < NR0 * NW * 32; e += NT) {
         const int row = e / (NW * 32), px = e - row * (NW * 32);
         const int y = y0 - Hd + row, x = xs + px;
         const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
       }
     }
     if (a.xin != nullptr && a.rgb_f32) {
-      for (int e = tid; e < 3 * TH * (TW / 4); e += 256) {
+      for (int e = tid; e < 3 * TH * (TW / 4); e += NT) {
         const int c = e / (TH * TW / 4), rem = e - c * (TH * TW / 4);
         const int ty = rem / (TW / 4), q = rem - ty * (TW / 4);
         const int y = y0 + ty, x = x0 + 4 * q;
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
       }
     } else if (a.xin != nullptr && a.rgb_u8) {
       uint8_t* dst = reinterpret_cast<uint8_t*>(&sm.rgb[0][0][0]);  // [TH][TW][3] bytes
-      for (int e = tid; e < TH * TW * 3 / 4; e += 256) {
+      for (int e = tid; e < TH * TW * 3 / 4; e += NT) {
         const int ty = e / (TW * 3 / 4), q = e - ty * (TW * 3 / 4);
         const int y = y0 + ty;
         const bool v = y < a.H && x0 + (4 * q) / 3 < a.W;
@@ -120,33 +122,49 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
   }
 
   // 1. m0 -> bits (one warp per 32-pixel word, bytes from smem)
-  for (int e = warp; e < NR0 * NW; e += 8) {
+  for (int e = warp; e < NR0 * NW; e += NWARP) {
     const int row = e / NW, w = e - row * NW;
     const uint32_t word = __ballot_sync(0xffffffffu, sm.m0[row][32 * w + lane] != 0);
     if (lane == 0) sm.b0[row][w] = word;
   }
   __syncthreads();
 
-  // 2. m1 on rows y0-R .. y0+TH+R
-  for (int e = tid; e < NR1 * NW; e += 256) {
-    const int row = e / NW, w = e - row * NW;
-    const int y = y0 - R + row;
-    uint32_t acc = 0;
-    if (y >= 0 && y < a.H) {
-      const int r0 = row + (Hd - R);              // this row in b0
-      for (int dy = -r; dy <= r; ++dy) {
-        const int yy = y + dy;
-        if (yy < 0 || yy >= a.H) continue;
-        const int k = r - (dy < 0 ? -dy : dy);
-        const uint32_t* br = sm.b0[r0 + dy];
-        acc |= hdilate(br[w], w > 0 ? br[w - 1] : 0u, w + 1 < NW ? br[w + 1] : 0u, k);
+  // 2. m1 = r iterations of the 3x3 cross (masks._CROSS) over the whole b0 window, ping-pong
+  //    through smem; neighbours outside the window read 0.  The window's halo (>= r + R rows
+  //    and >= r + R pixels each side) keeps the rows y0-R .. y0+TH+R exact; off-frame bits set
+  //    on the way never create in-frame bits a frame-clipped iteration would not (the
+  //    Manhattan path between in-frame pixels stays in the frame).  Rows / pixels outside the
+  //    frame are cleared when b1 is extracted.
+  {
+    uint32_t (*cur)[NW_MAX] = sm.b0;
+    uint32_t (*nxt)[NW_MAX] = sm.bt;
+    for (int it = 0; it < r; ++it) {
+      for (int e = tid; e < NR0 * NW; e += NT) {
+        const int row = e / NW, w = e - row * NW;
+        const uint32_t c = cur[row][w];
+        const uint32_t up = row > 0 ? cur[row - 1][w] : 0u;
+        const uint32_t dn = row + 1 < NR0 ? cur[row + 1][w] : 0u;
+        const uint32_t lf = w > 0 ? cur[row][w - 1] : 0u;
+        const uint32_t rt = w + 1 < NW ? cur[row][w + 1] : 0u;
+        nxt[row][w] = c | up | dn | (c << 1) | (lf >> 31) | (c >> 1) | (rt << 31);
       }
-      // clear bits of pixels outside the frame
-      const int xw = xs + 32 * w;
-      if (xw < 0) acc &= xw + 32 <= 0 ? 0u : (0xffffffffu << (-xw));
-      if (xw + 32 > a.W) acc &= xw >= a.W ? 0u : (0xffffffffu >> (xw + 32 - a.W));
+      __syncthreads();
+      uint32_t (*t)[NW_MAX] = cur;
+      cur = nxt;
+      nxt = t;
     }
-    sm.b1[row][w] = acc;
+    for (int e = tid; e < NR1 * NW; e += NT) {
+      const int row = e / NW, w = e - row * NW;
+      const int y = y0 - R + row;
+      uint32_t acc = 0;
+      if (y >= 0 && y < a.H) {
+        acc = cur[row + (Hd - R)][w];
+        const int xw = xs + 32 * w;                   // clear pixels outside the frame
+        if (xw < 0) acc &= xw + 32 <= 0 ? 0u : (0xffffffffu << (-xw));
+        if (xw + 32 > a.W) acc &= xw >= a.W ? 0u : (0xffffffffu >> (xw + 32 - a.W));
+      }
+      sm.b1[row][w] = acc;
+    }
   }
   if (tid == 0 && R > 0) {                        // scipy-order sum of an all-ones window
     const double* wc = sm.w + R;
@@ -165,7 +183,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
   };
 
   // outputs: m1 bytes (+ binary alpha)
-  for (int e = tid; e < TH * TW; e += 256) {
+  for (int e = tid; e < TH * TW; e += NT) {
     const int ty = e / TW, tx = e - ty * TW;
     const int y = y0 + ty, x = x0 + tx;
     if (y >= a.H || x >= a.W) continue;
@@ -178,51 +196,55 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
   if (R > 0 && a.alpha) {
     const double* wc = sm.w + R;
     const int span = TW + 2 * R;
-    // 3a. per (tile row, b1 word): OR / AND of the 2R+1 clamped rows -> which columns
-    //     have an all-zero / all-one vertical window (exact fast paths)
-    for (int e = tid; e < TH * NW; e += 256) {
-      const int ty = e / NW, w = e - ty * NW;
-      uint32_t o = 0u, n = 0xffffffffu;
-      for (int j = -R; j <= R; ++j) {
-        int yy = y0 + ty + j;
+    const int NR1c = TH + 2 * R;
+    // 3a. column words by warp-ballot bit transposes: task (word w, 32-row chunk c); lane i
+    //     holds row y0-R+32c+i (clamped 'nearest'), ballot b yields window column 32w+b
+    for (int task = warp; task < NW * CW; task += NWARP) {
+      const int w = task % NW, c = task / NW;
+      const int j = 32 * c + lane;
+      uint32_t word = 0u;
+      if (j < NR1c) {
+        int yy = y0 - R + j;
         yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
-        const uint32_t b = sm.b1[yy - (y0 - R)][w];
-        o |= b;
-        n &= b;
+        word = sm.b1[yy - (y0 - R)][w];
       }
-      sm.vor[ty][w] = o;
-      sm.vand[ty][w] = n;
+      uint32_t mine = 0u;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t v = __ballot_sync(0xffffffffu, (word >> b) & 1u);
+        if (lane == b) mine = v;
+      }
+      sm.col[c][32 * w + lane] = mine;
     }
     __syncthreads();
-    // 3b. vertical pass (float64, scipy order) for columns x0-R .. x0+TW+R (clamped)
-    for (int e = tid; e < TH * span; e += 256) {
-      const int ty = e / span, tx = e - ty * span;
-      const int y = y0 + ty;
-      int x = x0 + tx - R;
-      x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
-      const int px = x - xs;
+    // 3b. vertical pass (float64, scipy order) for the tile rows x span columns; the
+    //     window of row ty is bits ty .. ty+2R of the column word
+    const uint64_t need = (2 * R + 1 == 64) ? ~0ull : ((1ull << (2 * R + 1)) - 1ull);
+    for (int tx = tid & 31, ty = tid >> 5; tx < span; tx += 32) {   // TH = 16 rows, NT = 512
       double acc;
-      if (y >= a.H || !((sm.vor[ty][px >> 5] >> (px & 31)) & 1u)) acc = 0.0;
-      else if ((sm.vand[ty][px >> 5] >> (px & 31)) & 1u) acc = sm.all_ones;
+      if (y0 + ty >= a.H) acc = 0.0;
       else {
-        uint64_t pat = 0;                          // bit j <-> row y - R + j
-        for (int j = 0; j <= 2 * R; ++j) {
-          int yy = y - R + j;
-          yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
-          pat |= (uint64_t)((sm.b1[yy - (y0 - R)][px >> 5] >> (px & 31)) & 1u) << j;
-        }
-        acc = __dmul_rn((double)((pat >> R) & 1u), wc[0]);
-        for (int jj = -R; jj < 0; ++jj) {
-          const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
-          acc = __dadd_rn(acc, __dmul_rn(pr, wc[jj]));
+        int x = x0 + tx - R;
+        x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
+        const int px = x - xs;
+        const uint64_t lo = (uint64_t)sm.col[0][px] | ((uint64_t)sm.col[1][px] << 32);
+        const uint64_t pat = ((lo >> ty) | (ty ? ((uint64_t)sm.col[2][px] << (64 - ty)) : 0ull)) & need;
+        if (pat == 0) acc = 0.0;
+        else if (pat == need) acc = sm.all_ones;
+        else {
+          acc = __dmul_rn((double)((pat >> R) & 1u), wc[0]);
+          for (int jj = -R; jj < 0; ++jj) {
+            const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
+            acc = __dadd_rn(acc, __dmul_rn(pr, wc[jj]));
+          }
         }
       }
       sm.vs[ty][tx] = (float)acc;
     }
     __syncthreads();
     // 3c. nonzero mask of every vertical-pass row (one ballot per 32 columns)
-    for (int e = warp; e < TH * 4; e += 8) {
-      const int ty = e >> 2, c = e & 3, tx = 32 * c + lane;
+    for (int e = warp; e < TH * 4; e += NWARP) {
+      const int ty = e >> 2, c = e & 3, tx = 32 * c + lane;   // span <= 126 < 4 words
       const bool nz = tx < span && sm.vs[ty][tx] != 0.f;
       const uint32_t m = __ballot_sync(0xffffffffu, nz);
       if (lane == 0) sm.nzm[ty][c] = m;
@@ -230,7 +252,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
     __syncthreads();
     // 3d. horizontal pass: alpha = 1 on m1, 0 where the whole window is zero, else sum.
     //     Off-frame columns of sm.vs already hold their clamped ('nearest') values.
-    for (int e = tid; e < TH * TW; e += 256) {
+    for (int e = tid; e < TH * TW; e += NT) {
       const int ty = e / TW, tx = e - ty * TW;
       const int y = y0 + ty, x = x0 + tx;
       if (y >= a.H || x >= a.W) continue;
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
   if (a.token_valid) {
     const int Cc = a.W / P, T = (a.H / P) * Cc;
     const int tr = TH / P, tcn = TW / P;
-    for (int tk = warp; tk < tr * tcn; tk += 8) {
+    for (int tk = warp; tk < tr * tcn; tk += NWARP) {
       const int ti = tk / tcn, tj = tk - ti * tcn;
       const int i = y0 / P + ti, j = x0 / P + tj;
       if (i * P >= a.H || j * P >= a.W) continue;
@@ -274,7 +296,7 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
         for (int kx = 0; kx < P; ++kx) {
           mb |= m1bit(y, xl + kx) << kx;
           const int px = xl + kx - xs, row = y - (y0 - Hd);
-          m0b |= ((sm.b0[row][px >> 5] >> (px & 31)) & 1u) << kx;
+          m0b |= (uint32_t)(sm.m0[row][px] != 0) << kx;   // raw m0 bytes (b0 is dilated in place)
         }
       }
       const bool any_unmasked = __any_sync(0xffffffffu, active && mb != ((1u << P) - 1u));
@@ -321,19 +343,27 @@ __global__ void __launch_bounds__(256) mask_fused_kernel(MaskArgs a) {
 
 }  // namespace
 
-void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
+template <int P, int WH>
+void launch_mask_t(const MaskArgs& a, cudaStream_t s, int smem) {
   static bool init = false;
-  const int smem = (int)sizeof(Smem) + 16;
   if (!init) {
-    cudaFuncSetAttribute(mask_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(mask_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mask_fused_kernel<P, WH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
   dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, a.frames);
-  if (a.patch == 4)
-    launch_pdl(mask_fused_kernel<4>, grid, dim3(256), smem, s, a);
-  else
-    launch_pdl(mask_fused_kernel<8>, grid, dim3(256), smem, s, a);
+  launch_pdl(mask_fused_kernel<P, WH>, grid, dim3(NT), smem, s, a);
+}
+
+void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
+  const int smem = (int)sizeof(Smem) + 16;
+  const int wh = (a.radius + a.feather_radius + 31) / 32;   // 0..2 halo words per side
+  if (a.patch == 4) {
+    if (wh <= 1) launch_mask_t<4, 1>(a, s, smem);
+    else launch_mask_t<4, 2>(a, s, smem);
+  } else {
+    if (wh <= 1) launch_mask_t<8, 1>(a, s, smem);
+    else launch_mask_t<8, 2>(a, s, smem);
+  }
 }
 
 }  // namespace dr

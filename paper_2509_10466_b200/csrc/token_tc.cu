@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   pdl_wait();
 
   uint32_t phase = 0;
-  float x[8];                                              // residual: 8 of 64 channels
+  float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // residual: 8 of 64 channels
   const int c0 = 8 * t.cg;
   auto store_resid = [&]() {
     if (!t.valid) return;

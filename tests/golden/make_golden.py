@@ -252,7 +252,81 @@ def gen_mask_aware() -> None:
          warm1=warm[1].numpy(), out=out.numpy(), slot=slot.numpy())
 
 
+def gen_frame_ops() -> None:
+    """Display path, mask producer and point-cloud transplant outputs of the reference
+    itself (pipeline.upscale2x / _composite_upscaled / transplant_pointcloud with their
+    numba kernels, masks.merge_private_masks / redact)."""
+    from dimreal import pipeline as ref_pipe
+    from dimreal.detection import Detection2D, PrivacyState, TrackedObject
+    from dimreal.scene import CameraIntrinsics
+    from dimreal.scene import FrameRGBD
+
+    rng = np.random.default_rng(2509)
+    out = {}
+    # upscale2x: ragged sizes, 1 and 3 channels
+    for i, (h, w, c) in enumerate([(1, 1, 3), (3, 5, 3), (7, 9, 1), (36, 64, 3), (45, 130, 3)]):
+        a = rng.integers(0, 256, size=(h, w, c) if c == 3 else (h, w), dtype=np.uint8)
+        out[f"up_in{i}"] = a
+        out[f"up_out{i}"] = ref_pipe.upscale2x(a)
+    # display composite at a display-like size (ellipse blobs + stroke near the border)
+    h, w = 90, 160
+    original = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    inpainted = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    yy, xx = np.mgrid[0:h, 0:w]
+    bits = ((yy - 40) ** 2 / 400 + (xx - 60) ** 2 / 900 < 1) | ((yy < 6) & (xx > 120))
+    bits[:, 0] |= (yy[:, 0] > 70)
+    mask = BinaryMask(bits)
+    up_orig = ref_pipe.upscale2x(original)
+    out.update(disp_original=original, disp_inpainted=inpainted, disp_mask=bits,
+               disp_out=ref_pipe._composite_upscaled(up_orig, inpainted, mask))
+    failed = up_orig.copy()
+    failed[mask.upscale_nearest(2).bits] = 0
+    out["disp_failed"] = failed
+    # merge_private_masks + redact
+    masks = rng.random((4, 24, 32)) > 0.7
+    states = [PrivacyState.PRIVATE, PrivacyState.PUBLIC, PrivacyState.PRIVATE,
+              PrivacyState.PUBLIC]
+    tracks = [TrackedObject(id=i, class_label="thing",
+                            latest=Detection2D.from_mask("thing", BinaryMask(m)), state=s)
+              for i, (m, s) in enumerate(zip(masks, states))]
+    merged = ref_masks.merge_private_masks(tracks, 32, 24)
+    rgb = rng.integers(0, 256, size=(24, 32, 3), dtype=np.uint8)
+    frame = FrameRGBD(rgb=rgb, depth=np.ones((24, 32), np.float32), frame_id=0, timestamp_ns=0)
+    out.update(mr_masks=masks, mr_private=np.array([s is PrivacyState.PRIVATE for s in states]),
+               mr_rgb=rgb, mr_merged=merged.bits, mr_redacted=ref_masks.redact(frame, merged).rgb)
+    # point clouds: random valid set, all-invalid, single principal-point pixel
+    intr = CameraIntrinsics(fx=100.0, fy=100.0, cx=32.0, cy=18.0, width=64, height=36)
+    out["pc_intr"] = np.array([intr.fx, intr.fy, intr.cx, intr.cy])
+    for i in range(3):
+        depth = (rng.random((36, 64)) * 4).astype(np.float32)
+        if i == 0:
+            depth[depth < 1.5] = 0.0
+        elif i == 1:
+            depth[:] = 0.0
+        else:
+            depth[:] = 0.0
+            depth[18, 32] = 2.0
+        rgbp = rng.integers(0, 256, size=(36, 64, 3), dtype=np.uint8)
+        cloud = ref_pipe.transplant_pointcloud(rgbp, depth, intr, frame_id=i)
+        out.update({f"pc_depth{i}": depth, f"pc_rgb{i}": rgbp, f"pc_xyz{i}": cloud.xyz,
+                    f"pc_col{i}": cloud.rgb})
+    # a larger case with a non-integer principal point
+    intr2 = CameraIntrinsics(fx=305.7, fy=304.9, cx=159.6, cy=90.3, width=320, height=180)
+    depth = (rng.random((180, 320)) * 5).astype(np.float32)
+    depth[rng.random((180, 320)) < 0.3] = 0.0
+    rgbp = rng.integers(0, 256, size=(180, 320, 3), dtype=np.uint8)
+    cloud = ref_pipe.transplant_pointcloud(rgbp, depth, intr2)
+    out.update(pc_intr3=np.array([intr2.fx, intr2.fy, intr2.cx, intr2.cy]), pc_depth3=depth,
+               pc_rgb3=rgbp, pc_xyz3=cloud.xyz, pc_col3=cloud.rgb)
+    save("frame_ops.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:                       # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_frame_ops()
     gen_masks()
     gen_attention()
     gen_vec2patch()

@@ -140,3 +140,24 @@ def test_c1_full_path_vs_reference():
     assert np.max(np.abs(res["fill"] - g["out_f16"].astype(np.float32))) < 1e-3
     assert abs(float(res["fill"].astype(np.float64).sum()) - float(g["out_sum"])) < 1e-2
     assert np.max(np.abs(res["out"] - g["comp_f16"].astype(np.float32))) < 1e-3
+
+
+# ------------------------------------------------------------------ frame byte kernels
+def test_frame_ops_oracle_vs_reference_fixtures():
+    """The numpy restatements of upscale2x / _composite_upscaled / merge+redact /
+    pack_pointcloud reproduce the reference's own outputs bit for bit."""
+    from oracle import frame_ops_oracle as F
+    g = golden("frame_ops.npz")
+    for i in range(5):
+        assert np.array_equal(F.upscale2x(g[f"up_in{i}"]), g[f"up_out{i}"]), i
+    assert np.array_equal(F.display_output(g["disp_original"], g["disp_inpainted"],
+                                           g["disp_mask"]), g["disp_out"])
+    assert np.array_equal(F.display_output(g["disp_original"], g["disp_inpainted"],
+                                           g["disp_mask"], engine_failed=True), g["disp_failed"])
+    merged = F.merge_private_masks(g["mr_masks"], g["mr_private"])
+    assert np.array_equal(merged, g["mr_merged"])
+    assert np.array_equal(F.redact(g["mr_rgb"], merged), g["mr_redacted"])
+    for i in range(4):
+        fx, fy, cx, cy = g["pc_intr3"] if i == 3 else g["pc_intr"]
+        xyz, col = F.pack_pointcloud(g[f"pc_depth{i}"], g[f"pc_rgb{i}"], fx, fy, cx, cy)
+        assert np.array_equal(xyz, g[f"pc_xyz{i}"]) and np.array_equal(col, g[f"pc_col{i}"]), i
