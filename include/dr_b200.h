@@ -104,10 +104,17 @@ int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, 
 
 /* One u8 frame through host buffers, like InpaintEngine.inpaint: copies rgb/mask in,
  * runs the path with the engine-held 2-slot memory (FIFO advanced once per call), copies
- * the composite out and synchronises.  Returns DR_ERR_INPUT if the frame is not
+ * the composite out and synchronises.  Rows that cannot change are filled from the input
+ * on the host while the GPU runs (see dr_host_d2h_bytes).  On an error return the
+ * contents of out_hwc are unspecified.  Returns DR_ERR_INPUT if the frame is not
  * redacted inside the mask, DR_ERR_NUMERIC on a non-finite network output. */
 int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
                        uint8_t* out_hwc, void* stream);
+
+/* Device->host bytes the last dr_inpaint_u8_host copied: only the rows within
+ * mask_dilate + feather radius of a masked row can differ from the input (the composite
+ * keeps the input byte where alpha = 0), so only that band is read back (+ 4 flag bytes). */
+int64_t dr_host_d2h_bytes(dr_engine* e);
 
 /* Reset the engine-held memory of dr_inpaint_u8_host to two zero slots. */
 int dr_reset_memory(dr_engine* e);
