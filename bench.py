@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C4", "C5"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--pool", type=int, default=8, help="distinct seeded frames per rank")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -62,15 +62,22 @@ def parse():
 
 
 # ---------------------------------------------------------------------------- workload
-def workload(name):
+C3_STREAMS = 8
+
+
+def workload(name, world=1):
     from paper_2509_10466_b200 import DsttConfig
-    size = {"C1": 256, "C2": 512, "C4": 1024, "C5": 512}[name]
+    size = {"C1": 256, "C2": 512, "C3": 512, "C4": 1024, "C5": 512}[name]
     cfg = DsttConfig.baseline(size, mask_dilate=5, mask_feather_sigma=3.0,
                               mask_aware_attention=(name == "C4"))
-    batch = 64 if name == "C5" else 1
-    carried = name in ("C1", "C2", "C4")
+    # C3: stream s runs on GPU s mod n; the co-resident streams of a GPU are one batch
+    # with per-stream memory slots ([B][T][C])
+    batch = {"C5": 64, "C3": max(1, C3_STREAMS // world)}.get(name, 1)
+    carried = name in ("C1", "C2", "C3", "C4")
     desc = {"C1": "C1: 1x3x256^2 single frame, r=5, sigma=3",
             "C2": "C2: batch-1 real-time 1x3x512^2, r=5, sigma=3, memory carried",
+            "C3": f"C3: {C3_STREAMS} video streams 3x512^2 (translating canvas, jittering "
+                  "ellipse), streams batched per GPU with per-stream memory",
             "C4": "C4: 1x3x1024^2, 30-45% occlusion, mask-aware attention",
             "C5": "C5: batch 64 x 3x512^2 independent frames (cold memory)"}[name]
     return cfg, batch, carried, desc
@@ -117,8 +124,18 @@ def frame_flops_reference(cfg):
             + f["vec2patch"] + f["decode0"] + f["decode2_composite"])
 
 
-def make_pool(name, n, rank, size):
+def make_pool(name, n, rank, size, world=1):
     from paper_2509_10466_b200 import synth
+    if name == "C3":                       # n = frames x streams of this rank, time-major
+        streams = [s for s in range(C3_STREAMS) if s % world == rank]
+        src = [synth.C3Stream(s, size) for s in streams]
+        imgs, masks = [], []
+        for t in range(n // len(src)):
+            for st in src:
+                img, m = st.frame(t)
+                imgs.append(img)
+                masks.append(m)
+        return np.stack(imgs), np.stack(masks)
     gen = {"C1": synth.c1_frame, "C2": synth.c2_frame, "C4": synth.c4_frame,
            "C5": synth.c5_frame}[name]
     imgs, masks = [], []
@@ -127,6 +144,16 @@ def make_pool(name, n, rank, size):
         imgs.append(img)
         masks.append(m)
     return np.stack(imgs), np.stack(masks)
+
+
+def traffic(stage, batch):
+    """DRAM bytes per launch of `stage` from the committed ncu capture (batch-1 C2 frames,
+    scripts/ncu_traffic.py), or None when there is no capture for this workload."""
+    p = REPO / "profiles" / "r01" / "ncu_traffic.json"
+    if batch != 1 or not p.exists():
+        return None
+    st = json.loads(p.read_text())["stages"].get(stage)
+    return None if st is None else round(st["dram_bytes_per_launch"])
 
 
 def peaks():
@@ -202,6 +229,7 @@ def cpu_oracle_rate(name, seconds, max_frames=64):
     """The CPU oracle (numpy port of the reference path) on this host: frames/s over a
     bounded sample of the workload, memory carried for the streaming configs."""
     from oracle import dstt_oracle as O
+    from paper_2509_10466_b200 import synth
     from paper_2509_10466_b200.weights import seed_parameters
     cfg, batch, carried, _ = workload(name)
     size = cfg.width
@@ -211,7 +239,11 @@ def cpu_oracle_rate(name, seconds, max_frames=64):
     t0 = time.perf_counter()
     n = 0
     while True:
-        img, m = make_pool(name, 1, 0, size) if name != "C2" else _c2(n)
+        if name == "C3":
+            img, m = synth.C3Stream(0, size).frame(n)
+            img, m = img[None], m[None]
+        else:
+            img, m = make_pool(name, 1, 0, size) if name != "C2" else _c2(n)
         res = O.inpaint_path(cfg, w, img, m, slots)
         if carried:
             slots = (slots[1], res["slot"][0])
@@ -257,8 +289,13 @@ def run_reference(args):
     warm = min(args.warmup, 1)
     zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
     slots = (zero, zero)
-    frames = [make_pool(args.config, 1, 0, cfg.width) if args.config != "C2" else _c2(i)
-              for i in range(min(steps + warm, 8))]
+    def one(i):
+        if args.config == "C3":                     # stream 0, memory carried
+            from paper_2509_10466_b200 import synth
+            img, m = synth.C3Stream(0, cfg.width).frame(i)
+            return img[None], m[None]
+        return make_pool(args.config, 1, 0, cfg.width) if args.config != "C2" else _c2(i)
+    frames = [one(i) for i in range(min(steps + warm, 8))]
     times = []
     for k in range(warm + steps):
         img, m = frames[k % len(frames)]
@@ -315,13 +352,13 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    cfg, B, carried, desc = workload(args.config)
+    cfg, B, carried, desc = workload(args.config, world)
     T, C, H, W = cfg.tokens, cfg.channels, cfg.height, cfg.width
     P = max(1, args.pool)
     if P % 3 == 0:                          # (k % P, k % 3) must cover every graph key
         P += 1
     t0 = time.perf_counter()
-    imgs, masks = make_pool(args.config, P * B, rank, W)
+    imgs, masks = make_pool(args.config, P * B, rank, W, world)
     log(f"[bench] rank {rank}: pool of {P * B} frames in {time.perf_counter() - t0:.1f}s")
     eng = DsttEngine(cfg, seed=0, device=local)
     d_img = torch.from_numpy(imgs).to(dev).reshape(P, B, 3, H, W)
@@ -424,7 +461,8 @@ def run_ours(args):
             ach = flops[dom] * B / (mean_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "kernel": dom, "achieved": round(ach, 2),
                     "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": round(ach / pk["bf16_tflops"], 4), "traffic": None,
+                    "frac": round(ach / pk["bf16_tflops"], 4),
+                    "traffic": traffic(dom, B if args.config == "C2" else -1),
                     "peak_source": f"{pk_src} dense bf16 burst (MEASURED_PEAKS.json)",
                     "mean_launch_ms": round(mean_ms, 5)}
             if dom.startswith("attn_"):

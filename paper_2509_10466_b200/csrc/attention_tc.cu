@@ -16,7 +16,7 @@
 //                 base, row max tracked on the side, fp16 pack, tcgen05.st P;
 //                 no shuffles, no HMMA, no per-key index math on the math warps
 //   producer warp cp.async.bulk of the 128-key K and V blocks into a 3-stage ring
-// The QKV producer (token_kernels.cu) stores q/k/v rows with the 16-byte chunk swizzle of
+// The QKV producer (token_tc.cu) stores q/k/v rows with the 16-byte chunk swizzle of
 // the UMMA 32-byte swizzle mode, so bulk copies land as valid SWIZZLE_32B operands.
 // The running max is rescaled lazily (only when a row max grows by > 2^8; exact because
 // numerator and denominator share the stale max); a rescale reads, scales and writes the

@@ -105,12 +105,6 @@ DR_DEV float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erf_v);
 }
 
-// Load a pre-packed B fragment pair (b0,b1) for (n-tile, k-tile) from a fragment-major
-// weight image: [..][lane] uint2, 256 B per fragment, coalesced.
-DR_DEV uint2 ld_frag(const uint2* __restrict__ base, int frag, int lane) {
-  return __ldg(base + frag * 32 + lane);
-}
-
 // ---------------------------------------------------------------- programmatic launch
 // Every kernel of the frame is launched with programmatic stream serialization: it lets
 // its dependent launch as soon as all of its CTAs are running (pdl_trigger at entry), does

@@ -42,6 +42,9 @@ struct __align__(1024) ConvSmem {
   static constexpr int HALO_STRIDE = (HALO_BYTES + 1023) & ~1023;   // keep 1024 alignment
   uint8_t halo[2][HALO_STRIDE];
   uint8_t w[9 * 8 * N * 16];                 // [tap][k-chunk][co][8 ci] fp16
+  // decode.0 store staging: per epilogue warp 16 pixels x 128 B (transpose for full-line
+  // coalesced stores: 8 lanes write one pixel's 128 B, one instruction = 4 whole lines)
+  uint8_t stage[N == 64 ? 8 : 1][N == 64 ? 16 * 128 : 16];
   uint64_t halo_full[2], halo_empty[2], tmem_full[2], tmem_empty[2], w_full;
   uint32_t tmem_base;
 };
@@ -178,25 +181,46 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 #pragma unroll
         for (int j = 0; j < N / 16; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
         tc::tmem_wait_ld();
-        if (y >= a.H || x >= a.W) continue;
-        const size_t pix = (size_t)y * a.W + x;
         if constexpr (EPI == 0) {
-          uint4* dst = reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + pix) * 64);
+          // fp16 + LeakyReLU in registers, then two 16-pixel rounds through the warp's
+          // staging buffer (16-B chunk c of pixel p at p*128 + ((c ^ (p & 7)) << 4): the
+          // row-per-lane writes and the lane-per-chunk reads are both conflict-free)
+          uint32_t pk[N / 2];
 #pragma unroll
-          for (int c8 = 0; c8 < N / 8; ++c8) {
-            uint32_t pk[4];
+          for (int c = 0; c < N; c += 2) {
+            float u0 = __uint_as_float(v[c]) + bias[c];
+            float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
+            u0 = u0 >= 0.f ? u0 : 0.2f * u0;
+            u1 = u1 >= 0.f ? u1 : 0.2f * u1;
+            pk[c / 2] = pack_half2(u0, u1);
+          }
+          uint8_t* st = sm.stage[warp - 2];
+          const bool row_ok = y < a.H;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = c8 * 8 + 2 * e;
-              float u0 = __uint_as_float(v[c]) + bias[c];
-              float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
-              u0 = u0 >= 0.f ? u0 : 0.2f * u0;
-              u1 = u1 >= 0.f ? u1 : 0.2f * u1;
-              pk[e] = pack_half2(u0, u1);
+          for (int half = 0; half < 2; ++half) {
+            const int p = lane - 16 * half;                  // pixel slot of this lane
+            if (p >= 0 && p < 16) {
+#pragma unroll
+              for (int c8 = 0; c8 < 8; ++c8)
+                *reinterpret_cast<uint4*>(st + p * 128 + ((c8 ^ (p & 7)) << 4)) =
+                    make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
             }
-            dst[c8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            __syncwarp();
+            const int x0w = tx * TX + 32 * q + 16 * half;    // first pixel of this round
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {                 // 4 pixels x 8 chunks per pass
+              const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
+              const int xx = x0w + pp;
+              if (row_ok && xx < a.W) {
+                const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
+                reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + (size_t)y * a.W + xx) * 64)[c8] = val;
+              }
+            }
+            __syncwarp();
           }
         } else {
+          if (y >= a.H || x >= a.W) continue;
+          const size_t pix = (size_t)y * a.W + x;
           const float alr = al[k];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {

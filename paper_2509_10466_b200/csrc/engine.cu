@@ -52,27 +52,6 @@ int fail(int code, const std::string& msg) {
       return fail(DR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
   } while (0)
 
-uint32_t h2(float lo, float hi) {
-  __half a = __float2half_rn(lo), b = __float2half_rn(hi);
-  uint16_t ua, ub;
-  std::memcpy(&ua, &a, 2);
-  std::memcpy(&ub, &b, 2);
-  return (uint32_t)ua | ((uint32_t)ub << 16);
-}
-
-// W is N x K row-major (W[n][k]); emits N/8 x K/16 fragments of 32 lanes (uint2 b0,b1)
-// in the m16n8k16 B layout: b0 = {W[n0+g][k0+2t], W[n0+g][k0+2t+1]}, b1 = k + 8.
-void pack_frags(const std::vector<float>& W, int N, int K, std::vector<uint2>& out) {
-  for (int nt = 0; nt < N / 8; ++nt)
-    for (int kt = 0; kt < K / 16; ++kt)
-      for (int lane = 0; lane < 32; ++lane) {
-        const int g = lane >> 2, t = lane & 3;
-        const int n = nt * 8 + g, k = kt * 16 + 2 * t;
-        const float* r = &W[(size_t)n * K];
-        out.push_back(make_uint2(h2(r[k], r[k + 1]), h2(r[k + 8], r[k + 9])));
-      }
-}
-
 // tcgen05 operand image of W (N x K row-major): K-atoms of 64 halves; atom kb = N rows of
 // 128 B, 16-byte chunk c of row n stored at chunk c ^ (n & 7) (the UMMA / TMA 128-byte
 // swizzle on a 1024-byte aligned base).
@@ -96,8 +75,6 @@ void append_f32(const float* v, int64_t n, std::vector<uint8_t>& out) {
 }
 
 struct Blk {
-  size_t ln1_w, ln1_b, bqkv, bo, ln2_w, ln2_b, b1, b2;      // float offsets
-  size_t wqkv, wo, w1, w2;                                  // frag offsets
   size_t img;                                               // tcgen05 image byte offset
   bool temporal;
 };
@@ -168,11 +145,9 @@ struct dr_engine {
   int device = 0;
   int H = 0, W = 0, R = 0, Cc = 0, T = 0, nb = 0, n_temporal = 0, feather_r = 0;
   std::vector<Blk> blk;
-  size_t we = 0, be = 0, bv2p = 0, bd0 = 0, bd2 = 0;
-  uint2* frags = nullptr;
-  float* fparams = nullptr;
-  uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We, then 64 KB per block
-  bool token_hmma = false;           // DR_TOKEN_HMMA=1: mma.sync token chains (A/B only)
+  size_t bv2p = 0, bd0 = 0, bd2 = 0;
+  float* fparams = nullptr;          // decoder biases (Vec2Patch, decode.0, decode.2)
+  uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We + be, then per block
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
   size_t wtc_d2 = 0, wtc_v2p = 0;    // byte offsets of the decode.2 / Vec2Patch images
@@ -209,23 +184,15 @@ struct dr_engine {
   }
 
   BlockW block_w(int i) const {
-    const Blk& b = blk[i];
     BlockW w;
-    w.ln1_w = fparams + b.ln1_w; w.ln1_b = fparams + b.ln1_b;
-    w.wqkv = frags + b.wqkv; w.bqkv = fparams + b.bqkv;
-    w.wo = frags + b.wo; w.bo = fparams + b.bo;
-    w.ln2_w = fparams + b.ln2_w; w.ln2_b = fparams + b.ln2_b;
-    w.w1 = frags + b.w1; w.b1 = fparams + b.b1;
-    w.w2 = frags + b.w2; w.b2 = fparams + b.b2;
-    w.img = timg + b.img;
+    w.img = timg + blk[i].img;
     return w;
   }
 
   size_t frame_px() const { return (size_t)H * W; }
 
   void launch_tok(int mode, const TokenArgs& a, cudaStream_t s) const {
-    if (token_hmma) launch_token(mode, a, s);
-    else launch_token_tc(mode, a, s);
+    launch_token_tc(mode, a, s);
   }
 
   // Slot K/V cache: KV_ENTRIES entries (3 per memory stream: slot0, slot1, new slot),
@@ -405,35 +372,20 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   e->R = e->H / p; e->Cc = e->W / p; e->T = e->R * e->Cc;
   e->nb = nb;
 
-  std::vector<uint2> fr;
   std::vector<float> fp;
   std::vector<uint8_t> ti;
+  // embed Conv2d(4, C, p, p): W[co][ci*p*p + ky*p + kx] is already the flatten order.
   pack_sw128(weights[0], c, 4 * p * p, ti);                    // We: 64 x 256
   append_f32(weights[1], numels[1], ti);                       // be
-  auto vec = [&](int idx) { return std::vector<float>(weights[idx], weights[idx] + numels[idx]); };
   auto addf = [&](int idx) { size_t o = fp.size(); fp.insert(fp.end(), weights[idx], weights[idx] + numels[idx]); return o; };
 
-  // embed Conv2d(4, C, p, p): W[co][ci*p*p + ky*p + kx] is already the flatten order.
-  e->we = fr.size(); pack_frags(vec(0), c, 4 * p * p, fr);
-  e->be = addf(1);
   for (int i = 0; i < nb; ++i) {
     const int base = 2 + 16 * i;
     Blk b;
     b.temporal = cfg->blocks[i] == 'T';
-    b.ln1_w = addf(base + 0); b.ln1_b = addf(base + 1);
-    std::vector<float> wqkv = vec(base + 2);
-    std::vector<float> wk = vec(base + 4), wv = vec(base + 6);
-    wqkv.insert(wqkv.end(), wk.begin(), wk.end());
-    wqkv.insert(wqkv.end(), wv.begin(), wv.end());
-    b.wqkv = fr.size(); pack_frags(wqkv, 3 * c, c, fr);
-    b.bqkv = addf(base + 3); addf(base + 5); addf(base + 7);       // contiguous q|k|v bias
-    b.wo = fr.size(); pack_frags(vec(base + 8), c, c, fr);
-    b.bo = addf(base + 9);
-    b.ln2_w = addf(base + 10); b.ln2_b = addf(base + 11);
-    b.w1 = fr.size(); pack_frags(vec(base + 12), 2 * c, c, fr);
-    b.b1 = addf(base + 13);
-    b.w2 = fr.size(); pack_frags(vec(base + 14), c, 2 * c, fr);
-    b.b2 = addf(base + 15);
+    std::vector<float> wqkv(weights[base + 2], weights[base + 2] + numels[base + 2]);
+    wqkv.insert(wqkv.end(), weights[base + 4], weights[base + 4] + numels[base + 4]);
+    wqkv.insert(wqkv.end(), weights[base + 6], weights[base + 6] + numels[base + 6]);
     b.img = ti.size();
     pack_sw128(wqkv.data(), 3 * c, c, ti);
     pack_sw128(weights[base + 8], c, c, ti);
@@ -483,14 +435,9 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
 
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
   e->feather_r = (int)(fw.size() / 2);
-  {
-    const char* ev = std::getenv("DR_TOKEN_HMMA");
-    e->token_hmma = ev && ev[0] == '1';
-  }
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
-  if (cudaMalloc(&e->frags, fr.size() * sizeof(uint2)) != cudaSuccess ||
-      cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
+  if (cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&e->feather_w, fw.size() * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&e->wtc, tcimg.size() * 2) != cudaSuccess ||
       cudaMalloc(&e->timg, ti.size()) != cudaSuccess)
@@ -498,8 +445,7 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   if (cudaMemcpy(e->wtc, tcimg.data(), tcimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(e->timg, ti.data(), ti.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return cleanup(fail(DR_ERR_CUDA, "weight upload failed"));
-  if (cudaMemcpy(e->frags, fr.data(), fr.size() * sizeof(uint2), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(e->fparams, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+  if (cudaMemcpy(e->fparams, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(e->feather_w, fw.data(), fw.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
     return cleanup(fail(DR_ERR_CUDA, "weight upload failed"));
   *out = e;
@@ -510,7 +456,6 @@ void dr_destroy(dr_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   e->free_ws();
-  cudaFree(e->frags);
   cudaFree(e->fparams);
   cudaFree(e->feather_w);
   cudaFree(e->wtc);
@@ -644,7 +589,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   {
     TokenArgs a{};
     a.n_tok = B * T; a.T = T;
-    a.xin = e->xin; a.we = e->frags + e->we; a.be = e->fparams + e->be; a.we_img = e->timg;
+    a.xin = e->xin; a.we_img = e->timg;
     a.kin = 4 * e->cfg.patch * e->cfg.patch;
     a.resid_out = e->resid[0];
     a.has_next = 1; a.next = e->block_w(0);

@@ -11,16 +11,10 @@ constexpr int HEADS = 4;
 constexpr int DH = 16;       // head dim
 constexpr int FF = 128;      // FFN hidden
 
-// Fragment-packed fp16 weights of one transformer block (see pack.cpp).
+// Weights of one transformer block for the tcgen05 token chains (token_tc.cu): one image,
+// K-major 128B-swizzled fp16 [Wqkv 192][Wo 64][W1 128][W2 2 K-atoms x 64] rows of 128 B,
+// then the block's fp32 LayerNorm affine and biases (token_tc_block_image_bytes()).
 struct BlockW {
-  const float* ln1_w; const float* ln1_b;
-  const uint2* wqkv; const float* bqkv;   // N=192 (q|k|v), K=64 : [24][4][32]
-  const uint2* wo;   const float* bo;     // N=64,  K=64  : [8][4][32]
-  const float* ln2_w; const float* ln2_b;
-  const uint2* w1;   const float* b1;     // N=128, K=64  : [16][4][32]
-  const uint2* w2;   const float* b2;     // N=64,  K=128 : [8][8][32]
-  // tcgen05 image (token_tc.cu): K-major 128B-swizzled fp16, [Wqkv 192][Wo 64][W1 128]
-  // [W2 2 K-atoms x 64] rows of 128 B, 64 KB per block
   const uint8_t* img;
 };
 
@@ -30,8 +24,8 @@ struct TokenArgs {
   int T;                  // tokens per frame
   // mode EMBED
   const __half* xin;      // [n_tok][kin] fp16 patch-major network input
-  const uint2* we; const float* be; int kin;
-  const uint8_t* we_img;  // tcgen05 image of We: 4 K-atoms x 64 rows x 128 B
+  int kin;
+  const uint8_t* we_img;  // tcgen05 image of We (4 K-atoms x 64 rows x 128 B), then be
   // mode POST (out-proj + residual + LN2 + FFN + residual)
   const __half* attn;     // [n_tok][64] fp16 attention output (heads concatenated)
   const float* resid_in;  // [n_tok][64] fp32 residual stream (also SLOTKV input)
@@ -54,7 +48,6 @@ constexpr int MAX_TEMPORAL = 4;
 
 enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
 
-void launch_token(int mode, const TokenArgs& a, cudaStream_t s);      // HMMA (mma.sync)
 void launch_token_tc(int mode, const TokenArgs& a, cudaStream_t s);   // tcgen05 + TMEM
 size_t token_tc_block_image_bytes();   // per block: weights + 704 fp32 params
 size_t token_tc_embed_image_bytes();   // We + be

@@ -13,7 +13,8 @@
 // row) serves every term as a descriptor offset.  A CTA = (128 positions, one py, frame):
 // 8 output phases px accumulate in 8 x 64 TMEM columns (the whole TMEM), 10 or 20 taps
 // of 8 KB weights sit in smem.  Warp 0 TMA, warp 1 MMA issue, warps 2-5 epilogue (bias,
-// fp16, 128-byte pixel stores), with a TMEM barrier per phase so stores overlap MMAs.
+// fp16, transposed through smem so 8 lanes store one pixel's 128 B), with a TMEM barrier
+// per phase so stores overlap MMAs.
 #include <cuda.h>
 
 #include "kernels.h"
@@ -31,6 +32,7 @@ constexpr int WIN_CHUNKS = 3;                          // window <= 384 rows (Cc
 struct __align__(1024) V2pSmem {
   uint8_t win[WIN_CHUNKS][M * 128];                    // token window, 128B-swizzled rows
   uint8_t w[20][TAP_BYTES];
+  uint8_t stage[4][32 * 128];                          // per epilogue warp: 32 pixels x 128 B
   uint64_t win_full, w_full, tmem_full[8];
   uint32_t tmem_base;
 };
@@ -106,11 +108,18 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   } else {                                             // ------------------- epilogue
     pdl_wait();                                        // raster is written below
     const int q = warp & 3;
-    const int m = 32 * q + lane;
-    const int P = P0 + m;
-    const int ii = P / PC, jj = P - ii * PC;
-    const int y = 8 * (ii - 1) + py - 1;
-    const bool row_ok = P < NP && y >= 0 && y < a.H && jj >= 1;
+    // pixel slots this lane stores (slot 4*it + lane/8 of the warp's 32 positions): raster
+    // row and x base of each, precomputed once for the 8 phases
+    int ys[8], xb[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int Pp = P0 + 32 * q + 4 * it + (lane >> 3);
+      const int ip = Pp / PC, jp = Pp - ip * PC;
+      const int yp = 8 * (ip - 1) + py - 1;
+      const bool ok = Pp < NP && yp >= 0 && yp < a.H && jp >= 1;
+      ys[it] = ok ? yp : -1;
+      xb[it] = 8 * (jp - 1) - 1;
+    }
     float bias[64];
 #pragma unroll
     for (int c = 0; c < 64; ++c) bias[c] = __ldg(a.bias + c);
@@ -123,20 +132,32 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
       tc::tmem_wait_ld();
-      const int x = 8 * (jj - 1) + px - 1;
-      if (row_ok && x >= 0 && x < a.W) {
-        uint4* dst = reinterpret_cast<uint4*>(a.raster + (((size_t)f * a.H + y) * a.W + x) * 64);
+      // bias + fp16 in registers, transpose through the warp's staging buffer (chunk c of
+      // pixel slot p at p*128 + ((c ^ (p & 7)) << 4)), then 8 lanes per pixel write its
+      // 128 B: each store instruction covers 4 whole lines instead of 32 half-sectors
+      uint8_t* st = sm.stage[q];
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          uint32_t pk[4];
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t pk[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = c8 * 8 + 2 * e;
-            pk[e] = pack_half2(__uint_as_float(v[c]) + bias[c], __uint_as_float(v[c + 1]) + bias[c + 1]);
-          }
-          dst[c8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        for (int e = 0; e < 4; ++e) {
+          const int c = c8 * 8 + 2 * e;
+          pk[e] = pack_half2(__uint_as_float(v[c]) + bias[c], __uint_as_float(v[c + 1]) + bias[c + 1]);
+        }
+        *reinterpret_cast<uint4*>(st + lane * 128 + ((c8 ^ (lane & 7)) << 4)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
+        const int yp = ys[it], xp = xb[it] + px;
+        if (yp >= 0 && xp >= 0 && xp < a.W) {
+          const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
+          reinterpret_cast<uint4*>(a.raster + (((size_t)f * a.H + yp) * a.W + xp) * 64)[c8] = val;
         }
       }
+      __syncwarp();
     }
   }
   tc::fence_before();

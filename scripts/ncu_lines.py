@@ -2,16 +2,21 @@
 per CUDA source line (top N) with the dominant stall reasons.
 
     ncu -i X.ncu-rep --page source --csv --print-source cuda,sass > src.csv
-    python scripts/ncu_lines.py src.csv [N]
+    python scripts/ncu_lines.py src.csv [N] [function-substring]
 """
 import csv
 import sys
 
 
-def main(path, top=25):
+def main(path, top=25, func=None):
     rows = list(csv.reader(open(path)))
-    files, cur, hdr = {}, None, None
+    files, cur, hdr, fn = {}, None, None, ""
     for r in rows:
+        if r and r[0] == "Function Name":
+            fn = r[1]
+            continue
+        if func and func not in fn:
+            continue
         if r and r[0] == "File Path":
             cur = r[1].split("/")[-1]
         elif r and r[0] == "Line No":
@@ -34,4 +39,5 @@ def main(path, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25,
+         sys.argv[3] if len(sys.argv) > 3 else None)
