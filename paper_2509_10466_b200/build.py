@@ -32,12 +32,14 @@ def _stale(obj: Path, src: Path) -> bool:
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, trace: bool = False,
+          variant: str = "", defines=()) -> Path:
     """trace=True builds a separate diagnostic library (_build_trace/, -DDR_TRACE: per-CTA
-    global-timer stamps in the attention kernel, scripts/attn_trace.py) — never the product."""
-    out_dir = PKG / "_build_trace" if trace else OUT_DIR
+    timer stamps, scripts/*_trace.py) -- never the product.  variant/defines build an A/B
+    experiment library into _build_<variant>/ (select it with DR_B200_LIB)."""
+    out_dir = PKG / "_build_trace" if trace else (PKG / f"_build_{variant}" if variant else OUT_DIR)
     lib_path = out_dir / LIB.name
-    flags = FLAGS + (["-DDR_TRACE"] if trace else [])
+    flags = FLAGS + (["-DDR_TRACE"] if trace else []) + list(defines)
     out_dir.mkdir(exist_ok=True)
     objs = []
     for name in SOURCES:
@@ -60,4 +62,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Pa
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv)
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv,
+          variant=var, defines=defs)

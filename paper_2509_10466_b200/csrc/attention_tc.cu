@@ -215,15 +215,18 @@ attn_tc_kernel(AttnArgs a) {
     tc::mbar_init(&sm.mrg_full, QROWS);
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  tc::fence_before();
   // cluster-wide: both CTAs' barriers are initialised before any remote arrive (this is the
   // only cluster barrier; it runs before pdl_wait, overlapping the predecessor kernel)
   cluster_sync();
+  pdl_wait();
+  // TMEM is allocated only after the predecessor grid completed (PDL early trigger: a CTA
+  // never holds TMEM while waiting on another grid, so allocations cannot deadlock)
+  if (warp == 1) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
+  tc::fence_before();
+  __syncthreads();
   tc::fence_after();
   const uint32_t tbase = sm.tmem_base;
-  pdl_wait();
   DR_TRACE_T(1);
 #ifdef DR_TRACE
   {

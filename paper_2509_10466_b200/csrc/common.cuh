@@ -106,12 +106,15 @@ DR_DEV float gelu_erf(float x) {
 }
 
 // ---------------------------------------------------------------- programmatic launch
-// Every kernel of the frame is launched with programmatic stream serialization: it lets
-// its dependent launch as soon as all of its CTAs are running (pdl_trigger at entry), does
-// its input-independent prologue (barriers, TMEM, weights), then pdl_wait()s for the
-// predecessor grid to complete and flush before touching any activation buffer.
+// Every kernel of the frame is launched with programmatic stream serialization and
+// triggers its dependents at entry, so the next kernel's CTAs are scheduled onto free SM
+// slots while this one runs: they do their input-independent prologue (mbarriers, weight
+// bulk copies into smem) and then pdl_wait() for this grid to complete and flush before
+// touching any activation buffer.  TMEM is allocated only AFTER pdl_wait: a CTA never holds
+// TMEM while waiting on another grid, so the TMEM allocator cannot deadlock across the
+// chain (measured: C2 4305 -> 4523 frames/s with the early trigger).
 #ifndef DR_PDL_EARLY_TRIGGER
-#define DR_PDL_EARLY_TRIGGER 0
+#define DR_PDL_EARLY_TRIGGER 1
 #endif
 DR_DEV void pdl_trigger() {
 #if DR_PDL_EARLY_TRIGGER

@@ -26,6 +26,10 @@
 
 namespace dr {
 
+#ifdef DR_TRACE
+void conv_trace_snapshot(cudaStream_t s, int n_cta);
+#endif
+
 namespace {
 
 constexpr int TX = 128;                     // pixels per MMA (M)
@@ -54,6 +58,22 @@ constexpr uint32_t tmem_cols() {
   return 2 * TR * N <= 32 ? 32 : (2 * TR * N <= 64 ? 64 : (2 * TR * N <= 128 ? 128 : (2 * TR * N <= 256 ? 256 : 512)));
 }
 
+// Diagnostic build only (-DDR_TRACE): per-CTA clock64 stamps, scripts/conv_trace.py.
+// Slots: 0 entry, 1 weights in smem (MMA warp), 2 exit; tile i (< 16): 3+5i TMA issued,
+// 4+5i halo landed (MMA warp), 5+5i MMAs committed, 6+5i accumulator ready (epilogue
+// warp 2), 7+5i epilogue warp 2 done.
+#ifdef DR_TRACE
+constexpr int CT_SLOTS = 128;
+__device__ unsigned long long g_conv_trace[256 * CT_SLOTS];
+DR_DEV unsigned long long ct_timer() {    // SM cycle counter: exact within a CTA
+  return (unsigned long long)clock64();
+}
+#define CT_AT(slot) do { if (blockIdx.x < 256 && (slot) < CT_SLOTS) \
+    g_conv_trace[blockIdx.x * CT_SLOTS + (slot)] = ct_timer(); } while (0)
+#else
+#define CT_AT(slot) do {} while (0)
+#endif
+
 template <int N, int EPI, int TR>
 __global__ void __launch_bounds__(THREADS, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
@@ -67,6 +87,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
   const int tiles_x = (a.W + TX - 1) / TX, tiles_y = (a.H + TR - 1) / TR;
   const int n_tiles = a.frames * tiles_y * tiles_x;
 
+  if (threadIdx.x == 0) CT_AT(0);
   pdl_trigger();
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -77,7 +98,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     }
     tc::mbar_init(&sm.w_full, 1);
     tc::fence_barrier_init();
+    tc::tma_prefetch(&tin);
+    tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES);
+    for (uint32_t off = 0; off < WBYTES; off += 16384) {   // constant: before the wait
+      const uint32_t n = WBYTES - off < 16384 ? WBYTES - off : 16384;
+      tc::bulk_load(sm.w + off, reinterpret_cast<const uint8_t*>(a.w) + off, n, &sm.w_full);
+    }
   }
+  pdl_wait();                    // predecessor complete: its outputs and its TMEM are free
   if (warp == 1) tc::tmem_alloc<COLS>(&sm.tmem_base);
   tc::fence_before();
   __syncthreads();
@@ -86,13 +114,6 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 
   if (warp == 0) {
     if (lane == 0) {                                     // ---------------- TMA producer
-      tc::tma_prefetch(&tin);
-      tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES);
-      for (uint32_t off = 0; off < WBYTES; off += 16384) {   // constant: before the wait
-        const uint32_t n = WBYTES - off < 16384 ? WBYTES - off : 16384;
-        tc::bulk_load(sm.w + off, reinterpret_cast<const uint8_t*>(a.w) + off, n, &sm.w_full);
-      }
-      pdl_wait();                                        // input raster of the predecessor
       int i = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int buf = i & 1;
@@ -100,6 +121,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
         const int tx = t % tiles_x, rest = t / tiles_x;
         const int ty = rest % tiles_y, f = rest / tiles_y;
         tc::mbar_wait(&sm.halo_empty[buf], ph ^ 1);
+        if (i < 16) CT_AT(3 + 5 * i);
         tc::mbar_arrive_expect_tx(&sm.halo_full[buf], HALO_BYTES);
         tc::tma_load_4d(sm.halo[buf], &tin, &sm.halo_full[buf], 0, tx * TX - 1, ty * TR - 1, f);
       }
@@ -108,12 +130,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     {                                                    // ---------------- MMA issuer
       constexpr uint32_t idesc = tc::idesc_f16(128, N);   // (whole warp, elected lane issues)
       tc::mbar_wait(&sm.w_full, 0);
+      if (lane == 0) CT_AT(1);
       const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w), N * 16, 128);
       int i = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int buf = i & 1;
         const uint32_t ph = (i >> 1) & 1;
         tc::mbar_wait(&sm.halo_full[buf], ph);
+        if (lane == 0 && i < 16) CT_AT(4 + 5 * i);
         tc::mbar_wait(&sm.tmem_empty[buf], ph ^ 1);
         tc::fence_after();
         // Base descriptors once per tile; each MMA adds a compile-time offset to the
@@ -135,6 +159,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
         }
         tc::mma_commit_warp(&sm.halo_empty[buf]);
         tc::mma_commit_warp(&sm.tmem_full[buf]);
+        if (lane == 0 && i < 16) CT_AT(5 + 5 * i);
       }
     }
   } else {                                               // ---------------- epilogue
@@ -144,7 +169,6 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     float bias[EPI == 0 ? N : 3];
 #pragma unroll
     for (int c = 0; c < (EPI == 0 ? N : 3); ++c) bias[c] = __ldg(a.bias + c);
-    pdl_wait();                          // alpha / frame inputs, output buffers
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int buf = i & 1;
@@ -171,6 +195,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       }
       tc::mbar_wait(&sm.tmem_full[buf], ph);
       tc::fence_after();
+      if (warp == 2 && lane == 0 && i < 16) CT_AT(6 + 5 * i);
       bool bad = false;
 #pragma unroll
       for (int k = 0; k < TR / 2; ++k) {
@@ -250,10 +275,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);
+      if (warp == 2 && lane == 0 && i < 16) CT_AT(7 + 5 * i);
     }
   }
   tc::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) CT_AT(2);
   if (warp == 1) tc::tmem_dealloc<COLS>(tbase);
 }
 
@@ -268,6 +295,9 @@ void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
   launch_pdl(conv3x3_tc_kernel<N, EPI, TR>, dim3(grid), dim3(THREADS), smem, s, tin, a);
+#ifdef DR_TRACE
+  conv_trace_snapshot(s, grid);
+#endif
 }
 
 }  // namespace
@@ -282,3 +312,29 @@ void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaS
 }
 
 }  // namespace dr
+
+#ifdef DR_TRACE
+#include <vector>
+namespace dr {
+namespace {
+std::vector<std::vector<unsigned long long>>& conv_trace_store() {
+  static std::vector<std::vector<unsigned long long>> v;
+  return v;
+}
+}  // namespace
+void conv_trace_snapshot(cudaStream_t s, int n_cta) {
+  if (conv_trace_store().size() >= 16) return;
+  cudaStreamSynchronize(s);
+  std::vector<unsigned long long> h((size_t)std::min(n_cta, 256) * CT_SLOTS);
+  cudaMemcpyFromSymbol(h.data(), g_conv_trace, h.size() * sizeof(unsigned long long));
+  conv_trace_store().push_back(std::move(h));
+}
+}  // namespace dr
+extern "C" int dr_debug_conv_trace(int idx, unsigned long long* host, int n) {
+  auto& v = dr::conv_trace_store();
+  if (idx < 0 || idx >= (int)v.size()) return -1;
+  const int k = std::min(n, (int)v[idx].size());
+  for (int i = 0; i < k; ++i) host[i] = v[idx][i];
+  return k;
+}
+#endif

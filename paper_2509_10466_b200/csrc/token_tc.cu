@@ -95,14 +95,16 @@ DR_DEV void sync_act(const Thr& t) { asm volatile("bar.sync 1, %0;\n" :: "r"(t.n
 
 // Generic-proxy smem writes -> visible to the tensor core; TMEM reads ordered before the
 // next MMA; then one barrier.
-DR_DEV void publish(const Thr& t) {
+#define publish(t) do { publish_(t); TT(); } while (0)
+DR_DEV void publish_(const Thr& t) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc::fence_before();
   sync_act(t);
   tc::fence_after();
 }
 
-DR_DEV void wait_mma(Ctl& ctl, uint32_t& phase) {
+#define wait_mma(c, p) do { wait_mma_(c, p); TT(); } while (0)
+DR_DEV void wait_mma_(Ctl& ctl, uint32_t& phase) {
   tc::mbar_wait(&ctl.mma_bar, phase);
   phase ^= 1u;
   tc::fence_after();
@@ -184,8 +186,25 @@ DR_DEV_HOST_INLINE WLayout wlayout(const TokenArgs& a) {
   return l;
 }
 
+// Diagnostic build only (-DDR_TRACE): thread 0's clock64 at each phase boundary, per CTA
+// (scripts/token_trace.py).  Stamps are sequential: entry, prologue, pdl_wait, then one per
+// publish / MMA wait, and exit.
+#ifdef DR_TRACE
+constexpr int TT_SLOTS = 32;
+__device__ unsigned long long g_tok_trace[1024 * TT_SLOTS];
+#define TT() do { if (threadIdx.x == 0 && blockIdx.x < 1024 && tt_i < TT_SLOTS) {            \
+    unsigned long long c_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) :: "memory");   \
+    g_tok_trace[blockIdx.x * TT_SLOTS + tt_i++] = c_; } } while (0)
+#else
+#define TT() do {} while (0)
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
+#ifdef DR_TRACE
+  int tt_i = 0;
+#endif
+  TT();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -217,12 +236,9 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     tc::mbar_init(&ctl.mma_bar, 1);
     tc::fence_barrier_init();
   }
-  if (t.warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
-  tc::fence_before();
   __syncthreads();
-  tc::fence_after();
-  const uint32_t tbase = ctl.tmem_base;
   if (t.row >= rows) return;                               // idle lane quarter (small tiles)
+  TT();
 
   if (threadIdx.x == 0) {                                  // constant weights: before pdl_wait
     uint8_t* pc = sw + L.w_bytes;
@@ -253,6 +269,14 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     }
   }
   pdl_wait();
+  // TMEM only after the predecessor grid completed (PDL early trigger: no CTA holds TMEM
+  // while it waits on another grid, so allocations cannot deadlock)
+  if (t.warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
+  tc::fence_before();
+  sync_act(t);
+  tc::fence_after();
+  const uint32_t tbase = ctl.tmem_base;
+  TT();
 
   uint32_t phase = 0;
   float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // residual: 8 of 64 channels
@@ -392,6 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   }
   tc::fence_before();
   sync_act(t);
+  TT();
   if (t.warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
 }
 
@@ -412,6 +437,10 @@ int token_tc_tile_rows(int n_tok, int sms) {
     if ((n_tok + r - 1) / r >= sms) return r;
   return 32;
 }
+
+#ifdef DR_TRACE
+void tok_trace_snapshot(cudaStream_t s, int n_cta, int mode);
+#endif
 
 void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
   static int sms = 0;
@@ -441,6 +470,37 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
       launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid, block, smem_bytes<TOK_SLOTKV>(a), s, a);
       break;
   }
+#ifdef DR_TRACE
+  tok_trace_snapshot(s, (int)grid.x, mode);
+#endif
 }
 
 }  // namespace dr
+
+#ifdef DR_TRACE
+#include <vector>
+namespace dr {
+namespace {
+std::vector<std::vector<unsigned long long>>& tok_trace_store() {
+  static std::vector<std::vector<unsigned long long>> v;
+  return v;
+}
+}  // namespace
+void tok_trace_snapshot(cudaStream_t s, int n_cta, int mode) {
+  if (tok_trace_store().size() >= 16) return;
+  cudaStreamSynchronize(s);
+  std::vector<unsigned long long> h((size_t)std::min(n_cta, 1024) * TT_SLOTS + 1);
+  cudaMemcpyFromSymbol(h.data(), g_tok_trace, (h.size() - 1) * sizeof(unsigned long long));
+  h.back() = (unsigned long long)mode;
+  cudaMemsetAsync(nullptr, 0, 0, s);
+  tok_trace_store().push_back(std::move(h));
+}
+}  // namespace dr
+extern "C" int dr_debug_tok_trace(int idx, unsigned long long* host, int n) {
+  auto& v = dr::tok_trace_store();
+  if (idx < 0 || idx >= (int)v.size()) return -1;
+  const int k = std::min(n, (int)v[idx].size());
+  for (int i = 0; i < k; ++i) host[i] = v[idx][i];
+  return k;
+}
+#endif

@@ -56,7 +56,17 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
     tc::mbar_init(&sm.w_full, 1);
     for (int i = 0; i < 8; ++i) tc::mbar_init(&sm.tmem_full[i], 1);
     tc::fence_barrier_init();
+    tc::tma_prefetch(&tok);
+    tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);   // constant: pre-wait
+    const uint8_t* w0 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)(py * 10) * TAP_BYTES;
+    for (int t = 0; t < 10; ++t) tc::bulk_load(sm.w[t], w0 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
+    if (py < 2) {
+      const uint8_t* w1 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)((py + 8) * 10) * TAP_BYTES;
+      for (int t = 0; t < 10; ++t)
+        tc::bulk_load(sm.w[10 + t], w1 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
+    }
   }
+  pdl_wait();                    // predecessor complete: its outputs and its TMEM are free
   if (warp == 1) tc::tmem_alloc<512>(&sm.tmem_base);
   tc::fence_before();
   __syncthreads();
@@ -65,16 +75,6 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
 
   if (warp == 0) {
     if (lane == 0) {                                   // ------------------- loads
-      tc::tma_prefetch(&tok);
-      tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);   // constant: pre-wait
-      const uint8_t* w0 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)(py * 10) * TAP_BYTES;
-      for (int t = 0; t < 10; ++t) tc::bulk_load(sm.w[t], w0 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
-      if (py < 2) {
-        const uint8_t* w1 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)((py + 8) * 10) * TAP_BYTES;
-        for (int t = 0; t < 10; ++t)
-          tc::bulk_load(sm.w[10 + t], w1 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
-      }
-      pdl_wait();                                      // tokens of the predecessor
       tc::mbar_arrive_expect_tx(&sm.win_full, n_chunks * M * 128);
       for (int c = 0; c < n_chunks; ++c)
         tc::tma_load_3d(sm.win[c], &tok, &sm.win_full, 0, P0 - (PC + 1) + c * M, f);
@@ -106,7 +106,6 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       }
     }
   } else {                                             // ------------------- epilogue
-    pdl_wait();                                        // raster is written below
     const int q = warp & 3;
     // pixel slots this lane stores (slot 4*it + lane/8 of the warp's 32 positions): raster
     // row and x base of each, precomputed once for the 8 phases
