@@ -151,6 +151,7 @@ struct dr_engine {
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
   size_t wtc_d2 = 0, wtc_v2p = 0;    // byte offsets of the decode.2 / Vec2Patch images
+  size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
   CUtensorMap map_raster{}, map_d0{}, map_tok{};
   // workspace
   int cap = 0;
@@ -271,7 +272,7 @@ struct dr_engine {
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
     int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
     if (rc) return rc;
-    rc = make_nhwc_map(&map_d0, d0, frames, H, W, conv_tc_rows(16) + 2);
+    rc = make_nhwc_map(&map_d0, d0, frames, H, W, dec2_te_rows() + 2);
     if (rc) return rc;
     return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
   }
@@ -407,6 +408,16 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
     e->blk.push_back(b);
   }
   const int tb = 2 + 16 * nb;
+  {   // decode.2 tap-expanded weights: row u = 3*(3*ky + kx) + co, K = ci (27 rows of 32)
+    std::vector<float> te(32 * (size_t)c, 0.f);
+    const float* w2 = weights[tb + 4];                          // [3][c][3][3]
+    for (int co = 0; co < 3; ++co)
+      for (int ci = 0; ci < c; ++ci)
+        for (int tap = 0; tap < 9; ++tap) te[(size_t)(3 * tap + co) * c + ci] = w2[((size_t)co * c + ci) * 9 + tap];
+    while (ti.size() % 1024) ti.push_back(0);
+    e->te_d2 = ti.size();
+    pack_sw128(te.data(), 32, c, ti);
+  }
   e->bv2p = addf(tb + 1);
   e->bd0 = addf(tb + 3);
   e->bd2 = addf(tb + 5);
@@ -670,10 +681,10 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   e->mark(7, s);
   ConvTcArgs c2{};
   c2.frames = B; c2.H = e->H; c2.W = e->W;
-  c2.w = e->wtc + e->wtc_d2; c2.bias = e->fparams + e->bd2;
+  c2.w = e->timg + e->te_d2; c2.bias = e->fparams + e->bd2;
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
-  launch_conv3x3_tc(16, e->map_d0, c2, s);
+  launch_dec2_te(e->map_d0, c2, s);
   e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
   e->mark(8, s);
   CUDA_TRY(cudaGetLastError());

@@ -129,6 +129,10 @@ struct V2pArgs {
 size_t v2p_tc_weight_bytes();
 void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s);
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
+// decode.2 + tail as a tap-expanded GEMM (conv_tc.cu); w = [u 32][ci 64] fp16 K-major SW128
+// image, u = 3*(3*ky + kx) + co (27 real rows); input halo box = dec2_te_rows() + 2 rows
+void launch_dec2_te(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
+int dec2_te_rows();
 
 // ---------------------------------------------------------------- frame byte kernels
 // (frame_ops.cu): display composite / upscale2x, merge + redact, point-cloud pack.

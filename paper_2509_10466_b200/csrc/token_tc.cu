@@ -168,6 +168,32 @@ DR_DEV void store_chunk(const float (&v)[8], const float* bias, __half* dst, int
   r[c ^ ((t.tk >> 2) & 1)] = pack8(v, bias);
 }
 
+// Small tiles (rows < 128) leave lane quarters idle; the FFN1 GELU, the one heavy
+// elementwise phase, is spread over all 1024 threads of the CTA: the active warps dump the
+// raw FFN1 accumulator to smem (fp32 [rows][128]) and every thread evaluates rows/8
+// contiguous columns (bias + GELU -> fp16 into the 128B-swizzled H operand).  Named
+// barriers 2 and 3 span the whole CTA (the idle warps join only for this phase).
+DR_DEV void gelu_spread(const float* gscr, const float* b1, uint8_t* big, int rows) {
+  const int n = rows >> 3;                                 // 4 (32 rows) or 8 (64 rows)
+  const int e0 = threadIdx.x * n;
+  const int row = e0 >> 7, col = e0 & 127;
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < n) v[i] = gelu_erf(gscr[e0 + i] + b1[col + i]);
+  uint8_t* dst = big + (col >> 6) * ATOM_A + sw128(row, (col & 63) >> 3) + ((col & 7) << 1);
+  if (n == 8) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]),
+                                                pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
+  } else {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]));
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc::fence_before();
+  asm volatile("bar.sync 3, %0;\n" :: "r"(THREADS) : "memory");
+  tc::fence_after();
+}
+
 // Smem layout after the activation tiles: weight images (1024-aligned), then the fp32
 // params blocks (current block, then next block or one per slot-K/V block).
 struct WLayout {
@@ -229,6 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   const float* prm = reinterpret_cast<const float*>(sw + L.w_bytes);
   auto prm_nx = [&](int j) { return prm + (1 + j) * (PRM_BYTES / 4); };
   Ctl& ctl = *reinterpret_cast<Ctl*>(sw + L.total());
+  float* gscr = reinterpret_cast<float*>(sw + L.total() + ((sizeof(Ctl) + 15) & ~15));
 
   pdl_trigger();
   if (threadIdx.x == 0) {
@@ -237,7 +264,14 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     tc::fence_barrier_init();
   }
   __syncthreads();
-  if (t.row >= rows) return;                               // idle lane quarter (small tiles)
+  if (t.row >= rows) {                                     // idle lane quarter (small tiles)
+    if constexpr (MODE == TOK_POST) {                      // ... joins only the GELU phase
+      tc::mbar_wait(&ctl.w_bar, 0);                        // FFN1 bias is in smem
+      asm volatile("bar.sync 2, %0;\n" :: "r"(THREADS) : "memory");
+      gelu_spread(gscr, prm + Prm::b1, big, rows);
+    }
+    return;
+  }
   TT();
 
   if (threadIdx.x == 0) {                                  // constant weights: before pdl_wait
@@ -342,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     publish(t);
     if (t.warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), w1, 128, 1, &ctl.mma_bar);
     wait_mma(ctl, phase);
-    {
+    if (rows == 128) {
       const int col = 16 * t.cg;                           // FFN columns [16cg, 16cg+16)
       float v[16];
       tmem_row<16>(tbase, t, 64 + col, v);
@@ -354,8 +388,19 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
       const int ch = (col & 63) >> 3;
       *reinterpret_cast<uint4*>(atom + sw128(t.row, ch)) = pack8(v, zero);
       *reinterpret_cast<uint4*>(atom + sw128(t.row, ch + 1)) = pack8(v + 8, zero);
+      publish(t);
+    } else {
+      const int col = 16 * t.cg;
+      float v[16];
+      tmem_row<16>(tbase, t, 64 + col, v);
+      float4* g4 = reinterpret_cast<float4*>(gscr + t.row * 128 + col);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) g4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      tc::fence_before();                                  // D2 reads done before D3 MMAs
+      asm volatile("bar.sync 2, %0;\n" :: "r"(THREADS) : "memory");
+      gelu_spread(gscr, prm + Prm::b1, big, rows);
+      TT();
     }
-    publish(t);
     // ---------------------------------------------------------- FFN2 + residual
     if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(big), w2, 64, 2, &ctl.mma_bar);
     wait_mma(ctl, phase);
@@ -423,7 +468,8 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
 template <int MODE>
 int smem_bytes(const TokenArgs& a) {
   constexpr int big = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
-  return ATOM_A + big + wlayout<MODE>(a).total() + (int)sizeof(Ctl) + 1024;
+  const int gscr = (MODE == TOK_POST && a.tile_rows < 128) ? a.tile_rows * 128 * 4 : 0;
+  return ATOM_A + big + wlayout<MODE>(a).total() + (((int)sizeof(Ctl) + 15) & ~15) + gscr + 1024;
 }
 
 }  // namespace

@@ -37,6 +37,10 @@ __global__ void bench(float seed) {
         hx[i] ^= r;
       } else if (KIND == 3) {
         asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x[i]));
+      } else if (KIND == 5) {
+        asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+      } else if (KIND == 6) {
+        asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
       } else if (KIND == 4) {
         asm volatile(
             "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -56,11 +60,13 @@ __global__ void bench(float seed) {
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const char* names[] = {"ex2.f32", "ex2.f16x2", "cvt.f16x2.f32", "ffma", "hmma.m16n8k16"};
-  for (int kind = 0; kind < 5; ++kind) {
+  const char* names[] = {"ex2.f32", "ex2.f16x2", "cvt.f16x2.f32", "ffma", "hmma.m16n8k16",
+                         "rcp.approx.f32", "rsqrt.approx.f32"};
+  for (int kind = 0; kind < 7; ++kind) {
     for (int warps : {8, 16, 32}) {
       void (*k)(float) = kind == 0 ? bench<0> : kind == 1 ? bench<1> : kind == 2 ? bench<2>
-                       : kind == 3 ? bench<3> : bench<4>;
+                       : kind == 3 ? bench<3> : kind == 4 ? bench<4> : kind == 5 ? bench<5>
+                       : bench<6>;
       k<<<sms, warps * 32>>>(1.0f);
       k<<<sms, warps * 32>>>(1.0f);
       cudaDeviceSynchronize();
