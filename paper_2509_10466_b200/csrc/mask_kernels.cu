@@ -57,6 +57,19 @@ DR_DEV void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(s), "l"(gmem), "r"(n));
 }
 
+// Diagnostic build only (-DDR_TRACE): thread 0's clock64 at each phase boundary per CTA,
+// read back by scripts/mask_trace.py.
+#ifdef DR_TRACE
+constexpr int MT_SLOTS = 16;
+__device__ unsigned long long g_mask_trace[4096 * MT_SLOTS];
+#define MT(slot) do { if (threadIdx.x == 0) { unsigned long long c_;                       \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) :: "memory");                          \
+    const int b_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);           \
+    if (b_ < 4096) g_mask_trace[b_ * MT_SLOTS + (slot)] = c_; } } while (0)
+#else
+#define MT(slot) do {} while (0)
+#endif
+
 // WH = halo words per side (compile time: every word loop is shift/mask, no division)
 template <int P, int WH>
 __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
@@ -72,10 +85,12 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   const int NR0 = TH + 2 * Hd, NR1 = TH + 2 * R;
   const size_t plane = (size_t)a.H * a.W;
 
+  MT(0);
   pdl_trigger();
   if (tid == 0) sm.dirty = 0;
   for (int i = tid; i < 2 * R + 1; i += NT) sm.w[i] = a.feather_w[i];   // constant
   pdl_wait();
+  MT(1);
 
   // 0. one async round trip for every input of the tile: m0 bytes (+halo, 4-byte
   //    pieces, zero-filled off-frame; W % 8 == 0 keeps pieces inside a row) and rgb
@@ -120,6 +135,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     cp_async_wait<0>();
     __syncthreads();
   }
+  MT(2);
 
   // 1. m0 -> bits (one warp per 32-pixel word, bytes from smem)
   for (int e = warp; e < NR0 * NW; e += NWARP) {
@@ -128,6 +144,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     if (lane == 0) sm.b0[row][w] = word;
   }
   __syncthreads();
+  MT(3);
 
   // 2. m1 = r iterations of the 3x3 cross (masks._CROSS) over the whole b0 window, ping-pong
   //    through smem; neighbours outside the window read 0.  The window's halo (>= r + R rows
@@ -135,7 +152,52 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   //    on the way never create in-frame bits a frame-clipped iteration would not (the
   //    Manhattan path between in-frame pixels stays in the frame).  Rows / pixels outside the
   //    frame are cleared when b1 is extracted.
-  {
+  if (r <= 8) {
+    // small radius: warp-register form, no CTA barriers.  Warp k owns window rows
+    // g0 = k*(32-2r) .. g0+31 (one row per lane, NW words in registers); vertical neighbours
+    // come from shuffles (0 past the warp's rows), horizontal ones from the adjacent words.
+    // After r iterations lanes r .. 31-r are exact (lanes at the window's own top / bottom
+    // edge too, where the window border reads 0 like the smem form).
+    const int stride = 32 - 2 * r;
+    const int groups = NR0 <= 32 ? 1 : 1 + (NR0 - 32 + stride - 1) / stride;
+    if (warp < groups) {
+      const int g0 = warp * stride, row = g0 + lane;
+      uint32_t cur[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) cur[w] = row < NR0 ? sm.b0[row][w] : 0u;
+      for (int it = 0; it < r; ++it) {
+        uint32_t nx[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          uint32_t up = __shfl_up_sync(0xffffffffu, cur[w], 1);
+          uint32_t dn = __shfl_down_sync(0xffffffffu, cur[w], 1);
+          if (lane == 0) up = 0u;
+          if (lane == 31) dn = 0u;
+          const uint32_t lf = w > 0 ? cur[w - 1] : 0u;
+          const uint32_t rt = w + 1 < NW ? cur[w + 1] : 0u;
+          nx[w] = cur[w] | up | dn | (cur[w] << 1) | (lf >> 31) | (cur[w] >> 1) | (rt << 31);
+        }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) cur[w] = nx[w];
+      }
+      const bool exact = (lane >= r || g0 == 0) && (lane < 32 - r || row >= NR0 - 1);
+      const int b1row = row - (Hd - R);                 // = row - r
+      if (exact && b1row >= 0 && b1row < NR1) {
+        const int y = y0 - R + b1row;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          uint32_t acc = 0;
+          if (y >= 0 && y < a.H) {
+            acc = cur[w];
+            const int xw = xs + 32 * w;               // clear pixels outside the frame
+            if (xw < 0) acc &= xw + 32 <= 0 ? 0u : (0xffffffffu << (-xw));
+            if (xw + 32 > a.W) acc &= xw >= a.W ? 0u : (0xffffffffu >> (xw + 32 - a.W));
+          }
+          sm.b1[b1row][w] = acc;
+        }
+      }
+    }
+  } else {
     uint32_t (*cur)[NW_MAX] = sm.b0;
     uint32_t (*nxt)[NW_MAX] = sm.bt;
     for (int it = 0; it < r; ++it) {
@@ -192,6 +254,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     if (R == 0 && a.alpha) a.alpha[(size_t)f * plane + (size_t)y * a.W + x] = (float)b;
   }
 
+  MT(4);
   // 3. feather
   if (R > 0 && a.alpha) {
     const double* wc = sm.w + R;
@@ -217,6 +280,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
       sm.col[c][32 * w + lane] = mine;
     }
     __syncthreads();
+    MT(5);
     // 3b. vertical pass (float64, scipy order) for the tile rows x span columns; the
     //     window of row ty is bits ty .. ty+2R of the column word
     const uint64_t need = (2 * R + 1 == 64) ? ~0ull : ((1ull << (2 * R + 1)) - 1ull);
@@ -232,16 +296,21 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
         if (pat == 0) acc = 0.0;
         else if (pat == need) acc = sm.all_ones;
         else {
-          acc = __dmul_rn((double)((pat >> R) & 1u), wc[0]);
+          // four interleaved float64 partial sums (dependency depth R/4 instead of R; the
+          // float64 result rounds to the same float32 as scipy's serial order except in
+          // vanishingly rare ties -- tests gate max-abs 1e-6 and >= 99.9 % bit-identical)
+          double sp[4] = {__dmul_rn((double)((pat >> R) & 1u), wc[0]), 0.0, 0.0, 0.0};
           for (int jj = -R; jj < 0; ++jj) {
             const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
-            acc = __dadd_rn(acc, __dmul_rn(pr, wc[jj]));
+            sp[(jj + 64) & 3] = __fma_rn(pr, wc[jj], sp[(jj + 64) & 3]);
           }
+          acc = (sp[0] + sp[1]) + (sp[2] + sp[3]);
         }
       }
       sm.vs[ty][tx] = (float)acc;
     }
     __syncthreads();
+    MT(6);
     // 3c. nonzero mask of every vertical-pass row (one ballot per 32 columns)
     for (int e = warp; e < TH * 4; e += NWARP) {
       const int ty = e >> 2, c = e & 3, tx = 32 * c + lane;   // span <= 126 < 4 words
@@ -269,16 +338,17 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
         if (!(win & need)) out = 0.f;
         else {
           const float* v = &sm.vs[ty][tx + R];
-          double acc = __dmul_rn((double)v[0], wc[0]);
+          double sp[4] = {__dmul_rn((double)v[0], wc[0]), 0.0, 0.0, 0.0};
           for (int jj = -R; jj < 0; ++jj)
-            acc = __dadd_rn(acc, __dmul_rn(__dadd_rn((double)v[jj], (double)v[-jj]), wc[jj]));
-          out = fmaxf(0.f, (float)acc);
+            sp[(jj + 64) & 3] = __fma_rn(__dadd_rn((double)v[jj], (double)v[-jj]), wc[jj], sp[(jj + 64) & 3]);
+          out = fmaxf(0.f, (float)((sp[0] + sp[1]) + (sp[2] + sp[3])));
         }
       }
       a.alpha[(size_t)f * plane + (size_t)y * a.W + x] = out;
     }
   }
 
+  MT(7);
   // 4. tokens of this tile: one warp per token (lanes = 4 channels x P rows)
   if (a.token_valid) {
     const int Cc = a.W / P, T = (a.H / P) * Cc;
@@ -337,8 +407,10 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
       }
     }
   }
+  MT(8);
   __syncthreads();
   if (tid == 0 && sm.dirty && a.flags) atomicOr(a.flags + f, 2);
+  MT(9);
 }
 
 }  // namespace
@@ -367,3 +439,13 @@ void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
 }
 
 }  // namespace dr
+
+#ifdef DR_TRACE
+#include <vector>
+extern "C" int dr_debug_mask_trace(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  const int k = n < 4096 * dr::MT_SLOTS ? n : 4096 * dr::MT_SLOTS;
+  cudaMemcpyFromSymbol(host, dr::g_mask_trace, (size_t)k * sizeof(unsigned long long));
+  return k;
+}
+#endif
