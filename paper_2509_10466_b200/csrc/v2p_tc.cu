@@ -11,10 +11,11 @@
 // run of 128 consecutive padded positions the four neighbour sets are the same run shifted
 // by 0, -1, -(Cc+2), -(Cc+3) rows: one TMA window (128B-swizzled, 128 B = one token per
 // row) serves every term as a descriptor offset.  A CTA = (128 positions, one py, frame):
-// 8 output phases px accumulate in 8 x 64 TMEM columns (the whole TMEM), 10 or 20 taps
-// of 8 KB weights sit in smem.  Warp 0 TMA, warp 1 MMA issue, warps 2-5 epilogue (bias,
-// fp16, transposed through smem so 8 lanes store one pixel's 128 B), with a TMEM barrier
-// per phase so stores overlap MMAs.
+// the 8 output phases px accumulate in 4 rotating 64-column TMEM buffers, and the 10 or 20
+// 8 KB tap images stream through a 4-slot smem ring in consumption order, so a CTA needs
+// ~100 KB of smem and 256 TMEM columns: two CTAs per SM, one wave for a 512^2 frame.  Warp
+// 0 loads, warp 1 issues the MMAs, warps 2-5 run the epilogue (bias, fp16, transposed
+// through smem so 8 lanes store one pixel's 128 B), overlapping the next phases' MMAs.
 #include <cuda.h>
 
 #include "kernels.h"
@@ -28,16 +29,30 @@ constexpr int M = 128;
 constexpr int THREADS = 192;
 constexpr int TAP_BYTES = 64 * 64 * 2;                 // [k-chunk 8][co 64][8 ci] fp16
 constexpr int WIN_CHUNKS = 3;                          // window <= 384 rows (Cc <= 253)
+constexpr int NSLOT = 4;                               // tap ring
+constexpr int NBUF = 4;                                // TMEM phase buffers (64 columns)
 
 struct __align__(1024) V2pSmem {
   uint8_t win[WIN_CHUNKS][M * 128];                    // token window, 128B-swizzled rows
-  uint8_t w[20][TAP_BYTES];
+  uint8_t w[NSLOT][TAP_BYTES];
   uint8_t stage[4][32 * 128];                          // per epilogue warp: 32 pixels x 128 B
-  uint64_t win_full, w_full, tmem_full[8];
+  uint64_t win_full, w_full[NSLOT], w_empty[NSLOT], tmem_full[8], tmem_empty[NBUF];
   uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(THREADS, 1)
+// The taps of phase px in consumption order: (tap image index, token-window row offset).
+// Image index a*10 + b = kernel tap (a, b); window offsets for terms (i,j), (i,j-1),
+// (i-1,j), (i-1,j-1) are PC+1, PC, 1, 0.
+DR_DEV int phase_taps(int py, int px, int PC, int* img, int* off) {
+  int n = 0;
+  img[n] = py * 10 + px; off[n++] = PC + 1;
+  if (px < 2) { img[n] = py * 10 + px + 8; off[n++] = PC; }
+  if (py < 2) { img[n] = (py + 8) * 10 + px; off[n++] = 1; }
+  if (py < 2 && px < 2) { img[n] = (py + 8) * 10 + px + 8; off[n++] = 0; }
+  return n;
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
 v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   extern __shared__ uint8_t smem_raw[];
   V2pSmem& sm = *reinterpret_cast<V2pSmem*>(
@@ -48,26 +63,32 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   const int NP = (a.R + 2) * PC;
   const int win_rows = M + PC + 1;
   const int n_chunks = (win_rows + M - 1) / M;
-  const int n_taps = py < 2 ? 20 : 10;
 
   pdl_trigger();
   if (threadIdx.x == 0) {
     tc::mbar_init(&sm.win_full, 1);
-    tc::mbar_init(&sm.w_full, 1);
+    for (int i = 0; i < NSLOT; ++i) {
+      tc::mbar_init(&sm.w_full[i], 1);
+      tc::mbar_init(&sm.w_empty[i], 1);
+    }
     for (int i = 0; i < 8; ++i) tc::mbar_init(&sm.tmem_full[i], 1);
+    for (int i = 0; i < NBUF; ++i) tc::mbar_init(&sm.tmem_empty[i], 4);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tok);
-    tc::mbar_arrive_expect_tx(&sm.w_full, n_taps * TAP_BYTES);   // constant: pre-wait
-    const uint8_t* w0 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)(py * 10) * TAP_BYTES;
-    for (int t = 0; t < 10; ++t) tc::bulk_load(sm.w[t], w0 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
-    if (py < 2) {
-      const uint8_t* w1 = reinterpret_cast<const uint8_t*>(a.w) + (size_t)((py + 8) * 10) * TAP_BYTES;
-      for (int t = 0; t < 10; ++t)
-        tc::bulk_load(sm.w[10 + t], w1 + (size_t)t * TAP_BYTES, TAP_BYTES, &sm.w_full);
+    // the first NSLOT taps are constant: stream them before waiting on the predecessor
+    int k = 0;
+    for (int px = 0; px < 8 && k < NSLOT; ++px) {
+      int img[4], off[4];
+      const int n = phase_taps(py, px, PC, img, off);
+      for (int t = 0; t < n && k < NSLOT; ++t, ++k) {
+        tc::mbar_arrive_expect_tx(&sm.w_full[k], TAP_BYTES);
+        tc::bulk_load(sm.w[k], reinterpret_cast<const uint8_t*>(a.w) + (size_t)img[t] * TAP_BYTES,
+                      TAP_BYTES, &sm.w_full[k]);
+      }
     }
   }
   pdl_wait();                    // predecessor complete: its outputs and its TMEM are free
-  if (warp == 1) tc::tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 1) tc::tmem_alloc<64 * NBUF>(&sm.tmem_base);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -78,30 +99,48 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       tc::mbar_arrive_expect_tx(&sm.win_full, n_chunks * M * 128);
       for (int c = 0; c < n_chunks; ++c)
         tc::tma_load_3d(sm.win[c], &tok, &sm.win_full, 0, P0 - (PC + 1) + c * M, f);
+      int k = 0;                                       // tap ring, taps NSLOT.. of the CTA
+      for (int px = 0; px < 8; ++px) {
+        int img[4], off[4];
+        const int n = phase_taps(py, px, PC, img, off);
+        for (int t = 0; t < n; ++t, ++k) {
+          if (k < NSLOT) continue;                     // issued in the prologue
+          const int sl = k % NSLOT;
+          tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(k / NSLOT - 1) & 1u);
+          tc::mbar_arrive_expect_tx(&sm.w_full[sl], TAP_BYTES);
+          tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.w) + (size_t)img[t] * TAP_BYTES,
+                        TAP_BYTES, &sm.w_full[sl]);
+        }
+      }
     }
   } else if (warp == 1) {
     {                                                  // ------------------- MMA issue
       constexpr uint32_t idesc = tc::idesc_f16(128, 64);   // (whole warp, elected lane)
       tc::mbar_wait(&sm.win_full, 0);
-      tc::mbar_wait(&sm.w_full, 0);
       tc::fence_after();
       // base descriptors; per-MMA offsets in 16-byte units (row = 8, k-step = 2)
       const uint64_t a0 = tc::sdesc_sw128(tc::smem_u32(sm.win[0]), 0);
       const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 1024, 128);
-      auto term = [&](uint32_t d, int tap, int off, bool first) {
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc::mma_f16_warp(d, a0 + (uint64_t)(off * 8 + ks * 2),
-                           b0 + (uint64_t)(tap * (TAP_BYTES / 16) + ks * 128), idesc,
-                           !(first && ks == 0));
-      };
+      int k = 0;
 #pragma unroll 1
       for (int px = 0; px < 8; ++px) {
-        const uint32_t d = tbase + (uint32_t)(px * 64);
-        term(d, px, PC + 1, true);                                  // (i, j)
-        if (px < 2) term(d, px + 8, PC, false);                     // (i, j-1)
-        if (py < 2) term(d, 10 + px, 1, false);                     // (i-1, j)
-        if (py < 2 && px < 2) term(d, 18 + px, 0, false);           // (i-1, j-1)
+        const int buf = px & (NBUF - 1);
+        if (px >= NBUF) tc::mbar_wait(&sm.tmem_empty[buf], 0);   // epilogue drained px-4
+        const uint32_t d = tbase + (uint32_t)(buf * 64);
+        int img[4], off[4];
+        const int n = phase_taps(py, px, PC, img, off);
+        for (int t = 0; t < n; ++t) {
+          const int sl = (k + t) % NSLOT;
+          tc::mbar_wait(&sm.w_full[sl], (uint32_t)((k + t) / NSLOT) & 1u);
+          tc::fence_after();
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_f16_warp(d, a0 + (uint64_t)(off[t] * 8 + ks * 2),
+                             b0 + (uint64_t)(sl * (TAP_BYTES / 16) + ks * 128), idesc,
+                             (t | ks) != 0);
+        }
+        for (int t = 0; t < n; ++t) tc::mma_commit_warp(&sm.w_empty[(k + t) % NSLOT]);
+        k += n;
         tc::mma_commit_warp(&sm.tmem_full[px]);
       }
     }
@@ -127,10 +166,13 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       tc::mbar_wait(&sm.tmem_full[px], 0);
       tc::fence_after();
       uint32_t v[64];
-      const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(px * 64);
+      const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)((px & (NBUF - 1)) * 64);
 #pragma unroll
       for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
       tc::tmem_wait_ld();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[px & (NBUF - 1)]);
       // bias + fp16 in registers, transpose through the warp's staging buffer (chunk c of
       // pixel slot p at p*128 + ((c ^ (p & 7)) << 4)), then 8 lanes per pixel write its
       // 128 B: each store instruction covers 4 whole lines instead of 32 half-sectors
@@ -161,7 +203,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc<512>(tbase);
+  if (warp == 1) tc::tmem_dealloc<64 * NBUF>(tbase);
 }
 
 }  // namespace

@@ -24,3 +24,12 @@ class EngineNumericError(RuntimeError):
 
 class DeviceError(RuntimeError):
     """A CUDA call inside the B200 extension failed (C-ABI code DR_ERR_CUDA)."""
+
+
+class ProtocolError(ValueError):
+    """A transport message failed validation (reference errors.py:21-30); ``field`` names
+    the offending field."""
+
+    def __init__(self, field: str, message: str = ""):
+        self.field = field
+        super().__init__(f"{field}: {message}" if message else field)
