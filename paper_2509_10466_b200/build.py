@@ -20,8 +20,7 @@ SOURCES = ["engine.cu", "mask_kernels.cu", "token_tc.cu", "attention_tc.cu",
 HEADERS = ["common.cuh", "kernels.h", "tc.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
-         "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 
 
@@ -55,7 +54,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
     if force or not lib_path.exists() or any(o.stat().st_mtime > lib_path.stat().st_mtime
                                              for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", str(lib_path), *map(str, objs), "-lcudart_static",
-               "-lrt", "-ldl", "-lpthread", "-lgomp"]
+               "-lrt", "-ldl", "-lpthread"]
         print("[build] link", lib_path.relative_to(PKG), flush=True)
         subprocess.run(cmd, check=True)
     return lib_path

@@ -7,6 +7,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -23,21 +28,96 @@ namespace {
 
 thread_local std::string g_err;
 
-// Host staging copies (pageable <-> pinned) split over a few OpenMP threads: one core moves
-// ~20 GB/s, so a 512^2 frame's 1.8 MB of staging would otherwise cost ~100 us per call.
-void par_memcpy(void* dst, const void* src, size_t n) {
-  constexpr size_t kChunk = 128 * 1024;
-  const long chunks = (long)((n + kChunk - 1) / kChunk);
-  if (chunks <= 1) {
-    std::memcpy(dst, src, n);
-    return;
+// Host staging copies (pageable <-> pinned) split over a small pool of worker threads: one
+// core moves ~20 GB/s, so a 512^2 frame's ~1.8 MB of staging would otherwise cost ~100 us
+// per call.  The workers spin for ~2 ms after each job (a frame loop calls again well
+// within that) and then sleep, so back-to-back calls pay no thread wake-up latency.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
   }
-#pragma omp parallel for num_threads(8) schedule(static)
-  for (long c = 0; c < chunks; ++c) {
-    const size_t o = (size_t)c * kChunk;
-    std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o,
-                std::min(kChunk, n - o));
+  void copy(void* dst, const void* src, size_t n) {
+    constexpr size_t kMin = 192 * 1024;
+    if (n < kMin || workers_.empty()) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    std::lock_guard<std::mutex> job(job_mu_);            // one job at a time (engines on
+    const int parts = (int)workers_.size() + 1;         // several host threads)
+    const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<uint8_t*>(dst);
+      src_ = static_cast<const uint8_t*>(src);
+      n_ = n;
+      chunk_ = chunk;
+      pending_.store(parts - 1, std::memory_order_relaxed);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(chunk, n));          // the caller takes part 0
+    while (pending_.load(std::memory_order_acquire) != 0) {
+    }
   }
+  ~CopyPool() {
+    stop_.store(true);
+    gen_.fetch_add(1);
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int n = (int)std::min(7u, hw > 1 ? hw - 1 : 0u);
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i + 1); });
+  }
+  void run(int part) {
+    uint64_t seen = 0;
+    while (true) {
+      // spin ~2 ms for the next job, then block on the condition variable
+      auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(2)) {
+      }
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+      }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
+      const size_t o = (size_t)part * chunk_;
+      if (o < n_) std::memcpy(dst_ + o, src_ + o, std::min(chunk_, n_ - o));
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex job_mu_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0};
+  std::atomic<bool> stop_{false};
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t n_ = 0, chunk_ = 0;
+};
+
+void par_memcpy(void* dst, const void* src, size_t n) { CopyPool::get().copy(dst, src, n); }
+
+// any nonzero byte in a row (8 bytes at a time)
+bool row_any(const uint8_t* row, int w) {
+  int x = 0;
+  for (; x + 8 <= w; x += 8) {
+    uint64_t v;
+    std::memcpy(&v, row + x, 8);
+    if (v) return true;
+  }
+  for (; x < w; ++x)
+    if (row[x]) return true;
+  return false;
 }
 
 int fail(int code, const std::string& msg) {
@@ -805,17 +885,10 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   // input byte exactly): copy back that band, and fill the other rows from the
   // input on the host while the GPU runs.  (On an error return `out` holds partial data.)
   const int H = e->H, W = e->W, halo = e->cfg.mask_dilate + e->feather_r;
-  int ymin = H, ymax = -1;
-#pragma omp parallel for num_threads(8) reduction(min : ymin) reduction(max : ymax)
-  for (int y = 0; y < H; ++y) {
-    const uint8_t* row = mask_hw + (size_t)y * W;
-    bool any = false;
-    for (int x = 0; x < W && !any; ++x) any = row[x] != 0;
-    if (any) {
-      ymin = std::min(ymin, y);
-      ymax = std::max(ymax, y);
-    }
-  }
+  int ymin = 0, ymax = H - 1;                     // first / last masked row (scan inward)
+  while (ymin < H && !row_any(mask_hw + (size_t)ymin * W, W)) ++ymin;
+  if (ymin == H) ymax = -1;
+  while (ymax >= ymin && ymax >= 0 && !row_any(mask_hw + (size_t)ymax * W, W)) --ymax;
   int b0 = 0, b1 = 0;                // band [b0, b1) of rows that may change
   if (ymax >= 0) {
     b0 = std::max(0, ymin - halo);
