@@ -4,8 +4,7 @@
 //   decode.2  Conv2d(64, 3, 3, pad 1), (tanh+1)/2, u8 conversion, non-finite guard and
 //             the alpha composite                               dstt.py:243, :267, :322-325;
 //                                                               base.py:87-88
-//             -- as a tap-expanded GEMM (dec2_te_kernel below); the generic kernel's
-//             EPI == 1 tail is kept for N = 16 instantiations (op tests)
+//             -- as a tap-expanded GEMM (dec2_te_kernel below)
 //
 // Implicit GEMM, M = 128 pixels of one output row, N = output channels (64, or 16 with
 // 3 real for decode.2), K = 9 taps x 64 input channels.  A persistent CTA owns the whole
@@ -76,7 +75,7 @@ DR_DEV unsigned long long ct_timer() {    // SM cycle counter: exact within a CT
 #define CT_AT(slot) do {} while (0)
 #endif
 
-template <int N, int EPI, int TR>
+template <int N, int TR>
 __global__ void __launch_bounds__(THREADS, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
   using Smem = ConvSmem<N, TR>;
@@ -168,37 +167,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     const int q = warp & 3;              // TMEM lanes 32q..32q+31 (fixed by warp id % 4)
     const int rh = (warp - 2) >> 2;      // warps 2-5 rows 0,2,..; warps 6-9 rows 1,3,..
     const size_t plane = (size_t)a.H * a.W;
-    float bias[EPI == 0 ? N : 3];
+    float bias[N];
 #pragma unroll
-    for (int c = 0; c < (EPI == 0 ? N : 3); ++c) bias[c] = __ldg(a.bias + c);
+    for (int c = 0; c < N; ++c) bias[c] = __ldg(a.bias + c);
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int buf = i & 1;
       const uint32_t ph = (i >> 1) & 1;
       const int tx = t % tiles_x, rest = t / tiles_x;
       const int ty = rest % tiles_y, f = rest / tiles_y;
-      const int x = tx * TX + 32 * q + lane;
-      // decode.2: fetch alpha / frame pixels while the MMAs of this tile run
-      float al[TR / 2], fr[TR / 2][3];
-      uint8_t fr8[TR / 2][3];
-      if constexpr (EPI == 1) {
-#pragma unroll
-        for (int k = 0; k < TR / 2; ++k) {
-          const int y = ty * TR + rh + 2 * k;
-          const bool ok = y < a.H && x < a.W;
-          const size_t pix = (size_t)(ok ? y : 0) * a.W + (ok ? x : 0);
-          al[k] = ok && a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            fr[k][ch] = ok && a.out_f32 ? __ldg(a.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix) : 0.f;
-            fr8[k][ch] = ok && a.out_u8 ? __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch) : 0;
-          }
-        }
-      }
       tc::mbar_wait(&sm.tmem_full[buf], ph);
       tc::fence_after();
       if (warp == 2 && lane == 0 && i < 16) CT_AT(6 + 5 * i);
-      bool bad = false;
 #pragma unroll
       for (int k = 0; k < TR / 2; ++k) {
         const int r = rh + 2 * k;
@@ -208,71 +188,42 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 #pragma unroll
         for (int j = 0; j < N / 16; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
         tc::tmem_wait_ld();
-        if constexpr (EPI == 0) {
-          // fp16 + LeakyReLU in registers, then two 16-pixel rounds through the warp's
-          // staging buffer (16-B chunk c of pixel p at p*128 + ((c ^ (p & 7)) << 4): the
-          // row-per-lane writes and the lane-per-chunk reads are both conflict-free)
-          uint32_t pk[N / 2];
+        // fp16 + LeakyReLU in registers, then two 16-pixel rounds through the warp's
+        // staging buffer (16-B chunk c of pixel p at p*128 + ((c ^ (p & 7)) << 4): the
+        // row-per-lane writes and the lane-per-chunk reads are both conflict-free)
+        uint32_t pk[N / 2];
 #pragma unroll
-          for (int c = 0; c < N; c += 2) {
-            float u0 = __uint_as_float(v[c]) + bias[c];
-            float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
-            u0 = u0 >= 0.f ? u0 : 0.2f * u0;
-            u1 = u1 >= 0.f ? u1 : 0.2f * u1;
-            pk[c / 2] = pack_half2(u0, u1);
-          }
-          uint8_t* st = sm.stage[warp - 2];
-          const bool row_ok = y < a.H;
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int p = lane - 16 * half;                  // pixel slot of this lane
-            if (p >= 0 && p < 16) {
-#pragma unroll
-              for (int c8 = 0; c8 < 8; ++c8)
-                *reinterpret_cast<uint4*>(st + p * 128 + ((c8 ^ (p & 7)) << 4)) =
-                    make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
-            }
-            __syncwarp();
-            const int x0w = tx * TX + 32 * q + 16 * half;    // first pixel of this round
-#pragma unroll
-            for (int it = 0; it < 4; ++it) {                 // 4 pixels x 8 chunks per pass
-              const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
-              const int xx = x0w + pp;
-              if (row_ok && xx < a.W) {
-                const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
-                reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + (size_t)y * a.W + xx) * 64)[c8] = val;
-              }
-            }
-            __syncwarp();
-          }
-        } else {
-          if (y >= a.H || x >= a.W) continue;
-          const size_t pix = (size_t)y * a.W + x;
-          const float alr = al[k];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const float raw = __uint_as_float(v[ch]) + bias[ch];
-            const float out01 = (tanhf(raw) + 1.0f) * 0.5f;
-            bad |= !isfinite(out01);
-            const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
-            if (a.fill) a.fill[pl] = out01;
-            if (a.out_f32)
-              a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), fr[k][ch]));
-            if (a.out_u8) {
-              const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
-              const uint8_t src8 = fr8[k][ch];
-              uint8_t o;
-              if (alr == 0.f) o = src8;
-              else if (alr == 1.f) o = fill8;
-              else o = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
-                                                             __fmul_rn(__fsub_rn(1.0f, alr), (float)src8))), 0.f), 255.f);
-              a.out_u8[((size_t)f * plane + pix) * 3 + ch] = o;
-            }
-          }
+        for (int c = 0; c < N; c += 2) {
+          float u0 = __uint_as_float(v[c]) + bias[c];
+          float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
+          u0 = u0 >= 0.f ? u0 : 0.2f * u0;
+          u1 = u1 >= 0.f ? u1 : 0.2f * u1;
+          pk[c / 2] = pack_half2(u0, u1);
         }
-      }
-      if constexpr (EPI == 1) {
-        if (bad) atomicOr(a.flags + f, 1);
+        uint8_t* st = sm.stage[warp - 2];
+        const bool row_ok = y < a.H;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int p = lane - 16 * half;                  // pixel slot of this lane
+          if (p >= 0 && p < 16) {
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8)
+              *reinterpret_cast<uint4*>(st + p * 128 + ((c8 ^ (p & 7)) << 4)) =
+                  make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+          }
+          __syncwarp();
+          const int x0w = tx * TX + 32 * q + 16 * half;    // first pixel of this round
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {                 // 4 pixels x 8 chunks per pass
+            const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
+            const int xx = x0w + pp;
+            if (row_ok && xx < a.W) {
+              const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
+              reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + (size_t)y * a.W + xx) * 64)[c8] = val;
+            }
+          }
+          __syncwarp();
+        }
       }
       tc::fence_before();
       __syncwarp();
@@ -504,17 +455,17 @@ dec2_te_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
   if (warp == 1) tc::tmem_dealloc<COLS>(tbase);
 }
 
-template <int N, int EPI, int TR>
+template <int N, int TR>
 void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   static int sms = 0;
   const int smem = (int)sizeof(ConvSmem<N, TR>);
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<N, EPI, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<N, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
-  launch_pdl(conv3x3_tc_kernel<N, EPI, TR>, dim3(grid), dim3(THREADS), smem, s, tin, a);
+  launch_pdl(conv3x3_tc_kernel<N, TR>, dim3(grid), dim3(THREADS), smem, s, tin, a);
 #ifdef DR_TRACE
   conv_trace_snapshot(s, grid);
 #endif
@@ -545,7 +496,7 @@ void launch_dec2_te(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s)
 
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   (void)n;                                     // decode.0 only (decode.2: launch_dec2_te)
-  launch<64, 0, 2>(tin, a, s);
+  launch<64, 2>(tin, a, s);
 }
 
 }  // namespace dr

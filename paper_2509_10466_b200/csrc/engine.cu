@@ -230,7 +230,7 @@ struct dr_engine {
   uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We + be, then per block
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
-  size_t wtc_d2 = 0, wtc_v2p = 0;    // byte offsets of the decode.2 / Vec2Patch images
+  size_t wtc_v2p = 0;                // byte offset of the Vec2Patch image
   size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
   CUtensorMap map_raster{}, map_d0{}, map_tok{};
   // workspace
@@ -503,12 +503,10 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   e->bd0 = addf(tb + 3);
   e->bd2 = addf(tb + 5);
   // tcgen05 weight images, K-major no-swizzle core matrices [tap][k-chunk][co][8 ci] fp16:
-  // decode.0 (N=64), decode.2 (N=16, 3 real), then Vec2Patch (100 taps a*10+b, B[n=co][k=ci]
+  // decode.0 (N=64), then Vec2Patch (100 taps a*10+b, B[n=co][k=ci]
   // = ConvTranspose2d weight[ci][co][a][b]).
   std::vector<uint16_t> tcimg;
   pack_conv_tc(weights[tb + 2], c, c, 64, tcimg);
-  e->wtc_d2 = tcimg.size() * 2;
-  pack_conv_tc(weights[tb + 4], c, 3, 16, tcimg);
   e->wtc_v2p = tcimg.size() * 2;
   {
     const float* wt = weights[tb];
