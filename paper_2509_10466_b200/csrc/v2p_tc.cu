@@ -40,6 +40,18 @@ struct __align__(1024) V2pSmem {
   uint32_t tmem_base;
 };
 
+// Diagnostic build only (-DDR_TRACE): clock64 stamps per CTA (scripts/v2p_trace.py).
+// Slots: 0 entry, 1 TMEM allocated, 2 window landed (MMA warp), 3+px MMAs of phase px
+// issued, 11+px epilogue (warp 2) done with phase px, 19 exit.
+#ifdef DR_TRACE
+__device__ unsigned long long g_v2p_trace[4096 * 20];
+#define VT(slot) do { unsigned long long c_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) :: "memory"); \
+    const int b_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);                      \
+    if (b_ < 4096) g_v2p_trace[b_ * 20 + (slot)] = c_; } while (0)
+#else
+#define VT(slot) do {} while (0)
+#endif
+
 // The taps of phase px in consumption order: (tap image index, token-window row offset).
 // Image index a*10 + b = kernel tap (a, b); window offsets for terms (i,j), (i,j-1),
 // (i-1,j), (i-1,j-1) are PC+1, PC, 1, 0.
@@ -64,6 +76,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   const int win_rows = M + PC + 1;
   const int n_chunks = (win_rows + M - 1) / M;
 
+  if (threadIdx.x == 0) VT(0);
   pdl_trigger();
   if (threadIdx.x == 0) {
     tc::mbar_init(&sm.win_full, 1);
@@ -93,6 +106,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = sm.tmem_base;
+  if (threadIdx.x == 0) VT(1);
 
   if (warp == 0) {
     if (lane == 0) {                                   // ------------------- loads
@@ -118,6 +132,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       constexpr uint32_t idesc = tc::idesc_f16(128, 64);   // (whole warp, elected lane)
       tc::mbar_wait(&sm.win_full, 0);
       tc::fence_after();
+      if (lane == 0) VT(2);
       // base descriptors; per-MMA offsets in 16-byte units (row = 8, k-step = 2)
       const uint64_t a0 = tc::sdesc_sw128(tc::smem_u32(sm.win[0]), 0);
       const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 1024, 128);
@@ -142,6 +157,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
         for (int t = 0; t < n; ++t) tc::mma_commit_warp(&sm.w_empty[(k + t) % NSLOT]);
         k += n;
         tc::mma_commit_warp(&sm.tmem_full[px]);
+        if (lane == 0) VT(3 + px);
       }
     }
   } else {                                             // ------------------- epilogue
@@ -199,10 +215,12 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
         }
       }
       __syncwarp();
+      if (warp == 2 && lane == 0) VT(11 + px);
     }
   }
   tc::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) VT(19);
   if (warp == 1) tc::tmem_dealloc<64 * NBUF>(tbase);
 }
 
@@ -223,3 +241,12 @@ void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s) {
 }
 
 }  // namespace dr
+
+#ifdef DR_TRACE
+extern "C" int dr_debug_v2p_trace(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  const int k = n < 4096 * 20 ? n : 4096 * 20;
+  cudaMemcpyFromSymbol(host, dr::g_v2p_trace, (size_t)k * sizeof(unsigned long long));
+  return k;
+}
+#endif
