@@ -4,10 +4,14 @@
 //   decode.2  Conv2d(64, 3, 3, pad 1), (tanh+1)/2, u8 conversion, non-finite guard and
 //             the alpha composite                               dstt.py:243, :267, :322-325;
 //                                                               base.py:87-88
-//             -- as a tap-expanded GEMM (dec2_te_kernel below)
+//             -- as a tap-expanded GEMM fused into decode.0's epilogue: per pixel
+//             E[3*tap + co] = sum_ci d0[ci] * W2[co][ci][tap] (a 128x32x64 MMA with the
+//             fp16 d0 row as a TMEM A operand), stored as fp16 planes; dec2_gather_kernel
+//             sums the 3x3 neighbourhood and runs the tail.  The 64-channel d0 raster is
+//             never written.
 //
-// Implicit GEMM, M = 128 pixels of one output row, N = output channels (64, or 16 with
-// 3 real for decode.2), K = 9 taps x 64 input channels.  A persistent CTA owns the whole
+// Implicit GEMM, M = 128 pixels of one output row, N = 64 output channels, K = 9 taps x 64
+// input channels.  A persistent CTA owns the whole
 // fp16 weight image in smem (one bulk copy) and walks TR-row x 128-pixel tiles:
 //   warp 0      TMA: the (TR+2) x 130-pixel x 64-channel input halo of the next tile, one
 //               box, 128B-swizzled K-major rows (128 B = one pixel); off-image rows and
@@ -15,10 +19,10 @@
 //   warp 1      one thread issues TR x 9 x 4 tcgen05.mma (128 x N x 16) per tile into a
 //               double-buffered TMEM accumulator; tap (dy,dx) is just a descriptor offset
 //   warps 2-9   epilogue (two warps per TMEM lane quarter, alternate rows): tcgen05.ld
-//               (lane = pixel), bias (registers) + activation, stores; decode.2
-//               prefetches alpha / rgb of the next tile before waiting on the accumulator
-// Double-buffered halo and TMEM let TMA, MMA and the epilogue overlap.  decode.0 uses
-// 2-row tiles (74 KB of weights + 2 x 65 KB halo), decode.2 4-row tiles (1.5x halo reuse).
+//               (lane = pixel), bias (registers) + LeakyReLU, fp16; fused: into TMEM as the
+//               A operand of E, E planes stored one tile later
+// Double-buffered halo and TMEM let TMA, MMA and the epilogue overlap; 2-row tiles (74 KB
+// of weights + 2 x 65 KB halo).
 #include <cuda.h>
 #include <math.h>
 
@@ -41,21 +45,23 @@ constexpr int THREADS = 320;                // TMA warp, MMA warp, 8 epilogue wa
 // smem address bits (like TMA), so such row-shifted descriptors need base_offset 0
 // (tests/test_gpu_ops.py pins this; base_offset = row & 7 produces garbage).
 
-template <int N, int TR>
+template <int N, int TR, bool FUSE>
 struct __align__(1024) ConvSmem {
   static constexpr int HALO_BYTES = (TR + 2) * HX * 128;    // [row][px][64 ch] fp16
   static constexpr int HALO_STRIDE = (HALO_BYTES + 1023) & ~1023;   // keep 1024 alignment
   uint8_t halo[2][HALO_STRIDE];
   uint8_t w[9 * 8 * N * 16];                 // [tap][k-chunk][co][8 ci] fp16
-  // decode.0 store staging: per epilogue warp 16 pixels x 128 B (transpose for full-line
+  uint8_t w2[FUSE ? 32 * 128 : 16];          // fused: decode.2 tap-expanded weights (SW128)
+  // raster store staging: per epilogue warp 16 pixels x 128 B (transpose for full-line
   // coalesced stores: 8 lanes write one pixel's 128 B, one instruction = 4 whole lines)
-  uint8_t stage[N == 64 ? 8 : 1][N == 64 ? 16 * 128 : 16];
+  uint8_t stage[FUSE ? 1 : 8][FUSE ? 16 : 16 * 128];
   uint64_t halo_full[2], halo_empty[2], tmem_full[2], tmem_empty[2], w_full;
+  uint64_t a2_full[2], e_full[2];            // fused: A2 (fp16 d0 in TMEM) ready / E ready
   uint32_t tmem_base;
 };
 
 template <int N, int TR>
-constexpr uint32_t tmem_cols() {
+constexpr uint32_t tmem_cols_d() {
   return 2 * TR * N <= 32 ? 32 : (2 * TR * N <= 64 ? 64 : (2 * TR * N <= 128 ? 128 : (2 * TR * N <= 256 ? 256 : 512)));
 }
 
@@ -75,13 +81,20 @@ DR_DEV unsigned long long ct_timer() {    // SM cycle counter: exact within a CT
 #define CT_AT(slot) do {} while (0)
 #endif
 
-template <int N, int TR>
+// FUSE (decode.0 -> decode.2): after the D0 epilogue (bias, LeakyReLU, fp16) writes its
+// row back into the first 32 TMEM columns of the same D0 row, the MMA warp multiplies that
+// A operand (TMEM, 128 px x 64 ci) by w2 (smem, 32 x 64) into E (TMEM columns 256 + ..):
+// E[p][3*tap + co] = sum_ci d0[p][ci] * W2[co][ci][tap]; the epilogue stores its 27
+// columns as fp16 planes.  The 64-channel d0 raster is never written.
+template <int N, int TR, bool FUSE>
 __global__ void __launch_bounds__(THREADS, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
-  using Smem = ConvSmem<N, TR>;
+  using Smem = ConvSmem<N, TR, FUSE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  constexpr uint32_t COLS = tmem_cols<N, TR>();
+  constexpr uint32_t COLS = FUSE ? 512 : tmem_cols_d<N, TR>();
+  constexpr uint32_t ACOL = 2 * TR * N;       // fused: A2 columns (2 buffers x TR x 32)
+  constexpr uint32_t ECOL = ACOL + 2 * TR * 32;   // fused: E columns (2 buffers x TR x 32)
   constexpr uint32_t WBYTES = 9 * 8 * N * 16;
   constexpr int HALO_BYTES = Smem::HALO_BYTES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,15 +109,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       tc::mbar_init(&sm.halo_empty[b], 1);
       tc::mbar_init(&sm.tmem_full[b], 1);
       tc::mbar_init(&sm.tmem_empty[b], 8);
+      tc::mbar_init(&sm.a2_full[b], 8);
+      tc::mbar_init(&sm.e_full[b], 1);
     }
     tc::mbar_init(&sm.w_full, 1);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tin);
-    tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES);
+    tc::mbar_arrive_expect_tx(&sm.w_full, WBYTES + (FUSE ? 32 * 128 : 0));
     for (uint32_t off = 0; off < WBYTES; off += 16384) {   // constant: before the wait
       const uint32_t n = WBYTES - off < 16384 ? WBYTES - off : 16384;
       tc::bulk_load(sm.w + off, reinterpret_cast<const uint8_t*>(a.w) + off, n, &sm.w_full);
     }
+    if constexpr (FUSE) tc::bulk_load(sm.w2, a.w2, 32 * 128, &sm.w_full);
   }
   pdl_wait();                    // predecessor complete: its outputs and its TMEM are free
   if (warp == 1) tc::tmem_alloc<COLS>(&sm.tmem_base);
@@ -133,6 +149,22 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
       tc::mbar_wait(&sm.w_full, 0);
       if (lane == 0) CT_AT(1);
       const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w), N * 16, 128);
+      // fused: E(j) = A2(j) [TMEM, fp16 d0 rows] x w2^T once the epilogue wrote A2(j)
+      auto e_mma = [&](int j) {
+        const int bj = j & 1;
+        tc::mbar_wait(&sm.a2_full[bj], (uint32_t)(j >> 1) & 1u);
+        tc::fence_after();
+        constexpr uint32_t idesc2 = tc::idesc_f16(128, 32);
+        const uint64_t bw2 = tc::sdesc_sw128(tc::smem_u32(sm.w2), 0);
+#pragma unroll
+        for (int r = 0; r < TR; ++r)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_ts_f16_warp(tbase + ECOL + (uint32_t)(bj * TR * 32 + r * 32),
+                                tbase + ACOL + (uint32_t)(bj * TR * 32 + r * 32 + 8 * ks),
+                                bw2 + (uint64_t)(2 * ks), idesc2, ks != 0);
+        tc::mma_commit_warp(&sm.e_full[bj]);
+      };
       int i = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int buf = i & 1;
@@ -161,7 +193,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
         tc::mma_commit_warp(&sm.halo_empty[buf]);
         tc::mma_commit_warp(&sm.tmem_full[buf]);
         if (lane == 0 && i < 16) CT_AT(5 + 5 * i);
+        if constexpr (FUSE) if (i > 0) e_mma(i - 1);      // behind D0(i) in the pipe
       }
+      if constexpr (FUSE) if (i > 0) e_mma(i - 1);
     }
   } else {                                               // ---------------- epilogue
     const int q = warp & 3;              // TMEM lanes 32q..32q+31 (fixed by warp id % 4)
@@ -170,6 +204,29 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
     float bias[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) bias[c] = __ldg(a.bias + c);
+    // fused: store the 27 E columns of tile j (tile index t_j) as fp16 planes
+    auto e_phase = [&](int j, int t_j) {
+      const int bj = j & 1;
+      tc::mbar_wait(&sm.e_full[bj], (uint32_t)(j >> 1) & 1u);
+      tc::fence_after();
+      const int txj = t_j % tiles_x, restj = t_j / tiles_x;
+      const int tyj = restj % tiles_y, fj = restj / tiles_y;
+#pragma unroll
+      for (int k = 0; k < TR / 2; ++k) {
+        const int r = rh + 2 * k;
+        const int y = tyj * TR + r, x = txj * TX + 32 * q + lane;
+        uint32_t ev[32];
+        const uint32_t eaddr = tbase + ((uint32_t)(32 * q) << 16) + ECOL + (uint32_t)(bj * TR * 32 + r * 32);
+        tc::tmem_ld16(eaddr, ev);
+        tc::tmem_ld16(eaddr + 16, ev + 16);
+        tc::tmem_wait_ld();
+        if (y < a.H && x < a.W) {
+          __half* ep = a.e_planes + ((size_t)fj * 27 * plane) + (size_t)y * a.W + x;
+#pragma unroll
+          for (int u = 0; u < 27; ++u) ep[(size_t)u * plane] = __float2half_rn(__uint_as_float(ev[u]));
+        }
+      }
+    };
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const int buf = i & 1;
@@ -188,48 +245,78 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 #pragma unroll
         for (int j = 0; j < N / 16; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
         tc::tmem_wait_ld();
-        // fp16 + LeakyReLU in registers, then two 16-pixel rounds through the warp's
-        // staging buffer (16-B chunk c of pixel p at p*128 + ((c ^ (p & 7)) << 4): the
-        // row-per-lane writes and the lane-per-chunk reads are both conflict-free)
-        uint32_t pk[N / 2];
+        if constexpr (FUSE) {
+          // fp16 LeakyReLU(d0) into this row's A2 columns = the A operand of E
+          uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < N; c += 2) {
-          float u0 = __uint_as_float(v[c]) + bias[c];
-          float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
-          u0 = u0 >= 0.f ? u0 : 0.2f * u0;
-          u1 = u1 >= 0.f ? u1 : 0.2f * u1;
-          pk[c / 2] = pack_half2(u0, u1);
-        }
-        uint8_t* st = sm.stage[warp - 2];
-        const bool row_ok = y < a.H;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int p = lane - 16 * half;                  // pixel slot of this lane
-          if (p >= 0 && p < 16) {
-#pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8)
-              *reinterpret_cast<uint4*>(st + p * 128 + ((c8 ^ (p & 7)) << 4)) =
-                  make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+          for (int c = 0; c < 64; c += 2) {
+            float u0 = __uint_as_float(v[c]) + bias[c];
+            float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
+            u0 = u0 >= 0.f ? u0 : 0.2f * u0;
+            u1 = u1 >= 0.f ? u1 : 0.2f * u1;
+            pk[c / 2] = pack_half2(u0, u1);
           }
-          __syncwarp();
-          const int x0w = tx * TX + 32 * q + 16 * half;    // first pixel of this round
+          tc::tmem_st32(tbase + ((uint32_t)(32 * q) << 16) + ACOL + (uint32_t)(buf * TR * 32 + r * 32), pk);
+          tc::tmem_wait_st();
+        } else {
+          // fp16 + LeakyReLU in registers, then two 16-pixel rounds through the warp's
+          // staging buffer (16-B chunk c of pixel p at p*128 + ((c ^ (p & 7)) << 4): the
+          // row-per-lane writes and the lane-per-chunk reads are both conflict-free)
+          uint32_t pk[N / 2];
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {                 // 4 pixels x 8 chunks per pass
-            const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
-            const int xx = x0w + pp;
-            if (row_ok && xx < a.W) {
-              const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
-              reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + (size_t)y * a.W + xx) * 64)[c8] = val;
+          for (int c = 0; c < N; c += 2) {
+            float u0 = __uint_as_float(v[c]) + bias[c];
+            float u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
+            u0 = u0 >= 0.f ? u0 : 0.2f * u0;
+            u1 = u1 >= 0.f ? u1 : 0.2f * u1;
+            pk[c / 2] = pack_half2(u0, u1);
+          }
+          uint8_t* st = sm.stage[warp - 2];
+          const bool row_ok = y < a.H;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int p = lane - 16 * half;                  // pixel slot of this lane
+            if (p >= 0 && p < 16) {
+#pragma unroll
+              for (int c8 = 0; c8 < 8; ++c8)
+                *reinterpret_cast<uint4*>(st + p * 128 + ((c8 ^ (p & 7)) << 4)) =
+                    make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
             }
+            __syncwarp();
+            const int x0w = tx * TX + 32 * q + 16 * half;    // first pixel of this round
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {                 // 4 pixels x 8 chunks per pass
+              const int pp = 4 * it + (lane >> 3), c8 = lane & 7;
+              const int xx = x0w + pp;
+              if (row_ok && xx < a.W) {
+                const uint4 val = *reinterpret_cast<const uint4*>(st + pp * 128 + ((c8 ^ (pp & 7)) << 4));
+                reinterpret_cast<uint4*>(a.out16 + ((size_t)f * plane + (size_t)y * a.W + xx) * 64)[c8] = val;
+              }
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);
+      if constexpr (FUSE) {
+        // D0(i) is consumed (A2 has its own columns): free it for MMA1(i+2) at once, hand
+        // A2(i) to the MMA warp, then store E of the PREVIOUS tile (its MMA2 ran behind
+        // MMA1(i), so it is ready by now)
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(&sm.a2_full[buf]);
+          tc::mbar_arrive(&sm.tmem_empty[buf]);
+        }
+        if (i > 0) e_phase(i - 1, t - (int)gridDim.x);
+      }
+      if constexpr (!FUSE) {
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);
+      }
       if (warp == 2 && lane == 0 && i < 16) CT_AT(7 + 5 * i);
     }
+    if constexpr (FUSE) if (i > 0) e_phase(i - 1, (int)blockIdx.x + (i - 1) * (int)gridDim.x);
   }
   tc::fence_before();
   __syncthreads();
@@ -238,234 +325,72 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// decode.2 as a tap-expanded GEMM (3 output channels): instead of 9 taps x 4 K-steps of a
-// 128 x 16 MMA per output row (the A operand, 4 KB, re-read from smem 36 times), every halo
-// row is multiplied ONCE by the 27 (tap, co) filter columns:
-//     E[p][3*tap + co] = sum_ci d0[p][ci] * W2[co][ci][tap]       (M=128 pixels, N=32, K=64)
-// and the 3x3 neighbourhood is summed in the epilogue:
-//     out[y][x][co] = b[co] + sum_{dy,dx} E_{y+dy-1}[x+dx-1][3*(3dy+dx) + co]
-// (E = 0 off-image because TMA zero-fills d0 there = the conv's zero padding).  Per output
-// row and channel the three dx columns collapse to A = sum_dy E[.][dx=0], B = .., C = ..,
-// so out(lane) = A(lane-1) + B(lane) + C(lane+1): two warp shuffles plus a boundary value
-// through smem.  Tile: TR_TE output rows x 126 output pixels (the 128 MMA rows are pixels
-// x0-1 .. x0+126).  Warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (two per TMEM lane quarter,
-// each owning TR_TE/2 output rows; one named barrier per tile for the quarter edges).
-constexpr int TR_TE = 4;
-constexpr int TW_TE = 126;
-constexpr int EPI_TE = 8;                     // epilogue warps
-constexpr int ROWS_W = TR_TE / 2;             // output rows per epilogue warp
-constexpr int THREADS_TE = 64 + 32 * EPI_TE;
-
-struct __align__(1024) TeSmem {
-  static constexpr int HALO_BYTES = (TR_TE + 2) * HX * 128;
-  static constexpr int HALO_STRIDE = (HALO_BYTES + 1023) & ~1023;
-  uint8_t halo[2][HALO_STRIDE];
-  uint8_t w[32 * 128];                        // [u 32][ci 64] fp16, K-major 128B-swizzled
-  float edge[2][TR_TE][4][2][3];              // per buffer, row, quarter: (A lane 31, C lane 0)
-  uint64_t halo_full[2], halo_empty[2], tmem_full[2], tmem_empty[2], w_full;
-  uint32_t tmem_base;
-};
-
-__global__ void __launch_bounds__(THREADS_TE, 1)
-dec2_te_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  TeSmem& sm = *reinterpret_cast<TeSmem*>(smem_raw);
-  constexpr uint32_t COLS = 512;              // 2 buffers x (TR_TE+2) rows x 32 columns
-  constexpr int HALO_BYTES = TeSmem::HALO_BYTES;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_x = (a.W + TW_TE - 1) / TW_TE, tiles_y = (a.H + TR_TE - 1) / TR_TE;
-  const int n_tiles = a.frames * tiles_y * tiles_x;
-
-  if (threadIdx.x == 0) CT_AT(0);
+// decode.2 gather + tail over the fused decode.0's E planes: one thread per output pixel,
+// out[co] = b[co] + sum_{dy,dx} E[3*(3dy+dx)+co][y+dy-1][x+dx-1] (0 off-image = the conv's
+// zero padding), then (tanh + 1) / 2, non-finite guard and the alpha composite.  Each E
+// value feeds exactly one output pixel, so the 27 reads per pixel are coalesced plane rows
+// with no reuse to stage.
+__global__ void __launch_bounds__(256) dec2_gather_kernel(ConvTcArgs a) {
+  const int x = blockIdx.x * 256 + threadIdx.x, y = blockIdx.y, f = blockIdx.z;
   pdl_trigger();
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&sm.halo_full[b], 1);
-      tc::mbar_init(&sm.halo_empty[b], 1);
-      tc::mbar_init(&sm.tmem_full[b], 1);
-      tc::mbar_init(&sm.tmem_empty[b], EPI_TE);
-    }
-    tc::mbar_init(&sm.w_full, 1);
-    tc::fence_barrier_init();
-    tc::tma_prefetch(&tin);
-    tc::mbar_arrive_expect_tx(&sm.w_full, 32 * 128);
-    tc::bulk_load(sm.w, a.w, 32 * 128, &sm.w_full);
-  }
-  pdl_wait();                    // predecessor complete: its outputs and its TMEM are free
-  if (warp == 1) tc::tmem_alloc<COLS>(&sm.tmem_base);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tbase = sm.tmem_base;
-
-  if (warp == 0) {
-    if (lane == 0) {                                     // ---------------- TMA producer
-      int i = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-        const int buf = i & 1;
-        const uint32_t ph = (i >> 1) & 1;
-        const int tx = t % tiles_x, rest = t / tiles_x;
-        const int ty = rest % tiles_y, f = rest / tiles_y;
-        tc::mbar_wait(&sm.halo_empty[buf], ph ^ 1);
-        if (i < 16) CT_AT(3 + 5 * i);
-        tc::mbar_arrive_expect_tx(&sm.halo_full[buf], HALO_BYTES);
-        tc::tma_load_4d(sm.halo[buf], &tin, &sm.halo_full[buf], 0, tx * TW_TE - 1, ty * TR_TE - 1, f);
-      }
-    }
-  } else if (warp == 1) {                                // ---------------- MMA issuer
-    constexpr uint32_t idesc = tc::idesc_f16(128, 32);
-    tc::mbar_wait(&sm.w_full, 0);
-    if (lane == 0) CT_AT(1);
-    const uint64_t b0 = tc::sdesc_sw128(tc::smem_u32(sm.w), 0);
-    int i = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-      const int buf = i & 1;
-      const uint32_t ph = (i >> 1) & 1;
-      tc::mbar_wait(&sm.halo_full[buf], ph);
-      if (lane == 0 && i < 16) CT_AT(4 + 5 * i);
-      tc::mbar_wait(&sm.tmem_empty[buf], ph ^ 1);
-      tc::fence_after();
-      const uint64_t a0 = tc::sdesc_sw128(tc::smem_u32(sm.halo[buf]), 0);
+  float bias[3];
 #pragma unroll
-      for (int hr = 0; hr < TR_TE + 2; ++hr) {
-        const uint32_t d = tbase + (uint32_t)(buf * (TR_TE + 2) * 32 + hr * 32);
+  for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
+  pdl_wait();
+  if (x >= a.W) return;
+  const size_t plane = (size_t)a.H * a.W;
+  const __half* ep = a.e_planes + (size_t)f * 27 * plane;
+  float o[3] = {bias[0], bias[1], bias[2]};
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc::mma_f16_warp(d, a0 + (uint64_t)(hr * HX * 8 + ks * 2), b0 + (uint64_t)(ks * 2), idesc,
-                           ks != 0);
-      }
-      tc::mma_commit_warp(&sm.halo_empty[buf]);
-      tc::mma_commit_warp(&sm.tmem_full[buf]);
-      if (lane == 0 && i < 16) CT_AT(5 + 5 * i);
-    }
-  } else {                                               // ---------------- epilogue
-    const int q = warp & 3;                              // lanes 32q.. = pixels x0-1+32q..
-    const int rh = (warp - 2) >> 2;                      // output rows ROWS_W*rh ..
-    const int l = 32 * q + lane;
-    const size_t plane = (size_t)a.H * a.W;
-    float bias[3];
+  for (int dy = 0; dy < 3; ++dy) {
+    const int yy = y + dy - 1;
+    if (yy < 0 || yy >= a.H) continue;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
-    int i = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-      const int buf = i & 1;
-      const uint32_t ph = (i >> 1) & 1;
-      const int tx = t % tiles_x, rest = t / tiles_x;
-      const int ty = rest % tiles_y, f = rest / tiles_y;
-      const int x = tx * TW_TE - 1 + l;                  // this lane's pixel
-      const bool out_lane = l >= 1 && l <= TW_TE && x < a.W;
-      // alpha / frame of this lane's output pixels, fetched while the MMAs run
-      float al[ROWS_W], fr[ROWS_W][3];
-      uint8_t fr8[ROWS_W][3];
+    for (int dx = 0; dx < 3; ++dx) {
+      const int xx = x + dx - 1;
+      if (xx < 0 || xx >= a.W) continue;
+      const size_t pix = (size_t)yy * a.W + xx;
 #pragma unroll
-      for (int k = 0; k < ROWS_W; ++k) {
-        const int y = ty * TR_TE + ROWS_W * rh + k;
-        const bool ok = out_lane && y < a.H;
-        const size_t pix = (size_t)(ok ? y : 0) * a.W + (ok ? x : 0);
-        al[k] = ok && a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          fr[k][ch] = ok && a.out_f32 ? __ldg(a.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix) : 0.f;
-          fr8[k][ch] = ok && a.out_u8 ? __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch) : 0;
-        }
-      }
-      tc::mbar_wait(&sm.tmem_full[buf], ph);
-      tc::fence_after();
-      if (warp == 2 && lane == 0 && i < 16) CT_AT(6 + 5 * i);
-      // E rows ROWS_W*rh .. +ROWS_W+1 for this lane: column 3*tap + co, tap = 3*dy + dx
-      float e[ROWS_W + 2][27];
-#pragma unroll
-      for (int hr = 0; hr < ROWS_W + 2; ++hr) {
-        uint32_t v[32];
-        const uint32_t taddr = tbase + ((uint32_t)(32 * q) << 16) +
-                               (uint32_t)(buf * (TR_TE + 2) * 32 + (ROWS_W * rh + hr) * 32);
-        tc::tmem_ld16(taddr, v);
-        tc::tmem_ld16(taddr + 16, v + 16);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 27; ++u) e[hr][u] = __uint_as_float(v[u]);
-      }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.tmem_empty[buf]);   // TMEM free for tile i+2
-      // per output row and channel: A (dx=0), B (dx=1), C (dx=2) summed over dy
-      float A[ROWS_W][3], B[ROWS_W][3], Cc[ROWS_W][3];
-#pragma unroll
-      for (int k = 0; k < ROWS_W; ++k)
-#pragma unroll
-        for (int co = 0; co < 3; ++co) {
-          A[k][co] = e[k][co] + e[k + 1][9 + co] + e[k + 2][18 + co];
-          B[k][co] = e[k][3 + co] + e[k + 1][12 + co] + e[k + 2][21 + co];
-          Cc[k][co] = e[k][6 + co] + e[k + 1][15 + co] + e[k + 2][24 + co];
-        }
-      // lane 31's A and lane 0's C cross to the neighbouring quarter (one barrier per tile;
-      // the edge slots are double-buffered by tile parity)
-#pragma unroll
-      for (int k = 0; k < ROWS_W; ++k) {
-        float* ed = &sm.edge[buf][ROWS_W * rh + k][q][0][0];
-        if (lane == 31) { ed[0] = A[k][0]; ed[1] = A[k][1]; ed[2] = A[k][2]; }
-        if (lane == 0) { ed[3] = Cc[k][0]; ed[4] = Cc[k][1]; ed[5] = Cc[k][2]; }
-      }
-      asm volatile("bar.sync 1, %0;\n" :: "r"(32 * EPI_TE) : "memory");
-      bool bad = false;
-#pragma unroll
-      for (int k = 0; k < ROWS_W; ++k) {
-        const int r = ROWS_W * rh + k;
-        float o[3];
-#pragma unroll
-        for (int co = 0; co < 3; ++co) {
-          float left = __shfl_up_sync(0xffffffffu, A[k][co], 1);
-          float right = __shfl_down_sync(0xffffffffu, Cc[k][co], 1);
-          if (lane == 0) left = q > 0 ? sm.edge[buf][r][q - 1][0][co] : 0.f;
-          if (lane == 31) right = q < 3 ? sm.edge[buf][r][q + 1][1][co] : 0.f;
-          o[co] = left + B[k][co] + right;
-        }
-        const int y = ty * TR_TE + r;
-        if (!out_lane || y >= a.H) continue;
-        const size_t pix = (size_t)y * a.W + x;
-        const float alr = al[k];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float raw = o[ch] + bias[ch];
-          const float out01 = (tanhf(raw) + 1.0f) * 0.5f;
-          bad |= !isfinite(out01);
-          const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
-          if (a.fill) a.fill[pl] = out01;
-          if (a.out_f32)
-            a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), fr[k][ch]));
-          if (a.out_u8) {
-            const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
-            const uint8_t src8 = fr8[k][ch];
-            uint8_t ov;
-            if (alr == 0.f) ov = src8;
-            else if (alr == 1.f) ov = fill8;
-            else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
-                                                            __fmul_rn(__fsub_rn(1.0f, alr), (float)src8))), 0.f), 255.f);
-            a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
-          }
-        }
-      }
-      if (bad) atomicOr(a.flags + f, 1);
-      if (warp == 2 && lane == 0 && i < 16) CT_AT(7 + 5 * i);
+      for (int co = 0; co < 3; ++co)
+        o[co] += __half2float(ep[(size_t)(3 * (3 * dy + dx) + co) * plane + pix]);
     }
   }
-  tc::fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) CT_AT(2);
-  if (warp == 1) tc::tmem_dealloc<COLS>(tbase);
+  const size_t pix = (size_t)y * a.W + x;
+  const float alr = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
+  bool bad = false;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float out01 = (tanhf(o[ch]) + 1.0f) * 0.5f;
+    bad |= !isfinite(out01);
+    const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
+    if (a.fill) a.fill[pl] = out01;
+    if (a.out_f32)
+      a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), __ldg(a.rgb_f32 + pl)));
+    if (a.out_u8) {
+      const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
+      const uint8_t src8 = __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch);
+      uint8_t ov;
+      if (alr == 0.f) ov = src8;
+      else if (alr == 1.f) ov = fill8;
+      else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
+                                                      __fmul_rn(__fsub_rn(1.0f, alr), (float)src8))), 0.f), 255.f);
+      a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && bad) atomicOr(a.flags + f, 1);
 }
 
-template <int N, int TR>
+template <int N, int TR, bool FUSE>
 void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
   static int sms = 0;
-  const int smem = (int)sizeof(ConvSmem<N, TR>);
+  const int smem = (int)sizeof(ConvSmem<N, TR, FUSE>);
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<N, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<N, TR, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
-  launch_pdl(conv3x3_tc_kernel<N, TR>, dim3(grid), dim3(THREADS), smem, s, tin, a);
+  launch_pdl(conv3x3_tc_kernel<N, TR, FUSE>, dim3(grid), dim3(THREADS), smem, s, tin, a);
 #ifdef DR_TRACE
   conv_trace_snapshot(s, grid);
 #endif
@@ -477,26 +402,15 @@ size_t conv_tc_weight_bytes(int n) { return (size_t)9 * 8 * n * 16; }
 
 int conv_tc_rows(int n) { return n == 64 ? 2 : 4; }   // decode.0 tiles: 2 output rows
 
-int dec2_te_rows() { return TR_TE; }
-
-void launch_dec2_te(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
-  static int sms = 0;
-  const int smem = (int)sizeof(TeSmem);
-  if (!sms) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaFuncSetAttribute(dec2_te_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  }
-  const int tiles = a.frames * ((a.H + TR_TE - 1) / TR_TE) * ((a.W + TW_TE - 1) / TW_TE);
-  const int grid = tiles < sms ? tiles : sms;
-  launch_pdl(dec2_te_kernel, dim3(grid), dim3(THREADS_TE), smem, s, tin, a);
-#ifdef DR_TRACE
-  conv_trace_snapshot(s, grid);
-#endif
+void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s) {
+  dim3 grid((a.W + 255) / 256, a.H, a.frames);
+  launch_pdl(dec2_gather_kernel, grid, dim3(256), 0, s, a);
 }
 
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
-  (void)n;                                     // decode.0 only (decode.2: launch_dec2_te)
-  launch<64, 2>(tin, a, s);
+  (void)n;                                     // decode.0 only (decode.2: E planes + gather)
+  if (a.e_planes) launch<64, 2, true>(tin, a, s);
+  else launch<64, 2, false>(tin, a, s);
 }
 
 }  // namespace dr

@@ -232,7 +232,7 @@ struct dr_engine {
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
   size_t wtc_v2p = 0;                // byte offset of the Vec2Patch image
   size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
-  CUtensorMap map_raster{}, map_d0{}, map_tok{};
+  CUtensorMap map_raster{}, map_tok{};
   // workspace
   int cap = 0;
   void* ws = nullptr;
@@ -240,7 +240,7 @@ struct dr_engine {
   uint8_t *m1 = nullptr, *tv = nullptr;
   float *alpha = nullptr, *resid[2] = {nullptr, nullptr};
   __half *xin = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr,
-         *tok16 = nullptr, *raster = nullptr, *d0 = nullptr, *slotkv = nullptr;
+         *tok16 = nullptr, *raster = nullptr, *eplanes = nullptr, *slotkv = nullptr;
   int* flags = nullptr;
   // host-buffer path (dr_inpaint_u8_host): device frame buffers + 3-slot ring
   uint8_t *h_rgb = nullptr, *h_m0 = nullptr, *h_out = nullptr;   // device
@@ -336,7 +336,7 @@ struct dr_engine {
     const size_t o_q = take(tok * C * 2), o_k = take(tok * C * 2), o_v = take(tok * C * 2);
     const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
     const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
-    const size_t o_ras = take(px * C * 2), o_d0 = take(px * C * 2);
+    const size_t o_ras = take(px * C * 2), o_ep = take(px * 27 * 2);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
     CUDA_TRY(cudaMalloc(&ws, off));
@@ -347,13 +347,11 @@ struct dr_engine {
     xin = (__half*)(b + o_xin);
     q = (__half*)(b + o_q); k = (__half*)(b + o_k); v = (__half*)(b + o_v);
     attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
-    raster = (__half*)(b + o_ras); d0 = (__half*)(b + o_d0);
+    raster = (__half*)(b + o_ras); eplanes = (__half*)(b + o_ep);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
     cap = frames;
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
     int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
-    if (rc) return rc;
-    rc = make_nhwc_map(&map_d0, d0, frames, H, W, dec2_te_rows() + 2);
     if (rc) return rc;
     return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
   }
@@ -764,19 +762,22 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   DR_STOP_CHECK();
   launch_v2p_tc(e->map_tok, vp, s);
   e->mark(6, s);
+  // decode.0 with decode.2's tap-expanded GEMM fused into its epilogue (E planes), then
+  // the decode.2 gather + tanh + composite
   ConvTcArgs cv{};
   cv.frames = B; cv.H = e->H; cv.W = e->W;
-  cv.w = e->wtc; cv.bias = e->fparams + e->bd0; cv.out16 = e->d0;
+  cv.w = e->wtc; cv.bias = e->fparams + e->bd0;
+  cv.e_planes = e->eplanes; cv.w2 = e->timg + e->te_d2;
   DR_STOP_CHECK();
   launch_conv3x3_tc(64, e->map_raster, cv, s);
   e->mark(7, s);
   ConvTcArgs c2{};
   c2.frames = B; c2.H = e->H; c2.W = e->W;
-  c2.w = e->timg + e->te_d2; c2.bias = e->fparams + e->bd2;
+  c2.bias = e->fparams + e->bd2; c2.e_planes = e->eplanes;
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
   DR_STOP_CHECK();
-  launch_dec2_te(e->map_d0, c2, s);
+  launch_dec2_gather(c2, s);
   e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
   e->mark(8, s);
 #undef DR_STOP_CHECK

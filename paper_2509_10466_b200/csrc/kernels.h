@@ -110,6 +110,12 @@ struct ConvTcArgs {
   float* out_f32;
   uint8_t* out_u8;
   int* flags;
+  // fused decode.0 -> decode.2 (tap-expanded): decode.0's epilogue multiplies its fp16
+  // LeakyReLU output by w2 (K-major 128B-swizzled [32 u][64 ci], u = 3*(3*ky+kx)+co) on
+  // the tensor cores and stores E as fp16 planes [frames][27][H][W] instead of the 64-ch
+  // raster; launch_dec2_gather then sums the 3x3 neighbourhood and runs the tail
+  __half* e_planes;
+  const void* w2;
 };
 }  // namespace dr
 #include <cuda.h>
@@ -129,10 +135,8 @@ struct V2pArgs {
 size_t v2p_tc_weight_bytes();
 void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s);
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
-// decode.2 + tail as a tap-expanded GEMM (conv_tc.cu); w = [u 32][ci 64] fp16 K-major SW128
-// image, u = 3*(3*ky + kx) + co (27 real rows); input halo box = dec2_te_rows() + 2 rows
-void launch_dec2_te(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
-int dec2_te_rows();
+// decode.2 gather + tail over the E planes the fused decode.0 wrote (conv_tc.cu)
+void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- frame byte kernels
 // (frame_ops.cu): display composite / upscale2x, merge + redact, point-cloud pack.
