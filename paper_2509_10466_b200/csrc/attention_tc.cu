@@ -164,7 +164,19 @@ DR_DEV unsigned long long gtimer() {
     if (warp == 2 && lane == 0 && cta_ < TRACE_CTAS) g_trace[cta_ * 16 + (slot)] = (value);   \
   } while (0)
 #define DR_TRACE_T(slot) DR_TRACE_AT(slot, gtimer())
+// cycle accumulators (clock64): 11 softmax wait on S, 12 softmax wait on the S TMEM load,
+// 13 softmax loop total, 14 rescale passes, 15 MMA warp wait on P (warp 1)
+#define DR_CYC(var) long long var = clock64()
+#define DR_ACC(acc, since) acc += clock64() - (since)
+#define DR_TRACE_W1(slot, value)                                                             \
+  do {                                                                                       \
+    const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);        \
+    if (warp == 1 && lane == 0 && cta_ < TRACE_CTAS) g_trace[cta_ * 16 + (slot)] = (value);   \
+  } while (0)
 #else
+#define DR_CYC(var) do {} while (0)
+#define DR_ACC(acc, since) do {} while (0)
+#define DR_TRACE_W1(slot, value) do {} while (0)
 #define DR_TRACE_AT(slot, value) do {} while (0)
 #define DR_TRACE_T(slot) do {} while (0)
 #endif
@@ -318,9 +330,18 @@ attn_tc_kernel(AttnArgs a) {
     };
     if (nb > 0) s_mma(0);
     if (nb > 1) s_mma(1);
+#ifdef DR_TRACE
+    long long cyc_p = 0;
+#endif
     for (int j = 0; j < nb; ++j) {
       const int st = j % STAGES, b = j & 1;
+#ifdef DR_TRACE
+      DR_CYC(t_p);
+#endif
       tc::mbar_wait(&sm.p_full[b], (uint32_t)(j >> 1) & 1u);
+#ifdef DR_TRACE
+      DR_ACC(cyc_p, t_p);
+#endif
       tc::fence_after();
       const uint64_t vd = sdesc_sw32(tc::smem_u32(&sm.v[st][0][0][0]), KB * ROW_BYTES, 256);
       const uint32_t pcol = tbase + TM_P + (KB / 2) * b;
@@ -335,6 +356,9 @@ attn_tc_kernel(AttnArgs a) {
     // pv_done may trail the softmax by two phases at the end (parity aliasing), so the
     // final O read has its own single-phase barrier
     if (nb > 0) tc::mma_commit_warp(&sm.o_done);
+#ifdef DR_TRACE
+    DR_TRACE_W1(15, (unsigned long long)cyc_p);
+#endif
   } else {
     // ---------------------------------------------------------------- softmax warps
     const int q = warp & 3;                            // TMEM lanes 32q.. (warp id % 4)
@@ -345,8 +369,18 @@ attn_tc_kernel(AttnArgs a) {
     uint32_t r[KB];                                    // this row's scores of S(j)
     // wait for S(jj) (its commit also says P(jj-2)*V has released P buffer jj&1) and start
     // the TMEM loads; the registers are scoreboarded, the consumer waits on first use
+#ifdef DR_TRACE
+    long long cyc_s = 0, cyc_ld = 0, n_resc = 0;
+    const long long cyc_loop0 = clock64();
+#endif
     auto load_s = [&](int jj) {
+#ifdef DR_TRACE
+      DR_CYC(t_s);
+#endif
       tc::mbar_wait(&sm.s_full[jj & 1], (uint32_t)(jj >> 1) & 1u);
+#ifdef DR_TRACE
+      DR_ACC(cyc_s, t_s);
+#endif
       tc::fence_after();
       const uint32_t s_col = lane_base + TM_S + KB * (jj & 1);
 #pragma unroll
@@ -357,7 +391,13 @@ attn_tc_kernel(AttnArgs a) {
       const int st = j % STAGES, b = j & 1;
       const int n_valid = min(KB, n_keys - (kb0 + j) * KB);
       const uint32_t p_col = lane_base + TM_P + (KB / 2) * b;
+#ifdef DR_TRACE
+      DR_CYC(t_ld);
+#endif
       tc::tmem_wait_ld();
+#ifdef DR_TRACE
+      DR_ACC(cyc_ld, t_ld);
+#endif
       if (j == 0) DR_TRACE_T(2);
       // key bias / tail mask for score column c of this block
       auto adjust = [&](float v, int c) -> float {
@@ -403,6 +443,9 @@ attn_tc_kernel(AttnArgs a) {
       // after the first block).  S(j) is still intact: P lives in its own columns.
       const bool need = rmax > m + RESCALE_SLACK;
       if (__any_sync(0xffffffffu, need)) {
+#ifdef DR_TRACE
+        ++n_resc;
+#endif
         const float mn = need ? rmax : m;
         if (j > 0) {                                   // rescale this warp's O rows
           // P(j-1)*V has landed in O.  Unambiguous: S(j) ready implies P(j-2)*V complete,
@@ -430,6 +473,12 @@ attn_tc_kernel(AttnArgs a) {
       if (lane == 0) tc::mbar_arrive(&sm.p_full[b]);
     }
     DR_TRACE_T(3);
+#ifdef DR_TRACE
+    DR_TRACE_AT(11, (unsigned long long)cyc_s);
+    DR_TRACE_AT(12, (unsigned long long)cyc_ld);
+    DR_TRACE_AT(13, (unsigned long long)(clock64() - cyc_loop0));
+    DR_TRACE_AT(14, (unsigned long long)n_resc);
+#endif
     float o[16], l = 0.f;
     if (nb > 0) {
       tc::mbar_wait(&sm.o_done, 0);                   // committed once, after the last P*V

@@ -71,6 +71,11 @@ def main():
         print("  pair loop-end gap", pct(pair_gap))
         print("  tail            ", pct(rel[:, 5] - rel[:, 4]))
         print("  exit            ", pct(rel[:, 5]))
+        cyc = t[:, 11:16].astype(np.float64) / 1965.0        # us at 1965 MHz
+        print("  softmax warp: wait S p50 %.2f, wait S ld p50 %.2f, loop p50 %.2f us; rescales p50 %d"
+              % (np.median(cyc[:, 0]), np.median(cyc[:, 1]), np.median(cyc[:, 2]),
+                 np.median(t[:, 14])))
+        print("  MMA warp: wait P p50 %.2f us" % np.median(cyc[:, 4]))
         per_sm = Counter(t[:, 6])
         print("  CTAs per SM     ", Counter(per_sm.values()), "SMs used", len(per_sm))
         # per-SM busy span: first entry to last exit
