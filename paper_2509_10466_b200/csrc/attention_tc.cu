@@ -4,18 +4,19 @@
 // spatial blocks attend over the whole frame (:146-150), temporal blocks attend a row band
 // of queries to cat[band(cur), band(slot0), band(slot1)] (:166-191).
 //
-// One CTA = 128 queries x one head x half of the keys; a 2-CTA cluster covers all keys and
-// merges the two halves through distributed shared memory.  Per 128-key block:
-//   MMA warp      S = Q K^T         tcgen05.mma M=128 N=128 K=16, smem x smem -> TMEM
-//                 O += P [V | 1]    8 x tcgen05.mma M=128 N=32 K=16, A = P from TMEM, B = V
+// One CTA = 128 queries x one head x one of `ksplit` key parts (1 or 2, per launch); the
+// parts of a tile form a thread-block cluster and merge through distributed shared memory
+// into rank 0.  Per 64-key block:
+//   MMA warp      S = Q K^T         tcgen05.mma M=128 N=64 K=16, smem x smem -> TMEM
+//                 O += P [V | 1]    4 x tcgen05.mma M=128 N=32 K=16, A = P from TMEM, B = V
 //                                   (MN-major) plus a constant ones block at the LBO offset,
 //                                   so column 16 of O accumulates the softmax row sum
-//   4 softmax warps (thread = query row = TMEM lane): ONE tcgen05.ld sweep of its 128
-//                 scores (TMEM read bandwidth, not MUFU, bounds a two-pass softmax here):
-//                 one FFMA + one MUFU ex2 per score (log2 domain) against the running
-//                 base, row max tracked on the side, fp16 pack, tcgen05.st P;
-//                 no shuffles, no HMMA, no per-key index math on the math warps
-//   producer warp cp.async.bulk of the 128-key K and V blocks into a 3-stage ring
+//   4 softmax warps (thread = query row = TMEM lane): ONE tcgen05.ld sweep of its 64
+//                 scores, released at once so that S(j+1) is computed under softmax(j):
+//                 one FFMA + one ex2 per score (log2 domain; a quarter of them on the FMA
+//                 pipe) against the running base, row max tracked on the side, fp16 pack,
+//                 tcgen05.st P; no shuffles, no per-key index math on the math warps
+//   producer warp cp.async.bulk of the 64-key K and V blocks into a 4-stage ring
 // The QKV producer (token_tc.cu) stores q/k/v rows with the 16-byte chunk swizzle of
 // the UMMA 32-byte swizzle mode, so bulk copies land as valid SWIZZLE_32B operands.
 // The running max is rescaled lazily (only when a row max grows by > 2^8; exact because
@@ -41,9 +42,18 @@ constexpr int QROWS = 128;
 constexpr int KB = 64;                        // keys per block
 constexpr int STAGES = 4;
 constexpr int THREADS = 192;                  // warp 0 loads, warp 1 MMA, warps 2-5 softmax
-// TMEM (double-buffered S and P so that S(j+1) is ready when softmax(j) ends):
-//   S[b] fp32 64 cols at 64b, P[b] fp16 pairs 32 cols at 128 + 32b, O 32 cols (16 + row sum)
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 192, TM_COLS = 256;
+// Two CTAs per SM (168 registers per thread).  A third CTA needs <= 96 registers (the
+// register file is split per SM sub-partition and a 6-warp CTA puts two warps on two of
+// them); measured, the 96-register softmax is ~40% slower per block, which three-way
+// interleaving does not recover (0.42 vs 0.37 us per 128x64 block per SM).  The keys of a
+// query tile are split over `ksplit` CTAs (chosen per launch, attention_ksplit): 2 at
+// batch 1 (256 CTAs for 148 SMs), 1 at large batch (no merge at all).
+constexpr int CTAS_PER_SM = 2;
+constexpr int MAX_KSPLIT = 2;                 // larger clusters pack poorly into GPCs
+// TMEM, 128 columns (up to four CTAs per SM): S fp32 64 cols (single: the softmax warps
+// release it as soon as S(j) is in registers, so S(j+1) is computed under softmax(j)),
+// P fp16 pairs 32 cols, O 32 cols (16 + row sum)
+constexpr uint32_t TM_S = 0, TM_P = 64, TM_O = 96, TM_COLS = 128;
 constexpr float RESCALE_SLACK = 8.f;          // log2 units: p <= 2^8 between rescales
 #ifndef DR_POLY_EVERY
 #define DR_POLY_EVERY 4
@@ -56,9 +66,9 @@ struct __align__(1024) Smem {
   __half k[STAGES][KB][DH];                   // SW32 K-major B operand of S
   __half v[STAGES][2][KB][DH];                // [0] V block, [1] constant ones block (+4 KB)
   float bias[STAGES][KB];                     // mask-aware mode only
-  float mrg[QROWS][20];                       // cluster merge: m, l, o[16] of key half 1 (+pad)
-  uint64_t q_full, kv_full[STAGES], kv_empty[STAGES], s_full[2], p_full[2], pv_done, o_done;
-  uint64_t mrg_full;                          // rank 0: 128 remote arrivals of rank 1's rows
+  uint64_t q_full, kv_full[STAGES], kv_empty[STAGES], s_full, s_free, p_full, pv_done, o_done;
+  float mrg[MAX_KSPLIT - 1][QROWS][20];       // rank 0: m, l, o[16] of ranks 1.. (+pad)
+  uint64_t mrg_full;                          // rank 0: remote arrivals of the other ranks' rows
   uint32_t tmem_base;
 };
 
@@ -149,7 +159,7 @@ DR_DEV int seg_of(int kk, int band) { return kk >= band ? (kk >= 2 * band ? 2 : 
 // Diagnostic build only (-DDR_TRACE, build.py --trace): global-timer stamps per CTA taken by
 // softmax warp 2, read back by scripts/attn_trace.py.  Slots: 0 entry, 1 after pdl_wait,
 // 2 S(0) in registers, 3 softmax loop done, 4 merge done, 5 exit, 6 SM id, 7 blocks,
-// 8 O in registers, 9 DSMEM stores issued, 10 cluster rank.
+// 8 O in registers, 9 DSMEM stores issued, 10 key part.
 #ifdef DR_TRACE
 constexpr int TRACE_CTAS = 8192;
 __device__ unsigned long long g_trace[TRACE_CTAS * 16];
@@ -181,20 +191,21 @@ DR_DEV unsigned long long gtimer() {
 #define DR_TRACE_T(slot) do {} while (0)
 #endif
 
-template <bool MASKED>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 2)
+template <bool MASKED, int KSPLIT>
+__global__ void __cluster_dims__(KSPLIT, 1, 1) __launch_bounds__(THREADS, CTAS_PER_SM)
 attn_tc_kernel(AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_rank();                 // key half
-  const int qtile = blockIdx.x >> 1, h = blockIdx.y;
+  constexpr int ksplit = KSPLIT;
+  const int qtile = blockIdx.x / ksplit, h = blockIdx.y;
+  const int crank = (int)cluster_rank();                  // key part
   const int frame = blockIdx.z / a.groups, grp = blockIdx.z - frame * a.groups;
   const int band0 = grp * a.band;
   const int q0 = qtile * QROWS;
   const int n_keys = a.n_seg * a.band;
   const int n_kb = (n_keys + KB - 1) / KB;
-  const int nkb_h = (n_kb + 1) / 2;
+  const int nkb_h = (n_kb + ksplit - 1) / ksplit;
   const int kb0 = crank * nkb_h;
   const int nb = max(0, min(n_kb, kb0 + nkb_h) - kb0);   // this CTA's blocks
 
@@ -218,19 +229,18 @@ attn_tc_kernel(AttnArgs a) {
       tc::mbar_init(&sm.kv_full[s], 1);
       tc::mbar_init(&sm.kv_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&sm.s_full[b], 1);
-      tc::mbar_init(&sm.p_full[b], 4);
-    }
+    tc::mbar_init(&sm.s_full, 1);
+    tc::mbar_init(&sm.s_free, 4);
+    tc::mbar_init(&sm.p_full, 4);
     tc::mbar_init(&sm.pv_done, 1);
     tc::mbar_init(&sm.o_done, 1);
-    tc::mbar_init(&sm.mrg_full, QROWS);
+    if (ksplit > 1) tc::mbar_init(&sm.mrg_full, (ksplit - 1) * QROWS);
     tc::fence_barrier_init();
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  // cluster-wide: both CTAs' barriers are initialised before any remote arrive (this is the
-  // only cluster barrier; it runs before pdl_wait, overlapping the predecessor kernel)
-  cluster_sync();
+  // cluster-wide: all ranks' barriers are initialised before any remote arrive (the only
+  // cluster barrier; it runs before pdl_wait, overlapping the predecessor kernel)
+  if (ksplit > 1) cluster_sync();
   pdl_wait();
   // TMEM is allocated only after the predecessor grid completed (PDL early trigger: a CTA
   // never holds TMEM while waiting on another grid, so allocations cannot deadlock)
@@ -312,12 +322,11 @@ attn_tc_kernel(AttnArgs a) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = tc::idesc_f16(128, KB);                   // K-major B
     constexpr uint32_t idesc_pv = tc::idesc_f16(128, 32) | (1u << 16);     // MN-major B
-    // Issue order: S(0), S(1), then per block j: [p_full(j): softmax has read S(j) and
-    // written P(j)] O += P(j) V_j -> kv_empty, pv_done; S(j+2) into the freed S buffer.
-    // tcgen05 ops complete in issue order, so the commit of S(j+1) (issued after P(j-1)V)
-    // certifies that P(j-1)V has read P buffer (j+1)&1 before softmax(j+1) overwrites it;
-    // O itself may still be accumulating P(j)V during softmax(j+1), which therefore waits on
-    // pv_done(j) before it rescales O (the rare path).
+    // Issue order: S(0), then per block j: [s_free(j): S(j) is in the softmax registers]
+    // S(j+1) -> s_full; [p_full(j): P(j) written] O += P(j) V_j -> kv_empty, pv_done.
+    // Softmax(j+1) waits pv_done(j) before it overwrites P or rescales O.  tcgen05 ops
+    // complete in issue order, so S(j) ready implies P(j-2)V complete: pv_done is then in
+    // phase j-1 or later, never two phases behind (no parity aliasing).
     const uint64_t qd = sdesc_sw32(tc::smem_u32(&sm.q[0][0]), 16, 256);
     tc::mbar_wait(&sm.q_full, 0);
     auto s_mma = [&](int jj) {
@@ -325,36 +334,38 @@ attn_tc_kernel(AttnArgs a) {
       tc::mbar_wait(&sm.kv_full[st], (uint32_t)(jj / STAGES) & 1u);
       tc::fence_after();
       const uint64_t kd = sdesc_sw32(tc::smem_u32(&sm.k[st][0][0]), 16, 256);
-      tc::mma_f16_warp(tbase + TM_S + KB * (jj & 1), qd, kd, idesc_s, 0);
-      tc::mma_commit_warp(&sm.s_full[jj & 1]);
+      tc::mma_f16_warp(tbase + TM_S, qd, kd, idesc_s, 0);
+      tc::mma_commit_warp(&sm.s_full);
     };
     if (nb > 0) s_mma(0);
-    if (nb > 1) s_mma(1);
 #ifdef DR_TRACE
     long long cyc_p = 0;
 #endif
     for (int j = 0; j < nb; ++j) {
-      const int st = j % STAGES, b = j & 1;
+      const int st = j % STAGES;
+      if (j + 1 < nb) {
+        tc::mbar_wait(&sm.s_free, (uint32_t)j & 1u);
+        tc::fence_after();
+        s_mma(j + 1);
+      }
 #ifdef DR_TRACE
       DR_CYC(t_p);
 #endif
-      tc::mbar_wait(&sm.p_full[b], (uint32_t)(j >> 1) & 1u);
+      tc::mbar_wait(&sm.p_full, (uint32_t)j & 1u);
 #ifdef DR_TRACE
       DR_ACC(cyc_p, t_p);
 #endif
       tc::fence_after();
       const uint64_t vd = sdesc_sw32(tc::smem_u32(&sm.v[st][0][0][0]), KB * ROW_BYTES, 256);
-      const uint32_t pcol = tbase + TM_P + (KB / 2) * b;
+      const uint32_t pcol = tbase + TM_P;
 #pragma unroll
       for (int kk = 0; kk < KB / 16; ++kk)
         mma_ts_warp(tbase + TM_O, pcol + 8 * kk, vd + (uint64_t)(kk * 16 * ROW_BYTES / 16),
                     idesc_pv, (j | kk) != 0);
       tc::mma_commit_warp(&sm.kv_empty[st]);
       tc::mma_commit_warp(&sm.pv_done);
-      if (j + 2 < nb) s_mma(j + 2);
     }
-    // pv_done may trail the softmax by two phases at the end (parity aliasing), so the
-    // final O read has its own single-phase barrier
+    // the final O read has its own single-phase barrier
     if (nb > 0) tc::mma_commit_warp(&sm.o_done);
 #ifdef DR_TRACE
     DR_TRACE_W1(15, (unsigned long long)cyc_p);
@@ -367,8 +378,8 @@ attn_tc_kernel(AttnArgs a) {
     const float sl2 = 0.25f * 1.4426950408889634f;     // 1/sqrt(16) * log2(e)
     float m = -INFINITY;
     uint32_t r[KB];                                    // this row's scores of S(j)
-    // wait for S(jj) (its commit also says P(jj-2)*V has released P buffer jj&1) and start
-    // the TMEM loads; the registers are scoreboarded, the consumer waits on first use
+    // wait for S(jj) and start the TMEM loads; the registers are scoreboarded, the consumer
+    // waits on first use
 #ifdef DR_TRACE
     long long cyc_s = 0, cyc_ld = 0, n_resc = 0;
     const long long cyc_loop0 = clock64();
@@ -377,20 +388,20 @@ attn_tc_kernel(AttnArgs a) {
 #ifdef DR_TRACE
       DR_CYC(t_s);
 #endif
-      tc::mbar_wait(&sm.s_full[jj & 1], (uint32_t)(jj >> 1) & 1u);
+      tc::mbar_wait(&sm.s_full, (uint32_t)jj & 1u);
 #ifdef DR_TRACE
       DR_ACC(cyc_s, t_s);
 #endif
       tc::fence_after();
-      const uint32_t s_col = lane_base + TM_S + KB * (jj & 1);
+      const uint32_t s_col = lane_base + TM_S;
 #pragma unroll
       for (int ch = 0; ch < KB / 32; ++ch) DR_TMEM_LD32(s_col + 32 * ch, (r + 32 * ch));
     };
     if (nb > 0) load_s(0);
     for (int j = 0; j < nb; ++j) {
-      const int st = j % STAGES, b = j & 1;
+      const int st = j % STAGES;
       const int n_valid = min(KB, n_keys - (kb0 + j) * KB);
-      const uint32_t p_col = lane_base + TM_P + (KB / 2) * b;
+      const uint32_t p_col = lane_base + TM_P;
 #ifdef DR_TRACE
       DR_CYC(t_ld);
 #endif
@@ -398,6 +409,10 @@ attn_tc_kernel(AttnArgs a) {
 #ifdef DR_TRACE
       DR_ACC(cyc_ld, t_ld);
 #endif
+      // S(j) is in registers: hand the S columns back to the MMA warp for S(j+1)
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.s_free);
       if (j == 0) DR_TRACE_T(2);
       // key bias / tail mask for score column c of this block
       auto adjust = [&](float v, int c) -> float {
@@ -431,6 +446,12 @@ attn_tc_kernel(AttnArgs a) {
             else
               pk[c] = pack_half2(ex2(fmaf(s0, sl2, -base)), ex2(fmaf(s1, sl2, -base)));
           }
+          // P(j-1)*V must have read the P columns (first chunk only; a redo sweep finds
+          // the phase already complete: P(j)*V is not issued before this warp arrives)
+          if (ch == 0 && j > 0) {
+            tc::mbar_wait(&sm.pv_done, (uint32_t)(j - 1) & 1u);
+            tc::fence_after();
+          }
           DR_TMEM_ST16(p_col + 16 * ch, pk);
         }
         return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
@@ -440,7 +461,7 @@ attn_tc_kernel(AttnArgs a) {
                               : sweep(base0, std::true_type{}, std::false_type{});
       // The running base m may lag the true max by RESCALE_SLACK (p <= 2^8, exact since
       // numerator and denominator share it); past that, rescale O and redo the sweep (rare
-      // after the first block).  S(j) is still intact: P lives in its own columns.
+      // after the first block).  S(j) is still intact in registers.
       const bool need = rmax > m + RESCALE_SLACK;
       if (__any_sync(0xffffffffu, need)) {
 #ifdef DR_TRACE
@@ -448,29 +469,29 @@ attn_tc_kernel(AttnArgs a) {
 #endif
         const float mn = need ? rmax : m;
         if (j > 0) {                                   // rescale this warp's O rows
-          // P(j-1)*V has landed in O.  Unambiguous: S(j) ready implies P(j-2)*V complete,
-          // and P(j)*V is not issued before this warp arrives, so pv_done is in phase j-1 or j.
-          tc::mbar_wait(&sm.pv_done, (uint32_t)(j - 1) & 1u);
-          tc::fence_after();
+          // P(j-1)*V has landed in O (waited in the sweep above)
           const float cfac = (need && m != -INFINITY) ? ex2(m - mn) : (need ? 0.f : 1.f);
-          uint32_t o[32];
-          DR_TMEM_LD32(lane_base + TM_O, o);
-          tc::tmem_wait_ld();
+#pragma unroll 1
+          for (int h16 = 0; h16 < 2; ++h16) {          // 16 columns at a time (registers)
+            uint32_t o[16];
+            tc::tmem_ld16(lane_base + TM_O + 16 * h16, o);
+            tc::tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * cfac);
-          DR_TMEM_ST32(lane_base + TM_O, o);
+            for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * cfac);
+            DR_TMEM_ST16(lane_base + TM_O + 16 * h16, o);
+          }
         }
         m = mn;
         tmem_wait_st();                                // P stores of the optimistic sweep
         sweep(m == -INFINITY ? 0.f : m, std::false_type{}, std::false_type{});  // any block
       }
-      // prefetch S(j+1) (normally complete already: S is double-buffered) so its TMEM load
-      // latency overlaps the completion of the P(j) stores and the hand-off
+      // prefetch S(j+1) (normally complete already: issued when S(j) was released) so its
+      // TMEM load latency overlaps the completion of the P(j) stores and the hand-off
       if (j + 1 < nb) load_s(j + 1);
       tmem_wait_st();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.p_full[b]);
+      if (lane == 0) tc::mbar_arrive(&sm.p_full);
     }
     DR_TRACE_T(3);
 #ifdef DR_TRACE
@@ -495,36 +516,53 @@ attn_tc_kernel(AttnArgs a) {
     }
     DR_TRACE_T(8);
     DR_TRACE_AT(10, crank);
-    // ---- merge the key halves: rank 1 ships its (m, l, o) row into rank 0's shared memory
-    // (5 vector DSMEM stores) and arrives on rank 0's mrg_full with release semantics; rank
-    // 0 acquires it.  No end-of-kernel cluster barrier: rank 1 may retire at once, rank 0
-    // (the only CTA whose shared memory is accessed remotely) outlives the stores it waits on.
-    if (crank == 1) {
-      const uint32_t dst = map_cluster(tc::smem_u32(&sm.mrg[row][0]), 0);
+    // ---- merge the key parts: ranks 1.. ship their (m, l, o) row into rank 0's shared
+    // memory (5 vector DSMEM stores) and arrive on rank 0's mrg_full with release
+    // semantics; rank 0 acquires it.  No end-of-kernel cluster barrier: the other ranks may
+    // retire at once, rank 0 (the only CTA whose shared memory is accessed remotely)
+    // outlives the stores it waits on.
+    if (crank != 0) {
+      const uint32_t dst = map_cluster(tc::smem_u32(&sm.mrg[crank - 1][row][0]), 0);
       st_cluster_v4(dst, m, l, 0.f, 0.f);
 #pragma unroll
       for (int d = 0; d < 16; d += 4) st_cluster_v4(dst + 16 + 4 * d, o[d], o[d + 1], o[d + 2], o[d + 3]);
       mbar_arrive_remote(map_cluster(tc::smem_u32(&sm.mrg_full), 0));
       DR_TRACE_T(9);
-    } else {
+    } else if (ksplit > 1) {
       DR_TRACE_T(9);
       mbar_wait_cluster(&sm.mrg_full, 0);
+      float M = m;
+#pragma unroll
+      for (int r1 = 0; r1 < ksplit - 1; ++r1) M = fmaxf(M, sm.mrg[r1][row][0]);
+      const float b = M == -INFINITY ? 0.f : M;
+      const float a0 = ex2(m - b);
+      l *= a0;
+#pragma unroll
+      for (int d = 0; d < 16; ++d) o[d] *= a0;
+#pragma unroll
+      for (int r1 = 0; r1 < ksplit - 1; ++r1) {
+        const float4* mr = reinterpret_cast<const float4*>(&sm.mrg[r1][row][0]);
+        const float4 ml = mr[0];
+        const float a1 = ex2(ml.x - b);
+        l += ml.y * a1;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 o1 = mr[1 + q4];
+          o[4 * q4] += o1.x * a1;
+          o[4 * q4 + 1] += o1.y * a1;
+          o[4 * q4 + 2] += o1.z * a1;
+          o[4 * q4 + 3] += o1.w * a1;
+        }
+      }
     }
     DR_TRACE_T(4);
     if (crank == 0 && q0 + row < a.band) {
-      const float4* mr = reinterpret_cast<const float4*>(&sm.mrg[row][0]);
-      const float4 ml = mr[0];
-      const float M = fmaxf(m, ml.x);
-      const float b = M == -INFINITY ? 0.f : M;
-      const float a0 = ex2(m - b), a1 = ex2(ml.x - b);
-      const float lt = l * a0 + ml.y * a1;
-      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
       uint32_t outp[8];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        const float4 o1 = mr[1 + q4];
-        outp[2 * q4] = pack_half2((o[4 * q4] * a0 + o1.x * a1) * inv, (o[4 * q4 + 1] * a0 + o1.y * a1) * inv);
-        outp[2 * q4 + 1] = pack_half2((o[4 * q4 + 2] * a0 + o1.z * a1) * inv, (o[4 * q4 + 3] * a0 + o1.w * a1) * inv);
+        outp[2 * q4] = pack_half2(o[4 * q4] * inv, o[4 * q4 + 1] * inv);
+        outp[2 * q4 + 1] = pack_half2(o[4 * q4 + 2] * inv, o[4 * q4 + 3] * inv);
       }
       uint4* dst = reinterpret_cast<uint4*>(a.out + ((size_t)frame * a.T + band0 + q0 + row) * C + h * DH);
       dst[0] = make_uint4(outp[0], outp[1], outp[2], outp[3]);
@@ -543,23 +581,60 @@ attn_tc_kernel(AttnArgs a) {
 void trace_snapshot(cudaStream_t s, int n_cta);
 #endif
 
-void launch_attention(const AttnArgs& a, cudaStream_t s) {
+namespace {
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+int q_tiles(const AttnArgs& a) { return (a.band + QROWS - 1) / QROWS * HEADS * a.frames * a.groups; }
+}  // namespace
+
+// Key split of a launch: the k in 1..MAX_KSPLIT minimising waves x (blocks per CTA + merge cost) x
+// the per-block time at the SM concurrency the launch reaches (measured, see CTAS_PER_SM).
+int attention_ksplit(const AttnArgs& a) {
+  const int sms = sm_count(), tiles = q_tiles(a);
+  const int n_kb = (a.n_seg * a.band + KB - 1) / KB;
+  const double t_conc[CTAS_PER_SM + 1] = {0.0, 0.575, 0.74};   // us per block per CTA
+  int best = 1;
+  double best_cost = 1e30;
+  for (int k = 1; k <= MAX_KSPLIT; ++k) {
+    const long n_cta = (long)tiles * k;
+    const long slots = (long)sms * CTAS_PER_SM;
+    const long waves = (n_cta + slots - 1) / slots;
+    const int conc = waves > 1 ? CTAS_PER_SM : (int)((n_cta + sms - 1) / sms);
+    const double cost = (double)waves * ((n_kb + k - 1) / k + (k > 1 ? 1 : 0)) * t_conc[conc];
+    if (cost < best_cost * 0.98) { best_cost = cost; best = k; }
+  }
+  return best;
+}
+
+void launch_attention(const AttnArgs& a_in, cudaStream_t s) {
   static bool init = false;
-  // TMEM holds exactly two CTAs (2 x 256 columns): pad shared memory so that a third CTA
-  // is never co-resident (it would spin in tcgen05.alloc and stall its cluster partner).
-  constexpr int SMEM_2PER_SM = 80 * 1024;
-  static_assert(sizeof(Smem) <= SMEM_2PER_SM, "attention smem exceeds the 2-per-SM pad");
-  const int smem = SMEM_2PER_SM;
+  // Residency is capped by registers (168 per thread, two CTAs); TMEM (128 columns per CTA)
+  // holds four, so tcgen05.alloc never waits; shared memory must not be the cap.
+  static_assert(sizeof(Smem) + 1024 <= 227 * 1024 / CTAS_PER_SM, "attention smem caps residency");
+  static_assert(CTAS_PER_SM * TM_COLS <= 512, "TMEM over-subscribed");
+  const int smem = (int)sizeof(Smem);
   if (!init) {
-    cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_tc_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
-  dim3 grid(2 * ((a.band + QROWS - 1) / QROWS), HEADS, a.frames * a.groups);
-  if (a.mask_mode != 0 && a.key_valid)
-    launch_pdl(attn_tc_kernel<true>, grid, dim3(THREADS), smem, s, a);
+  AttnArgs a = a_in;
+  const int k = (a.ksplit >= 1 && a.ksplit <= MAX_KSPLIT) ? a.ksplit : attention_ksplit(a);
+  const dim3 grid(k * ((a.band + QROWS - 1) / QROWS), HEADS, a.frames * a.groups);
+  const bool masked = a.mask_mode != 0 && a.key_valid;
+  if (k == 2)
+    launch_pdl(masked ? attn_tc_kernel<true, 2> : attn_tc_kernel<false, 2>, grid, dim3(THREADS), smem, s, a);
   else
-    launch_pdl(attn_tc_kernel<false>, grid, dim3(THREADS), smem, s, a);
+    launch_pdl(masked ? attn_tc_kernel<true, 1> : attn_tc_kernel<false, 1>, grid, dim3(THREADS), smem, s, a);
 #ifdef DR_TRACE
   trace_snapshot(s, (int)(grid.x * grid.y * grid.z));
 #endif
@@ -592,3 +667,17 @@ extern "C" int dr_debug_attn_trace(int idx, unsigned long long* host, int n) {
   return k;
 }
 #endif
+
+// Occupancy diagnostics of the attention kernel: out[0] CTAs per SM, out[1] registers per
+// thread, out[2] static smem, out[3] dynamic smem, out[4] last CUDA error.
+extern "C" int dr_debug_attn_occupancy(int* out) {
+  const int smem = (int)sizeof(dr::Smem);
+  cudaFuncSetAttribute(dr::attn_tc_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, dr::attn_tc_kernel<false, 2>);
+  int n = -1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dr::attn_tc_kernel<false, 2>, dr::THREADS, smem);
+  out[0] = n; out[1] = fa.numRegs; out[2] = (int)fa.sharedSizeBytes; out[3] = smem;
+  out[4] = (int)cudaGetLastError();
+  return 0;
+}

@@ -69,8 +69,11 @@ struct AttnArgs {
   const uint8_t* key_valid;
   int mask_mode;             // 0 off, 1 spatial (fallback if none valid), 2 temporal raw,
                              // 3 temporal collapsed (mask iff frame has no valid token)
+  // key split: CTAs (one cluster) per query tile, 1..4; 0 = chosen by attention_ksplit
+  int ksplit;
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+int attention_ksplit(const AttnArgs& a);
 
 // ---------------------------------------------------------------- mask stage
 struct MaskArgs {

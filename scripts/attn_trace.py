@@ -80,14 +80,10 @@ def main():
         print("  CTAs per SM     ", Counter(per_sm.values()), "SMs used", len(per_sm))
         # per-SM busy span: first entry to last exit
         loop = rel[:, 3] - rel[:, 2]
-        two = [s for s, c in per_sm.items() if c >= 2]
-        one = [s for s, c in per_sm.items() if c == 1]
         sm = t[:, 6]
-        if two:
-            print("  loop on 2-CTA SMs", pct(loop[np.isin(sm, two)]))
-        if one:
-            print("  loop on 1-CTA SMs", pct(loop[np.isin(sm, one)]))
-
+        for cnt in sorted(set(per_sm.values()), reverse=True):
+            sms = [s for s, c in per_sm.items() if c == cnt]
+            print(f"  loop on {cnt}-CTA SMs", pct(loop[np.isin(sm, sms)]))
 
 if __name__ == "__main__":
     main()

@@ -32,7 +32,7 @@ def stage_of(name: str, grid: str) -> str:
         return "vec2patch"
     if "conv3x3_tc_kernel<64" in name:
         return "decode0"
-    if "conv3x3_tc_kernel<16" in name or "dec2_te" in name:
+    if "conv3x3_tc_kernel<16" in name or "dec2_te" in name or "dec2_gather" in name:
         return "decode2_composite"
     return "other:" + name[:40]
 
