@@ -325,19 +325,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// decode.2 gather + tail over the fused decode.0's E planes: one thread per output pixel,
-// out[co] = b[co] + sum_{dy,dx} E[3*(3dy+dx)+co][y+dy-1][x+dx-1] (0 off-image = the conv's
-// zero padding), then (tanh + 1) / 2, non-finite guard and the alpha composite.  Each E
-// value feeds exactly one output pixel, so the 27 reads per pixel are coalesced plane rows
-// with no reuse to stage.
-__global__ void __launch_bounds__(256) dec2_gather_kernel(ConvTcArgs a) {
-  const int x = blockIdx.x * 256 + threadIdx.x, y = blockIdx.y, f = blockIdx.z;
-  pdl_trigger();
-  float bias[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
-  pdl_wait();
-  if (x >= a.W) return;
+DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int y, int f) {
   const size_t plane = (size_t)a.H * a.W;
   const __half* ep = a.e_planes + (size_t)f * 27 * plane;
   float o[3] = {bias[0], bias[1], bias[2]};
@@ -377,8 +365,41 @@ __global__ void __launch_bounds__(256) dec2_gather_kernel(ConvTcArgs a) {
       a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
     }
   }
-  if (__any_sync(0xffffffffu, bad) && bad) atomicOr(a.flags + f, 1);
+  if (bad) {
+    atomicOr(a.flags + f, 1);
+    __threadfence();                 // performed before this CTA counts itself done
+  }
 }
+
+// decode.2 gather + tail over the fused decode.0's E planes: one thread per output pixel,
+// out[co] = b[co] + sum_{dy,dx} E[3*(3dy+dx)+co][y+dy-1][x+dx-1] (0 off-image = the conv's
+// zero padding), then (tanh + 1) / 2, non-finite guard and the alpha composite.  Each E
+// value feeds exactly one output pixel, so the 27 reads per pixel are coalesced plane rows
+// with no reuse to stage.
+__global__ void __launch_bounds__(256) dec2_gather_kernel(ConvTcArgs a) {
+  const int x = blockIdx.x * 256 + threadIdx.x, y = blockIdx.y, f = blockIdx.z;
+  pdl_trigger();
+  float bias[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
+  pdl_wait();
+  if (x < a.W) gather_pixel(a, bias, x, y, f);
+  if (a.flags_mirror) {
+    // the CTA that finishes last publishes the flags words (every CTA's atomicOr happens
+    // before its counter increment; the last one acquires them all)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+      if (atomicAdd(a.done, 1u) == total - 1) {
+        __threadfence();
+        for (int i = 0; i < a.frames; ++i) a.flags_mirror[i] = atomicOr(a.flags + i, 0);
+        *a.done = 0;
+      }
+    }
+  }
+}
+
 
 template <int N, int TR, bool FUSE>
 void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <immintrin.h>
+
 #include "../../include/dr_b200.h"
 #include "kernels.h"
 
@@ -28,38 +30,74 @@ namespace {
 
 thread_local std::string g_err;
 
+// memcpy with non-temporal (streaming) stores for buffers a DMA engine reads next: lines
+// left dirty in the CPU caches make the H2D snoop them (measured on the B200 box, 1 MB:
+// 34.9 us after memcpy vs 25.3 us after streaming stores, scripts/pcie_microbench.cu).
+void memcpy_nt(uint8_t* dst, const uint8_t* src, size_t n) {
+  size_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head; src += head; n -= head;
+  size_t i = 0;
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
+// Evict lines from the CPU caches: a DMA write into lines the CPU holds is slowed by the
+// snoops (768 KB D2H: 30.4 us into just-read lines, 19.9 us after clflushopt,
+// scripts/pcie_microbench.cu).  Run on the pinned D2H staging buffer after the copy-out,
+// off the caller's critical path (CopyPool::evict_async).
+__attribute__((target("clflushopt"))) void evict_lines(const uint8_t* p, size_t n) {
+  const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)63, a1 = (uintptr_t)p + n;
+  for (uintptr_t a = a0; a < a1; a += 64) _mm_clflushopt(reinterpret_cast<void*>(a));
+  _mm_sfence();
+}
+
 // Host staging copies (pageable <-> pinned) split over a small pool of worker threads: one
 // core moves ~20 GB/s, so a 512^2 frame's ~1.8 MB of staging would otherwise cost ~100 us
 // per call.  The workers spin for ~2 ms after each job (a frame loop calls again well
 // within that) and then sleep, so back-to-back calls pay no thread wake-up latency.
+// Modes: plain; CP_NT streaming stores (the destination is a pinned buffer a DMA reads
+// next); CP_EVICT (internal) evict `src` lines, no copy.
+enum CopyMode { CP_PLAIN = 0, CP_NT = 1, CP_EVICT = 2 };
 class CopyPool {
  public:
   static CopyPool& get() {
     static CopyPool pool;
     return pool;
   }
-  void copy(void* dst, const void* src, size_t n) {
+  void copy(void* dst, const void* src, size_t n, int nt) {
     constexpr size_t kMin = 192 * 1024;
     if (n < kMin || workers_.empty()) {
-      std::memcpy(dst, src, n);
+      part_copy(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n, nt);
       return;
     }
     std::lock_guard<std::mutex> job(job_mu_);            // one job at a time (engines on
     const int parts = (int)workers_.size() + 1;         // several host threads)
     const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      dst_ = static_cast<uint8_t*>(dst);
-      src_ = static_cast<const uint8_t*>(src);
-      n_ = n;
-      chunk_ = chunk;
-      pending_.store(parts - 1, std::memory_order_relaxed);
-      gen_.fetch_add(1, std::memory_order_release);
-    }
-    cv_.notify_all();
-    std::memcpy(dst, src, std::min(chunk, n));          // the caller takes part 0
+    post(dst, src, n, chunk, nt, 1);
+    part_copy(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), std::min(chunk, n),
+              nt);                                       // the caller takes part 0
     while (pending_.load(std::memory_order_acquire) != 0) {
     }
+  }
+  // Evict [p, p + n) from the CPU caches on the workers and return at once; the next job
+  // waits for it.
+  void evict_async(const void* p, size_t n) {
+    if (workers_.empty() || n == 0) return;
+    std::lock_guard<std::mutex> job(job_mu_);
+    const int parts = (int)workers_.size();
+    post(nullptr, p, n, ((n + parts - 1) / parts + 63) & ~(size_t)63, CP_EVICT, 0);
   }
   ~CopyPool() {
     stop_.store(true);
@@ -73,6 +111,22 @@ class CopyPool {
     const unsigned hw = std::thread::hardware_concurrency();
     const int n = (int)std::min(7u, hw > 1 ? hw - 1 : 0u);
     for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i + 1); });
+  }
+  // publish a job once the previous (possibly asynchronous) one has drained; workers take
+  // parts (worker index - first), the caller part 0 when first == 1
+  void post(void* dst, const void* src, size_t n, size_t chunk, int mode, int first) {
+    while (pending_.load(std::memory_order_acquire) != 0) {
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    dst_ = static_cast<uint8_t*>(dst);
+    src_ = static_cast<const uint8_t*>(src);
+    n_ = n;
+    chunk_ = chunk;
+    nt_ = mode;
+    first_ = first;
+    pending_.store((int)workers_.size(), std::memory_order_relaxed);
+    gen_.fetch_add(1, std::memory_order_release);
+    cv_.notify_all();
   }
   void run(int part) {
     uint64_t seen = 0;
@@ -88,10 +142,15 @@ class CopyPool {
       }
       seen = gen_.load(std::memory_order_acquire);
       if (stop_.load()) return;
-      const size_t o = (size_t)part * chunk_;
-      if (o < n_) std::memcpy(dst_ + o, src_ + o, std::min(chunk_, n_ - o));
+      const size_t o = (size_t)(part - 1 + first_) * chunk_;
+      if (o < n_) part_copy(dst_ + o, src_ + o, std::min(chunk_, n_ - o), nt_);
       pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
+  }
+  static void part_copy(uint8_t* d, const uint8_t* s, size_t n, int mode) {
+    if (mode == CP_NT) memcpy_nt(d, s, n);
+    else if (mode == CP_EVICT) evict_lines(s, n);
+    else std::memcpy(d, s, n);
   }
   std::vector<std::thread> workers_;
   std::mutex job_mu_;
@@ -103,9 +162,13 @@ class CopyPool {
   uint8_t* dst_ = nullptr;
   const uint8_t* src_ = nullptr;
   size_t n_ = 0, chunk_ = 0;
+  int nt_ = CP_PLAIN;
+  int first_ = 1;
 };
 
-void par_memcpy(void* dst, const void* src, size_t n) { CopyPool::get().copy(dst, src, n); }
+void par_memcpy(void* dst, const void* src, size_t n, int nt = CP_PLAIN) {
+  CopyPool::get().copy(dst, src, n, nt);
+}
 
 // any nonzero byte in a row (8 bytes at a time)
 bool row_any(const uint8_t* row, int w) {
@@ -251,7 +314,8 @@ struct dr_engine {
   size_t last_d2h = 0;                                           // host path: D2H bytes
   int stop_after = -1;               // DR_STOP_AFTER=k (diagnostics): launch only k kernels
   uint8_t* pin = nullptr;                                        // pinned staging
-  int* pin_flags = nullptr;
+  int* flags_mirror = nullptr;       // host path: decode.2's last CTA copies flags here
+  unsigned* d_done = nullptr;        // decode.2 finished-CTA counter (flags mirror)
   // optional per-stage CUDA events (dr_profile): ev[0] before the first stage
   static constexpr int kMaxEv = 64;
   int profiling = 0, n_ev = 0;
@@ -550,12 +614,11 @@ void dr_destroy(dr_engine* e) {
   cudaFree(e->wtc);
   cudaFree(e->timg);
   cudaFree(e->h_rgb);
-  cudaFree(e->h_m0);
-  cudaFree(e->h_out);
+  cudaFree(e->h_out);                          // (h_m0 lives inside h_rgb)
+  cudaFree(e->d_done);
   for (auto* r : e->ring) cudaFree(r);
   for (auto& ev : e->ev) if (ev) cudaEventDestroy(ev);
   if (e->pin) cudaFreeHost(e->pin);
-  if (e->pin_flags) cudaFreeHost(e->pin_flags);
   delete e;
 }
 
@@ -776,6 +839,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   c2.bias = e->fparams + e->bd2; c2.e_planes = e->eplanes;
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
+  c2.flags_mirror = e->flags_mirror; c2.done = e->d_done;
   DR_STOP_CHECK();
   launch_dec2_gather(c2, s);
   e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
@@ -846,43 +910,71 @@ int dr_reset_memory(dr_engine* e) {
   return DR_OK;
 }
 
+// Diagnostics (DR_E2E_TRACE=1): host phase times of the last dr_inpaint_u8_host call (us):
+// staging in, H2D + forward enqueue, D2H enqueue + host fill, stream sync, band copy-out;
+// device times from events: H2D, forward, D2H.  Read by scripts/e2e_breakdown.py.
+namespace {
+struct E2eTrace {
+  bool on = std::getenv("DR_E2E_TRACE") != nullptr;
+  double host[5] = {};
+  float dev[3] = {};
+  cudaEvent_t ev[4] = {};
+};
+E2eTrace& e2e_trace() {
+  static E2eTrace t;
+  return t;
+}
+double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+extern "C" int dr_debug_e2e_trace(double* out8) {
+  E2eTrace& t = e2e_trace();
+  if (!t.on) return -1;
+  for (int i = 0; i < 5; ++i) out8[i] = t.host[i];
+  for (int i = 0; i < 3; ++i) out8[5 + i] = t.dev[i];
+  return 0;
+}
+
 int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
                        uint8_t* out_hwc, void* stream) {
   if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
   CUDA_TRY(cudaSetDevice(e->device));
   const size_t px = e->frame_px();
   if (!e->h_rgb) {
-    CUDA_TRY(cudaMalloc(&e->h_rgb, px * 3));
-    CUDA_TRY(cudaMalloc(&e->h_m0, px));
-    CUDA_TRY(cudaMalloc(&e->h_out, px * 3));
-    CUDA_TRY(cudaMallocHost(&e->pin, px * 7));
-    CUDA_TRY(cudaMallocHost(&e->pin_flags, sizeof(int)));
+    CUDA_TRY(cudaMalloc(&e->h_rgb, px * 4));         // rgb then mask: one H2D
+    e->h_m0 = e->h_rgb + px * 3;
+    CUDA_TRY(cudaMalloc(&e->h_out, px * 3 + 64));    // + room for the flags mirror
+    CUDA_TRY(cudaMalloc(&e->d_done, sizeof(unsigned)));
+    CUDA_TRY(cudaMemset(e->d_done, 0, sizeof(unsigned)));
+    CUDA_TRY(cudaMallocHost(&e->pin, px * 7 + 64));
     int rc = dr_reset_memory(e);
     if (rc) return rc;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  E2eTrace& tr = e2e_trace();
+  double tt[6] = {};
+  if (tr.on) {
+    if (!tr.ev[0])
+      for (auto& ev : tr.ev) cudaEventCreate(&ev);
+    tt[0] = now_us();
+  }
   uint8_t* p_rgb = e->pin;
   uint8_t* p_m0 = e->pin + px * 3;
   uint8_t* p_out = e->pin + px * 4;
-  par_memcpy(p_rgb, rgb_hwc, px * 3);
-  par_memcpy(p_m0, mask_hw, px);
-  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, px, cudaMemcpyHostToDevice, s));
-  int fresh = 0;
-  while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
-  dr_frame_io io{};
-  io.frames = 1;
-  io.rgb_u8 = e->h_rgb; io.mask_m0 = e->h_m0;
-  io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
-  io.new_slot = e->ring[fresh];
-  io.out_u8 = e->h_out;
-  io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
-  int rc = dr_forward(e, &io, stream);
-  if (rc) return rc;
-  e->ring_own[fresh] = true;         // contents and slot K/V cache entry now agree
+  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
+  par_memcpy(p_m0, mask_hw, px, CP_NT);
+  if (tr.on) {
+    tt[1] = now_us();
+    cudaEventRecord(tr.ev[0], s);
+  }
+  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 4, cudaMemcpyHostToDevice, s));
+  if (tr.on) cudaEventRecord(tr.ev[1], s);
   // Only rows within r + R of a masked row can differ from the input (alpha = 0 keeps the
   // input byte exactly): copy back that band, and fill the other rows from the
-  // input on the host while the GPU runs.  (On an error return `out` holds partial data.)
+  // input on the host while the GPU runs.  The decode.2 kernel's last CTA mirrors the
+  // frame's flags word just past the band, so one D2H brings both back.
   const int H = e->H, W = e->W, halo = e->cfg.mask_dilate + e->feather_r;
   int ymin = 0, ymax = H - 1;                     // first / last masked row (scan inward)
   while (ymin < H && !row_any(mask_hw + (size_t)ymin * W, W)) ++ymin;
@@ -894,19 +986,51 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
     b1 = std::min(H, ymax + halo + 1);
   }
   const size_t rowb = (size_t)W * 3;
-  if (b1 > b0)
-    CUDA_TRY(cudaMemcpyAsync(p_out + b0 * rowb, e->h_out + b0 * rowb, (b1 - b0) * rowb,
-                             cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(e->pin_flags, e->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  const size_t mirror = (b1 * rowb + 3) & ~(size_t)3;            // byte offset in h_out
+  e->flags_mirror = reinterpret_cast<int*>(e->h_out + mirror);
+  int fresh = 0;
+  while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
+  dr_frame_io io{};
+  io.frames = 1;
+  io.rgb_u8 = e->h_rgb; io.mask_m0 = e->h_m0;
+  io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
+  io.new_slot = e->ring[fresh];
+  io.out_u8 = e->h_out;
+  io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
+  int rc = dr_forward(e, &io, stream);
+  e->flags_mirror = nullptr;
+  if (rc) return rc;
+  if (tr.on) {
+    cudaEventRecord(tr.ev[2], s);
+    tt[2] = now_us();
+  }
+  e->ring_own[fresh] = true;         // contents and slot K/V cache entry now agree
+  // (On an error return `out` holds partial data.)
+  CUDA_TRY(cudaMemcpyAsync(p_out + b0 * rowb, e->h_out + b0 * rowb, mirror + 4 - b0 * rowb,
+                           cudaMemcpyDeviceToHost, s));
+  if (tr.on) cudaEventRecord(tr.ev[3], s);
   par_memcpy(out_hwc, rgb_hwc, b0 * rowb);
   par_memcpy(out_hwc + b1 * rowb, rgb_hwc + b1 * rowb, (H - b1) * rowb);
+  if (tr.on) tt[3] = now_us();
   CUDA_TRY(cudaStreamSynchronize(s));
-  const int fl = *e->pin_flags;
+  if (tr.on) tt[4] = now_us();
+  int fl;
+  std::memcpy(&fl, p_out + mirror, sizeof(int));
   if (fl & DR_FLAG_UNREDACTED)
     return fail(DR_ERR_INPUT, "input is not redacted: nonzero pixels inside mask");
   if (fl & DR_FLAG_NONFINITE) return fail(DR_ERR_NUMERIC, "model produced non-finite output");
   par_memcpy(out_hwc + b0 * rowb, p_out + b0 * rowb, (b1 - b0) * rowb);
-  e->last_d2h = (b1 - b0) * rowb + sizeof(int);
+  CopyPool::get().evict_async(p_out + b0 * rowb, mirror + 4 - b0 * rowb);
+  if (tr.on) {
+    tt[5] = now_us();
+    for (int i = 0; i < 5; ++i) tr.host[i] = tt[i + 1] - tt[i];
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      const cudaError_t err = cudaEventElapsedTime(&ms, tr.ev[i], tr.ev[i + 1]);
+      tr.dev[i] = err == cudaSuccess ? 1e3f * ms : -(float)err;
+    }
+  }
+  e->last_d2h = mirror + 4 - b0 * rowb;
   e->mem0 = e->mem1;
   e->mem1 = fresh;
   return DR_OK;

@@ -119,6 +119,10 @@ struct ConvTcArgs {
   // raster; launch_dec2_gather then sums the 3x3 neighbourhood and runs the tail
   __half* e_planes;
   const void* w2;
+  // decode.2 gather (optional): the last CTA to finish copies flags[0..frames) here;
+  // `done` is a zeroed counter the last CTA re-arms
+  int* flags_mirror;
+  unsigned* done;
 };
 }  // namespace dr
 #include <cuda.h>

@@ -231,6 +231,32 @@ def test_host_buffer_path_equals_device_path(rng):
         assert np.array_equal(a.rgb, b)
 
 
+def test_host_buffer_path_edges_and_errors(rng):
+    """Host path: empty mask (no band, flags-only read-back), full mask (flags mirror past
+    the last row), unredacted input and non-finite output reported through the mirror."""
+    cfg = DsttConfig.baseline(64, mask_dilate=2, mask_feather_sigma=1.5)
+    eng = DsttEngine(cfg, seed=4)
+    mem = eng.zero_memory()
+    rgb = rng.integers(0, 256, (64, 64, 3), dtype=np.uint8)
+    empty = np.zeros((64, 64), bool)
+    a = eng.inpaint(rgb, BinaryMask(empty), mem)
+    assert np.array_equal(eng.inpaint_host(rgb, empty), a.rgb)
+    full = np.ones((64, 64), bool)
+    z = np.zeros_like(rgb)
+    b = eng.inpaint(z, BinaryMask(full), a.memory)
+    assert np.array_equal(eng.inpaint_host(z, full), b.rgb)
+    bits = np.zeros((64, 64), bool)
+    bits[10:20, 10:20] = True
+    with pytest.raises(InputError):
+        eng.inpaint_host(np.full((64, 64, 3), 7, np.uint8), bits)          # not redacted
+    w = seed_parameters(cfg, 0)
+    w[-4] = np.full_like(w[-4], np.nan)
+    bad = DsttEngine.from_arrays(cfg, w)
+    for m in (empty, full):
+        with pytest.raises(EngineNumericError):
+            bad.inpaint_host(np.zeros((64, 64, 3), np.uint8), m)
+
+
 def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
     """Carried engine outputs reuse their cached K/V; clones recompute; bit-identical."""
     cfg = DsttConfig.baseline(128, mask_dilate=2, mask_feather_sigma=1.0)
