@@ -504,7 +504,7 @@ def run_ours(args):
                "p50_ms_host": round(statistics.median(host_ms), 4),
                "p99_ms_host": round(float(np.percentile(host_ms, 99)), 4),
                "api": "dr_inpaint_u8_host (u8 HWC frame + mask in, u8 composite out, "
-                      "engine-held memory; only rows within r+R of the mask are read back)"}
+                      "engine-held memory; only the per-row spans within r+R of the mask are read back, packed)"}
     barrier()
 
     cpu = None

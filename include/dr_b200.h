@@ -111,9 +111,10 @@ int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, 
 int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
                        uint8_t* out_hwc, void* stream);
 
-/* Device->host bytes the last dr_inpaint_u8_host copied: only the rows within
- * mask_dilate + feather radius of a masked row can differ from the input (the composite
- * keeps the input byte where alpha = 0), so only that band is read back (+ 4 flag bytes). */
+/* Device->host bytes the last dr_inpaint_u8_host copied: only pixels within mask_dilate +
+ * feather radius (square) of a masked pixel can differ from the input (the composite keeps
+ * the input byte where alpha = 0), so only each row's span covering them is read back,
+ * packed (+ 4 flag bytes). */
 int64_t dr_host_d2h_bytes(dr_engine* e);
 
 /* Reset the engine-held memory of dr_inpaint_u8_host to two zero slots. */

@@ -345,6 +345,9 @@ DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int
   }
   const size_t pix = (size_t)y * a.W + x;
   const float alr = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
+  int4 sp = make_int4(0, 0, 0, 0);
+  if (a.packed) sp = __ldg(a.spans + y);
+  const bool in_span = a.packed && x >= sp.x && x < sp.y;
   bool bad = false;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
@@ -354,7 +357,7 @@ DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int
     if (a.fill) a.fill[pl] = out01;
     if (a.out_f32)
       a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), __ldg(a.rgb_f32 + pl)));
-    if (a.out_u8) {
+    if (a.out_u8 || in_span) {
       const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
       const uint8_t src8 = __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch);
       uint8_t ov;
@@ -362,7 +365,8 @@ DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int
       else if (alr == 1.f) ov = fill8;
       else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
                                                       __fmul_rn(__fsub_rn(1.0f, alr), (float)src8))), 0.f), 255.f);
-      a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
+      if (a.out_u8) a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
+      if (in_span) a.packed[sp.z + 3 * (x - sp.x) + ch] = ov;
     }
   }
   if (bad) {

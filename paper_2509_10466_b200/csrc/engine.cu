@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -56,50 +57,49 @@ void memcpy_nt(uint8_t* dst, const uint8_t* src, size_t n) {
 // Evict lines from the CPU caches: a DMA write into lines the CPU holds is slowed by the
 // snoops (768 KB D2H: 30.4 us into just-read lines, 19.9 us after clflushopt,
 // scripts/pcie_microbench.cu).  Run on the pinned D2H staging buffer after the copy-out,
-// off the caller's critical path (CopyPool::evict_async).
+// off the caller's critical path (WorkPool::run_async).
 __attribute__((target("clflushopt"))) void evict_lines(const uint8_t* p, size_t n) {
   const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)63, a1 = (uintptr_t)p + n;
   for (uintptr_t a = a0; a < a1; a += 64) _mm_clflushopt(reinterpret_cast<void*>(a));
   _mm_sfence();
 }
 
-// Host staging copies (pageable <-> pinned) split over a small pool of worker threads: one
-// core moves ~20 GB/s, so a 512^2 frame's ~1.8 MB of staging would otherwise cost ~100 us
-// per call.  The workers spin for ~2 ms after each job (a frame loop calls again well
-// within that) and then sleep, so back-to-back calls pay no thread wake-up latency.
-// Modes: plain; CP_NT streaming stores (the destination is a pinned buffer a DMA reads
-// next); CP_EVICT (internal) evict `src` lines, no copy.
-enum CopyMode { CP_PLAIN = 0, CP_NT = 1, CP_EVICT = 2 };
-class CopyPool {
+// Host staging work (pageable <-> pinned copies, span scatter, cache eviction) split over a
+// small pool of worker threads: one core moves ~20 GB/s, so a 512^2 frame's ~1.8 MB of
+// staging would otherwise cost ~100 us per call.  The workers spin for ~2 ms after each job
+// (a frame loop calls again well within that) and then sleep, so back-to-back calls pay no
+// thread wake-up latency.  A job is fn(part, parts); run() has the caller take part 0 and
+// waits, run_async() leaves every part to the workers and returns (the next job waits).
+class WorkPool {
  public:
-  static CopyPool& get() {
-    static CopyPool pool;
+  using Fn = std::function<void(int, int)>;
+  static WorkPool& get() {
+    static WorkPool pool;
     return pool;
   }
-  void copy(void* dst, const void* src, size_t n, int nt) {
-    constexpr size_t kMin = 192 * 1024;
-    if (n < kMin || workers_.empty()) {
-      part_copy(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n, nt);
+  int parts() const { return (int)workers_.size() + 1; }
+  void run(Fn fn) {
+    if (workers_.empty()) {
+      fn(0, 1);
       return;
     }
     std::lock_guard<std::mutex> job(job_mu_);            // one job at a time (engines on
-    const int parts = (int)workers_.size() + 1;         // several host threads)
-    const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
-    post(dst, src, n, chunk, nt, 1);
-    part_copy(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), std::min(chunk, n),
-              nt);                                       // the caller takes part 0
+    post(std::move(fn), 1);                              // several host threads)
+    fn_(0, parts());
     while (pending_.load(std::memory_order_acquire) != 0) {
     }
   }
-  // Evict [p, p + n) from the CPU caches on the workers and return at once; the next job
-  // waits for it.
-  void evict_async(const void* p, size_t n) {
-    if (workers_.empty() || n == 0) return;
+  void run_async(Fn fn) {
+    if (workers_.empty()) {
+      fn(0, 1);
+      return;
+    }
     std::lock_guard<std::mutex> job(job_mu_);
-    const int parts = (int)workers_.size();
-    post(nullptr, p, n, ((n + parts - 1) / parts + 63) & ~(size_t)63, CP_EVICT, 0);
+    post(std::move(fn), 0);
   }
-  ~CopyPool() {
+  ~WorkPool() {
+    while (pending_.load(std::memory_order_acquire) != 0) {
+    }
     stop_.store(true);
     gen_.fetch_add(1);
     cv_.notify_all();
@@ -107,28 +107,24 @@ class CopyPool {
   }
 
  private:
-  CopyPool() {
+  WorkPool() {
     const unsigned hw = std::thread::hardware_concurrency();
     const int n = (int)std::min(7u, hw > 1 ? hw - 1 : 0u);
-    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i + 1); });
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
   }
-  // publish a job once the previous (possibly asynchronous) one has drained; workers take
-  // parts (worker index - first), the caller part 0 when first == 1
-  void post(void* dst, const void* src, size_t n, size_t chunk, int mode, int first) {
+  // publish a job once the previous (possibly asynchronous) one has drained; worker w
+  // (1..n) takes part w - 1 + first of parts n + first
+  void post(Fn fn, int first) {
     while (pending_.load(std::memory_order_acquire) != 0) {
     }
     std::lock_guard<std::mutex> lk(mu_);
-    dst_ = static_cast<uint8_t*>(dst);
-    src_ = static_cast<const uint8_t*>(src);
-    n_ = n;
-    chunk_ = chunk;
-    nt_ = mode;
+    fn_ = std::move(fn);
     first_ = first;
     pending_.store((int)workers_.size(), std::memory_order_relaxed);
     gen_.fetch_add(1, std::memory_order_release);
     cv_.notify_all();
   }
-  void run(int part) {
+  void loop(int w) {
     uint64_t seen = 0;
     while (true) {
       // spin ~2 ms for the next job, then block on the condition variable
@@ -142,15 +138,9 @@ class CopyPool {
       }
       seen = gen_.load(std::memory_order_acquire);
       if (stop_.load()) return;
-      const size_t o = (size_t)(part - 1 + first_) * chunk_;
-      if (o < n_) part_copy(dst_ + o, src_ + o, std::min(chunk_, n_ - o), nt_);
+      fn_(w - 1 + first_, (int)workers_.size() + first_);
       pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
-  }
-  static void part_copy(uint8_t* d, const uint8_t* s, size_t n, int mode) {
-    if (mode == CP_NT) memcpy_nt(d, s, n);
-    else if (mode == CP_EVICT) evict_lines(s, n);
-    else std::memcpy(d, s, n);
   }
   std::vector<std::thread> workers_;
   std::mutex job_mu_;
@@ -159,28 +149,93 @@ class CopyPool {
   std::atomic<uint64_t> gen_{0};
   std::atomic<int> pending_{0};
   std::atomic<bool> stop_{false};
-  uint8_t* dst_ = nullptr;
-  const uint8_t* src_ = nullptr;
-  size_t n_ = 0, chunk_ = 0;
-  int nt_ = CP_PLAIN;
+  Fn fn_;
   int first_ = 1;
 };
 
-void par_memcpy(void* dst, const void* src, size_t n, int nt = CP_PLAIN) {
-  CopyPool::get().copy(dst, src, n, nt);
+// [part * n / parts, (part + 1) * n / parts) rounded to 64-byte boundaries
+inline void part_range(size_t n, int part, int parts, size_t* b, size_t* e) {
+  const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
+  *b = std::min(n, (size_t)part * chunk);
+  *e = std::min(n, *b + chunk);
 }
 
-// any nonzero byte in a row (8 bytes at a time)
-bool row_any(const uint8_t* row, int w) {
-  int x = 0;
-  for (; x + 8 <= w; x += 8) {
-    uint64_t v;
-    std::memcpy(&v, row + x, 8);
-    if (v) return true;
+// Copy modes: plain; CP_NT streaming stores (the destination is a pinned buffer a DMA
+// reads next).
+enum CopyMode { CP_PLAIN = 0, CP_NT = 1 };
+
+// Copy split over the pool (small copies inline).
+void par_memcpy(void* dst, const void* src, size_t n, int mode = CP_PLAIN) {
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  auto one = [mode](uint8_t* dd, const uint8_t* ss, size_t nn) {
+    if (mode == CP_NT) memcpy_nt(dd, ss, nn);
+    else std::memcpy(dd, ss, nn);
+  };
+  if (n < 192 * 1024) {
+    one(d, s, n);
+    return;
   }
-  for (; x < w; ++x)
-    if (row[x]) return true;
-  return false;
+  WorkPool::get().run([&](int part, int parts) {
+    size_t b, e;
+    part_range(n, part, parts, &b, &e);
+    if (e > b) one(d + b, s + b, e - b);
+  });
+}
+
+// out[y] = op over v[y - r .. y + r] (clipped to [0, n)), op = min or max, in O(n):
+// van Herk / Gil-Werman prefix and suffix runs over blocks of 2r + 1 on an array padded
+// with the identity.
+template <bool MAX>
+void window_reduce(const int* v, int n, int r, int identity, int* out, std::vector<int>& buf) {
+  const int k = 2 * r + 1, m = n + 2 * r;
+  const int mb = (m + k - 1) / k * k;
+  buf.assign(3 * (size_t)mb, identity);
+  int* a = buf.data();
+  int* g = a + mb;
+  int* h = g + mb;
+  auto op = [](int x, int y) { return MAX ? std::max(x, y) : std::min(x, y); };
+  for (int i = 0; i < n; ++i) a[i + r] = v[i];
+  for (int b = 0; b < mb; b += k) {
+    g[b] = a[b];
+    for (int i = b + 1; i < b + k; ++i) g[i] = op(g[i - 1], a[i]);
+    h[b + k - 1] = a[b + k - 1];
+    for (int i = b + k - 2; i >= b; --i) h[i] = op(h[i + 1], a[i]);
+  }
+  for (int y = 0; y < n; ++y) out[y] = op(h[y], g[y + 2 * r]);   // padded window [y, y + 2r]
+}
+
+// first / last nonzero byte of a row (-1, -1 if none), 16 bytes at a time
+void row_extent(const uint8_t* row, int w, int* first, int* last) {
+  int x = 0, f = -1;
+  for (; x + 16 <= w && f < 0; x += 16) {
+    const int nz = ~_mm_movemask_epi8(_mm_cmpeq_epi8(
+                       _mm_loadu_si128(reinterpret_cast<const __m128i*>(row + x)), _mm_setzero_si128())) & 0xFFFF;
+    if (nz) f = x + __builtin_ctz(nz);
+  }
+  for (; x < w && f < 0; ++x)
+    if (row[x]) f = x;
+  *first = f;
+  if (f < 0) {
+    *last = -1;
+    return;
+  }
+  int l = f, e = w;
+  for (; e - 16 >= f; e -= 16) {
+    const int nz = ~_mm_movemask_epi8(_mm_cmpeq_epi8(
+                       _mm_loadu_si128(reinterpret_cast<const __m128i*>(row + e - 16)), _mm_setzero_si128())) & 0xFFFF;
+    if (nz) {
+      l = e - 16 + 31 - __builtin_clz(nz);
+      *last = l;
+      return;
+    }
+  }
+  for (int xx = e - 1; xx > f; --xx)
+    if (row[xx]) {
+      l = xx;
+      break;
+    }
+  *last = l;
 }
 
 int fail(int code, const std::string& msg) {
@@ -315,6 +370,10 @@ struct dr_engine {
   int stop_after = -1;               // DR_STOP_AFTER=k (diagnostics): launch only k kernels
   uint8_t* pin = nullptr;                                        // pinned staging
   int* flags_mirror = nullptr;       // host path: decode.2's last CTA copies flags here
+  const int4* pack_spans = nullptr;  // host path: per-row [x0, x1, byte offset] (device)
+  uint8_t* pack_out = nullptr;       // host path: span-packed composite (device)
+  std::vector<int> span_first, span_last;   // host path scratch: masked extent per row
+  std::vector<int> span_wmin, span_wmax, span_buf;
   unsigned* d_done = nullptr;        // decode.2 finished-CTA counter (flags mirror)
   // optional per-stage CUDA events (dr_profile): ev[0] before the first stage
   static constexpr int kMaxEv = 64;
@@ -840,6 +899,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
   c2.flags_mirror = e->flags_mirror; c2.done = e->d_done;
+  if (B == 1) { c2.spans = e->pack_spans; c2.packed = e->pack_out; }
   DR_STOP_CHECK();
   launch_dec2_gather(c2, s);
   e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
@@ -942,13 +1002,19 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
   CUDA_TRY(cudaSetDevice(e->device));
   const size_t px = e->frame_px();
+  const int H = e->H, W = e->W, halo = e->cfg.mask_dilate + e->feather_r;
+  // input staging: [rgb px*3][mask px][pad to 16][row spans H x int4], one H2D; output
+  // staging: span-packed composite bytes + the flags word
+  const size_t in_spans = (px * 4 + 15) & ~(size_t)15;
+  const size_t in_bytes = in_spans + (size_t)H * 16;
+  const size_t out_cap = px * 3 + 64;
   if (!e->h_rgb) {
-    CUDA_TRY(cudaMalloc(&e->h_rgb, px * 4));         // rgb then mask: one H2D
+    CUDA_TRY(cudaMalloc(&e->h_rgb, in_bytes));
     e->h_m0 = e->h_rgb + px * 3;
-    CUDA_TRY(cudaMalloc(&e->h_out, px * 3 + 64));    // + room for the flags mirror
+    CUDA_TRY(cudaMalloc(&e->h_out, out_cap));
     CUDA_TRY(cudaMalloc(&e->d_done, sizeof(unsigned)));
     CUDA_TRY(cudaMemset(e->d_done, 0, sizeof(unsigned)));
-    CUDA_TRY(cudaMallocHost(&e->pin, px * 7 + 64));
+    CUDA_TRY(cudaMallocHost(&e->pin, in_bytes + out_cap));
     int rc = dr_reset_memory(e);
     if (rc) return rc;
   }
@@ -962,32 +1028,54 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   }
   uint8_t* p_rgb = e->pin;
   uint8_t* p_m0 = e->pin + px * 3;
-  uint8_t* p_out = e->pin + px * 4;
+  int* p_span = reinterpret_cast<int*>(e->pin + in_spans);        // [H][x0, x1, off, 0]
+  uint8_t* p_out = e->pin + in_bytes;
+  // Only pixels within r + R (square) of a masked pixel can differ from the input (alpha
+  // = 0 keeps the input byte exactly).  Per row, the span [x0, x1) covering
+  // them is the union of the masked extents of the rows within r + R, widened by r + R;
+  // decode.2 writes only those bytes, packed row after row, and its last CTA appends the
+  // frame's flags word: one D2H of ~the masked area instead of the frame.
+  std::vector<int>& fl_x = e->span_first;
+  std::vector<int>& ll_x = e->span_last;
+  fl_x.resize(H);
+  ll_x.resize(H);
+  WorkPool::get().run([&](int part, int parts) {
+    for (int y = part * H / parts; y < (part + 1) * H / parts; ++y)
+      row_extent(mask_hw + (size_t)y * W, W, &fl_x[y], &ll_x[y]);
+  });
+  for (int y = 0; y < H; ++y)
+    if (fl_x[y] < 0) fl_x[y] = W;                  // empty row: identity of the min
+  std::vector<int>& wmin = e->span_wmin;
+  std::vector<int>& wmax = e->span_wmax;
+  wmin.resize(H);
+  wmax.resize(H);
+  window_reduce<false>(fl_x.data(), H, halo, W, wmin.data(), e->span_buf);
+  window_reduce<true>(ll_x.data(), H, halo, -1, wmax.data(), e->span_buf);
+  size_t total = 0;
+  int n_rows = 0;
+  for (int y = 0; y < H; ++y) {
+    const int x0 = wmin[y], x1 = wmax[y];
+    int* sp = p_span + 4 * y;
+    if (x1 < 0) {
+      sp[0] = sp[1] = 0;
+    } else {
+      sp[0] = std::max(0, x0 - halo);
+      sp[1] = std::min(W, x1 + halo + 1);
+      ++n_rows;
+    }
+    sp[2] = (int)total;
+    sp[3] = 0;
+    total += (size_t)(sp[1] - sp[0]) * 3;
+  }
+  const size_t mirror = (total + 3) & ~(size_t)3;                 // flags word offset
   par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
   par_memcpy(p_m0, mask_hw, px, CP_NT);
   if (tr.on) {
     tt[1] = now_us();
     cudaEventRecord(tr.ev[0], s);
   }
-  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 4, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, in_bytes, cudaMemcpyHostToDevice, s));
   if (tr.on) cudaEventRecord(tr.ev[1], s);
-  // Only rows within r + R of a masked row can differ from the input (alpha = 0 keeps the
-  // input byte exactly): copy back that band, and fill the other rows from the
-  // input on the host while the GPU runs.  The decode.2 kernel's last CTA mirrors the
-  // frame's flags word just past the band, so one D2H brings both back.
-  const int H = e->H, W = e->W, halo = e->cfg.mask_dilate + e->feather_r;
-  int ymin = 0, ymax = H - 1;                     // first / last masked row (scan inward)
-  while (ymin < H && !row_any(mask_hw + (size_t)ymin * W, W)) ++ymin;
-  if (ymin == H) ymax = -1;
-  while (ymax >= ymin && ymax >= 0 && !row_any(mask_hw + (size_t)ymax * W, W)) --ymax;
-  int b0 = 0, b1 = 0;                // band [b0, b1) of rows that may change
-  if (ymax >= 0) {
-    b0 = std::max(0, ymin - halo);
-    b1 = std::min(H, ymax + halo + 1);
-  }
-  const size_t rowb = (size_t)W * 3;
-  const size_t mirror = (b1 * rowb + 3) & ~(size_t)3;            // byte offset in h_out
-  e->flags_mirror = reinterpret_cast<int*>(e->h_out + mirror);
   int fresh = 0;
   while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
   dr_frame_io io{};
@@ -995,9 +1083,13 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   io.rgb_u8 = e->h_rgb; io.mask_m0 = e->h_m0;
   io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
   io.new_slot = e->ring[fresh];
-  io.out_u8 = e->h_out;
   io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
+  e->pack_spans = reinterpret_cast<const int4*>(e->h_rgb + in_spans);
+  e->pack_out = e->h_out;
+  e->flags_mirror = reinterpret_cast<int*>(e->h_out + mirror);
   int rc = dr_forward(e, &io, stream);
+  e->pack_spans = nullptr;
+  e->pack_out = nullptr;
   e->flags_mirror = nullptr;
   if (rc) return rc;
   if (tr.on) {
@@ -1006,11 +1098,9 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   }
   e->ring_own[fresh] = true;         // contents and slot K/V cache entry now agree
   // (On an error return `out` holds partial data.)
-  CUDA_TRY(cudaMemcpyAsync(p_out + b0 * rowb, e->h_out + b0 * rowb, mirror + 4 - b0 * rowb,
-                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(p_out, e->h_out, mirror + 4, cudaMemcpyDeviceToHost, s));
   if (tr.on) cudaEventRecord(tr.ev[3], s);
-  par_memcpy(out_hwc, rgb_hwc, b0 * rowb);
-  par_memcpy(out_hwc + b1 * rowb, rgb_hwc + b1 * rowb, (H - b1) * rowb);
+  par_memcpy(out_hwc, rgb_hwc, px * 3);           // the unchanged pixels, while the GPU runs
   if (tr.on) tt[3] = now_us();
   CUDA_TRY(cudaStreamSynchronize(s));
   if (tr.on) tt[4] = now_us();
@@ -1019,8 +1109,25 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   if (fl & DR_FLAG_UNREDACTED)
     return fail(DR_ERR_INPUT, "input is not redacted: nonzero pixels inside mask");
   if (fl & DR_FLAG_NONFINITE) return fail(DR_ERR_NUMERIC, "model produced non-finite output");
-  par_memcpy(out_hwc + b0 * rowb, p_out + b0 * rowb, (b1 - b0) * rowb);
-  CopyPool::get().evict_async(p_out + b0 * rowb, mirror + 4 - b0 * rowb);
+  if (n_rows > 0) {
+    const size_t rowb = (size_t)W * 3;
+    WorkPool::get().run([&](int part, int parts) {
+      for (int y = part * H / parts; y < (part + 1) * H / parts; ++y) {
+        const int* sp = p_span + 4 * y;
+        if (sp[1] > sp[0])
+          std::memcpy(out_hwc + y * rowb + 3 * sp[0], p_out + sp[2], 3 * (size_t)(sp[1] - sp[0]));
+      }
+    });
+  }
+  {
+    const uint8_t* ev = p_out;
+    const size_t nev = mirror + 4;
+    WorkPool::get().run_async([ev, nev](int part, int parts) {
+      size_t b, e;
+      part_range(nev, part, parts, &b, &e);
+      if (e > b) evict_lines(ev + b, e - b);
+    });
+  }
   if (tr.on) {
     tt[5] = now_us();
     for (int i = 0; i < 5; ++i) tr.host[i] = tt[i + 1] - tt[i];
@@ -1030,7 +1137,7 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
       tr.dev[i] = err == cudaSuccess ? 1e3f * ms : -(float)err;
     }
   }
-  e->last_d2h = mirror + 4 - b0 * rowb;
+  e->last_d2h = mirror + 4;
   e->mem0 = e->mem1;
   e->mem1 = fresh;
   return DR_OK;

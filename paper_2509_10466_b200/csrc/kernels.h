@@ -123,6 +123,10 @@ struct ConvTcArgs {
   // `done` is a zeroed counter the last CTA re-arms
   int* flags_mirror;
   unsigned* done;
+  // decode.2 gather (optional, one frame): also write the u8 composite of the pixels in
+  // row y's span [spans[y].x, spans[y].y) to packed + spans[y].z + 3 * (x - x0)
+  const int4* spans;
+  uint8_t* packed;
 };
 }  // namespace dr
 #include <cuda.h>
