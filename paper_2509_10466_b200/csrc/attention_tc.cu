@@ -28,6 +28,8 @@
 // falls back to unmasked attention (per-block mode resolved on the host, engine.cu).
 #include <math.h>
 
+#include <algorithm>
+
 #include <type_traits>
 
 #include "common.cuh"
@@ -594,8 +596,10 @@ int sm_count() {
 int q_tiles(const AttnArgs& a) { return (a.band + QROWS - 1) / QROWS * HEADS * a.frames * a.groups; }
 }  // namespace
 
-// Key split of a launch: the k in 1..MAX_KSPLIT minimising waves x (blocks per CTA + merge cost) x
-// the per-block time at the SM concurrency the launch reaches (measured, see CTAS_PER_SM).
+// Key split of a launch: the k in 1..MAX_KSPLIT minimising the modelled makespan -- full
+// waves of CTAS_PER_SM CTAs per SM, then a tail wave at the concurrency it reaches -- of CTAs
+// of ceil(blocks / k) key blocks (+1 block-equivalent of merge for k > 1), with the measured
+// per-block time per CTA at 1 / 2 resident CTAs (see CTAS_PER_SM).
 int attention_ksplit(const AttnArgs& a) {
   const int sms = sm_count(), tiles = q_tiles(a);
   const int n_kb = (a.n_seg * a.band + KB - 1) / KB;
@@ -605,9 +609,10 @@ int attention_ksplit(const AttnArgs& a) {
   for (int k = 1; k <= MAX_KSPLIT; ++k) {
     const long n_cta = (long)tiles * k;
     const long slots = (long)sms * CTAS_PER_SM;
-    const long waves = (n_cta + slots - 1) / slots;
-    const int conc = waves > 1 ? CTAS_PER_SM : (int)((n_cta + sms - 1) / sms);
-    const double cost = (double)waves * ((n_kb + k - 1) / k + (k > 1 ? 1 : 0)) * t_conc[conc];
+    const double blocks = (n_kb + k - 1) / k + (k > 1 ? 1 : 0);
+    const long full = n_cta / slots, rem = n_cta - full * slots;
+    const int conc_tail = (int)std::min<long>(CTAS_PER_SM, (rem + sms - 1) / sms);
+    const double cost = blocks * (full * t_conc[CTAS_PER_SM] + (rem ? t_conc[conc_tail] : 0.0));
     if (cost < best_cost * 0.98) { best_cost = cost; best = k; }
   }
   return best;

@@ -325,6 +325,22 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
+// The CTA that finishes last publishes the flags words (every CTA's atomicOr happens before
+// its counter increment; the last one acquires them all) when a mirror is requested.
+DR_DEV void mirror_flags(const ConvTcArgs& a) {
+  if (!a.flags_mirror) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(a.done, 1u) == total - 1) {
+      __threadfence();
+      for (int i = 0; i < a.frames; ++i) a.flags_mirror[i] = atomicOr(a.flags + i, 0);
+      *a.done = 0;
+    }
+  }
+}
+
 DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int y, int f) {
   const size_t plane = (size_t)a.H * a.W;
   const __half* ep = a.e_planes + (size_t)f * 27 * plane;
@@ -388,20 +404,146 @@ __global__ void __launch_bounds__(256) dec2_gather_kernel(ConvTcArgs a) {
   for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
   pdl_wait();
   if (x < a.W) gather_pixel(a, bias, x, y, f);
-  if (a.flags_mirror) {
-    // the CTA that finishes last publishes the flags words (every CTA's atomicOr happens
-    // before its counter increment; the last one acquires them all)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-      if (atomicAdd(a.done, 1u) == total - 1) {
-        __threadfence();
-        for (int i = 0; i < a.frames; ++i) a.flags_mirror[i] = atomicOr(a.flags + i, 0);
-        *a.done = 0;
+  mirror_flags(a);
+}
+
+// PX consecutive pixels per thread (W % PX == 0): each (dy, dx, co) E plane row segment is
+// one 2*PX-byte load; the x - 1 / x + PX neighbours come from the adjacent lanes (shuffles)
+// or, at warp edges, one 2-byte load.  Same summation order and tail as gather_pixel.
+template <int PX> struct VecOf;
+template <> struct VecOf<2> { using T = uint32_t; };
+template <> struct VecOf<4> { using T = uint2; };
+template <> struct VecOf<8> { using T = uint4; };
+template <int PX>
+DR_DEV void unpack_vec(const typename VecOf<PX>::T& v, float* e) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < PX / 2; ++i) {
+    const float2 p2 = unpack_half2(w[i]);
+    e[2 * i] = p2.x;
+    e[2 * i + 1] = p2.y;
+  }
+}
+
+template <int PX, int TPB>
+__global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
+  using V = typename VecOf<PX>::T;
+  const int lane = threadIdx.x & 31;
+  const int x0 = PX * (blockIdx.x * TPB + threadIdx.x), y = blockIdx.y, f = blockIdx.z;
+  pdl_trigger();
+  float bias[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bias[c] = __ldg(a.bias + c);
+  pdl_wait();
+  const bool act = x0 < a.W;
+  const size_t plane = (size_t)a.H * a.W;
+  const __half* ep = a.e_planes + (size_t)f * 27 * plane;
+  float o[3][PX];
+#pragma unroll
+  for (int co = 0; co < 3; ++co)
+#pragma unroll
+    for (int i = 0; i < PX; ++i) o[co][i] = bias[co];
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy) {
+    const int yy = y + dy - 1;
+    const bool rowok = yy >= 0 && yy < a.H;          // uniform over the CTA
+    if (!rowok) continue;
+#pragma unroll
+    for (int co = 0; co < 3; ++co) {
+      float e[3][PX];
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const __half* pl = ep + (size_t)(3 * (3 * dy + dx) + co) * plane + (size_t)yy * a.W;
+        V v;
+        if (act) v = __ldg(reinterpret_cast<const V*>(pl + x0));
+        else memset(&v, 0, sizeof(v));
+        unpack_vec<PX>(v, e[dx]);
+      }
+      // dx = 0 needs E at x - 1 (x = x0 .. x0 + PX - 1); dx = 2 at x + 1
+      float left = __shfl_up_sync(0xffffffffu, e[0][PX - 1], 1);
+      float right = __shfl_down_sync(0xffffffffu, e[2][0], 1);
+      if (lane == 0) {
+        const __half* pl = ep + (size_t)(3 * (3 * dy + 0) + co) * plane + (size_t)yy * a.W;
+        left = (act && x0 > 0) ? __half2float(pl[x0 - 1]) : 0.f;
+      }
+      if (lane == 31 || x0 + PX >= a.W) {
+        const __half* pl = ep + (size_t)(3 * (3 * dy + 2) + co) * plane + (size_t)yy * a.W;
+        right = (act && x0 + PX < a.W) ? __half2float(pl[x0 + PX]) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        const float l = i == 0 ? left : e[0][i - 1];
+        const float r = i == PX - 1 ? right : e[2][i + 1];
+        o[co][i] += l;
+        o[co][i] += e[1][i];
+        o[co][i] += r;
       }
     }
   }
+  if (act) {
+    const size_t pix0 = (size_t)y * a.W + x0;
+    float alr[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) alr[i] = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix0 + i) : 1.f;
+    int4 sp = make_int4(0, 0, 0, 0);
+    if (a.packed) sp = __ldg(a.spans + y);
+    uint8_t src[3 * PX], dst[3 * PX];
+    if (a.out_u8 || a.packed) {                   // 3*PX bytes, 2*PX-byte aligned
+      const uint16_t* s8 = reinterpret_cast<const uint16_t*>(a.rgb_u8 + ((size_t)f * plane + pix0) * 3);
+#pragma unroll
+      for (int k = 0; k < 3 * PX / 2; ++k) *reinterpret_cast<uint16_t*>(src + 2 * k) = __ldg(s8 + k);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float out01[PX];
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        out01[i] = (tanhf(o[ch][i]) + 1.0f) * 0.5f;
+        bad |= !isfinite(out01[i]);
+      }
+      const size_t pl = ((size_t)f * 3 + ch) * plane + pix0;
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        if (a.fill) a.fill[pl + i] = out01[i];
+        if (a.out_f32)
+          a.out_f32[pl + i] = __fadd_rn(__fmul_rn(alr[i], out01[i]),
+                                        __fmul_rn(__fsub_rn(1.0f, alr[i]), __ldg(a.rgb_f32 + pl + i)));
+      }
+      if (a.out_u8 || a.packed) {
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+          const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01[i], 255.0f)), 0.f), 255.f);
+          const uint8_t src8 = src[3 * i + ch];
+          uint8_t ov;
+          if (alr[i] == 0.f) ov = src8;
+          else if (alr[i] == 1.f) ov = fill8;
+          else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr[i], (float)fill8),
+                                                          __fmul_rn(__fsub_rn(1.0f, alr[i]), (float)src8))), 0.f), 255.f);
+          dst[3 * i + ch] = ov;
+        }
+      }
+    }
+    if (a.out_u8) {
+      uint16_t* d8 = reinterpret_cast<uint16_t*>(a.out_u8 + ((size_t)f * plane + pix0) * 3);
+#pragma unroll
+      for (int k = 0; k < 3 * PX / 2; ++k) d8[k] = *reinterpret_cast<const uint16_t*>(dst + 2 * k);
+    }
+    if (a.packed) {
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        const int x = x0 + i;
+        if (x >= sp.x && x < sp.y)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) a.packed[sp.z + 3 * (x - sp.x) + ch] = dst[3 * i + ch];
+      }
+    }
+    if (bad) {
+      atomicOr(a.flags + f, 1);
+      __threadfence();               // performed before this CTA counts itself done
+    }
+  }
+  mirror_flags(a);
 }
 
 
@@ -428,6 +570,15 @@ size_t conv_tc_weight_bytes(int n) { return (size_t)9 * 8 * n * 16; }
 int conv_tc_rows(int n) { return n == 64 ? 2 : 4; }   // decode.0 tiles: 2 output rows
 
 void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s) {
+#ifndef DR_GATHER_PX
+#define DR_GATHER_PX 4
+#endif
+  constexpr int PX = DR_GATHER_PX, TPB = 256 / (PX / 2) > 256 ? 256 : 512 / PX;
+  if (a.W % PX == 0) {
+    dim3 grid((a.W / PX + TPB - 1) / TPB, a.H, a.frames);
+    launch_pdl(dec2_gather_vec_kernel<PX, TPB>, grid, dim3(TPB), 0, s, a);
+    return;
+  }
   dim3 grid((a.W + 255) / 256, a.H, a.frames);
   launch_pdl(dec2_gather_kernel, grid, dim3(256), 0, s, a);
 }

@@ -12,3 +12,5 @@ timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/b
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 0 -c 2 -o gpurun_out/attn_full python scripts/profile_frame.py --frames 2 > gpurun_out/ncu_a.log 2>&1
 cp profiles/r01/ncu_traffic.json gpurun_out/
 cat gpurun_out/pytest_gpu.log
+python scripts/graph_prefix.py 2>&1 | tail -13 > gpurun_out/graph_prefix.txt
+python scripts/e2e_trace.py > gpurun_out/e2e_trace.txt 2>&1
