@@ -19,11 +19,11 @@ from collections import defaultdict
 def stage_of(name: str, grid: str) -> str:
     if "mask_fused" in name:
         return "mask_stage"
-    if "token_tc_kernel<0>" in name or "token_kernel<0>" in name:
+    if "token_tc_kernel<0>" in name or "token_small_kernel<0" in name:
         return "embed_qkv"
-    if "token_tc_kernel<2>" in name or "token_kernel<2>" in name:
+    if "token_tc_kernel<2>" in name or "token_small_kernel<2" in name:
         return "slot_kv"
-    if "token_tc_kernel<1>" in name or "token_kernel<1>" in name:
+    if "token_tc_kernel<1>" in name or "token_small_kernel<1" in name:
         return "mlp_qkv"
     if "attn_tc_kernel" in name:
         z = int(grid.strip("()").split(",")[2])
@@ -32,7 +32,7 @@ def stage_of(name: str, grid: str) -> str:
         return "vec2patch"
     if "conv3x3_tc_kernel<64" in name:
         return "decode0"
-    if "conv3x3_tc_kernel<16" in name or "dec2_te" in name or "dec2_gather" in name:
+    if "dec2_gather" in name:
         return "decode2_composite"
     return "other:" + name[:40]
 
