@@ -58,7 +58,10 @@ constexpr int MAX_KSPLIT = 2;                 // larger clusters pack poorly int
 constexpr uint32_t TM_S = 0, TM_P = 64, TM_O = 96, TM_COLS = 128;
 constexpr float RESCALE_SLACK = 8.f;          // log2 units: p <= 2^8 between rescales
 #ifndef DR_POLY_EVERY
-#define DR_POLY_EVERY 4
+#define DR_POLY_EVERY 3
+#endif
+#ifndef DR_ATTN_F32X2
+#define DR_ATTN_F32X2 1                        // packed fp32 pairs (FFMA2) in the softmax
 #endif
 constexpr int POLY_EVERY = DR_POLY_EVERY;     // 1 pair in POLY_EVERY via ex2_poly (0 = none)
 constexpr int ROW_BYTES = DH * 2;             // 32 B per token row
@@ -429,6 +432,9 @@ attn_tc_kernel(AttnArgs a) {
       auto sweep = [&](float base, auto track, auto full_tag) -> float {
         constexpr bool FULL = decltype(full_tag)::value;
         float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#if DR_ATTN_F32X2
+        const uint64_t sl2_2 = f2_pack(sl2, sl2), nbase2 = f2_pack(-base, -base);
+#endif
 #pragma unroll
         for (int ch = 0; ch < KB / 32; ++ch) {
           uint32_t pk[16];
@@ -441,12 +447,24 @@ attn_tc_kernel(AttnArgs a) {
               s1 = adjust(s1, k0 + 1);
             }
             if constexpr (decltype(track)::value) mx[c & 3] = fmaxf(mx[c & 3], fmaxf(s0, s1));
+            // x = s * scale - base for both scores in one packed FFMA2
+#if DR_ATTN_F32X2
+            const float2 xv = f2_unpack(f2_fma(f2_pack(s0, s1), sl2_2, nbase2));
+#else
+            const float2 xv = make_float2(fmaf(s0, sl2, -base), fmaf(s1, sl2, -base));
+#endif
             // FULL sweeps evaluate POLY_SHARE of the exponentials on the FMA pipe (MUFU
             // offload; the polynomial's 7.5e-5 relative error is below P's fp16 rounding)
-            if (FULL && POLY_EVERY > 0 && c % POLY_EVERY == POLY_EVERY - 1)
-              pk[c] = pack_half2(ex2_poly(fmaf(s0, sl2, -base)), ex2_poly(fmaf(s1, sl2, -base)));
-            else
-              pk[c] = pack_half2(ex2(fmaf(s0, sl2, -base)), ex2(fmaf(s1, sl2, -base)));
+            if (FULL && POLY_EVERY > 0 && c % POLY_EVERY == POLY_EVERY - 1) {
+#if DR_ATTN_F32X2
+              const float2 e = f2_unpack(ex2_poly2(f2_pack(xv.x, xv.y)));
+              pk[c] = pack_half2(e.x, e.y);
+#else
+              pk[c] = pack_half2(ex2_poly(xv.x), ex2_poly(xv.y));
+#endif
+            } else {
+              pk[c] = pack_half2(ex2(xv.x), ex2(xv.y));
+            }
           }
           // P(j-1)*V must have read the P columns (first chunk only; a redo sweep finds
           // the phase already complete: P(j)*V is not issued before this warp arrives)

@@ -78,6 +78,43 @@ DR_DEV float ex2_poly(float x) {
   p = fmaf(f, p, 0.99992806f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two IEEE fp32 lanes per instruction, each
+// rounded exactly like its scalar form).
+DR_DEV uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+DR_DEV float2 f2_unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+DR_DEV uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+DR_DEV uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// ex2_poly on a packed pair: same clamp, magic-add rounding, polynomial and exponent add,
+// bit-identical per lane, about half the instructions.
+DR_DEV uint64_t ex2_poly2(uint64_t x2) {
+  const float2 xv = f2_unpack(x2);
+  const uint64_t x = f2_pack(fmaxf(xv.x, -125.f), fmaxf(xv.y, -125.f));
+  const uint64_t r = f2_add(x, f2_pack(12582912.f, 12582912.f));
+  const uint64_t j = f2_add(r, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2_fma(j, f2_pack(-1.f, -1.f), x);          // x - j, exact
+  uint64_t p = f2_fma(f, f2_pack(0.05517161f, 0.05517161f), f2_pack(0.24261111f, 0.24261111f));
+  p = f2_fma(f, p, f2_pack(0.69326097f, 0.69326097f));
+  p = f2_fma(f, p, f2_pack(0.99992806f, 0.99992806f));
+  const float2 pv = f2_unpack(p), rv = f2_unpack(r);
+  return f2_pack(__int_as_float(__float_as_int(pv.x) + (__float_as_int(rv.x) << 23)),
+                 __int_as_float(__float_as_int(pv.y) + (__float_as_int(rv.y) << 23)));
+}
 DR_DEV float quad_sum(float v) {
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
