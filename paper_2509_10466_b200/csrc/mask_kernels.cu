@@ -65,7 +65,13 @@ __device__ unsigned long long g_mask_trace[4096 * MT_SLOTS];
 #define MT(slot) do { if (threadIdx.x == 0) { unsigned long long c_;                       \
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) :: "memory");                          \
     const int b_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);           \
-    if (b_ < 4096) g_mask_trace[b_ * MT_SLOTS + (slot)] = c_; } } while (0)
+    if (b_ < 4096) g_mask_trace[b_ * MT_SLOTS + (slot)] = c_;                                \
+    if ((slot) == 0 || (slot) == 9) {                    /* 11/12: global ns, 13: SM id */   \
+      unsigned long long g_; unsigned sm_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                                 \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                       \
+      if (b_ < 4096) { g_mask_trace[b_ * MT_SLOTS + ((slot) ? 12 : 11)] = g_;                \
+                       g_mask_trace[b_ * MT_SLOTS + 13] = sm_; } } } } while (0)
 #else
 #define MT(slot) do {} while (0)
 #endif

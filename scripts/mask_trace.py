@@ -42,6 +42,16 @@ def main():
     print(f"mask stage: 256 CTAs, CTA span p50 {np.median(span):.2f} max {span.max():.2f} us")
     for i in range(9):
         print(f"  {NAMES[i]:28s} p50 {np.median(d[:, i]):6.2f}  max {d[:, i].max():6.2f} us")
+    g0 = t[:, 11].min()
+    start, end = (t[:, 11] - g0) / 1e3, (t[:, 12] - g0) / 1e3
+    from collections import Counter
+    per_sm = Counter(t[:, 13])
+    print(f"  global: start p50 {np.median(start):.2f} max {start.max():.2f}, end p50 "
+          f"{np.median(end):.2f} max {end.max():.2f} us; CTAs per SM {Counter(per_sm.values())}")
+    order = np.argsort(-span)[:8]
+    print("  slowest CTAs (block, span us, start us, SM, CTAs on SM):",
+          [(int(b), round(float(span[b]), 2), round(float(start[b]), 2), int(t[b, 13]),
+            per_sm[t[b, 13]]) for b in order])
 
 
 if __name__ == "__main__":
