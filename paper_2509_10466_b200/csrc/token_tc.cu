@@ -482,19 +482,28 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
 // all 32 warps run the epilogue warp-per-row: lane l owns channels 2l, 2l+1 of the row,
 // LayerNorm statistics are butterfly shuffles (no barrier), the residual stream stays in
 // registers across the chain.  Two CTA barriers per GEMM (dump -> epilogue -> MMA).
+#ifndef DR_TOK_SMALL_WARPS
+#define DR_TOK_SMALL_WARPS 32
+#endif
+constexpr int SW = DR_TOK_SMALL_WARPS;      // warps of the small-tile kernel (16 or 32)
+constexpr int SGROUPS = SW / 4;             // column groups per lane quarter
+constexpr int R32 = 32 / SW, R64 = 64 / SW; // rows per warp at 32 / 64-row tiles
+
 template <int N>
 DR_DEV void dump_d(uint32_t tbase, int col0, float* dump, int rows) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, g = warp >> 2;
   if (32 * q >= rows) return;
-  constexpr int CW = N / 8, P = N + 4;
+  constexpr int CW = N / SGROUPS, P = N + 4;
   const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(col0 + g * CW);
   uint32_t r[CW];
-  if constexpr (CW == 8) {
+  if constexpr (CW % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < CW / 16; ++i) tc::tmem_ld16(ta + 16 * i, r + 16 * i);
+  } else if constexpr (CW == 8) {
     tc::tmem_ld8(ta, r);
-  } else if constexpr (CW == 16) {
-    tc::tmem_ld16(ta, r);
   } else {
+    static_assert(CW == 24, "column group width");
     tc::tmem_ld16(ta, r);
     tc::tmem_ld8(ta + 16, r + 16);
   }
@@ -545,7 +554,7 @@ DR_DEV void publish_all() {
 }
 
 template <int MODE, int RPW>
-__global__ void __launch_bounds__(THREADS, 1) token_small_kernel(TokenArgs a) {
+__global__ void __launch_bounds__(32 * SW, SW == 16 ? 2 : 1) token_small_kernel(TokenArgs a) {
 #ifdef DR_TRACE
   int tt_i = 0;
 #endif
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_small_kernel(TokenArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  constexpr int ROWS = 32 * RPW;
+  constexpr int ROWS = SW * RPW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* sa = sm + OFF_A;
   uint8_t* big = sm + OFF_BIG;
@@ -812,12 +821,12 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
     cudaFuncSetAttribute(token_tc_kernel<TOK_EMBED>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_tc_kernel<TOK_POST>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_tc_kernel<TOK_SLOTKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_POST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_POST, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_POST, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_POST, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     init = true;
   }
   TokenArgs a = a_in;
@@ -825,16 +834,17 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
     a.tile_rows = token_tc_tile_rows(a.n_tok, sms);
   dim3 grid((a.n_tok + a.tile_rows - 1) / a.tile_rows), block(THREADS);
   if (a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
+    block = dim3(32 * SW);
     const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
                    : (mode == TOK_POST ? smem_bytes<TOK_POST>(a) : smem_bytes<TOK_SLOTKV>(a));
     if (a.tile_rows == 32) {
-      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, 1>, grid, block, smem, s, a);
-      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, 1>, grid, block, smem, s, a);
-      else launch_pdl(token_small_kernel<TOK_SLOTKV, 1>, grid, block, smem, s, a);
+      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, R32>, grid, block, smem, s, a);
+      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, R32>, grid, block, smem, s, a);
+      else launch_pdl(token_small_kernel<TOK_SLOTKV, R32>, grid, block, smem, s, a);
     } else {
-      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, 2>, grid, block, smem, s, a);
-      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, 2>, grid, block, smem, s, a);
-      else launch_pdl(token_small_kernel<TOK_SLOTKV, 2>, grid, block, smem, s, a);
+      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, R64>, grid, block, smem, s, a);
+      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, R64>, grid, block, smem, s, a);
+      else launch_pdl(token_small_kernel<TOK_SLOTKV, R64>, grid, block, smem, s, a);
     }
 #ifdef DR_TRACE
     tok_trace_snapshot(s, (int)grid.x, mode);
