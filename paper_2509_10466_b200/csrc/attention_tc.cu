@@ -29,6 +29,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <type_traits>
 
@@ -622,6 +623,11 @@ int attention_ksplit(const AttnArgs& a) {
   const int sms = sm_count(), tiles = q_tiles(a);
   const int n_kb = (a.n_seg * a.band + KB - 1) / KB;
   const double t_conc[CTAS_PER_SM + 1] = {0.0, 0.575, 0.74};   // us per block per CTA
+  static const int forced = [] {
+    const char* e = std::getenv("DR_ATTN_KSPLIT");            // tests / diagnostics
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced >= 1 && forced <= MAX_KSPLIT) return forced;
   int best = 1;
   double best_cost = 1e30;
   for (int k = 1; k <= MAX_KSPLIT; ++k) {

@@ -42,3 +42,38 @@ def test_tcgen05_conv3x3_vs_reference(shape):
     ref = conv3x3_ref(x.astype(np.float64), w.astype(np.float16).astype(np.float64), b)
     err = np.abs(got - ref)
     assert err.max() < 1e-2 + 2e-3 * np.abs(ref).max(), err.max()
+
+
+_SPLIT_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[2])
+from paper_2509_10466_b200 import DsttConfig, DsttEngine, synth
+cfg = DsttConfig.baseline(256, mask_dilate=2, mask_feather_sigma=1.0)
+eng = DsttEngine(cfg, seed=0)
+imgs, masks = synth.frame_pool("C1", 2, size=256)
+rng = np.random.default_rng(1)
+slots = [torch.from_numpy(rng.normal(0, 1, (2, cfg.tokens, 64)).astype(np.float32)).cuda()
+         for _ in range(2)]
+res = eng.run(torch.from_numpy(imgs).cuda(), torch.from_numpy(masks).cuda(), slots)
+np.save(sys.argv[1], res["fill"].cpu().numpy() if "fill" in res else res["out"].cpu().numpy())
+"""
+
+
+def test_attention_key_split_one_and_two_agree(tmp_path):
+    """The per-launch key split (attention_ksplit: 1 CTA per query tile at large batch, a
+    DSMEM-merged pair at small batch) must not change the result beyond fp32 merge rounding."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    repo = str(Path(__file__).resolve().parents[1])
+    outs = []
+    for k in (1, 2):
+        dst = tmp_path / f"k{k}.npy"
+        subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, str(dst), repo], check=True,
+                       env={**os.environ, "DR_ATTN_KSPLIT": str(k)}, timeout=300)
+        outs.append(np.load(dst))
+    assert outs[0].shape == outs[1].shape
+    assert np.abs(outs[0].astype(np.float64) - outs[1]).max() <= 2e-3
