@@ -370,6 +370,9 @@ struct dr_engine {
   int stop_after = -1;               // DR_STOP_AFTER=k (diagnostics): launch only k kernels
   uint8_t* pin = nullptr;                                        // pinned staging
   int* flags_mirror = nullptr;       // host path: decode.2's last CTA copies flags here
+  cudaEvent_t rgb_ready = nullptr;   // host path: rgb upload done (split uploads), else null
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t rgb_event = nullptr;
   const int4* pack_spans = nullptr;  // host path: per-row [x0, x1, byte offset] (device)
   uint8_t* pack_out = nullptr;       // host path: span-packed composite (device)
   std::vector<int> span_first, span_last;   // host path scratch: masked extent per row
@@ -667,7 +670,10 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
 void dr_destroy(dr_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
+  if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   e->free_ws();
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+  if (e->rgb_event) cudaEventDestroy(e->rgb_event);
   cudaFree(e->fparams);
   cudaFree(e->feather_w);
   cudaFree(e->wtc);
@@ -765,8 +771,23 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   float* alpha = io->alpha ? io->alpha : e->alpha;
   fill_mask_args(e, m, B, io->mask_m0, io->dilated, alpha, tv, flags);
   m.rgb_f32 = io->rgb_f32; m.rgb_u8 = io->rgb_u8; m.xin = e->xin;
-  DR_STOP_CHECK();
-  launch_mask_stage(m, s);
+  const bool split = e->rgb_ready != nullptr && io->rgb_u8 != nullptr;
+  if (split) {
+    // host path, split uploads: the stage runs on the mask alone while the rgb is still in
+    // flight on the copy stream; the input pack follows once it has landed
+    MaskArgs mo = m;
+    mo.rgb_f32 = nullptr; mo.rgb_u8 = nullptr; mo.xin = nullptr;
+    if (!mo.m1) mo.m1 = e->m1;
+    DR_STOP_CHECK();
+    launch_mask_stage(mo, s);
+    CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, 0));
+    MaskArgs pk = m;
+    pk.m1 = mo.m1;
+    launch_pack_input(pk, s);
+  } else {
+    DR_STOP_CHECK();
+    launch_mask_stage(m, s);
+  }
   e->mark(0, s);
 
   // 2. memory-slot K/V of every temporal block (LN1 + k/v projection of each slot,
@@ -902,7 +923,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   if (B == 1) { c2.spans = e->pack_spans; c2.packed = e->pack_out; }
   DR_STOP_CHECK();
   launch_dec2_gather(c2, s);
-  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3;
+  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0);
   e->mark(8, s);
 #undef DR_STOP_CHECK
   CUDA_TRY(cudaGetLastError());
@@ -1068,13 +1089,19 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
     total += (size_t)(sp[1] - sp[0]) * 3;
   }
   const size_t mirror = (total + 3) & ~(size_t)3;                 // flags word offset
-  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
-  par_memcpy(p_m0, mask_hw, px, CP_NT);
-  if (tr.on) {
-    tt[1] = now_us();
-    cudaEventRecord(tr.ev[0], s);
+  // split uploads: mask (+ span table) first on the compute stream, so the mask stage can
+  // run while the rgb crosses PCIe on the copy stream
+  if (!e->copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&e->rgb_event, cudaEventDisableTiming));
   }
-  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, in_bytes, cudaMemcpyHostToDevice, s));
+  if (tr.on) cudaEventRecord(tr.ev[0], s);
+  par_memcpy(p_m0, mask_hw, px, CP_NT);
+  CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, in_bytes - px * 3, cudaMemcpyHostToDevice, s));
+  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
+  if (tr.on) tt[1] = now_us();
+  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
+  CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
   if (tr.on) cudaEventRecord(tr.ev[1], s);
   int fresh = 0;
   while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
@@ -1087,10 +1114,12 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   e->pack_spans = reinterpret_cast<const int4*>(e->h_rgb + in_spans);
   e->pack_out = e->h_out;
   e->flags_mirror = reinterpret_cast<int*>(e->h_out + mirror);
+  e->rgb_ready = e->rgb_event;
   int rc = dr_forward(e, &io, stream);
   e->pack_spans = nullptr;
   e->pack_out = nullptr;
   e->flags_mirror = nullptr;
+  e->rgb_ready = nullptr;
   if (rc) return rc;
   if (tr.on) {
     cudaEventRecord(tr.ev[2], s);

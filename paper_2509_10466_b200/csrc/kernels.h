@@ -94,6 +94,8 @@ struct MaskArgs {
   int* flags;                // [frames] out: bit1 = input not redacted inside m0
 };
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s);
+// xin + redaction check alone, from u8 rgb, m0 and the stage's m1 bytes
+void launch_pack_input(const MaskArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- decoder
 // tcgen05 3x3 convolution (conv_tc.cu).  Input = TMA tensor map over an NHWC fp16

@@ -432,6 +432,71 @@ void launch_mask_t(const MaskArgs& a, cudaStream_t s, int smem) {
   launch_pdl(mask_fused_kernel<P, WH>, grid, dim3(NT), smem, s, a);
 }
 
+// Network input pack on its own (host path with split uploads: the mask stage runs on the
+// mask while the rgb is still crossing PCIe; this kernel then builds the same xin as the
+// fused stage from rgb u8 + the stage's m1 bytes, and the redaction check from m0).  One
+// warp per token, lanes = 4 channels x P rows, exactly the fused stage's per-lane math.
+template <int P>
+__global__ void __launch_bounds__(256) pack_input_kernel(MaskArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int Cc = a.W / P, T = (a.H / P) * Cc;
+  const long gtok = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  pdl_trigger();
+  pdl_wait();
+  if (gtok >= (long)a.frames * T) return;
+  const int f = (int)(gtok / T), tok = (int)(gtok - (long)f * T);
+  const int i = tok / Cc, j = tok - i * Cc;
+  const bool active = lane < 4 * P;
+  const int c = lane / P, ky = lane % P;
+  const size_t plane = (size_t)a.H * a.W;
+  const int y = i * P + ky, xl = j * P;
+  uint32_t mb = 0, m0b = 0;
+  if (active) {
+    const uint8_t* m1r = a.m1 + (size_t)f * plane + (size_t)y * a.W + xl;
+    const uint8_t* m0r = a.m0 + (size_t)f * plane + (size_t)y * a.W + xl;
+#pragma unroll
+    for (int kx = 0; kx < P; ++kx) {
+      mb |= (uint32_t)(m1r[kx] != 0) << kx;
+      m0b |= (uint32_t)(m0r[kx] != 0) << kx;
+    }
+  }
+  float v[P];
+  bool dirty = false;
+  if (!active) {
+#pragma unroll
+    for (int kx = 0; kx < P; ++kx) v[kx] = 0.f;
+  } else if (c == 3) {
+#pragma unroll
+    for (int kx = 0; kx < P; ++kx) v[kx] = (float)((mb >> kx) & 1u);
+  } else {
+    const uint8_t* src = a.rgb_u8 + ((size_t)f * plane + (size_t)y * a.W + xl) * 3 + c;
+#pragma unroll
+    for (int kx = 0; kx < P; ++kx) {
+      const uint8_t u = src[3 * kx];
+      dirty |= ((m0b >> kx) & 1u) && u != 0;
+      v[kx] = ((mb >> kx) & 1u) ? 0.f : __fdiv_rn((float)u, 255.0f);
+    }
+  }
+  if (__any_sync(0xffffffffu, dirty) && lane == 0 && a.flags) atomicOr(a.flags + f, 2);
+  if (!active) return;
+  __half* dst = a.xin + ((size_t)f * T + tok) * (4 * P * P) + c * P * P + ky * P;
+  uint32_t packed[P / 2];
+#pragma unroll
+  for (int kx = 0; kx < P; kx += 2) packed[kx / 2] = pack_half2(v[kx], v[kx + 1]);
+  if constexpr (P == 8) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  } else {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
+  }
+}
+
+void launch_pack_input(const MaskArgs& a, cudaStream_t s) {
+  const long tokens = (long)a.frames * (a.H / a.patch) * (a.W / a.patch);
+  const dim3 grid((unsigned)((tokens + 7) / 8));
+  if (a.patch == 4) launch_pdl(pack_input_kernel<4>, grid, dim3(256), 0, s, a);
+  else launch_pdl(pack_input_kernel<8>, grid, dim3(256), 0, s, a);
+}
+
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
   const int smem = (int)sizeof(Smem) + 16;
   const int wh = (a.radius + a.feather_radius + 31) / 32;   // 0..2 halo words per side
