@@ -786,6 +786,357 @@ __global__ void __launch_bounds__(32 * SW, SW == 16 ? 2 : 1) token_small_kernel(
   if (warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
 }
 
+// ---------------------------------------------------------------------------------------
+// Small tiles, quarter-spread (default): the tile's rows are placed RQ = ROWS/4 per TMEM
+// lane quarter (A row 32q + j), so every quarter -- every SM sub-partition -- owns rows,
+// and the 16x256b TMEM load shape (thread t: lanes t/4 and t/4 + 8, columns 2(t%4), +1 of
+// each 8-column group; measured, scripts/tmem_layout_probe.cu) hands a warp its quarter's
+// rows 4 threads per row.  Epilogues run straight from TMEM on the quarter's warps (row
+// statistics: two xor shuffles), with no accumulator round trip through shared memory.
+// 16 warps: quarter q = w % 4, column slice w / 4 (64 columns each).
+constexpr int QWARPS = 16;
+
+#define DR_TMEM_LD_16x256b_X8(taddr, r)                                                     \
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"  \
+               "%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29," \
+               "%30,%31}, [%32];\n"                                                         \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),    \
+                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),  \
+                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),           \
+                 "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),           \
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]),           \
+                 "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
+               : "r"(taddr))
+
+// 64 accumulator columns of this warp's quarter: v[h][2k + e] = row (t/4 + 8h), column
+// col0 + 8k + 2(t%4) + e
+template <int NH>
+DR_DEV void q_load64(uint32_t tbase, int quarter, int col0, float (&v)[NH][16]) {
+  uint32_t r[32];
+  DR_TMEM_LD_16x256b_X8(tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)col0, r);
+  tc::tmem_wait_ld();
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      v[h][2 * k] = __uint_as_float(r[4 * k + 2 * h]);
+      v[h][2 * k + 1] = __uint_as_float(r[4 * k + 2 * h + 1]);
+    }
+}
+
+DR_DEV float quad4_sum(float v) {                // the 4 threads of a row (t%4)
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+// LayerNorm of one row held as 16 values per thread (4 threads per row) -> fp16 into the
+// A atom at row arow, chunks k, bytes 4*(t%4)
+DR_DEV void q_ln_to_a(const float (&x)[16], const float* w, const float* b, uint8_t* sa,
+                      int arow, int cl) {
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) sum += x[i];
+  const float mu = quad4_sum(sum) * (1.f / 64.f);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float d = x[i] - mu;
+    q += d * d;
+  }
+  const float rs = rsqrtf(quad4_sum(q) * (1.f / 64.f) + 1e-5f);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = 8 * k + cl;
+    const float y0 = (x[2 * k] - mu) * rs * w[c] + b[c];
+    const float y1 = (x[2 * k + 1] - mu) * rs * w[c + 1] + b[c + 1];
+    *reinterpret_cast<uint32_t*>(sa + sw128(arow, k) + 2 * cl) = pack_half2(y0, y1);
+  }
+}
+
+template <int MODE, int RQ>
+__global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
+#ifdef DR_TRACE
+  int tt_i = 0;
+#endif
+  TT();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  constexpr int ROWS = 4 * RQ, NH = RQ / 8;      // rows per tile, rows per thread (1 or 2)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, slice = warp >> 2;
+  const int cl = 2 * (lane & 3);                  // this thread's column pair in each group
+  uint8_t* sa = sm + OFF_A;
+  uint8_t* big = sm + OFF_BIG;
+  constexpr int big_bytes = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
+  uint8_t* sw = big + big_bytes;
+  const WLayout L = wlayout<MODE>(a);
+  const float* prm = reinterpret_cast<const float*>(sw + L.w_bytes);
+  auto prm_nx = [&](int j) { return prm + (1 + j) * (PRM_BYTES / 4); };
+  Ctl& ctl = *reinterpret_cast<Ctl*>(sw + L.total());
+
+  // this thread's rows (in its quarter): j = lane/4 + 8h -> token n, frame f, token tk
+  int nq[NH], fq[NH], tkq[NH];
+  bool vq[NH];
+#pragma unroll
+  for (int h = 0; h < NH; ++h) {
+    const int j = (lane >> 2) + 8 * h;
+    nq[h] = blockIdx.x * ROWS + quarter * RQ + j;
+    vq[h] = nq[h] < a.n_tok;
+    fq[h] = nq[h] / a.T;
+    tkq[h] = nq[h] - fq[h] * a.T;
+  }
+  auto arow = [&](int h) { return 32 * quarter + (lane >> 2) + 8 * h; };
+
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&ctl.w_bar, 1);
+    tc::mbar_init(&ctl.mma_bar, 1);
+    tc::fence_barrier_init();
+    uint8_t* pc = sw + L.w_bytes;                          // constant weights: before pdl_wait
+    if constexpr (MODE == TOK_EMBED) {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + 256 + PRM_BYTES));
+      tc::bulk_load(sw, a.we_img, WE_BYTES, &ctl.w_bar);
+      tc::bulk_load(sw + WE_BYTES, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
+      tc::bulk_load(pc, a.we_img + WE_BYTES, 256, &ctl.w_bar);
+      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+    } else if constexpr (MODE == TOK_POST) {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)L.total());
+      tc::bulk_load(sw, a.cur.img + IMG_O, IMG_PRM - IMG_O, &ctl.w_bar);
+      tc::bulk_load(pc, a.cur.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+      uint8_t* d = sw + (IMG_PRM - IMG_O);
+      if (a.has_next) {
+        tc::bulk_load(d, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
+        tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+      } else {
+        for (int j = 0; j < a.n_kv; ++j) {
+          tc::bulk_load(d + j * 128 * 128, a.kv_w[j].img + IMG_KV, 128 * 128, &ctl.w_bar);
+          tc::bulk_load(pc + (1 + j) * PRM_BYTES, a.kv_w[j].img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+        }
+      }
+    } else {
+      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + PRM_BYTES));
+      tc::bulk_load(sw, a.next.img + IMG_KV, 128 * 128, &ctl.w_bar);
+      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
+    }
+  }
+  __syncthreads();                              // barriers initialised before any wait
+  TT();
+  pdl_wait();
+  // TMEM only after the predecessor grid completed (see token_tc_kernel)
+  if (warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
+  TT();
+
+  uint32_t phase = 0;
+  auto mma_wait = [&](bool consumer) {          // consumers wait; everybody flips the phase
+    if (consumer) {
+      tc::mbar_wait(&ctl.mma_bar, phase);
+      tc::fence_after();
+    }
+    phase ^= 1u;
+  };
+
+  // ------------------------------------------------------------ first GEMM input
+  // A rows of token row r of the tile: 32 * (r / RQ) + r % RQ
+  if constexpr (MODE == TOK_EMBED) {
+    for (int e = threadIdx.x; e < ROWS * 32; e += 32 * QWARPS) {   // 16-byte chunks of xin
+      const int r = e >> 5, ch = e & 31;
+      const int n = blockIdx.x * ROWS + r;
+      const uint4 v = n < a.n_tok ? __ldg(reinterpret_cast<const uint4*>(a.xin + (size_t)n * a.kin) + ch)
+                                  : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(big + (ch >> 3) * ATOM_A + sw128(32 * (r / RQ) + r % RQ, ch & 7)) = v;
+    }
+  } else if constexpr (MODE == TOK_POST) {
+    for (int e = threadIdx.x; e < ROWS * 8; e += 32 * QWARPS) {    // 16-byte chunks of attn
+      const int r = e >> 3, ch = e & 7;
+      const int n = blockIdx.x * ROWS + r;
+      const uint4 v = n < a.n_tok ? __ldg(reinterpret_cast<const uint4*>(a.attn + (size_t)n * C) + ch)
+                                  : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(sa + sw128(32 * (r / RQ) + r % RQ, ch)) = v;
+    }
+  }
+  // residual stream: warps 0-3 (slice 0) own it, 16 values per row and thread
+  float x[NH][16];
+  const bool xw = slice == 0;
+  if constexpr (MODE != TOK_EMBED) {
+    if (xw) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 v = vq[h] ? __ldg(reinterpret_cast<const float2*>(a.resid_in + (size_t)nq[h] * C + 8 * k + cl))
+                                 : make_float2(0.f, 0.f);
+          x[h][2 * k] = v.x;
+          x[h][2 * k + 1] = v.y;
+        }
+    }
+  }
+  tc::mbar_wait(&ctl.w_bar, 0);                 // weights and params in smem
+  publish_all();
+  TT();
+  const uint32_t tbase = ctl.tmem_base;
+  auto store_resid = [&]() {
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+      if (vq[h])
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float2*>(a.resid_out + (size_t)nq[h] * C + 8 * k + cl) =
+              make_float2(x[h][2 * k], x[h][2 * k + 1]);
+  };
+  auto add_acc = [&](const float* bias) {       // x += D[:, 0..63] + bias (slice-0 warps)
+    float d[NH][16];
+    q_load64<NH>(tbase, quarter, 0, d);
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        x[h][2 * k] += d[h][2 * k] + bias[8 * k + cl];
+        x[h][2 * k + 1] += d[h][2 * k + 1] + bias[8 * k + cl + 1];
+      }
+  };
+
+  if constexpr (MODE == TOK_EMBED) {
+    if (warp == 0) gemm_issue(tbase, tc::smem_u32(big), tc::smem_u32(sw), 64, 4, &ctl.mma_bar);
+    mma_wait(xw);
+    if (xw) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[h][i] = 0.f;
+      add_acc(prm);
+      store_resid();
+    }
+    TT();
+  }
+  if constexpr (MODE == TOK_POST) {
+    const uint32_t wo = tc::smem_u32(sw), w1 = wo + (IMG_1 - IMG_O), w2 = wo + (IMG_2 - IMG_O);
+    // ---------------------------------------------------------- out-proj + residual, LN2
+    if (warp == 0) gemm_issue(tbase, tc::smem_u32(sa), wo, 64, 1, &ctl.mma_bar);
+    mma_wait(xw);
+    if (xw) {
+      add_acc(prm + Prm::bo);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) q_ln_to_a(x[h], prm + Prm::ln2_w, prm + Prm::ln2_b, sa, arow(h), cl);
+    }
+    publish_all();
+    TT();
+    // ---------------------------------------------------------- FFN1 + GELU (2 slices)
+    if (warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), w1, 128, 1, &ctl.mma_bar);
+    mma_wait(slice < 2);
+    if (slice < 2) {
+      float d[NH][16];
+      q_load64<NH>(tbase, quarter, 64 + 64 * slice, d);
+      const float* b1 = prm + Prm::b1 + 64 * slice;
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int c = 8 * k + cl;
+          const uint32_t hv = pack_half2(gelu_erf(d[h][2 * k] + b1[c]), gelu_erf(d[h][2 * k + 1] + b1[c + 1]));
+          *reinterpret_cast<uint32_t*>(big + slice * ATOM_A + sw128(arow(h), k) + 2 * cl) = hv;
+        }
+    }
+    publish_all();
+    TT();
+    // ---------------------------------------------------------- FFN2 + residual
+    if (warp == 0) gemm_issue(tbase, tc::smem_u32(big), w2, 64, 2, &ctl.mma_bar);
+    mma_wait(xw);
+    if (xw) {
+      add_acc(prm + Prm::b2);
+      store_resid();
+    }
+    TT();
+  }
+
+  // ------------------------------------------------------------ LN1' + projections
+  const uint32_t wnext = tc::smem_u32(sw) + (MODE == TOK_EMBED ? WE_BYTES
+                                            : (MODE == TOK_POST ? IMG_PRM - IMG_O : 0));
+  const bool qkv = MODE == TOK_EMBED || (MODE == TOK_POST && a.has_next);
+  if (qkv) {
+    const float* pn = prm_nx(0);
+    if (xw) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h) q_ln_to_a(x[h], pn + Prm::ln1_w, pn + Prm::ln1_b, sa, arow(h), cl);
+    }
+    publish_all();
+    TT();
+    if (warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), wnext, 192, 1, &ctl.mma_bar);
+    mma_wait(slice < 3);
+    if (slice < 3) {                            // 64 of the 192 q|k|v columns per slice
+      float d[NH][16];
+      q_load64<NH>(tbase, quarter, 64 + 64 * slice, d);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        if (!vq[h]) continue;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int u = 8 * slice + k, p = u >> 1, which = p >> 2, hd = p & 3, c = u & 1;
+          __half* dst = which == 0 ? a.q : (which == 1 ? a.k : a.v);
+          const float* bias = pn + Prm::bqkv + 8 * u + cl;
+          uint8_t* row = reinterpret_cast<uint8_t*>(dst + ((size_t)(fq[h] * HEADS + hd) * a.T + tkq[h]) * DH);
+          *reinterpret_cast<uint32_t*>(row + 16 * (c ^ ((tkq[h] >> 2) & 1)) + 2 * cl) =
+              pack_half2(d[h][2 * k] + bias[0], d[h][2 * k + 1] + bias[1]);
+        }
+      }
+    }
+  } else {
+    // k|v only: SLOTKV (one block) or the last block's slot K/V for every temporal block
+    const int n_kv = MODE == TOK_SLOTKV ? 1 : a.n_kv;
+    if constexpr (MODE == TOK_POST) {
+      if (a.tok16 && xw) {                      // fp16 tokens for Vec2Patch
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          if (vq[h]) {
+            const int ti = tkq[h] / a.Cc, tj = tkq[h] - ti * a.Cc;
+            const size_t pos = ((size_t)fq[h] * (a.R + 2) + ti + 1) * (a.Cc + 2) + tj + 1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<uint32_t*>(a.tok16 + pos * C + 8 * k + cl) = pack_half2(x[h][2 * k], x[h][2 * k + 1]);
+          }
+      }
+    }
+    for (int j = 0; j < n_kv; ++j) {
+      const float* pn = prm_nx(j);
+      __half* kd = MODE == TOK_SLOTKV ? a.k : a.kv_k[j];
+      __half* vd = MODE == TOK_SLOTKV ? a.v : a.kv_v[j];
+      if (xw) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) q_ln_to_a(x[h], pn + Prm::ln1_w, pn + Prm::ln1_b, sa, arow(h), cl);
+      }
+      publish_all();
+      if (warp == 0)
+        gemm_issue(tbase + 64, tc::smem_u32(sa), wnext + j * 128 * 128, 128, 1, &ctl.mma_bar);
+      mma_wait(slice < 2);
+      if (slice < 2) {                          // k (slice 0) | v (slice 1), 64 columns each
+        float d[NH][16];
+        q_load64<NH>(tbase, quarter, 64 + 64 * slice, d);
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          if (!vq[h]) continue;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int u = 8 * slice + k, p = 4 + (u >> 1), hd = p & 3, c = u & 1;
+            const float* bias = pn + Prm::bqkv + 64 + 8 * u + cl;
+            uint8_t* row = reinterpret_cast<uint8_t*>((p < 8 ? kd : vd) + ((size_t)(fq[h] * HEADS + hd) * a.T + tkq[h]) * DH);
+            *reinterpret_cast<uint32_t*>(row + 16 * (c ^ ((tkq[h] >> 2) & 1)) + 2 * cl) =
+                pack_half2(d[h][2 * k] + bias[0], d[h][2 * k + 1] + bias[1]);
+          }
+        }
+      }
+      // the next block's LN rewrites A only after this MMA completed (consumers waited)
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  TT();
+  if (warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
+}
+
 template <int MODE>
 int smem_bytes(const TokenArgs& a) {
   constexpr int big = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
@@ -827,12 +1178,39 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
     cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_small_kernel<TOK_POST, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_EMBED, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_POST, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_SLOTKV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_EMBED, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_POST, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(token_q_kernel<TOK_SLOTKV, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     init = true;
   }
   TokenArgs a = a_in;
   if (a.tile_rows != 32 && a.tile_rows != 64 && a.tile_rows != 128)
     a.tile_rows = token_tc_tile_rows(a.n_tok, sms);
   dim3 grid((a.n_tok + a.tile_rows - 1) / a.tile_rows), block(THREADS);
+#ifndef DR_TOK_QUARTER
+#define DR_TOK_QUARTER 1
+#endif
+  if (DR_TOK_QUARTER && a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
+    const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
+                   : (mode == TOK_POST ? smem_bytes<TOK_POST>(a) : smem_bytes<TOK_SLOTKV>(a));
+    const dim3 qb(32 * QWARPS);
+    if (a.tile_rows == 32) {
+      if (mode == TOK_EMBED) launch_pdl(token_q_kernel<TOK_EMBED, 8>, grid, qb, smem, s, a);
+      else if (mode == TOK_POST) launch_pdl(token_q_kernel<TOK_POST, 8>, grid, qb, smem, s, a);
+      else launch_pdl(token_q_kernel<TOK_SLOTKV, 8>, grid, qb, smem, s, a);
+    } else {
+      if (mode == TOK_EMBED) launch_pdl(token_q_kernel<TOK_EMBED, 16>, grid, qb, smem, s, a);
+      else if (mode == TOK_POST) launch_pdl(token_q_kernel<TOK_POST, 16>, grid, qb, smem, s, a);
+      else launch_pdl(token_q_kernel<TOK_SLOTKV, 16>, grid, qb, smem, s, a);
+    }
+#ifdef DR_TRACE
+    tok_trace_snapshot(s, (int)grid.x, mode);
+#endif
+    return;
+  }
   if (a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
     block = dim3(32 * SW);
     const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
