@@ -824,6 +824,28 @@ DR_DEV void q_load64(uint32_t tbase, int quarter, int col0, float (&v)[NH][16]) 
     }
 }
 
+#define DR_TMEM_LD_16x256b_X4(taddr, r)                                                     \
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"  \
+               "%11,%12,%13,%14,%15}, [%16];\n"                                               \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),    \
+                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),  \
+                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                         \
+               : "r"(taddr))
+// 32 accumulator columns: v[h][2k + e] = row (t/4 + 8h), column col0 + 8k + 2(t%4) + e
+template <int NH>
+DR_DEV void q_load32(uint32_t tbase, int quarter, int col0, float (&v)[NH][8]) {
+  uint32_t r[16];
+  DR_TMEM_LD_16x256b_X4(tbase + ((uint32_t)(32 * quarter) << 16) + (uint32_t)col0, r);
+  tc::tmem_wait_ld();
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      v[h][2 * k] = __uint_as_float(r[4 * k + 2 * h]);
+      v[h][2 * k + 1] = __uint_as_float(r[4 * k + 2 * h + 1]);
+    }
+}
+
 DR_DEV float quad4_sum(float v) {                // the 4 threads of a row (t%4)
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -1022,20 +1044,21 @@ __global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
     }
     publish_all();
     TT();
-    // ---------------------------------------------------------- FFN1 + GELU (2 slices)
+    // ---------------------------------------------------------- FFN1 + GELU (4 slices of 32)
     if (warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), w1, 128, 1, &ctl.mma_bar);
-    mma_wait(slice < 2);
-    if (slice < 2) {
-      float d[NH][16];
-      q_load64<NH>(tbase, quarter, 64 + 64 * slice, d);
-      const float* b1 = prm + Prm::b1 + 64 * slice;
+    mma_wait(true);
+    {
+      float d[NH][8];
+      q_load32<NH>(tbase, quarter, 64 + 32 * slice, d);
+      const float* b1 = prm + Prm::b1 + 32 * slice;
+      uint8_t* atom = big + (slice >> 1) * ATOM_A;
 #pragma unroll
       for (int h = 0; h < NH; ++h)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 4; ++k) {
           const int c = 8 * k + cl;
           const uint32_t hv = pack_half2(gelu_erf(d[h][2 * k] + b1[c]), gelu_erf(d[h][2 * k + 1] + b1[c + 1]));
-          *reinterpret_cast<uint32_t*>(big + slice * ATOM_A + sw128(arow(h), k) + 2 * cl) = hv;
+          *reinterpret_cast<uint32_t*>(atom + sw128(arow(h), 4 * (slice & 1) + k) + 2 * cl) = hv;
         }
     }
     publish_all();
