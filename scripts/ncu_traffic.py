@@ -17,13 +17,13 @@ from collections import defaultdict
 
 
 def stage_of(name: str, grid: str) -> str:
-    if "mask_fused" in name:
+    if "mask_fused" in name or "pack_input" in name:
         return "mask_stage"
-    if "token_tc_kernel<0>" in name or "token_small_kernel<0" in name:
+    if "token_tc_kernel<0>" in name or "token_small_kernel<0" in name or "token_q_kernel<0" in name:
         return "embed_qkv"
-    if "token_tc_kernel<2>" in name or "token_small_kernel<2" in name:
+    if "token_tc_kernel<2>" in name or "token_small_kernel<2" in name or "token_q_kernel<2" in name:
         return "slot_kv"
-    if "token_tc_kernel<1>" in name or "token_small_kernel<1" in name:
+    if "token_tc_kernel<1>" in name or "token_small_kernel<1" in name or "token_q_kernel<1" in name:
         return "mlp_qkv"
     if "attn_tc_kernel" in name:
         z = int(grid.strip("()").split(",")[2])
