@@ -814,6 +814,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
         a.resid_in = sp[sl];
         a.next = e->block_w(i);
         a.k = e->kv_ptr(ent[sl], ti, 0); a.v = e->kv_ptr(ent[sl], ti, 1);
+        a.late_wait = 1;
         DR_STOP_CHECK();
         e->launch_tok(TOK_SLOTKV, a, s);
         ++n_slotkv;
@@ -875,8 +876,16 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     a.q = e->q; a.k = e->k; a.v = e->v;
     a.tok16 = e->tok16;
     a.R = e->R; a.Cc = e->Cc;
+#ifndef DR_KV_FILL_IN_LAST
+#define DR_KV_FILL_IN_LAST 0
+#endif
+    // The new slot's K/V (next frame's temporal blocks) are projected by the next forward's
+    // slot K/V launches, which overlap that frame's mask stage (late_wait), instead of
+    // lengthening this frame's last block (DR_KV_FILL_IN_LAST=1: the in-kernel fill).
+    if (last)
+      for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // stale
     int en = -1;
-    if (last && e->n_temporal > 0) {                  // fill the cache for io->new_slot
+    if (DR_KV_FILL_IN_LAST && last && e->n_temporal > 0) {  // fill the cache for new_slot
       en = e->kv_pick(ent[0], ent[1], io->new_slot);
       int tj = 0;
       for (int j = 0; j < e->nb; ++j) {

@@ -40,6 +40,9 @@ struct TokenArgs {
   int R, Cc;              // token grid
   // last block only: K/V of the new memory slot for every temporal block (slot K/V cache)
   int n_kv;
+  // SLOTKV only: skip the entry pdl_wait (the slot input is not produced by the previous
+  // kernel) and wait at exit, so the projection overlaps the predecessor (the mask stage)
+  int late_wait;
   BlockW kv_w[4];
   __half* kv_k[4];
   __half* kv_v[4];

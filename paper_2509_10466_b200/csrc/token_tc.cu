@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
       tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
     }
   }
-  pdl_wait();
+  // SLOTKV with late_wait reads only the caller-provided slot: it runs alongside its
+  // predecessor and waits for it at exit instead (after releasing TMEM)
+  if (!(MODE == TOK_SLOTKV && a.late_wait)) pdl_wait();
   // TMEM only after the predecessor grid completed (PDL early trigger: no CTA holds TMEM
   // while it waits on another grid, so allocations cannot deadlock)
   if (t.warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   sync_act(t);
   TT();
   if (t.warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
+  if (MODE == TOK_SLOTKV && a.late_wait) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -620,7 +623,9 @@ __global__ void __launch_bounds__(32 * SW, SW == 16 ? 2 : 1) token_small_kernel(
   }
   __syncthreads();                              // barriers initialised before any wait
   TT();
-  pdl_wait();
+  // SLOTKV with late_wait reads only the caller-provided slot: it runs alongside its
+  // predecessor and waits for it at exit instead (after releasing TMEM)
+  if (!(MODE == TOK_SLOTKV && a.late_wait)) pdl_wait();
   // TMEM only after the predecessor grid completed (PDL early trigger: no CTA holds TMEM
   // while it waits on another grid, so allocations cannot deadlock)
   if (warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
@@ -784,6 +789,7 @@ __global__ void __launch_bounds__(32 * SW, SW == 16 ? 2 : 1) token_small_kernel(
   }
   TT();
   if (warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
+  if (MODE == TOK_SLOTKV && a.late_wait) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -945,7 +951,9 @@ __global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
   }
   __syncthreads();                              // barriers initialised before any wait
   TT();
-  pdl_wait();
+  // SLOTKV with late_wait reads only the caller-provided slot: it runs alongside its
+  // predecessor and waits for it at exit instead (after releasing TMEM)
+  if (!(MODE == TOK_SLOTKV && a.late_wait)) pdl_wait();
   // TMEM only after the predecessor grid completed (see token_tc_kernel)
   if (warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
   TT();
@@ -1158,6 +1166,7 @@ __global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
   __syncthreads();
   TT();
   if (warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
+  if (MODE == TOK_SLOTKV && a.late_wait) pdl_wait();
 }
 
 template <int MODE>

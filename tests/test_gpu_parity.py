@@ -269,9 +269,11 @@ def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
         launches.append(eng.kernels_per_forward())
         outs_a.append((ra["out"], ra["slot"]))
         mem_a = mem_a.push(ra["slot"][0])
-    # cold: one zero slot (2 temporal blocks) re-projected; then the zero slot0 only;
-    # steady state: both slots cached -> 1 mask + 1 embed + 2 x 4 blocks + 3 decoder
-    assert launches == [15, 15, 13, 13, 13]
+    # every frame projects its newest slot's K/V (2 temporal blocks) at the start, next to
+    # the mask stage; the older slot is cached from the previous frame:
+    # 1 mask + 2 slot K/V + 1 embed + 2 x 4 blocks + 3 decoder (frame 1 also projects the
+    # second zero slot of the cold memory)
+    assert launches == [15, 17, 15, 15, 15]
     mem_b = eng.zero_memory()
     for t in range(5):                           # stream B: clones, always recomputed
         rb = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]),
