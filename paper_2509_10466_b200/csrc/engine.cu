@@ -398,6 +398,11 @@ struct dr_engine {
   }
 
   size_t frame_px() const { return (size_t)H * W; }
+  int sm_count() {
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return sms;
+  }
+  int sms = 0;
 
   void launch_tok(int mode, const TokenArgs& a, cudaStream_t s) const {
     launch_token_tc(mode, a, s);
@@ -876,16 +881,15 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     a.q = e->q; a.k = e->k; a.v = e->v;
     a.tok16 = e->tok16;
     a.R = e->R; a.Cc = e->Cc;
-#ifndef DR_KV_FILL_IN_LAST
-#define DR_KV_FILL_IN_LAST 0
-#endif
-    // The new slot's K/V (next frame's temporal blocks) are projected by the next forward's
-    // slot K/V launches, which overlap that frame's mask stage (late_wait), instead of
-    // lengthening this frame's last block (DR_KV_FILL_IN_LAST=1: the in-kernel fill).
+    // Small batches (32/64-token tiles): the new slot's K/V (next frame's temporal blocks)
+    // are projected by the next forward's slot K/V launches, which overlap that frame's
+    // mask stage (late_wait), instead of lengthening this frame's latency-bound last block.
+    // Large batches (128-token tiles, throughput-bound): filled here, inside the last block.
     if (last)
       for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // stale
     int en = -1;
-    if (DR_KV_FILL_IN_LAST && last && e->n_temporal > 0) {  // fill the cache for new_slot
+    const bool fill_here = token_tc_tile_rows(B * T, e->sm_count()) == 128;
+    if (fill_here && last && e->n_temporal > 0) {     // fill the cache for new_slot
       en = e->kv_pick(ent[0], ent[1], io->new_slot);
       int tj = 0;
       for (int j = 0; j < e->nb; ++j) {

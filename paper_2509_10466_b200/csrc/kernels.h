@@ -54,6 +54,7 @@ enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
 void launch_token_tc(int mode, const TokenArgs& a, cudaStream_t s);   // tcgen05 + TMEM
 size_t token_tc_block_image_bytes();   // per block: weights + 704 fp32 params
 size_t token_tc_embed_image_bytes();   // We + be
+int token_tc_tile_rows(int n_tok, int sms);   // tokens per CTA the token kernels use
 
 // ---------------------------------------------------------------- attention
 struct AttnArgs {
