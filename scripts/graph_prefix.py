@@ -11,8 +11,9 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-NAMES = ["mask", "embed+qkv", "attn S", "post", "attn T", "post", "attn S", "post", "attn T",
-         "post(last)", "vec2patch", "decode.0", "decode.2+composite"]
+NAMES = ["mask", "slot K/V", "slot K/V", "embed+qkv", "attn S", "post", "attn T", "post",
+         "attn S", "post", "attn T", "post(last)", "vec2patch", "decode.0",
+         "decode.2+composite"]
 
 
 def time_prefix(k, reps=200):
