@@ -109,7 +109,9 @@ class WorkPool {
  private:
   WorkPool() {
     const unsigned hw = std::thread::hardware_concurrency();
-    const int n = (int)std::min(7u, hw > 1 ? hw - 1 : 0u);
+    unsigned cap = 11;                          // DR_POOL_THREADS: worker count override
+    if (const char* e = std::getenv("DR_POOL_THREADS")) cap = (unsigned)std::max(0, std::atoi(e));
+    const int n = (int)std::min(cap, hw > 1 ? hw - 1 : 0u);
     for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
   }
   // publish a job once the previous (possibly asynchronous) one has drained; worker w
