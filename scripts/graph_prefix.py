@@ -11,9 +11,9 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-NAMES = ["mask", "slot K/V", "slot K/V", "embed+qkv", "attn S", "post", "attn T", "post",
-         "attn S", "post", "attn T", "post(last)", "vec2patch", "decode.0",
-         "decode.2+composite"]
+NAMES13 = ["mask", "embed+qkv", "attn S", "post", "attn T", "post", "attn S", "post", "attn T",
+           "post(last)", "vec2patch", "decode.0", "decode.2+composite"]
+NAMES = NAMES13                      # replaced by the 15-launch list when slot K/V run
 
 
 def time_prefix(k, reps=200):
@@ -37,6 +37,7 @@ def time_prefix(k, reps=200):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             eng.run(img, msk, (ring[0], ring[1]), out={"out": out, "slot": ring[2]}, sync=False)
+        KERNELS[0] = eng.kernels_per_forward()
         ts = []
         for _ in range(reps):
             flush.zero_()
@@ -49,8 +50,16 @@ def time_prefix(k, reps=200):
     return float(np.median(ts))
 
 
+KERNELS = [0]
+
+
 def main():
+    global NAMES
     prev = 0.0
+    full = time_prefix(99)
+    if KERNELS[0] == 15:
+        NAMES = NAMES13[:1] + ["slot K/V", "slot K/V"] + NAMES13[1:]
+    print(f"{KERNELS[0]} kernels per captured forward, full graph {full:.2f} us")
     for k in range(1, len(NAMES) + 1):
         t = time_prefix(k)
         print(f"k={k:2d} +{NAMES[k-1]:20s} prefix {t:7.2f} us  increment {t - prev:6.2f} us", flush=True)
