@@ -308,12 +308,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return encode;
 }
 
-int make_nhwc_map(CUtensorMap* map, void* base, int frames, int H, int W, int box_rows) {
+int make_nhwc_map(CUtensorMap* map, void* base, int frames, int H, int W, int box_rows,
+                  int box_px = 130) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)frames};
   const cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
-  const cuuint32_t box[4] = {64, 130, (cuuint32_t)box_rows, 1};
+  const cuuint32_t box[4] = {64, (cuuint32_t)box_px, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -350,6 +351,16 @@ struct dr_engine {
   uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We + be, then per block
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
+  // combined Vec2Patch o decode.0 (DR_V2P_COMB): 144 taps of the 12x12 kernel, combined
+  // bias, fp32 Vec2Patch / decode.0 weights for the border corrections
+  bool comb = false;
+  uint8_t* wcomb = nullptr;
+  float* bcomb = nullptr;
+  float* wv32 = nullptr;
+  float* wc32 = nullptr;
+  float* canv_ring = nullptr;        // Vec2Patch canvas just outside the image
+  float* bdelta = nullptr;           // decode.0 border corrections
+  CUtensorMap map_rows{};
   size_t wtc_v2p = 0;                // byte offset of the Vec2Patch image
   size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
   CUtensorMap map_raster{}, map_tok{};
@@ -472,6 +483,9 @@ struct dr_engine {
     const size_t o_ras = take(px * C * 2), o_ep = take(px * 27 * 2);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
+    const size_t n_ring = (size_t)frames * (2 * (W + 2) + 2 * H) * 64;
+    const size_t n_delta = (size_t)frames * (2 * W + 2 * (H - 2)) * 64;
+    const size_t o_ring = take(comb ? n_ring * 4 : 0), o_delta = take(comb ? n_delta * 4 : 0);
     CUDA_TRY(cudaMalloc(&ws, off));
     uint8_t* b = static_cast<uint8_t*>(ws);
     bits0 = (uint32_t*)(b + o_b0); bits1 = (uint32_t*)(b + o_b1);
@@ -482,10 +496,16 @@ struct dr_engine {
     attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
     raster = (__half*)(b + o_ras); eplanes = (__half*)(b + o_ep);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
+    canv_ring = comb ? (float*)(b + o_ring) : nullptr;
+    bdelta = comb ? (float*)(b + o_delta) : nullptr;
     cap = frames;
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
     int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
     if (rc) return rc;
+    if (comb) {
+      rc = make_nhwc_map(&map_rows, raster, frames, H, W, 1, 128);
+      if (rc) return rc;
+    }
     return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
   }
 
@@ -654,6 +674,76 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
             }
   }
 
+#ifndef DR_V2P_COMB
+#define DR_V2P_COMB 0
+#endif
+  // Vec2Patch o decode.0 as one transposed convolution: Wcomb[co][ci][u][v]
+  // = sum_{dy,dx,c'} Wc[co][c'][dy][dx] Wv[ci][c'][u+dy][v+dx], u, v in [-2, 9], packed like
+  // the Vec2Patch taps; bcomb = bc + sum Wc bv (double accumulation)
+  std::vector<uint16_t> combimg;
+  std::vector<float> bcomb;
+  // (the combined taps need a token window of 128 + 2 (Cc + 2) + 2 rows <= 3 x 128: W <= 1000)
+  if (DR_V2P_COMB && kk == 10 && c == 64 && 2 * (e->Cc + 2) + 130 <= 384) {
+    e->comb = true;
+    const float* wv = weights[tb];
+    const float* wc = weights[tb + 2];
+    combimg.resize((size_t)144 * 64 * 64);
+    WorkPool::get().run([&](int part, int parts) {
+      std::vector<double> acc((size_t)64 * 64);
+      for (int tap = part; tap < 144; tap += parts) {
+        const int u = tap / 12 - 2, v = tap % 12 - 2;
+        std::fill(acc.begin(), acc.end(), 0.0);
+        for (int dy = 0; dy < 3; ++dy)
+          for (int dx = 0; dx < 3; ++dx) {
+            const int ay = u + dy, ax = v + dx;
+            if (ay < 0 || ay >= 10 || ax < 0 || ax >= 10) continue;
+            for (int co = 0; co < 64; ++co)
+              for (int cp = 0; cp < 64; ++cp) {
+                const double wcv = wc[((size_t)co * 64 + cp) * 9 + dy * 3 + dx];
+                for (int ci = 0; ci < 64; ++ci)
+                  acc[(size_t)co * 64 + ci] += wcv * wv[(((size_t)ci * 64 + cp) * 10 + ay) * 10 + ax];
+              }
+          }
+        uint16_t* dst = combimg.data() + (size_t)tap * 64 * 64;    // [k-chunk][co][8 ci]
+        for (int ch = 0; ch < 8; ++ch)
+          for (int co = 0; co < 64; ++co)
+            for (int j = 0; j < 8; ++j) {
+              const __half hv = __float2half_rn((float)acc[(size_t)co * 64 + ch * 8 + j]);
+              std::memcpy(dst + ((size_t)ch * 64 + co) * 8 + j, &hv, 2);
+            }
+      }
+    });
+    const float* bv = weights[tb + 1];
+    const float* bc = weights[tb + 3];
+    bcomb.resize(64);
+    for (int co = 0; co < 64; ++co) {
+      double b = bc[co];
+      for (int cp = 0; cp < 64; ++cp)
+        for (int t = 0; t < 9; ++t) b += (double)wc[((size_t)co * 64 + cp) * 9 + t] * bv[cp];
+      bcomb[co] = (float)b;
+    }
+    // border-correction weights, output channel fastest (coalesced across threads):
+    // Vec2Patch [ky][kx][ci][c'], decode.0 [tap][c'][co]
+    std::vector<float> wvt((size_t)100 * 64 * 64), wct((size_t)9 * 64 * 64);
+    for (int ci = 0; ci < 64; ++ci)
+      for (int cp = 0; cp < 64; ++cp)
+        for (int k = 0; k < 100; ++k) wvt[((size_t)k * 64 + ci) * 64 + cp] = wv[((size_t)ci * 64 + cp) * 100 + k];
+    for (int co = 0; co < 64; ++co)
+      for (int cp = 0; cp < 64; ++cp)
+        for (int t = 0; t < 9; ++t) wct[((size_t)t * 64 + cp) * 64 + co] = wc[((size_t)co * 64 + cp) * 9 + t];
+    if (cudaMalloc(&e->wcomb, combimg.size() * 2) != cudaSuccess ||
+        cudaMalloc(&e->bcomb, 64 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&e->wv32, (size_t)64 * 64 * 100 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&e->wc32, (size_t)64 * 64 * 9 * sizeof(float)) != cudaSuccess ||
+        cudaMemcpy(e->wcomb, combimg.data(), combimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->bcomb, bcomb.data(), 64 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->wv32, wvt.data(), wvt.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->wc32, wct.data(), wct.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+      dr_destroy(e);
+      return fail(DR_ERR_CUDA, "combined decoder weight upload failed");
+    }
+  }
+
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
   e->feather_r = (int)(fw.size() / 2);
   if (const char* sa = std::getenv("DR_STOP_AFTER")) e->stop_after = std::atoi(sa);
@@ -682,6 +772,10 @@ void dr_destroy(dr_engine* e) {
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->rgb_event) cudaEventDestroy(e->rgb_event);
   cudaFree(e->fparams);
+  cudaFree(e->wcomb);
+  cudaFree(e->bcomb);
+  cudaFree(e->wv32);
+  cudaFree(e->wc32);
   cudaFree(e->feather_w);
   cudaFree(e->wtc);
   cudaFree(e->timg);
@@ -917,6 +1011,23 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   V2pArgs vp{};
   vp.frames = B; vp.H = e->H; vp.W = e->W; vp.R = e->R; vp.Cc = e->Cc;
   vp.w = e->wtc + e->wtc_v2p; vp.bias = e->fparams + e->bv2p; vp.raster = e->raster;
+  if (e->comb) {
+    // Vec2Patch o decode.0 in one transposed convolution (raster = LeakyReLU(decode.0)),
+    // after the border corrections, then decode.2's tap-expanded GEMM alone
+    BorderArgs ba{};
+    ba.frames = B; ba.H = e->H; ba.W = e->W; ba.R = e->R; ba.Cc = e->Cc;
+    ba.tok16 = e->tok16; ba.wv = e->wv32; ba.bv = e->fparams + e->bv2p; ba.wc = e->wc32;
+    ba.ring = e->canv_ring; ba.delta = e->bdelta;
+    DR_STOP_CHECK();
+    launch_border_corrections(ba, s);
+    vp.comb = 1; vp.w = e->wcomb; vp.bias = e->bcomb; vp.delta = e->bdelta;
+    DR_STOP_CHECK();
+    launch_v2p_tc(e->map_tok, vp, s);
+    e->mark(6, s);
+    DR_STOP_CHECK();
+    launch_e_only(e->map_rows, nullptr, e->timg + e->te_d2, e->eplanes, B, e->H, e->W, s);
+    e->mark(7, s);
+  } else {
   DR_STOP_CHECK();
   launch_v2p_tc(e->map_tok, vp, s);
   e->mark(6, s);
@@ -929,6 +1040,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   DR_STOP_CHECK();
   launch_conv3x3_tc(64, e->map_raster, cv, s);
   e->mark(7, s);
+  }
   ConvTcArgs c2{};
   c2.frames = B; c2.H = e->H; c2.W = e->W;
   c2.bias = e->fparams + e->bd2; c2.e_planes = e->eplanes;
@@ -938,7 +1050,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   if (B == 1) { c2.spans = e->pack_spans; c2.packed = e->pack_out; }
   DR_STOP_CHECK();
   launch_dec2_gather(c2, s);
-  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0);
+  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0) + (e->comb ? 2 : 0);
   e->mark(8, s);
 #undef DR_STOP_CHECK
   CUDA_TRY(cudaGetLastError());

@@ -272,8 +272,8 @@ def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
     # every frame projects its newest slot's K/V (2 temporal blocks) at the start, next to
     # the mask stage; the older slot is cached from the previous frame:
     # 1 mask + 2 slot K/V + 1 embed + 2 x 4 blocks + 3 decoder (frame 1 also projects the
-    # second zero slot of the cold memory)
-    assert launches == [15, 17, 15, 15, 15]
+    # second zero slot of the cold memory); +2 with the combined decoder (DR_V2P_COMB)
+    assert launches in ([15, 17, 15, 15, 15], [17, 19, 17, 17, 17])
     mem_b = eng.zero_memory()
     for t in range(5):                           # stream B: clones, always recomputed
         rb = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]),
