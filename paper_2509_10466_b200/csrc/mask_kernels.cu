@@ -26,8 +26,11 @@ namespace dr {
 
 namespace {
 
-constexpr int TH = 16, TW = 64;            // tile
-constexpr int NT = 512, NWARP = NT / 32;   // threads / warps per tile
+#ifndef DR_MASK_TH
+#define DR_MASK_TH 16
+#endif
+constexpr int TH = DR_MASK_TH, TW = 64;    // tile (rows x pixels)
+constexpr int NT = 32 * TH, NWARP = NT / 32;   // one warp per tile row (vertical pass)
 constexpr int MAXH = 62;                   // max halo r + R (r <= 31, R <= 31)
 constexpr int MAXR = 31;                   // 2R+1 <= 63: a column window fits a uint64
 constexpr int NW_MAX = 2 + 2 * (MAXH / 32);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     // 3b. vertical pass (float64, scipy order) for the tile rows x span columns; the
     //     window of row ty is bits ty .. ty+2R of the column word
     const uint64_t need = (2 * R + 1 == 64) ? ~0ull : ((1ull << (2 * R + 1)) - 1ull);
-    for (int tx = tid & 31, ty = tid >> 5; tx < span; tx += 32) {   // TH = 16 rows, NT = 512
+    for (int tx = tid & 31, ty = tid >> 5; tx < span; tx += 32) {   // ty < TH (NT = 32 TH)
       double acc;
       if (y0 + ty >= a.H) acc = 0.0;
       else {
