@@ -328,14 +328,20 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tin, ConvTcArgs a) {
 // The CTA that finishes last publishes the flags words (every CTA's atomicOr happens before
 // its counter increment; the last one acquires them all) when a mirror is requested.
 DR_DEV void mirror_flags(const ConvTcArgs& a) {
-  if (!a.flags_mirror) return;
+  if (!a.flags_mirror && !a.mirror_after_spans) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned total = gridDim.x * gridDim.y * gridDim.z;
     if (atomicAdd(a.done, 1u) == total - 1) {
       __threadfence();
-      for (int i = 0; i < a.frames; ++i) a.flags_mirror[i] = atomicOr(a.flags + i, 0);
+      int* fm = a.flags_mirror;
+      if (a.mirror_after_spans) {
+        const int4 sp = a.spans[a.H - 1];
+        const size_t n = (size_t)sp.z + 3 * (size_t)(sp.y - sp.x);
+        fm = reinterpret_cast<int*>(a.packed + ((n + 3) & ~(size_t)3));
+      }
+      for (int i = 0; i < a.frames; ++i) fm[i] = atomicOr(a.flags + i, 0);
       *a.done = 0;
     }
   }

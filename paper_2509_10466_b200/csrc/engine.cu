@@ -391,6 +391,19 @@ struct dr_engine {
   std::vector<int> span_first, span_last;   // host path scratch: masked extent per row
   std::vector<int> span_wmin, span_wmax, span_buf;
   unsigned* d_done = nullptr;        // decode.2 finished-CTA counter (flags mirror)
+  // host path CUDA graphs: dr_forward's launch sequence depends only on a few ring / slot
+  // K/V cache decisions, so each distinct signature is captured once and replayed
+  bool dry = false;                  // dr_forward: host-side decisions only, no launches
+  std::vector<intptr_t> sig;         // dr_forward: what its launches depended on
+  struct HostGraph { std::vector<intptr_t> key; cudaGraphExec_t exec; };
+  std::vector<HostGraph> hgraphs;
+  int host_graph = 1;                // DR_HOST_GRAPH=0: direct launches
+  cudaStream_t cap_stream = nullptr; // capture stream (the caller's may be the legacy one)
+  cudaEvent_t fork_ev = nullptr;
+  void clear_graphs() {
+    for (auto& g : hgraphs) cudaGraphExecDestroy(g.exec);
+    hgraphs.clear();
+  }
   // optional per-stage CUDA events (dr_profile): ev[0] before the first stage
   static constexpr int kMaxEv = 64;
   int profiling = 0, n_ev = 0;
@@ -460,6 +473,7 @@ struct dr_engine {
   }
 
   void free_ws() {
+    clear_graphs();
     if (ws) cudaFree(ws);
     ws = nullptr;
     cap = 0;
@@ -747,6 +761,7 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
   e->feather_r = (int)(fw.size() / 2);
   if (const char* sa = std::getenv("DR_STOP_AFTER")) e->stop_after = std::atoi(sa);
+  if (const char* hg = std::getenv("DR_HOST_GRAPH")) e->host_graph = std::atoi(hg);
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
   if (cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
@@ -771,6 +786,8 @@ void dr_destroy(dr_engine* e) {
   e->free_ws();
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->rgb_event) cudaEventDestroy(e->rgb_event);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
   cudaFree(e->fparams);
   cudaFree(e->wcomb);
   cudaFree(e->bcomb);
@@ -859,8 +876,10 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   const int T = e->T;
   int* flags = io->flags ? io->flags : e->flags;
   e->n_ev = 0;
-  e->mark(-1, s);
-  CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * B, s));
+  // e->dry: every host-side decision (and its state update) without the launches
+#define DR_L(x) do { if (!e->dry) { x; } } while (0)
+  DR_L(e->mark(-1, s));
+  DR_L(CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * B, s)));
   // diagnostics only (DR_STOP_AFTER): truncate the launch sequence to time graph prefixes
   int n_launched = 0;
 #define DR_STOP_CHECK() \
@@ -880,16 +899,16 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     mo.rgb_f32 = nullptr; mo.rgb_u8 = nullptr; mo.xin = nullptr;
     if (!mo.m1) mo.m1 = e->m1;
     DR_STOP_CHECK();
-    launch_mask_stage(mo, s);
-    CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, 0));
+    DR_L(launch_mask_stage(mo, s));
+    DR_L(CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, 0)));
     MaskArgs pk = m;
     pk.m1 = mo.m1;
-    launch_pack_input(pk, s);
+    DR_L(launch_pack_input(pk, s));
   } else {
     DR_STOP_CHECK();
-    launch_mask_stage(m, s);
+    DR_L(launch_mask_stage(m, s));
   }
-  e->mark(0, s);
+  DR_L(e->mark(0, s));
 
   // 2. memory-slot K/V of every temporal block (LN1 + k/v projection of each slot,
   //    dstt.py:188-190).  An LRU cache keyed by slot pointer holds them: the last block
@@ -897,7 +916,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   //    engine's own outputs back, slot_kv_reuse bits set) nothing is recomputed here.
   const int fs = io->slot_batched ? B : 1;
   int ent[2] = {0, 0};
-  int n_slotkv = 0;
+  int n_slotkv = 0, kv_computed = 0, en_fill = -1;
   if (e->n_temporal > 0) {
     const float* sp[2] = {io->slot0, io->slot1};
     for (int sl = 0; sl < 2; ++sl) {
@@ -907,6 +926,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
       if (ent[sl] >= 0) continue;
       ent[sl] = e->kv_pick(sl == 1 ? ent[0] : -1, -1, sp[sl]);
       e->kv_set(ent[sl], sp[sl], fs, io->slot_batched != 0);
+      kv_computed |= 1 << sl;
       int ti = 0;
       for (int i = 0; i < e->nb; ++i) {
         if (!e->blk[i].temporal) continue;
@@ -917,9 +937,9 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
         a.k = e->kv_ptr(ent[sl], ti, 0); a.v = e->kv_ptr(ent[sl], ti, 1);
         a.late_wait = 1;
         DR_STOP_CHECK();
-        e->launch_tok(TOK_SLOTKV, a, s);
+        DR_L(e->launch_tok(TOK_SLOTKV, a, s));
         ++n_slotkv;
-        e->mark(1, s);
+        DR_L(e->mark(1, s));
         ++ti;
       }
     }
@@ -935,8 +955,8 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     a.has_next = 1; a.next = e->block_w(0);
     a.q = e->q; a.k = e->k; a.v = e->v;
     DR_STOP_CHECK();
-    e->launch_tok(TOK_EMBED, a, s);
-    e->mark(2, s);
+    DR_L(e->launch_tok(TOK_EMBED, a, s));
+    DR_L(e->mark(2, s));
   }
 
   // 4. blocks; mask-aware validity (MAT update) resolved into a per-block mode
@@ -964,8 +984,8 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
       at.n_seg = 1; at.groups = 1; at.band = T;
     }
     DR_STOP_CHECK();
-    launch_attention(at, s);
-    e->mark(temporal ? 4 : 3, s);
+    DR_L(launch_attention(at, s));
+    DR_L(e->mark(temporal ? 4 : 3, s));
 
     const bool last = i == e->nb - 1;
     TokenArgs a{};
@@ -998,12 +1018,13 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
       a.n_kv = tj;
     }
     DR_STOP_CHECK();
-    e->launch_tok(TOK_POST, a, s);
+    DR_L(e->launch_tok(TOK_POST, a, s));
+    if (en >= 0) en_fill = en;
     if (en >= 0) {
       for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // alias
       e->kv_set(en, io->new_slot, B, true);
     }
-    e->mark(5, s);
+    DR_L(e->mark(5, s));
     cur ^= 1;
   }
 
@@ -1019,18 +1040,18 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     ba.tok16 = e->tok16; ba.wv = e->wv32; ba.bv = e->fparams + e->bv2p; ba.wc = e->wc32;
     ba.ring = e->canv_ring; ba.delta = e->bdelta;
     DR_STOP_CHECK();
-    launch_border_corrections(ba, s);
+    DR_L(launch_border_corrections(ba, s));
     vp.comb = 1; vp.w = e->wcomb; vp.bias = e->bcomb; vp.delta = e->bdelta;
     DR_STOP_CHECK();
-    launch_v2p_tc(e->map_tok, vp, s);
-    e->mark(6, s);
+    DR_L(launch_v2p_tc(e->map_tok, vp, s));
+    DR_L(e->mark(6, s));
     DR_STOP_CHECK();
-    launch_e_only(e->map_rows, nullptr, e->timg + e->te_d2, e->eplanes, B, e->H, e->W, s);
-    e->mark(7, s);
+    DR_L(launch_e_only(e->map_rows, nullptr, e->timg + e->te_d2, e->eplanes, B, e->H, e->W, s));
+    DR_L(e->mark(7, s));
   } else {
   DR_STOP_CHECK();
-  launch_v2p_tc(e->map_tok, vp, s);
-  e->mark(6, s);
+  DR_L(launch_v2p_tc(e->map_tok, vp, s));
+  DR_L(e->mark(6, s));
   // decode.0 with decode.2's tap-expanded GEMM fused into its epilogue (E planes), then
   // the decode.2 gather + tanh + composite
   ConvTcArgs cv{};
@@ -1038,8 +1059,8 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   cv.w = e->wtc; cv.bias = e->fparams + e->bd0;
   cv.e_planes = e->eplanes; cv.w2 = e->timg + e->te_d2;
   DR_STOP_CHECK();
-  launch_conv3x3_tc(64, e->map_raster, cv, s);
-  e->mark(7, s);
+  DR_L(launch_conv3x3_tc(64, e->map_raster, cv, s));
+  DR_L(e->mark(7, s));
   }
   ConvTcArgs c2{};
   c2.frames = B; c2.H = e->H; c2.W = e->W;
@@ -1047,11 +1068,21 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
   c2.flags_mirror = e->flags_mirror; c2.done = e->d_done;
-  if (B == 1) { c2.spans = e->pack_spans; c2.packed = e->pack_out; }
+  if (B == 1 && e->pack_spans) {
+    c2.spans = e->pack_spans; c2.packed = e->pack_out; c2.mirror_after_spans = 1;
+  }
   DR_STOP_CHECK();
-  launch_dec2_gather(c2, s);
+  DR_L(launch_dec2_gather(c2, s));
   e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0) + (e->comb ? 2 : 0);
-  e->mark(8, s);
+  DR_L(e->mark(8, s));
+  e->sig = {B, split, (intptr_t)io->rgb_u8, (intptr_t)io->rgb_f32, (intptr_t)io->mask_m0,
+            (intptr_t)io->slot0, (intptr_t)io->slot1, (intptr_t)io->new_slot,
+            (intptr_t)io->slot_batched, (intptr_t)flags, (intptr_t)tv, (intptr_t)alpha,
+            (intptr_t)io->dilated, (intptr_t)io->fill, (intptr_t)io->out_u8,
+            (intptr_t)io->out_f32, (intptr_t)e->pack_spans, (intptr_t)e->pack_out,
+            (intptr_t)e->flags_mirror, (intptr_t)e->rgb_ready, ent[0], ent[1], kv_computed,
+            en_fill, e->comb};
+#undef DR_L
 #undef DR_STOP_CHECK
   CUDA_TRY(cudaGetLastError());
   return DR_OK;
@@ -1220,16 +1251,10 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   // run while the rgb crosses PCIe on the copy stream
   if (!e->copy_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&e->rgb_event, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
   }
-  if (tr.on) cudaEventRecord(tr.ev[0], s);
-  par_memcpy(p_m0, mask_hw, px, CP_NT);
-  CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, in_bytes - px * 3, cudaMemcpyHostToDevice, s));
-  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
-  if (tr.on) tt[1] = now_us();
-  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
-  CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
-  if (tr.on) cudaEventRecord(tr.ev[1], s);
   int fresh = 0;
   while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
   dr_frame_io io{};
@@ -1240,14 +1265,74 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
   e->pack_spans = reinterpret_cast<const int4*>(e->h_rgb + in_spans);
   e->pack_out = e->h_out;
-  e->flags_mirror = reinterpret_cast<int*>(e->h_out + mirror);
+  e->flags_mirror = nullptr;         // decode.2 places it after the packed bytes
   e->rgb_ready = e->rgb_event;
-  int rc = dr_forward(e, &io, stream);
-  e->pack_spans = nullptr;
-  e->pack_out = nullptr;
-  e->flags_mirror = nullptr;
-  e->rgb_ready = nullptr;
-  if (rc) return rc;
+  struct Restore {
+    dr_engine* e;
+    ~Restore() { e->pack_spans = nullptr; e->pack_out = nullptr; e->rgb_ready = nullptr; e->dry = false; }
+  } restore{e};
+  // uploads: mask + span table on s first (in flight while the rgb is staged), then the
+  // rgb on the copy stream (forked from s; inside the graph when graphed), so the mask
+  // stage runs while the rgb crosses PCIe
+  auto rgb_upload = [&](cudaStream_t st) -> int {
+    CUDA_TRY(cudaEventRecord(e->fork_ev, st));
+    CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->fork_ev, 0));
+    CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
+    CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
+    return DR_OK;
+  };
+  const bool graphed = e->host_graph && !e->profiling && e->stop_after < 0;
+  int rc = DR_OK;
+  if (tr.on) cudaEventRecord(tr.ev[0], s);
+  par_memcpy(p_m0, mask_hw, px, CP_NT);
+  CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, in_bytes - px * 3, cudaMemcpyHostToDevice, s));
+  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
+  if (tr.on) tt[1] = now_us();
+  if (!graphed) {
+    CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
+    CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
+    if (tr.on) cudaEventRecord(tr.ev[1], s);
+    rc = dr_forward(e, &io, stream);
+    if (rc) return rc;
+  } else {
+    // The whole upload + launch sequence as one graph launch.  A dry pass makes dr_forward's
+    // decisions (slot K/V cache, ring) and state updates; its signature selects the graph.
+    // A new signature rewinds the cache state and captures the real pass.
+    if (tr.on) cudaEventRecord(tr.ev[1], s);
+    dr_engine::KvEntry kvc0[dr_engine::KV_ENTRIES];
+    std::copy(std::begin(e->kvc), std::end(e->kvc), kvc0);
+    const uint64_t tick0 = e->kv_tick;
+    e->dry = true;
+    rc = dr_forward(e, &io, stream);
+    e->dry = false;
+    if (rc) return rc;
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : e->hgraphs)
+      if (g.key == e->sig) exec = g.exec;
+    if (!exec) {
+      const std::vector<intptr_t> key = e->sig;
+      std::copy(std::begin(kvc0), std::end(kvc0), e->kvc);
+      e->kv_tick = tick0;
+      if (e->hgraphs.size() >= 16) e->clear_graphs();
+      CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+      rc = rgb_upload(e->cap_stream);
+      if (!rc) rc = dr_forward(e, &io, e->cap_stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+      if (!rc && ce != cudaSuccess)
+        rc = fail(DR_ERR_CUDA, std::string("host-path graph capture: ") + cudaGetErrorString(ce));
+      if (!rc && e->sig != key) rc = fail(DR_ERR_CUDA, "host-path graph: signature changed");
+      if (!rc) {
+        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        if (ie != cudaSuccess)
+          rc = fail(DR_ERR_CUDA, std::string("host-path graph instantiate: ") + cudaGetErrorString(ie));
+      }
+      if (g) cudaGraphDestroy(g);
+      if (rc) return rc;
+      e->hgraphs.push_back({key, exec});
+    }
+    CUDA_TRY(cudaGraphLaunch(exec, s));
+  }
   if (tr.on) {
     cudaEventRecord(tr.ev[2], s);
     tt[2] = now_us();

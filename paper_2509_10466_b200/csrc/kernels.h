@@ -129,6 +129,10 @@ struct ConvTcArgs {
   // `done` is a zeroed counter the last CTA re-arms
   int* flags_mirror;
   unsigned* done;
+  // host path: with spans set, the mirror lives after the packed bytes, at
+  // align4(spans[H-1].z + 3 * (spans[H-1].y - spans[H-1].x)) (fixed kernel arguments, so
+  // the host path's launch sequence can be replayed from a CUDA graph)
+  int mirror_after_spans;
   // decode.2 gather (optional, one frame): also write the u8 composite of the pixels in
   // row y's span [spans[y].x, spans[y].y) to packed + spans[y].z + 3 * (x - x0)
   const int4* spans;
