@@ -218,13 +218,20 @@ def test_memory_fifo_and_memory_changes_output(rng):
     assert not np.array_equal(cold.rgb, warm.rgb)
 
 
-def test_host_buffer_path_equals_device_path(rng):
-    """dr_inpaint_u8_host (engine-held memory) == engine.inpaint with carried memory."""
+@pytest.mark.parametrize("graphed", ["1", "0"])
+def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed):
+    """dr_inpaint_u8_host (engine-held memory) == engine.inpaint with carried memory.  Nine
+    frames: the host path's CUDA graphs (one per ring / slot K/V-cache signature) are
+    captured on the first cycle and replayed after, with masks of different areas (so the
+    flags word lands at a different offset of the packed read-back every frame)."""
+    monkeypatch.setenv("DR_HOST_GRAPH", graphed)       # read at engine creation
     cfg = DsttConfig.baseline(64, mask_dilate=2, mask_feather_sigma=1.5)
     eng = DsttEngine(cfg, seed=4)
     mem = eng.zero_memory()
-    for _ in range(4):
-        rgb, bits = _redacted(rng, 64, 64, 0.2)
+    for i in range(9):
+        rgb, bits = _redacted(rng, 64, 64, 0.2 if i % 3 == 0 else 0.0)
+        bits[20:22 + 3 * i, 30:31 + 2 * i] = True
+        rgb[bits] = 0
         a = eng.inpaint(rgb, BinaryMask(bits), mem)
         mem = a.memory
         b = eng.inpaint_host(rgb, bits)
