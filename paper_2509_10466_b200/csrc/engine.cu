@@ -394,6 +394,8 @@ struct dr_engine {
   // host path CUDA graphs: dr_forward's launch sequence depends only on a few ring / slot
   // K/V cache decisions, so each distinct signature is captured once and replayed
   bool dry = false;                  // dr_forward: host-side decisions only, no launches
+  bool capturing = false;            // dr_forward under host-path graph capture
+  int rgb_chunks = 1;                // DR_RGB_CHUNKS: host-path rgb staging/upload pieces
   std::vector<intptr_t> sig;         // dr_forward: what its launches depended on
   struct HostGraph { std::vector<intptr_t> key; cudaGraphExec_t exec; };
   std::vector<HostGraph> hgraphs;
@@ -762,6 +764,8 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   e->feather_r = (int)(fw.size() / 2);
   if (const char* sa = std::getenv("DR_STOP_AFTER")) e->stop_after = std::atoi(sa);
   if (const char* hg = std::getenv("DR_HOST_GRAPH")) e->host_graph = std::atoi(hg);
+  if (const char* rcn = std::getenv("DR_RGB_CHUNKS"))
+    e->rgb_chunks = std::min(8, std::max(1, std::atoi(rcn)));
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
   if (cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
@@ -900,7 +904,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     if (!mo.m1) mo.m1 = e->m1;
     DR_STOP_CHECK();
     DR_L(launch_mask_stage(mo, s));
-    DR_L(CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, 0)));
+    DR_L(CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, e->capturing ? cudaEventWaitExternal : 0)));
     MaskArgs pk = m;
     pk.m1 = mo.m1;
     DR_L(launch_pack_input(pk, s));
@@ -1269,33 +1273,36 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   e->rgb_ready = e->rgb_event;
   struct Restore {
     dr_engine* e;
-    ~Restore() { e->pack_spans = nullptr; e->pack_out = nullptr; e->rgb_ready = nullptr; e->dry = false; }
+    ~Restore() {
+      e->pack_spans = nullptr; e->pack_out = nullptr; e->rgb_ready = nullptr;
+      e->dry = false; e->capturing = false;
+    }
   } restore{e};
   // uploads: mask + span table on s first (in flight while the rgb is staged), then the
-  // rgb on the copy stream (forked from s; inside the graph when graphed), so the mask
-  // stage runs while the rgb crosses PCIe
-  auto rgb_upload = [&](cudaStream_t st) -> int {
-    CUDA_TRY(cudaEventRecord(e->fork_ev, st));
-    CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->fork_ev, 0));
-    CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
-    CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
-    return DR_OK;
-  };
+  // rgb on the copy stream in chunks, each sent as soon as it is staged, so the mask stage
+  // runs while the rgb crosses PCIe; the input pack waits for the rgb event
   const bool graphed = e->host_graph && !e->profiling && e->stop_after < 0;
   int rc = DR_OK;
   if (tr.on) cudaEventRecord(tr.ev[0], s);
   par_memcpy(p_m0, mask_hw, px, CP_NT);
   CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, in_bytes - px * 3, cudaMemcpyHostToDevice, s));
-  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
+  CUDA_TRY(cudaEventRecord(e->fork_ev, s));
+  CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->fork_ev, 0));
+  for (int c = 0; c < e->rgb_chunks; ++c) {
+    const size_t b0 = (px * 3 * c / e->rgb_chunks) & ~(size_t)63;
+    const size_t b1 = c + 1 == e->rgb_chunks ? px * 3 : (px * 3 * (c + 1) / e->rgb_chunks) & ~(size_t)63;
+    par_memcpy(p_rgb + b0, rgb_hwc + b0, b1 - b0, CP_NT);
+    CUDA_TRY(cudaMemcpyAsync(e->h_rgb + b0, p_rgb + b0, b1 - b0, cudaMemcpyHostToDevice,
+                             e->copy_stream));
+  }
+  CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
   if (tr.on) tt[1] = now_us();
   if (!graphed) {
-    CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
-    CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
     if (tr.on) cudaEventRecord(tr.ev[1], s);
     rc = dr_forward(e, &io, stream);
     if (rc) return rc;
   } else {
-    // The whole upload + launch sequence as one graph launch.  A dry pass makes dr_forward's
+    // The launch sequence as one graph launch.  A dry pass makes dr_forward's
     // decisions (slot K/V cache, ring) and state updates; its signature selects the graph.
     // A new signature rewinds the cache state and captures the real pass.
     if (tr.on) cudaEventRecord(tr.ev[1], s);
@@ -1315,8 +1322,9 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
       e->kv_tick = tick0;
       if (e->hgraphs.size() >= 16) e->clear_graphs();
       CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
-      rc = rgb_upload(e->cap_stream);
-      if (!rc) rc = dr_forward(e, &io, e->cap_stream);
+      e->capturing = true;             // the rgb event is recorded outside the graph
+      rc = dr_forward(e, &io, e->cap_stream);
+      e->capturing = false;
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
       if (!rc && ce != cudaSuccess)
