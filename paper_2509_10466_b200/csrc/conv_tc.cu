@@ -342,6 +342,7 @@ DR_DEV void mirror_flags(const ConvTcArgs& a) {
         fm = reinterpret_cast<int*>(a.packed + ((n + 3) & ~(size_t)3));
       }
       for (int i = 0; i < a.frames; ++i) fm[i] = atomicOr(a.flags + i, 0);
+      if (a.rgb_flag) *a.rgb_flag = 0;
       *a.done = 0;
     }
   }

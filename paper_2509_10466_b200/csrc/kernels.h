@@ -96,6 +96,10 @@ struct MaskArgs {
   uint8_t* token_valid;      // [frames][T] out
   __half* xin;               // [frames][T][4*p*p] out (optional)
   int* flags;                // [frames] out: bit1 = input not redacted inside m0
+  // input pack (host path): spin until the copy stream sets this word after the rgb upload
+  // (so the launch sequence can be enqueued before the rgb is even staged); bounded wait,
+  // bit2 of flags on timeout
+  unsigned* rgb_flag;
 };
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s);
 // xin + redaction check alone, from u8 rgb, m0 and the stage's m1 bytes
@@ -133,6 +137,7 @@ struct ConvTcArgs {
   // align4(spans[H-1].z + 3 * (spans[H-1].y - spans[H-1].x)) (fixed kernel arguments, so
   // the host path's launch sequence can be replayed from a CUDA graph)
   int mirror_after_spans;
+  unsigned* rgb_flag;        // host path: re-armed (zeroed) by the last CTA
   // decode.2 gather (optional, one frame): also write the u8 composite of the pixels in
   // row y's span [spans[y].x, spans[y].y) to packed + spans[y].z + 3 * (x - x0)
   const int4* spans;
