@@ -124,6 +124,11 @@ int dr_reset_memory(dr_engine* e);
 /* Number of kernels one dr_forward launches for `frames` frames (for accounting). */
 int32_t dr_kernels_per_forward(dr_engine* e);
 
+/* Tokens per CTA the token-chain kernels use for `frames` frames: 128 selects the
+ * throughput kernel (whose last block also fills the new slot's K/V cache), 32 / 64 the
+ * latency kernel (DR_TOK_ROWS at dr_create forces one). */
+int32_t dr_token_tile_rows(dr_engine* e, int32_t frames);
+
 /* Op-level entry for parity tests of the tcgen05 implicit-GEMM convolution
  * (decode.0 form, dstt.py:241-242): out = LeakyReLU_0.2(conv3x3(in) + bias), NHWC fp16
  * rasters [frames][H][W][64], weight [64][64][3][3] fp32 host, bias [64] fp32 host. */

@@ -57,6 +57,7 @@ SIGNATURES = {
                                           ctypes.c_void_p, ctypes.c_void_p]),
     "dr_reset_memory": (ctypes.c_int, [ctypes.c_void_p]),
     "dr_kernels_per_forward": (ctypes.c_int32, [ctypes.c_void_p]),
+    "dr_token_tile_rows": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),
     "dr_host_d2h_bytes": (ctypes.c_int64, [ctypes.c_void_p]),
     "dr_op_conv3x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

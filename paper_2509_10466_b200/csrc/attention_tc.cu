@@ -603,15 +603,7 @@ void trace_snapshot(cudaStream_t s, int n_cta);
 #endif
 
 namespace {
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+int sm_count() { return device_sms(); }
 int q_tiles(const AttnArgs& a) { return (a.band + QROWS - 1) / QROWS * HEADS * a.frames * a.groups; }
 }  // namespace
 
@@ -643,19 +635,18 @@ int attention_ksplit(const AttnArgs& a) {
 }
 
 void launch_attention(const AttnArgs& a_in, cudaStream_t s) {
-  static bool init = false;
+  static unsigned long long init = 0;
   // Residency is capped by registers (168 per thread, two CTAs); TMEM (128 columns per CTA)
   // holds four, so tcgen05.alloc never waits; shared memory must not be the cap.
   static_assert(sizeof(Smem) + 1024 <= 227 * 1024 / CTAS_PER_SM, "attention smem caps residency");
   static_assert(CTAS_PER_SM * TM_COLS <= 512, "TMEM over-subscribed");
   const int smem = (int)sizeof(Smem);
-  if (!init) {
+  once_per_device(init, [&] {
     cudaFuncSetAttribute(attn_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_tc_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
+  });
   AttnArgs a = a_in;
   const int k = (a.ksplit >= 1 && a.ksplit <= MAX_KSPLIT) ? a.ksplit : attention_ksplit(a);
   const dim3 grid(k * ((a.band + QROWS - 1) / QROWS), HEADS, a.frames * a.groups);

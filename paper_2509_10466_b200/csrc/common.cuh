@@ -160,6 +160,28 @@ DR_DEV void pdl_trigger() {
 }
 DR_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Host-side launcher setup that is per DEVICE (cudaFuncSetAttribute, SM counts): an engine
+// on a second GPU of the same process must not inherit the first GPU's state.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+inline int device_sms() {
+  static int sms[64] = {};
+  const int d = current_device() & 63;
+  if (!sms[d]) cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+  return sms[d];
+}
+// fn() once per device per `done` mask (a racing second call repeats fn: harmless)
+template <typename Fn>
+inline void once_per_device(unsigned long long& done, Fn fn) {
+  const unsigned long long bit = 1ull << (current_device() & 63);
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return;
+  fn();
+  __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args... args) {

@@ -556,12 +556,12 @@ __global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
 
 template <int N, int TR, bool FUSE>
 void launch(const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s) {
-  static int sms = 0;
+  static unsigned long long init = 0;
   const int smem = (int)sizeof(ConvSmem<N, TR, FUSE>);
-  if (!sms) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  once_per_device(init, [&] {
     cudaFuncSetAttribute(conv3x3_tc_kernel<N, TR, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  }
+  });
+  const int sms = device_sms();
   const int tiles = a.frames * ((a.H + TR - 1) / TR) * ((a.W + TX - 1) / TX);
   const int grid = tiles < sms ? tiles : sms;
   launch_pdl(conv3x3_tc_kernel<N, TR, FUSE>, dim3(grid), dim3(THREADS), smem, s, tin, a);
@@ -641,12 +641,11 @@ __global__ void __launch_bounds__(128) e_only_kernel(const __grid_constant__ CUt
 
 void launch_e_only(const CUtensorMap& d0_rows, const __half*, const void* w2, __half* e_planes,
                    int frames, int H, int W, cudaStream_t s) {
-  static bool init = false;
+  static unsigned long long init = 0;
   const int smem = (int)sizeof(EOnlySmem) + 1024;
-  if (!init) {
+  once_per_device(init, [&] {
     cudaFuncSetAttribute(e_only_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
+  });
   launch_pdl(e_only_kernel, dim3((W + 127) / 128, H, frames), dim3(128), smem, s, d0_rows, w2,
              e_planes, H, W);
 }

@@ -418,7 +418,12 @@ struct dr_engine {
     if (!profiling || n_ev >= kMaxEv) return;
     if (!ev[n_ev]) cudaEventCreate(&ev[n_ev]);
     ev_kind[n_ev] = kind;
-    cudaEventRecord(ev[n_ev++], s);
+    // under stream capture the record becomes an event node of the graph, so a replay
+    // re-records every stage boundary (in-graph stage times)
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev[n_ev++], s, cudaEventRecordExternal);
+    else cudaEventRecord(ev[n_ev++], s);
   }
 
   BlockW block_w(int i) const {
@@ -434,7 +439,13 @@ struct dr_engine {
   }
   int sms = 0;
 
-  void launch_tok(int mode, const TokenArgs& a, cudaStream_t s) const {
+  // DR_TOK_ROWS=32|64|128 (tests): force the token kernels' tile size, e.g. the 128-row
+  // throughput kernel (and its last-block slot K/V fill) on a batch-1 frame
+  int tok_rows = 0;
+  int tile_rows(int n_tok) { return tok_rows ? tok_rows : token_tc_tile_rows(n_tok, sm_count()); }
+  void launch_tok(int mode, const TokenArgs& a_in, cudaStream_t s) const {
+    TokenArgs a = a_in;
+    if (tok_rows) a.tile_rows = tok_rows;
     launch_token_tc(mode, a, s);
   }
 
@@ -766,6 +777,10 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   e->feather_r = (int)(fw.size() / 2);
   if (const char* sa = std::getenv("DR_STOP_AFTER")) e->stop_after = std::atoi(sa);
   if (const char* hg = std::getenv("DR_HOST_GRAPH")) e->host_graph = std::atoi(hg);
+  if (const char* tr = std::getenv("DR_TOK_ROWS")) {
+    const int r = std::atoi(tr);
+    e->tok_rows = (r == 32 || r == 64 || r == 128) ? r : 0;
+  }
   if (const char* rf = std::getenv("DR_RGB_FLAG")) e->use_rgb_flag = std::atoi(rf);
   if (const char* rcn = std::getenv("DR_RGB_CHUNKS"))
     e->rgb_chunks = std::min(8, std::max(1, std::atoi(rcn)));
@@ -813,6 +828,12 @@ void dr_destroy(dr_engine* e) {
 }
 
 int64_t dr_host_d2h_bytes(dr_engine* e) { return e ? (int64_t)e->last_d2h : 0; }
+
+int32_t dr_token_tile_rows(dr_engine* e, int32_t frames) {
+  if (!e || frames <= 0) return 0;
+  cudaSetDevice(e->device);
+  return e->tile_rows(frames * e->T);
+}
 
 int32_t dr_kernels_per_forward(dr_engine* e) {
   if (!e) return 0;
@@ -1013,7 +1034,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     if (last)
       for (auto& k : e->kvc) if (k.ptr == io->new_slot) k = {nullptr, 0, false, 0};  // stale
     int en = -1;
-    const bool fill_here = token_tc_tile_rows(B * T, e->sm_count()) == 128;
+    const bool fill_here = e->tile_rows(B * T) == 128;
     if (fill_here && last && e->n_temporal > 0) {     // fill the cache for new_slot
       en = e->kv_pick(ent[0], ent[1], io->new_slot);
       int tj = 0;

@@ -426,11 +426,10 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
 
 template <int P, int WH>
 void launch_mask_t(const MaskArgs& a, cudaStream_t s, int smem) {
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init = 0;
+  once_per_device(init, [&] {
     cudaFuncSetAttribute(mask_fused_kernel<P, WH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
+  });
   dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, a.frames);
   launch_pdl(mask_fused_kernel<P, WH>, grid, dim3(NT), smem, s, a);
 }

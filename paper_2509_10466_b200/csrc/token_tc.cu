@@ -476,77 +476,6 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   if (MODE == TOK_SLOTKV && a.late_wait) pdl_wait();
 }
 
-// ---------------------------------------------------------------------------------------
-// Small tiles (32 or 64 tokens per CTA, batch 1-2).  Only TMEM lane quarters 0 (and 1)
-// hold rows, and tcgen05.ld restricts lane quarter q to warps w with w % 4 == q -- which
-// all sit on SM sub-partition q.  Doing the epilogues there (the large-tile layout above)
-// would run the whole LN/GELU chain on one or two of the SM's four schedulers.  Here the
-// quarter's warps only dump each accumulator to shared memory (fp32, row pitch N + 4), and
-// all 32 warps run the epilogue warp-per-row: lane l owns channels 2l, 2l+1 of the row,
-// LayerNorm statistics are butterfly shuffles (no barrier), the residual stream stays in
-// registers across the chain.  Two CTA barriers per GEMM (dump -> epilogue -> MMA).
-#ifndef DR_TOK_SMALL_WARPS
-#define DR_TOK_SMALL_WARPS 32
-#endif
-constexpr int SW = DR_TOK_SMALL_WARPS;      // warps of the small-tile kernel (16 or 32)
-constexpr int SGROUPS = SW / 4;             // column groups per lane quarter
-constexpr int R32 = 32 / SW, R64 = 64 / SW; // rows per warp at 32 / 64-row tiles
-
-template <int N>
-DR_DEV void dump_d(uint32_t tbase, int col0, float* dump, int rows) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = warp & 3, g = warp >> 2;
-  if (32 * q >= rows) return;
-  constexpr int CW = N / SGROUPS, P = N + 4;
-  const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(col0 + g * CW);
-  uint32_t r[CW];
-  if constexpr (CW % 16 == 0) {
-#pragma unroll
-    for (int i = 0; i < CW / 16; ++i) tc::tmem_ld16(ta + 16 * i, r + 16 * i);
-  } else if constexpr (CW == 8) {
-    tc::tmem_ld8(ta, r);
-  } else {
-    static_assert(CW == 24, "column group width");
-    tc::tmem_ld16(ta, r);
-    tc::tmem_ld8(ta + 16, r + 16);
-  }
-  tc::tmem_wait_ld();
-  float4* d = reinterpret_cast<float4*>(dump + (size_t)(32 * q + lane) * P + g * CW);
-#pragma unroll
-  for (int i = 0; i < CW / 4; ++i)
-    d[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-}
-
-DR_DEV float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// LayerNorm of row r (eps 1e-5, biased variance, two-pass) from this lane's two channels;
-// the fp16 result goes into the 128B-swizzled A atom
-DR_DEV void ln_row_to_a(float2 x, const float* w, const float* b, uint8_t* sa, int r, int lane) {
-  const float mu = warp_sum(x.x + x.y) * (1.f / 64.f);
-  const float d0 = x.x - mu, d1 = x.y - mu;
-  const float var = warp_sum(d0 * d0 + d1 * d1) * (1.f / 64.f);
-  const float rs = rsqrtf(var + 1e-5f);
-  const int c = 2 * lane;
-  const float y0 = d0 * rs * w[c] + b[c], y1 = d1 * rs * w[c + 1] + b[c + 1];
-  *reinterpret_cast<uint32_t*>(sa + sw128(r, lane >> 2) + (lane & 3) * 4) = pack_half2(y0, y1);
-}
-
-// q|k|v (or k|v) 8-column chunks of a dumped projection row -> head-major fp16 outputs
-DR_DEV void store_proj_chunk(const float* drow, const float* bias, __half* dst, int T, int f,
-                             int tk, int h, int c) {
-  const float4 a0 = *reinterpret_cast<const float4*>(drow);
-  const float4 a1 = *reinterpret_cast<const float4*>(drow + 4);
-  const float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-  uint4* r = reinterpret_cast<uint4*>(dst + ((size_t)(f * HEADS + h) * T + tk) * DH);
-  r[c ^ ((tk >> 2) & 1)] = pack8(v, bias);
-}
-
-DR_DEV void sync_all() { __syncthreads(); }
 // generic-proxy A/H writes visible to the tensor core, TMEM reads ordered before the next
 // MMA, one CTA barrier
 DR_DEV void publish_all() {
@@ -554,242 +483,6 @@ DR_DEV void publish_all() {
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-}
-
-template <int MODE, int RPW>
-__global__ void __launch_bounds__(32 * SW, SW == 16 ? 2 : 1) token_small_kernel(TokenArgs a) {
-#ifdef DR_TRACE
-  int tt_i = 0;
-#endif
-  TT();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  constexpr int ROWS = SW * RPW;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* sa = sm + OFF_A;
-  uint8_t* big = sm + OFF_BIG;
-  constexpr int big_bytes = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
-  uint8_t* sw = big + big_bytes;
-  const WLayout L = wlayout<MODE>(a);
-  const float* prm = reinterpret_cast<const float*>(sw + L.w_bytes);
-  auto prm_nx = [&](int j) { return prm + (1 + j) * (PRM_BYTES / 4); };
-  Ctl& ctl = *reinterpret_cast<Ctl*>(sw + L.total());
-  float* dump = reinterpret_cast<float*>(sw + L.total() + ((sizeof(Ctl) + 15) & ~15));
-
-  // rows of this warp: r = warp * RPW + i; token n, frame f, token-in-frame tk
-  int nrow[RPW], frow[RPW], tkrow[RPW];
-  bool vrow[RPW];
-#pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    const int r = warp * RPW + i;
-    nrow[i] = blockIdx.x * ROWS + r;
-    vrow[i] = nrow[i] < a.n_tok;
-    frow[i] = nrow[i] / a.T;
-    tkrow[i] = nrow[i] - frow[i] * a.T;
-  }
-
-  pdl_trigger();
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&ctl.w_bar, 1);
-    tc::mbar_init(&ctl.mma_bar, 1);
-    tc::fence_barrier_init();
-    uint8_t* pc = sw + L.w_bytes;                          // constant weights: before pdl_wait
-    if constexpr (MODE == TOK_EMBED) {
-      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + 256 + PRM_BYTES));
-      tc::bulk_load(sw, a.we_img, WE_BYTES, &ctl.w_bar);
-      tc::bulk_load(sw + WE_BYTES, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
-      tc::bulk_load(pc, a.we_img + WE_BYTES, 256, &ctl.w_bar);
-      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
-    } else if constexpr (MODE == TOK_POST) {
-      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)L.total());
-      tc::bulk_load(sw, a.cur.img + IMG_O, IMG_PRM - IMG_O, &ctl.w_bar);
-      tc::bulk_load(pc, a.cur.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
-      uint8_t* d = sw + (IMG_PRM - IMG_O);
-      if (a.has_next) {
-        tc::bulk_load(d, a.next.img + IMG_QKV, 192 * 128, &ctl.w_bar);
-        tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
-      } else {
-        for (int j = 0; j < a.n_kv; ++j) {
-          tc::bulk_load(d + j * 128 * 128, a.kv_w[j].img + IMG_KV, 128 * 128, &ctl.w_bar);
-          tc::bulk_load(pc + (1 + j) * PRM_BYTES, a.kv_w[j].img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
-        }
-      }
-    } else {
-      tc::mbar_arrive_expect_tx(&ctl.w_bar, (uint32_t)(L.w_bytes + PRM_BYTES));
-      tc::bulk_load(sw, a.next.img + IMG_KV, 128 * 128, &ctl.w_bar);
-      tc::bulk_load(pc + PRM_BYTES, a.next.img + IMG_PRM, PRM_BYTES, &ctl.w_bar);
-    }
-  }
-  __syncthreads();                              // barriers initialised before any wait
-  TT();
-  // SLOTKV with late_wait reads only the caller-provided slot: it runs alongside its
-  // predecessor and waits for it at exit instead (after releasing TMEM)
-  if (!(MODE == TOK_SLOTKV && a.late_wait)) pdl_wait();
-  // TMEM only after the predecessor grid completed (PDL early trigger: no CTA holds TMEM
-  // while it waits on another grid, so allocations cannot deadlock)
-  if (warp == 0) tc::tmem_alloc<TM_COLS>(&ctl.tmem_base);
-  TT();
-
-  uint32_t phase = 0;
-  auto mma_wait_dump = [&](auto n_tag, int col0) {
-    constexpr int NN = decltype(n_tag)::value;
-    const int q = warp & 3;
-    if (32 * q < ROWS) {
-      tc::mbar_wait(&ctl.mma_bar, phase);
-      tc::fence_after();
-    }
-    phase ^= 1u;
-    TT();
-    dump_d<NN>(ctl.tmem_base, col0, dump, ROWS);
-    tc::fence_before();
-    sync_all();
-    tc::fence_after();
-    TT();
-  };
-  using N64 = std::integral_constant<int, 64>;
-  using N128 = std::integral_constant<int, 128>;
-  using N192 = std::integral_constant<int, 192>;
-
-  float2 x[RPW];
-  // ------------------------------------------------------------ first GEMM input
-  if constexpr (MODE == TOK_EMBED) {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {             // xin row: 256 halves = 32 chunks, one per lane
-      const int r = warp * RPW + i;
-      const uint4 v = vrow[i] ? __ldg(reinterpret_cast<const uint4*>(a.xin + (size_t)nrow[i] * a.kin) + lane)
-                              : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(big + (lane >> 3) * ATOM_A + sw128(r, lane & 7)) = v;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i)
-      x[i] = vrow[i] ? __ldg(reinterpret_cast<const float2*>(a.resid_in + (size_t)nrow[i] * C) + lane)
-                     : make_float2(0.f, 0.f);
-    if constexpr (MODE == TOK_POST) {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {           // attention row: 64 halves, 2 per lane
-        const int r = warp * RPW + i;
-        const uint32_t v = vrow[i] ? __ldg(reinterpret_cast<const uint32_t*>(a.attn + (size_t)nrow[i] * C) + lane) : 0u;
-        *reinterpret_cast<uint32_t*>(sa + sw128(r, lane >> 2) + (lane & 3) * 4) = v;
-      }
-    }
-  }
-  tc::mbar_wait(&ctl.w_bar, 0);                 // weights and params in smem
-  publish_all();
-  TT();
-  const uint32_t tbase = ctl.tmem_base;
-  auto store_resid = [&]() {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i)
-      if (vrow[i]) reinterpret_cast<float2*>(a.resid_out + (size_t)nrow[i] * C)[lane] = x[i];
-  };
-  auto add_row = [&](const float* bias) {       // x += D row (dump, pitch 68) + bias
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const float2 d = reinterpret_cast<const float2*>(dump + (size_t)(warp * RPW + i) * 68)[lane];
-      x[i].x += d.x + bias[2 * lane];
-      x[i].y += d.y + bias[2 * lane + 1];
-    }
-  };
-
-  if constexpr (MODE == TOK_EMBED) {
-    if (warp == 0) gemm_issue(tbase, tc::smem_u32(big), tc::smem_u32(sw), 64, 4, &ctl.mma_bar);
-    mma_wait_dump(N64{}, 0);
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) x[i] = make_float2(0.f, 0.f);
-    add_row(prm);
-    store_resid();
-  }
-  if constexpr (MODE == TOK_POST) {
-    const uint32_t wo = tc::smem_u32(sw), w1 = wo + (IMG_1 - IMG_O), w2 = wo + (IMG_2 - IMG_O);
-    // ---------------------------------------------------------- out-proj + residual
-    if (warp == 0) gemm_issue(tbase, tc::smem_u32(sa), wo, 64, 1, &ctl.mma_bar);
-    mma_wait_dump(N64{}, 0);
-    add_row(prm + Prm::bo);
-    // ---------------------------------------------------------- LN2 -> FFN1 -> GELU
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) ln_row_to_a(x[i], prm + Prm::ln2_w, prm + Prm::ln2_b, sa, warp * RPW + i, lane);
-    publish_all();
-    TT();
-    if (warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), w1, 128, 1, &ctl.mma_bar);
-    mma_wait_dump(N128{}, 64);
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {             // FFN columns 4l .. 4l+3 of row r
-      const int r = warp * RPW + i;
-      const float4 d = reinterpret_cast<const float4*>(dump + (size_t)r * 132)[lane];
-      const float* b1 = prm + Prm::b1 + 4 * lane;
-      const uint2 hv = make_uint2(pack_half2(gelu_erf(d.x + b1[0]), gelu_erf(d.y + b1[1])),
-                                  pack_half2(gelu_erf(d.z + b1[2]), gelu_erf(d.w + b1[3])));
-      *reinterpret_cast<uint2*>(big + (lane >> 4) * ATOM_A + sw128(r, (lane & 15) >> 1) + (lane & 1) * 8) = hv;
-    }
-    publish_all();
-    TT();
-    // ---------------------------------------------------------- FFN2 + residual
-    if (warp == 0) gemm_issue(tbase, tc::smem_u32(big), w2, 64, 2, &ctl.mma_bar);
-    mma_wait_dump(N64{}, 0);
-    add_row(prm + Prm::b2);
-    store_resid();
-  }
-
-  // ------------------------------------------------------------ LN1' + projections
-  const uint32_t wnext = tc::smem_u32(sw) + (MODE == TOK_EMBED ? WE_BYTES
-                                            : (MODE == TOK_POST ? IMG_PRM - IMG_O : 0));
-  const bool qkv = MODE == TOK_EMBED || (MODE == TOK_POST && a.has_next);
-  if (qkv) {
-    const float* pn = prm_nx(0);
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) ln_row_to_a(x[i], pn + Prm::ln1_w, pn + Prm::ln1_b, sa, warp * RPW + i, lane);
-    publish_all();
-    TT();
-    if (warp == 0) gemm_issue(tbase + 64, tc::smem_u32(sa), wnext, 192, 1, &ctl.mma_bar);
-    mma_wait_dump(N192{}, 64);
-    if (lane < 24) {                            // chunk u = lane of 24 (8 columns each)
-      const int u = lane, p = u >> 1, which = p >> 2, h = p & 3;
-      __half* dst = which == 0 ? a.q : (which == 1 ? a.k : a.v);
-#pragma unroll
-      for (int i = 0; i < RPW; ++i)
-        if (vrow[i])
-          store_proj_chunk(dump + (size_t)(warp * RPW + i) * 196 + 8 * u, pn + Prm::bqkv + 8 * u, dst,
-                           a.T, frow[i], tkrow[i], h, u & 1);
-    }
-  } else {
-    // k|v only: SLOTKV (one block) or the last block's slot K/V for every temporal block
-    const int n_kv = MODE == TOK_SLOTKV ? 1 : a.n_kv;
-    if constexpr (MODE == TOK_POST) {
-      if (a.tok16) {                            // fp16 tokens for Vec2Patch
-#pragma unroll
-        for (int i = 0; i < RPW; ++i)
-          if (vrow[i]) {
-            const int ti = tkrow[i] / a.Cc, tj = tkrow[i] - ti * a.Cc;
-            const size_t pos = ((size_t)frow[i] * (a.R + 2) + ti + 1) * (a.Cc + 2) + tj + 1;
-            reinterpret_cast<uint32_t*>(a.tok16 + pos * C)[lane] = pack_half2(x[i].x, x[i].y);
-          }
-      }
-    }
-    for (int j = 0; j < n_kv; ++j) {
-      const float* pn = prm_nx(j);
-      __half* kd = MODE == TOK_SLOTKV ? a.k : a.kv_k[j];
-      __half* vd = MODE == TOK_SLOTKV ? a.v : a.kv_v[j];
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) ln_row_to_a(x[i], pn + Prm::ln1_w, pn + Prm::ln1_b, sa, warp * RPW + i, lane);
-      publish_all();
-      if (warp == 0)
-        gemm_issue(tbase + 64, tc::smem_u32(sa), wnext + j * 128 * 128, 128, 1, &ctl.mma_bar);
-      mma_wait_dump(N128{}, 64);
-      if (lane < 16) {                          // chunks u = lane of 16 (k|v)
-        const int u = lane, p = 4 + (u >> 1), h = p & 3;
-#pragma unroll
-        for (int i = 0; i < RPW; ++i)
-          if (vrow[i])
-            store_proj_chunk(dump + (size_t)(warp * RPW + i) * 132 + 8 * u, pn + Prm::bqkv + 64 + 8 * u,
-                             p < 8 ? kd : vd, a.T, frow[i], tkrow[i], h, u & 1);
-      }
-    }
-  }
-  TT();
-  if (warp == 0) tc::tmem_dealloc<TM_COLS>(tbase);
-  if (MODE == TOK_SLOTKV && a.late_wait) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1194,38 +887,25 @@ void tok_trace_snapshot(cudaStream_t s, int n_cta, int mode);
 #endif
 
 void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
-  static int sms = 0;
-  static bool init = false;
-  if (!init) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static unsigned long long init = 0;
+  once_per_device(init, [] {
     const int mx = 227 * 1024;
     cudaFuncSetAttribute(token_tc_kernel<TOK_EMBED>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_tc_kernel<TOK_POST>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_tc_kernel<TOK_SLOTKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_POST, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_EMBED, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_POST, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(token_small_kernel<TOK_SLOTKV, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_EMBED, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_POST, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_SLOTKV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_EMBED, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_POST, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(token_q_kernel<TOK_SLOTKV, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    init = true;
-  }
+  });
+  const int sms = device_sms();
   TokenArgs a = a_in;
   if (a.tile_rows != 32 && a.tile_rows != 64 && a.tile_rows != 128)
     a.tile_rows = token_tc_tile_rows(a.n_tok, sms);
   dim3 grid((a.n_tok + a.tile_rows - 1) / a.tile_rows), block(THREADS);
-#ifndef DR_TOK_QUARTER
-#define DR_TOK_QUARTER 1
-#endif
-  if (DR_TOK_QUARTER && a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
+  if (a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
     const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
                    : (mode == TOK_POST ? smem_bytes<TOK_POST>(a) : smem_bytes<TOK_SLOTKV>(a));
     const dim3 qb(32 * QWARPS);
@@ -1237,24 +917,6 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
       if (mode == TOK_EMBED) launch_pdl(token_q_kernel<TOK_EMBED, 16>, grid, qb, smem, s, a);
       else if (mode == TOK_POST) launch_pdl(token_q_kernel<TOK_POST, 16>, grid, qb, smem, s, a);
       else launch_pdl(token_q_kernel<TOK_SLOTKV, 16>, grid, qb, smem, s, a);
-    }
-#ifdef DR_TRACE
-    tok_trace_snapshot(s, (int)grid.x, mode);
-#endif
-    return;
-  }
-  if (a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
-    block = dim3(32 * SW);
-    const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
-                   : (mode == TOK_POST ? smem_bytes<TOK_POST>(a) : smem_bytes<TOK_SLOTKV>(a));
-    if (a.tile_rows == 32) {
-      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, R32>, grid, block, smem, s, a);
-      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, R32>, grid, block, smem, s, a);
-      else launch_pdl(token_small_kernel<TOK_SLOTKV, R32>, grid, block, smem, s, a);
-    } else {
-      if (mode == TOK_EMBED) launch_pdl(token_small_kernel<TOK_EMBED, R64>, grid, block, smem, s, a);
-      else if (mode == TOK_POST) launch_pdl(token_small_kernel<TOK_POST, R64>, grid, block, smem, s, a);
-      else launch_pdl(token_small_kernel<TOK_SLOTKV, R64>, grid, block, smem, s, a);
     }
 #ifdef DR_TRACE
     tok_trace_snapshot(s, (int)grid.x, mode);

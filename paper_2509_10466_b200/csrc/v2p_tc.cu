@@ -299,13 +299,12 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
 size_t v2p_tc_weight_bytes() { return (size_t)100 * TAP_BYTES; }
 
 void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s) {
-  static bool init = false;
+  static unsigned long long init = 0;
   const int smem = (int)sizeof(V2pSmem) + 1024;
-  if (!init) {
+  once_per_device(init, [&] {
     cudaFuncSetAttribute(v2p_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(v2p_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
+  });
   const int NP = (a.R + 2) * (a.Cc + 2);
   dim3 grid((NP + M - 1) / M, 8, a.frames);
   if (a.comb) launch_pdl(v2p_tc_kernel<true>, grid, dim3(THREADS), smem, s, tok, a);

@@ -158,6 +158,11 @@ class DsttEngine(InpaintEngine):
     def kernels_per_forward(self) -> int:
         return int(_lib.load().dr_kernels_per_forward(self.handle))
 
+    def token_tile_rows(self, frames: int) -> int:
+        """Tokens per CTA of the token-chain kernels at `frames` frames (128 = the
+        throughput kernel with the last-block slot K/V fill)."""
+        return int(_lib.load().dr_token_tile_rows(self.handle, frames))
+
     # Slot K/V cache bookkeeping (dr_frame_io.slot_kv_reuse): a memory slot may reuse the
     # K/V the engine computed when it produced that slot only if it is the very tensor the
     # engine wrote (same storage pointer, version counter unchanged = no in-place edits).

@@ -46,16 +46,15 @@ def allreduce_max(value: float, device=None) -> float:
 
 
 def gather_to_rank0(t, device=None):
-    """Final gather of per-rank results (equal shapes) onto rank 0; None elsewhere."""
+    """Final gather of per-rank results (equal shapes) onto rank 0: a list ordered by
+    rank on rank 0, None elsewhere (`dist.gather`: NCCL on GPUs over NVLink / NVSwitch,
+    gloo on CPU)."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return [t]
-    ws = dist.get_world_size()
-    out = [torch.empty_like(t) for _ in range(ws)] if dist.get_rank() == 0 else None
-    if dist.get_backend() == "nccl":
-        buf = [torch.empty_like(t) for _ in range(ws)]
-        dist.all_gather(buf, t)
-        return buf if dist.get_rank() == 0 else None
+    t = t.contiguous()
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())] \
+        if dist.get_rank() == 0 else None
     dist.gather(t, out, dst=0)
     return out

@@ -65,3 +65,37 @@ def test_two_rank_replicas_gloo():
     assert results[0][2] == results[1][2] == 2.5                   # max over ranks
     assert results[1][3] is None
     assert np.allclose(results[0][3], [results[0][4], results[1][4]])   # gather order = rank
+
+
+def _bench_dry(*extra):
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, str(REPO / "bench.py"), "--gpus", "2", "--dry-run",
+                        "--steps", "2", "--warmup", "0", *extra],
+                       capture_output=True, text=True, timeout=300, cwd=str(REPO))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_self_launches_two_ranks_c5_gloo():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks; C5 weak
+    scaling shards 64 frames per rank (global batch 128), disjoint seeds, final gather of
+    every rank's results to rank 0 in rank order."""
+    d = _bench_dry("--config", "C5")
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 128
+    assert d["ranks_gathered"] == [0, 1]
+    assert d["frames_gathered"] == 2 * 64 * 2
+    seeds = [s for s, _ in d["ids"]]
+    assert len(set(seeds)) == len(seeds)
+    assert seeds[:3] == [0, 1, 2] and seeds[128:131] == [100003, 100004, 100005]
+
+
+def test_bench_self_launches_two_ranks_c3_streams_gloo():
+    """C3 at 2 GPUs: streams round-robin over ranks (4 per rank, batched)."""
+    d = _bench_dry("--config", "C3")
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 8
+    owned0 = {s for s, _ in d["ids"][:8]}
+    owned1 = {s for s, _ in d["ids"][8:]}
+    assert owned0 == {0, 2, 4, 6} and owned1 == {1, 3, 5, 7}
