@@ -687,7 +687,7 @@ def check_parity(eng2, cfg, B, stage, k_last, last, imgs, masks, P, rank, dev, s
         res.update({"oracle_frame": int(i), "oracle_max_abs": round(err, 6),
                     "oracle_psnr_db": round(ps, 2), "oracle_s": round(time.perf_counter() - t0, 1),
                     "tolerance": "max-abs <= 2e-2, PSNR >= 40 dB (north_star)"})
-        res["pass"] = res["graph_vs_eager_bitexact"] and err <= 2e-2 and ps >= 40.0
+        res["pass"] = bool(res["graph_vs_eager_bitexact"] and err <= 2e-2 and ps >= 40.0)
     return res
 
 

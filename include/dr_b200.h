@@ -112,6 +112,17 @@ int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, 
 int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
                        uint8_t* out_hwc, void* stream);
 
+/* dr_inpaint_u8_host with the memory passed explicitly, the reference signature
+ * InpaintEngine.inpaint(rgb, mask, memory) (base.py:52-89, called by
+ * LocalEngineClient.inpaint_frame, service.py:198-204): slot0 / slot1 are the memory's
+ * two device fp32 [T][C] slots (oldest first), new_slot receives the post-block tokens
+ * (the caller pushes it: memory.py:40-45).  Bit i of slot_kv_reuse may be set only if
+ * slot i is unchanged since this engine wrote it as a new_slot (its cached K/V are
+ * reused).  Same staging, graphs and errors as dr_inpaint_u8_host. */
+int dr_inpaint_u8_host_mem(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                           uint8_t* out_hwc, const float* slot0, const float* slot1,
+                           float* new_slot, int32_t slot_kv_reuse, void* stream);
+
 /* Device->host bytes the last dr_inpaint_u8_host copied: only pixels within mask_dilate +
  * feather radius (square) of a masked pixel can differ from the input (the composite keeps
  * the input byte where alpha = 0), so only each row's span covering them is read back,

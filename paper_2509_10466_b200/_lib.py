@@ -55,6 +55,9 @@ SIGNATURES = {
                                      ctypes.c_void_p, ctypes.c_void_p]),
     "dr_inpaint_u8_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "dr_inpaint_u8_host_mem": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
     "dr_reset_memory": (ctypes.c_int, [ctypes.c_void_p]),
     "dr_kernels_per_forward": (ctypes.c_int32, [ctypes.c_void_p]),
     "dr_token_tile_rows": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32]),

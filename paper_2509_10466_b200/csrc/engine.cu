@@ -97,6 +97,12 @@ class WorkPool {
     std::lock_guard<std::mutex> job(job_mu_);
     post(std::move(fn), 0);
   }
+  // wait for an asynchronous job (run_async) to finish, e.g. before freeing its buffer
+  void drain() {
+    std::lock_guard<std::mutex> job(job_mu_);
+    while (pending_.load(std::memory_order_acquire) != 0) {
+    }
+  }
   ~WorkPool() {
     while (pending_.load(std::memory_order_acquire) != 0) {
     }
@@ -823,7 +829,10 @@ void dr_destroy(dr_engine* e) {
   cudaFree(e->d_done);
   for (auto* r : e->ring) cudaFree(r);
   for (auto& ev : e->ev) if (ev) cudaEventDestroy(ev);
-  if (e->pin) cudaFreeHost(e->pin);
+  if (e->pin) {
+    WorkPool::get().drain();          // the cache-eviction job may still walk e->pin
+    cudaFreeHost(e->pin);
+  }
   delete e;
 }
 
@@ -1208,9 +1217,12 @@ extern "C" int dr_debug_e2e_trace(double* out8) {
   return 0;
 }
 
-int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
-                       uint8_t* out_hwc, void* stream) {
-  if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
+namespace {
+// One u8 frame through host buffers with the given memory slots (device fp32 [T][C]);
+// writes new_slot.  Shared by the engine-held-memory call and the explicit-slot call.
+int host_inpaint(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                 uint8_t* out_hwc, const float* slot0, const float* slot1, float* new_slot,
+                 int slot_kv_reuse, void* stream) {
   CUDA_TRY(cudaSetDevice(e->device));
   const size_t px = e->frame_px();
   const int H = e->H, W = e->W, halo = e->cfg.mask_dilate + e->feather_r;
@@ -1287,14 +1299,12 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
     CUDA_TRY(cudaEventCreateWithFlags(&e->rgb_event, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
   }
-  int fresh = 0;
-  while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
   dr_frame_io io{};
   io.frames = 1;
   io.rgb_u8 = e->h_rgb; io.mask_m0 = e->h_m0;
-  io.slot0 = e->ring[e->mem0]; io.slot1 = e->ring[e->mem1]; io.slot_batched = 1;
-  io.new_slot = e->ring[fresh];
-  io.slot_kv_reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
+  io.slot0 = slot0; io.slot1 = slot1; io.slot_batched = 1;
+  io.new_slot = new_slot;
+  io.slot_kv_reuse = slot_kv_reuse;
   e->pack_spans = reinterpret_cast<const int4*>(e->h_rgb + in_spans);
   e->pack_out = e->h_out;
   e->flags_mirror = nullptr;         // decode.2 places it after the packed bytes
@@ -1385,7 +1395,6 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
     cudaEventRecord(tr.ev[2], s);
     tt[2] = now_us();
   }
-  e->ring_own[fresh] = true;         // contents and slot K/V cache entry now agree
   // (On an error return `out` holds partial data.)
   CUDA_TRY(cudaMemcpyAsync(p_out, e->h_out, mirror + 4, cudaMemcpyDeviceToHost, s));
   if (tr.on) cudaEventRecord(tr.ev[3], s);
@@ -1432,9 +1441,44 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
     }
   }
   e->last_d2h = mirror + 4;
+  return DR_OK;
+}
+}  // namespace
+
+int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                       uint8_t* out_hwc, void* stream) {
+  if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  if (!e->ring[0]) {
+    int rc = dr_reset_memory(e);
+    if (rc) return rc;
+  }
+  int fresh = 0;
+  while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
+  const int reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
+  e->ring_own[fresh] = false;
+  const int rc = host_inpaint(e, rgb_hwc, mask_hw, out_hwc, e->ring[e->mem0], e->ring[e->mem1],
+                              e->ring[fresh], reuse, stream);
+  if (rc == DR_OK || rc == DR_ERR_INPUT || rc == DR_ERR_NUMERIC) {
+    // the launches ran: contents and slot K/V cache entry of `fresh` agree
+    e->ring_own[fresh] = true;
+  }
+  if (rc) return rc;
   e->mem0 = e->mem1;
   e->mem1 = fresh;
   return DR_OK;
+}
+
+int dr_inpaint_u8_host_mem(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
+                           uint8_t* out_hwc, const float* slot0, const float* slot1,
+                           float* new_slot, int32_t slot_kv_reuse, void* stream) {
+  if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
+  if (!slot0 || !slot1 || !new_slot)
+    return fail(DR_ERR_INPUT, "both memory slots and new_slot are required");
+  if (new_slot == slot0 || new_slot == slot1)
+    return fail(DR_ERR_INPUT, "new_slot must not alias a memory slot");
+  return host_inpaint(e, rgb_hwc, mask_hw, out_hwc, slot0, slot1, new_slot, slot_kv_reuse & 3,
+                      stream);
 }
 
 // ------------------------------------------------------------------ frame byte kernels

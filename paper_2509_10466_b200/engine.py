@@ -202,16 +202,63 @@ class DsttEngine(InpaintEngine):
 
     def inpaint(self, rgb: np.ndarray, mask: BinaryMask,
                 memory: InpaintMemory | None = None) -> EngineResult:
-        """InpaintEngine.inpaint (base.py:52-89) with the composite on the device."""
+        """InpaintEngine.inpaint (base.py:52-89): checks, the whole path on the device,
+        the composite back in a new array, memory.push(new slot).  One C-ABI host call
+        (dr_inpaint_u8_host_mem: pinned staging, one CUDA-graph launch, span-packed
+        read-back) with the memory's slots passed explicitly."""
+        import time
+
         import torch
         self._check_frame(rgb, mask)
         if memory is None:
             memory = self.zero_memory()
-        res = self.run(torch.from_numpy(np.ascontiguousarray(rgb))[None],
-                       torch.from_numpy(np.ascontiguousarray(mask.bits))[None], memory.slots)
-        out = res["out"][0].cpu().numpy()
-        return EngineResult(rgb=out, memory=memory.push(res["slot"][0]),
-                            inference_ms=res["ms"])
+        T, C = self.config.tokens, self.config.channels
+        slots = []
+        for s in memory.slots:
+            t = self._slot(s)
+            if tuple(t.shape) == (1, T, C):
+                t = t[0]
+            if tuple(t.shape) != (T, C):
+                raise ConfigError(f"memory slot shape {tuple(t.shape)} does not match tokens "
+                                  f"({T}, {C})")
+            slots.append(t)
+        reuse = sum(1 << i for i, s in enumerate(memory.slots) if self._is_own_slot(s))
+        new = self._fresh_slot(slots)
+        bits = np.ascontiguousarray(mask.bits)
+        if bits.dtype != np.uint8:
+            bits = bits.astype(np.uint8) if bits.dtype != np.bool_ else bits.view(np.uint8)
+        frame = np.ascontiguousarray(rgb)
+        out = np.empty_like(frame)
+        t0 = time.perf_counter()
+        _lib.check(self._native.lib.dr_inpaint_u8_host_mem(
+            self.handle, frame.ctypes.data, bits.ctypes.data, out.ctypes.data,
+            slots[0].data_ptr(), slots[1].data_ptr(), new.data_ptr(), reuse,
+            torch.cuda.current_stream(self.device).cuda_stream))
+        ms = (time.perf_counter() - t0) * 1e3
+        self._register_slot(new)
+        return EngineResult(rgb=out, memory=memory.push(new), inference_ms=ms)
+
+    def _fresh_slot(self, exclude):
+        """A device [T][C] buffer for the next new slot.  Engine-owned buffers are recycled
+        only when nothing outside the pool refers to them (no Python reference, no view of
+        the storage), so memories a caller still holds are never overwritten; recycling
+        keeps the host call's slot pointers, hence its CUDA graphs, to a few signatures."""
+        import sys
+
+        import torch
+        pool = self.__dict__.setdefault("_slot_pool", [])
+        busy = {t.data_ptr() for t in exclude}
+        for i in range(len(pool)):
+            t = pool[i]
+            # references: the pool list, `t`, getrefcount's argument
+            if (t.data_ptr() not in busy and sys.getrefcount(t) <= 3
+                    and torch._C._storage_Use_Count(t.untyped_storage()._cdata) <= 2):
+                return t
+        t = torch.empty((self.config.tokens, self.config.channels), dtype=torch.float32,
+                        device=self.device)
+        if len(pool) < 8:
+            pool.append(t)
+        return t
 
     # ------------------------------------------------------------------ batched API
     def model_forward(self, rgb, mask, memory):
@@ -345,7 +392,10 @@ class DsttEngine(InpaintEngine):
         rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
         if rgb.shape != (self.height, self.width, 3):
             raise ConfigError("frame does not match engine resolution")
-        m = np.ascontiguousarray(mask_bits, dtype=np.uint8)
+        m = np.ascontiguousarray(mask_bits)
+        if m.shape != (self.height, self.width):
+            raise ConfigError("mask dimensions do not match engine resolution")
+        m = m.view(np.uint8) if m.dtype == np.bool_ else np.ascontiguousarray(m, dtype=np.uint8)
         out = np.empty_like(rgb)
         _lib.check(self._native.lib.dr_inpaint_u8_host(
             self.handle, rgb.ctypes.data, m.ctypes.data, out.ctypes.data,

@@ -175,9 +175,12 @@ def test_u8_inpaint_matches_oracle_and_composite_guarantee(rng):
         fill, slot = O.model_forward(cfg, w, O.u8_to_unit(rgb),
                                      bits[None, None].astype(np.float32), slots)
         slots = (slots[1], slot[0])
+        # the u8 result against the fp32 oracle composite on [0,1] (north_star gate)
+        ref01 = O.composite(fill, O.u8_to_unit(rgb), bits[None].astype(np.float32))[0]
+        got01 = res.rgb.transpose(2, 0, 1) / 255.0
+        assert_close_img(got01, ref01, f"u8 frame {t}")
         ref = O.composite_u8(O.to_u8(fill)[0], rgb, bits.astype(np.float32))
-        diff = np.abs(res.rgb.astype(int) - ref.astype(int))
-        assert diff.max() <= 6 and psnr(res.rgb / 255.0, ref / 255.0) >= MIN_PSNR
+        assert np.abs(res.rgb.astype(int) - ref.astype(int)).max() <= 5     # < 2e-2 * 255
 
 
 def test_u8_inpaint_errors():
