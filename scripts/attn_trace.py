@@ -66,16 +66,13 @@ def main():
         print("  O read (o_done) ", pct(rel8[:, 0] - rel[:, 3]))
         print("  DSMEM stores    ", pct(rel8[:, 1] - rel8[:, 0]))
         print("  cluster_sync    ", pct(rel[:, 4] - rel8[:, 1]))
-        # partner imbalance: loop-end difference between the two CTAs of a cluster
-        pair_gap = np.abs(rel[0::2, 3] - rel[1::2, 3])
-        print("  pair loop-end gap", pct(pair_gap))
+        # cluster imbalance: loop-end spread within a cluster (key parts of one tile group)
+        k = int(t[:, 10].max()) + 1
+        if k > 1 and len(t) % k == 0:
+            ends = rel[:, 3].reshape(-1, k)
+            print("  cluster loop-end spread", pct(ends.max(1) - ends.min(1)))
         print("  tail            ", pct(rel[:, 5] - rel[:, 4]))
         print("  exit            ", pct(rel[:, 5]))
-        cyc = t[:, 11:16].astype(np.float64) / 1965.0        # us at 1965 MHz
-        print("  softmax warp: wait S p50 %.2f, wait S ld p50 %.2f, loop p50 %.2f us; rescales p50 %d"
-              % (np.median(cyc[:, 0]), np.median(cyc[:, 1]), np.median(cyc[:, 2]),
-                 np.median(t[:, 14])))
-        print("  MMA warp: wait P p50 %.2f us" % np.median(cyc[:, 4]))
         per_sm = Counter(t[:, 6])
         print("  CTAs per SM     ", Counter(per_sm.values()), "SMs used", len(per_sm))
         # per-SM busy span: first entry to last exit
