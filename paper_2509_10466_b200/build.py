@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_build"
 LIB = OUT_DIR / "libdrb200.so"
 SOURCES = ["engine.cu", "mask_kernels.cu", "token_tc.cu", "attention_tc.cu",
-           "conv_tc.cu", "v2p_tc.cu", "frame_ops.cu"]
+           "conv_tc.cu", "v2p_tc.cu", "dec_fused.cu", "frame_ops.cu"]
 HEADERS = ["common.cuh", "kernels.h", "tc.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,818 @@
+// The decoder tail on the 5th-gen tensor cores: Vec2Patch o decode.0 -> LeakyReLU ->
+// decode.2 -> (tanh + 1) / 2 -> alpha composite, without a 64-channel raster.
+// Reference: Vec2Patch dstt.py:198-221 (ConvTranspose2d(64, 64, k=10, s=8), crop 1),
+// decode dstt.py:240-244 (Conv3x3 64->64, LeakyReLU(0.2), Conv3x3 64->3), output :267,
+// composite SURVEY A16 (base.py:87-88).
+//
+// Algebra.  Both convolutions before the LeakyReLU are linear, so decode.0's pre-activation
+// is a stride-8 transposed convolution of the tokens with a 12 x 12 kernel
+//   K[u][v] = sum_{dy,dx} Wc[dy][dx] Wv[u+dy+1][v+dx+1],   u, v in [-2, 9],
+// plus the combined bias bc + sum Wc bv -- exact wherever decode.0's 3x3 window stays
+// inside the image.  Pixel (8ty+py, 8tx+px) takes tokens ty-1 (py <= 1), ty, ty+1
+// (py >= 6) and likewise in x: 144 taps over the 64 phases (py, px), 2.25 tokens x 64
+// channels per pixel instead of Vec2Patch + decode.0's 100 + 576 -- 4.8 GFLOP per 512^2
+// frame instead of 22.7.  On the image border decode.0 reads zero padding where the
+// combined form reads the cropped canvas ring: there the decode.0 taps that read the ring
+// are subtracted (per edge a 12-tap kernel over the edge's token row / column, corners add
+// back the doubly removed tap; tables built at dr_create, the algebra checked in float64).
+//
+// Kernels (one frame batch):
+//   dec_fused   one CTA per tile of 16 x 8 tokens = 128 x 64 pixels (and 1 of `groups`
+//               parts of its 64 phases).  Per phase:
+//                 MMA warp   D = sum over the phase's 1/2/4 taps of A x Wcomb[tap]^T
+//                            (M = 128 token positions, N = 64, K = 64); A = the TMA-loaded
+//                            halo'd token tile (18 x 10 tokens, 128B-swizzled rows, row
+//                            stride 10 -> descriptor SBO 1280), the tap's token shift is a
+//                            row offset; tap images stream through a smem ring
+//                 epilogue 1 (8 warps) D + bias -> LeakyReLU -> fp16 into TMEM (A2); image
+//                            border pixels also store their pre-activation for dec_border
+//                 E warp     E = A2 x W2te^T (TMEM A operand, N = 32: 27 = 9 taps x 3
+//                            channels of decode.2 per pixel)
+//                 epilogue 2 (4 warps) scatters E into the tile's fp32 output accumulator
+//                            in shared memory (+1 pixel ring), phase after phase (fixed
+//                            order: deterministic); image-border sources are skipped
+//               Four D, A2 and E buffers in TMEM let the phases overlap.  Then every pixel
+//               whose 3x3 window stays inside the tile and off the image border is finished
+//               (bias, tanh, composite, u8, non-finite flag); the others and the ring go to
+//               per-tile partial planes.
+//   dec_border  one warp per image-border pixel: its correct pre-activation (the stored
+//               combined one minus the ring taps), LeakyReLU, and its 27 decode.2 taps E
+//   dec_fixup   the remaining pixels: partial planes of every tile whose 1-pixel-expanded
+//               area holds the pixel (a fixed order), plus the border sources' E, then the
+//               tail; the last CTA mirrors the flags (host path)
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace dr {
+
+namespace {
+
+constexpr int TY = 16, TX = 8;                   // token cells per tile (M = 128)
+constexpr int TPY = 8 * TY, TPX = 8 * TX;        // 128 x 64 pixels
+constexpr int HTY = TY + 2, HTX = TX + 2;        // halo'd token tile
+constexpr int TAP_BYTES = 64 * 64 * 2;           // [k-chunk 8][co 64][8 ci] fp16
+constexpr int NSLOT = 8;                         // weight tap ring
+constexpr int NB4 = 4;                           // D / A2 / E buffers in TMEM
+constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
+constexpr int NWARP = 19;
+constexpr int THREADS = 32 * NWARP;
+constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 18;
+constexpr uint32_t TM_D = 0, TM_A2 = 256, TM_E = 384, TM_COLS = 512;
+
+struct __align__(1024) DecSmem {
+  uint8_t tok[HTY * HTX * 128];                  // 23040 B, SW128 rows (one token per row)
+  alignas(1024) uint8_t w2[32 * 128];            // SW128 [32][64] fp16
+  alignas(1024) uint8_t w[NSLOT][TAP_BYTES];
+  float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + 1]
+  float bias[64];
+  float b2[4];
+  uint64_t tok_full, w_full[NSLOT], w_empty[NSLOT];
+  uint64_t d_full[NB4], d_empty[NB4], a2_full[NB4], a2_empty[NB4], e_full[NB4], e_empty[NB4];
+  uint32_t tmem_base;
+};
+static_assert(sizeof(DecSmem) + 1024 <= 227 * 1024, "fused decoder shared memory");
+
+// 64 phases, row-major
+DR_DEV void phase_of(int k, int* py, int* px) {
+  *py = k >> 3;
+  *px = k & 7;
+}
+
+// taps of phase (py, px): (image index, token-tile row offset of the A operand)
+DR_DEV int phase_taps(int py, int px, int* img, int* off) {
+  int du[2], uu[2], nu = 0, dv[2], vv[2], nv = 0;
+  du[nu] = 0; uu[nu++] = py;
+  if (py <= 1) { du[nu] = -1; uu[nu++] = py + 8; }
+  if (py >= 6) { du[nu] = 1; uu[nu++] = py - 8; }
+  dv[nv] = 0; vv[nv++] = px;
+  if (px <= 1) { dv[nv] = -1; vv[nv++] = px + 8; }
+  if (px >= 6) { dv[nv] = 1; vv[nv++] = px - 8; }
+  int n = 0;
+  for (int a = 0; a < nu; ++a)
+    for (int b = 0; b < nv; ++b) {
+      img[n] = (uu[a] + 2) * 12 + (vv[b] + 2);
+      off[n++] = (1 + du[a]) * HTX + (1 + dv[b]);
+    }
+  return n;
+}
+
+// K-major SWIZZLE_128B descriptor with an explicit stride between 8-row groups
+DR_DEV uint64_t sdesc_sw128_sbo(uint32_t saddr, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+// accumulator column of tile pixel column c = qx + 1 (0..65) in row r = qy + 1: 8-column
+// blocks XOR-swizzled by the token row within 4 and the 32-pixel half, so the 32 lanes of
+// an epilogue-2 warp (4 token rows x 8 token columns, same phase) hit 32 banks
+DR_DEV int acc_col(int r, int c) {
+  const int g = ((r >> 3) & 3) | (((c >> 5) & 1) << 2);
+  return c ^ g;
+}
+
+// border-correction table layout (floats): edges [4][12][64 ci][64 co], edge bias [4][64],
+// corners [4][64 ci][64 co], corner bias [4][64]; edges 0 top, 1 bottom, 2 left, 3 right;
+// corners 0 TL, 1 TR, 2 BL, 3 BR
+constexpr size_t DK_EDGE = 0, DK_EB = (size_t)4 * 12 * 4096, DK_CORNER = DK_EB + 256,
+                 DK_CB = DK_CORNER + (size_t)4 * 4096, DK_TOTAL = DK_CB + 256;
+
+DR_DEV bool on_border(int y, int x, int H, int W) { return y == 0 || x == 0 || y == H - 1 || x == W - 1; }
+// index of an image-border pixel: top row, bottom row, left column, right column
+DR_DEV int border_index(int y, int x, int H, int W) {
+  if (y == 0) return x;
+  if (y == H - 1) return W + x;
+  if (x == 0) return 2 * W + (y - 1);
+  return 2 * W + (H - 2) + (y - 1);
+}
+
+#ifdef DR_TRACE
+// Diagnostic build only: per CTA, cycles spent in each wait (scripts/dec_trace.py).  Slots:
+// 0 start / 12 main loop end / 13 exit (globaltimer ns); cycles: 2 MMA w_full, 3 MMA
+// d_empty, 4 E-warp a2_full, 5 E-warp e_empty, 6 epi1 d_full, 8 epi1 a2_empty, 9 epi2
+// e_full, 10 epi2 phase barrier; 14 SM id
+__device__ unsigned long long g_dec_trace[4096 * 16];
+#define DT_CTA (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z))
+#define DT_SET(slot, v) do { if (DT_CTA < 4096) g_dec_trace[DT_CTA * 16 + (slot)] = (v); } while (0)
+#define DT_WAIT(slot, stmt) do { const long long t0_ = clock64(); stmt; \
+    if (lane == 0 && DT_CTA < 4096) atomicAdd(&g_dec_trace[DT_CTA * 16 + (slot)], (unsigned long long)(clock64() - t0_)); } while (0)
+DR_DEV unsigned long long dt_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#else
+#define DT_SET(slot, v) do {} while (0)
+#define DT_WAIT(slot, stmt) stmt
+#endif
+
+}  // namespace
+
+// Tail of one output pixel: o = decode.2 output before tanh (bias included); alr / src are
+// the pixel's alpha and input (preloaded by the caller).
+DR_DEV void dec_emit(const ConvTcArgs& a, int f, int y, int x, const float (&o)[3], float alr,
+                     const float (&srcf)[3], const uint8_t (&src8)[3]) {
+  const size_t plane = (size_t)a.H * a.W;
+  const size_t pix = (size_t)y * a.W + x;
+  int4 sp = make_int4(0, 0, 0, 0);
+  if (a.packed) sp = __ldg(a.spans + y);
+  const bool in_span = a.packed && x >= sp.x && x < sp.y;
+  bool bad = false;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float out01 = (tanhf(o[ch]) + 1.0f) * 0.5f;
+    bad |= !isfinite(out01);
+    const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
+    if (a.fill) a.fill[pl] = out01;
+    if (a.out_f32) a.out_f32[pl] = __fadd_rn(__fmul_rn(alr, out01), __fmul_rn(__fsub_rn(1.0f, alr), srcf[ch]));
+    if (a.out_u8 || in_span) {
+      const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01, 255.0f)), 0.f), 255.f);
+      uint8_t ov;
+      if (alr == 0.f) ov = src8[ch];
+      else if (alr == 1.f) ov = fill8;
+      else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
+                                                      __fmul_rn(__fsub_rn(1.0f, alr), (float)src8[ch]))), 0.f), 255.f);
+      if (a.out_u8) a.out_u8[((size_t)f * plane + pix) * 3 + ch] = ov;
+      if (in_span) a.packed[sp.z + 3 * (x - sp.x) + ch] = ov;
+    }
+  }
+  if (bad) atomicOr(a.flags + f, 1);
+}
+
+// inputs of one output pixel for dec_emit
+DR_DEV void dec_inputs(const ConvTcArgs& a, int f, int y, int x, float* alr, float (&srcf)[3],
+                       uint8_t (&src8)[3]) {
+  const size_t plane = (size_t)a.H * a.W;
+  const size_t pix = (size_t)y * a.W + x;
+  *alr = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix) : 1.f;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    srcf[ch] = a.out_f32 ? __ldg(a.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix) : 0.f;
+    src8[ch] = a.rgb_u8 ? __ldg(a.rgb_u8 + ((size_t)f * plane + pix) * 3 + ch) : 0;
+  }
+}
+
+namespace {
+
+// decode.2 taps TAP0 .. TAP0+NTAP-1 of source pixel (yl, xl) into the accumulator; the
+// targets are distinct, so load all, add, store all
+template <int TAP0, int NTAP>
+DR_DEV void epi2_rmw(DecSmem& sm, const uint32_t (&ev)[32], int yl, int xl) {
+  float cur[3 * NTAP];
+  int rr[NTAP], cc[NTAP];
+#pragma unroll
+  for (int k = 0; k < NTAP; ++k) {
+    const int tap = TAP0 + k, ky = tap / 3, kx = tap % 3;
+    rr[k] = yl - (ky - 1) + 1;
+    cc[k] = acc_col(rr[k], xl - (kx - 1) + 1);
+#pragma unroll
+    for (int co = 0; co < 3; ++co) cur[3 * k + co] = sm.acc[co][rr[k]][cc[k]];
+  }
+#pragma unroll
+  for (int k = 0; k < NTAP; ++k)
+#pragma unroll
+    for (int co = 0; co < 3; ++co)
+      sm.acc[co][rr[k]][cc[k]] = cur[3 * k + co] + __uint_as_float(ev[3 * (TAP0 + k) + co]);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_constant__ DecArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  DecSmem& sm = *reinterpret_cast<DecSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.groups;
+  const int tile_x = blockIdx.x, tile_y = blockIdx.y / G, grp = blockIdx.y - tile_y * G;
+  const int f = blockIdx.z;
+  const int ty0 = tile_y * TY, tx0 = tile_x * TX;          // first token cell
+  const int y0 = 8 * ty0, x0 = 8 * tx0;                    // first pixel
+  const int k0 = grp * 64 / G, k1 = (grp + 1) * 64 / G;   // this CTA's phases
+  const int nph = k1 - k0;
+  const int H = a.H, W = a.W;
+  const int NB = 2 * W + 2 * (H - 2);
+
+  pdl_trigger();
+#ifdef DR_TRACE
+  if (threadIdx.x < 16) DT_SET(threadIdx.x, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    DT_SET(0, dt_ns());
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    DT_SET(14, smid);
+  }
+#endif
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sm.tok_full, 1);
+    for (int i = 0; i < NSLOT; ++i) {
+      tc::mbar_init(&sm.w_full[i], 1);
+      tc::mbar_init(&sm.w_empty[i], 1);
+    }
+    for (int i = 0; i < NB4; ++i) {
+      tc::mbar_init(&sm.d_full[i], 1);
+      tc::mbar_init(&sm.d_empty[i], 8);
+      tc::mbar_init(&sm.a2_full[i], 8);
+      tc::mbar_init(&sm.a2_empty[i], 1);
+      tc::mbar_init(&sm.e_full[i], 1);
+      tc::mbar_init(&sm.e_empty[i], 8);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tokmap);
+    // constant weights: the first taps and decode.2's image before waiting on the
+    // predecessor grid
+    tc::mbar_arrive_expect_tx(&sm.tok_full, (uint32_t)(HTY * HTX * 128 + 32 * 128));
+    tc::bulk_load(sm.w2, a.w2, 32 * 128, &sm.tok_full);
+    int kk = 0;
+    for (int k = k0; k < k1 && kk < NSLOT; ++k) {
+      int py, px, img[4], off[4];
+      phase_of(k, &py, &px);
+      const int n = phase_taps(py, px, img, off);
+      for (int t = 0; t < n && kk < NSLOT; ++t, ++kk) {
+        tc::mbar_arrive_expect_tx(&sm.w_full[kk], TAP_BYTES);
+        tc::bulk_load(sm.w[kk], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)img[t] * TAP_BYTES,
+                      TAP_BYTES, &sm.w_full[kk]);
+      }
+    }
+  }
+  // zero the accumulator (the ring included), biases to smem
+  {
+    float4* z = reinterpret_cast<float4*>(&sm.acc[0][0][0]);
+    for (int i = threadIdx.x; i < 3 * ACC_ROWS * ACC_RS / 4; i += THREADS) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x < 64) sm.bias[threadIdx.x] = __ldg(a.bcomb + threadIdx.x);
+    if (threadIdx.x < 3) sm.b2[threadIdx.x] = __ldg(a.b2 + threadIdx.x);
+  }
+  pdl_wait();                    // predecessor complete: tokens written, its TMEM free
+  if (warp == W_MMA) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == W_LOAD) {
+    if (lane == 0) {                                       // ------------------- loads
+      tc::tma_load_4d(sm.tok, &tokmap, &sm.tok_full, 0, tx0, ty0, f);
+      int kk = 0;
+      for (int k = k0; k < k1; ++k) {
+        int py, px, img[4], off[4];
+        phase_of(k, &py, &px);
+        const int n = phase_taps(py, px, img, off);
+        for (int t = 0; t < n; ++t, ++kk) {
+          if (kk < NSLOT) continue;                        // issued in the prologue
+          const int sl = kk % NSLOT;
+          tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(kk / NSLOT - 1) & 1u);
+          tc::mbar_arrive_expect_tx(&sm.w_full[sl], TAP_BYTES);
+          tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)img[t] * TAP_BYTES,
+                        TAP_BYTES, &sm.w_full[sl]);
+        }
+      }
+    }
+  } else if (warp == W_MMA) {
+    // --------------------------------------------------------------- D = tokens x Wcomb
+    constexpr uint32_t idesc = tc::idesc_f16(128, 64);
+    tc::mbar_wait(&sm.tok_full, 0);
+    tc::fence_after();
+    const uint64_t a0 = sdesc_sw128_sbo(tc::smem_u32(sm.tok), HTX * 128);
+    const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 1024, 128);
+    int kk = 0;
+    for (int i = 0; i < nph; ++i) {
+      int py, px, img[4], off[4];
+      phase_of(k0 + i, &py, &px);
+      const int n = phase_taps(py, px, img, off);
+      const int b = i % NB4;
+      if (i >= NB4) DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
+      tc::fence_after();
+      for (int t = 0; t < n; ++t, ++kk) {
+        const int sl = kk % NSLOT;
+        DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(kk / NSLOT) & 1u));
+        tc::fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_f16_warp(tbase + TM_D + 64 * b, a0 + (uint64_t)(off[t] * 8 + ks * 2),
+                           b0 + (uint64_t)(sl * (TAP_BYTES / 16) + ks * 128), idesc,
+                           (t | ks) != 0);
+        tc::mma_commit_warp(&sm.w_empty[sl]);
+      }
+      tc::mma_commit_warp(&sm.d_full[b]);
+    }
+  } else if (warp == W_EMMA) {
+    // --------------------------------------------------------------- E = A2 x W2te
+    constexpr uint32_t idesc2 = tc::idesc_f16(128, 32);
+    tc::mbar_wait(&sm.tok_full, 0);                        // w2 landed with the tokens
+    const uint64_t bw2 = tc::sdesc_sw128(tc::smem_u32(sm.w2), 0);
+    for (int i = 0; i < nph; ++i) {
+      const int b = i % NB4;
+      DT_WAIT(4, tc::mbar_wait(&sm.a2_full[b], (uint32_t)(i / NB4) & 1u));
+      if (i >= NB4) DT_WAIT(5, tc::mbar_wait(&sm.e_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
+      tc::fence_after();
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        tc::mma_ts_f16_warp(tbase + TM_E + 32 * b, tbase + TM_A2 + 32 * b + 8 * ks,
+                            bw2 + (uint64_t)(2 * ks), idesc2, ks != 0);
+      tc::mma_commit_warp(&sm.e_full[b]);
+      tc::mma_commit_warp(&sm.a2_empty[b]);
+    }
+  } else if (warp < W_EPI2) {
+    // --------------------------------------------------------------- epilogue 1
+    const int q = warp & 3, h = (warp - W_EPI1) >> 2;    // lane quarter, column half
+    const int row = 32 * q + lane;                        // token position in the tile
+    const int tyl = row >> 3, txl = row & 7;
+    const uint32_t lrow = (uint32_t)(32 * q) << 16;
+    float bias[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) bias[c] = sm.bias[32 * h + c];
+    for (int i = 0; i < nph; ++i) {
+      int py, px;
+      phase_of(k0 + i, &py, &px);
+      const int b = i % NB4;
+      const int y = y0 + 8 * tyl + py, x = x0 + 8 * txl + px;
+      DT_WAIT(6, tc::mbar_wait(&sm.d_full[b], (uint32_t)(i / NB4) & 1u));
+      tc::fence_after();
+      uint32_t v[32];
+      DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * h, v);
+      DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * h + 16, (v + 16));
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) + bias[c]);
+      if (y < H && x < W && on_border(y, x, H, W)) {
+        // image border: the combined pre-activation is redone by dec_border
+        float4* dst = reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 32 * h);
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4)
+          dst[c4] = make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
+                                __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
+      }
+      uint32_t pk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const float u0 = __uint_as_float(v[c]), u1 = __uint_as_float(v[c + 1]);
+        pk[c / 2] = pack_half2(fmaxf(u0, 0.2f * u0), fmaxf(u1, 0.2f * u1));   // LeakyReLU(0.2)
+      }
+      if (i >= NB4) {
+        DT_WAIT(8, tc::mbar_wait(&sm.a2_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
+        tc::fence_after();
+      }
+      DR_TMEM_ST16(tbase + lrow + TM_A2 + 32 * b + 16 * h, pk);
+      tc::tmem_wait_st();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.a2_full[b]);
+    }
+  } else {
+    // --------------------------------------------------------------- epilogue 2
+    // two warps per lane quarter: decode.2 taps 0-4 / 5-8 of the same pixels (distinct
+    // targets within a phase), one barrier per phase orders the read-modify-writes
+    const int q = warp & 3, hh = (warp - W_EPI2) >> 2;
+    const int row = 32 * q + lane;
+    const int tyl = row >> 3, txl = row & 7;
+    const uint32_t lrow = (uint32_t)(32 * q) << 16;
+    for (int i = 0; i < nph; ++i) {
+      int py, px;
+      phase_of(k0 + i, &py, &px);
+      const int b = i % NB4;
+      DT_WAIT(9, tc::mbar_wait(&sm.e_full[b], (uint32_t)(i / NB4) & 1u));
+      tc::fence_after();
+      uint32_t ev[32];
+      DR_TMEM_LD16(tbase + lrow + TM_E + 32 * b, ev);
+      DR_TMEM_LD16(tbase + lrow + TM_E + 32 * b + 16, (ev + 16));
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.e_empty[b]);
+      const int yl = 8 * tyl + py, xl = 8 * txl + px;      // source pixel in the tile
+      const int y = y0 + yl, x = x0 + xl;
+      if (y < H && x < W && !on_border(y, x, H, W)) {
+        if (hh) epi2_rmw<5, 4>(sm, ev, yl, xl);
+        else epi2_rmw<0, 5>(sm, ev, yl, xl);
+      }
+      DT_WAIT(10, asm volatile("bar.sync 2, 256;\n" ::: "memory"));   // phase order of the RMWs
+    }
+  }
+
+  // ------------------------------------------------------------------- finish the tile
+  tc::fence_before();
+  __syncthreads();
+#ifdef DR_TRACE
+  if (threadIdx.x == 0) DT_SET(12, dt_ns());
+#endif
+  if (warp == W_MMA) tc::tmem_dealloc<TM_COLS>(tbase);
+  const int ye = min(TPY, H - y0), xe = min(TPX, W - x0);
+  const bool nb_up = y0 > 0, nb_dn = y0 + TPY < H, nb_l = x0 > 0, nb_r = x0 + TPX < W;
+  const int par = ((tile_y & 1) << 1) | (tile_x & 1);
+  const size_t plane = (size_t)H * W;
+  float* part = a.part + ((size_t)(grp * 4 + par) * a.frames + f) * 3 * plane;
+  // pixel of the tile (+ ring) that dec_fixup finishes: next to another tile, within one
+  // pixel of the image border, or every pixel when the phases are split over CTAs
+  auto is_fix = [&](int yl, int xl, int y, int x) {
+    return G > 1 || (yl == 0 && nb_up) || (yl == TPY - 1 && nb_dn) || (xl == 0 && nb_l) ||
+           (xl == TPX - 1 && nb_r) || y <= 1 || x <= 1 || y >= H - 2 || x >= W - 2;
+  };
+  // interior pixels in runs of 4 along x (vector loads / stores), two runs per thread per
+  // pass with the inputs loaded up front; runs holding a dec_fixup pixel go pixel by pixel
+  const int nq = xe >> 2;                                  // runs per row (xe % 8 == 0)
+  const ConvTcArgs& t = a.tail;
+  for (int idx = threadIdx.x; idx < ye * nq; idx += 2 * THREADS) {
+    int yy[2], xx[2];
+    bool act[2], fast[2];
+    float4 al[2], rf[2][3];
+    uint32_t r8[2][3];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int id = idx + j * THREADS;
+      act[j] = id < ye * nq;
+      const int yl = act[j] ? id / nq : 0, xl = act[j] ? 4 * (id - yl * nq) : 0;
+      yy[j] = y0 + yl;
+      xx[j] = x0 + xl;
+      fast[j] = act[j] && !is_fix(yl, xl, yy[j], xx[j]) && !is_fix(yl, xl + 3, yy[j], xx[j] + 3) &&
+                !t.packed;
+      if (fast[j]) {
+        const size_t pix = (size_t)yy[j] * W + xx[j];
+        al[j] = t.alpha ? __ldg(reinterpret_cast<const float4*>(t.alpha + (size_t)f * plane + pix))
+                        : make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          if (t.out_f32) rf[j][ch] = __ldg(reinterpret_cast<const float4*>(t.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix));
+          if (t.out_u8) r8[j][ch] = __ldg(reinterpret_cast<const uint32_t*>(t.rgb_u8 + ((size_t)f * plane + pix) * 3) + ch);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!act[j]) continue;
+      const int r = yy[j] - y0 + 1;
+      if (!fast[j]) {
+        for (int e = 0; e < 4; ++e) {
+          const int x = xx[j] + e, cc = acc_col(r, x - x0 + 1);
+          float o[3];
+#pragma unroll
+          for (int co = 0; co < 3; ++co) o[co] = sm.acc[co][r][cc];
+          if (is_fix(yy[j] - y0, x - x0, yy[j], x)) {
+#pragma unroll
+            for (int co = 0; co < 3; ++co) part[co * plane + (size_t)yy[j] * W + x] = o[co];
+          } else {
+#pragma unroll
+            for (int co = 0; co < 3; ++co) o[co] += sm.b2[co];
+            float alr, srcf[3];
+            uint8_t src8[3];
+            dec_inputs(t, f, yy[j], x, &alr, srcf, src8);
+            dec_emit(t, f, yy[j], x, o, alr, srcf, src8);
+          }
+        }
+        continue;
+      }
+      // 4 pixels: tanh tail, composite, vector stores
+      const float alv[4] = {al[j].x, al[j].y, al[j].z, al[j].w};
+      float out01[3][4];
+      bool bad = false;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int cc = acc_col(r, xx[j] + e - x0 + 1);
+#pragma unroll
+        for (int co = 0; co < 3; ++co) {
+          out01[co][e] = (tanhf(sm.acc[co][r][cc] + sm.b2[co]) + 1.0f) * 0.5f;
+          bad |= !isfinite(out01[co][e]);
+        }
+      }
+      const size_t pix = (size_t)yy[j] * W + xx[j];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
+        if (t.fill) *reinterpret_cast<float4*>(t.fill + pl) = make_float4(out01[ch][0], out01[ch][1], out01[ch][2], out01[ch][3]);
+        if (t.out_f32) {
+          const float src[4] = {rf[j][ch].x, rf[j][ch].y, rf[j][ch].z, rf[j][ch].w};
+          float o4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o4[e] = __fadd_rn(__fmul_rn(alv[e], out01[ch][e]), __fmul_rn(__fsub_rn(1.0f, alv[e]), src[e]));
+          *reinterpret_cast<float4*>(t.out_f32 + pl) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+        }
+      }
+      if (t.out_u8) {
+        uint8_t src[12], dst[12];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) *reinterpret_cast<uint32_t*>(src + 4 * ch) = r8[j][ch];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const uint8_t fill8 = (uint8_t)fminf(fmaxf(rintf(__fmul_rn(out01[ch][e], 255.0f)), 0.f), 255.f);
+            const uint8_t s8 = src[3 * e + ch];
+            const float alr = alv[e];
+            uint8_t ov;
+            if (alr == 0.f) ov = s8;
+            else if (alr == 1.f) ov = fill8;
+            else ov = (uint8_t)fminf(fmaxf(rintf(__fadd_rn(__fmul_rn(alr, (float)fill8),
+                                                            __fmul_rn(__fsub_rn(1.0f, alr), (float)s8))), 0.f), 255.f);
+            dst[3 * e + ch] = ov;
+          }
+        uint32_t* d8 = reinterpret_cast<uint32_t*>(t.out_u8 + ((size_t)f * plane + pix) * 3);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) d8[ch] = *reinterpret_cast<const uint32_t*>(dst + 4 * ch);
+      }
+      if (bad) atomicOr(t.flags + f, 1);
+    }
+  }
+  // the outer ring (contributions to the neighbouring tiles' pixels)
+  for (int idx = threadIdx.x; idx < 2 * (TPX + 2) + 2 * TPY; idx += THREADS) {
+    int yl, xl;
+    if (idx < TPX + 2) { yl = -1; xl = idx - 1; }
+    else if (idx < 2 * (TPX + 2)) { yl = TPY; xl = idx - (TPX + 2) - 1; }
+    else if (idx < 2 * (TPX + 2) + TPY) { yl = idx - 2 * (TPX + 2); xl = -1; }
+    else { yl = idx - 2 * (TPX + 2) - TPY; xl = TPX; }
+    const int y = y0 + yl, x = x0 + xl;
+    if (y < 0 || x < 0 || y >= H || x >= W) continue;
+    const int r = yl + 1, cc = acc_col(r, xl + 1);
+#pragma unroll
+    for (int co = 0; co < 3; ++co) part[co * plane + (size_t)y * W + x] = sm.acc[co][r][cc];
+  }
+#ifdef DR_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) DT_SET(13, dt_ns());
+#endif
+}
+
+// One warp per image-border pixel: pre-activation = combined (stored by dec_fused) minus
+// the decode.0 taps reading the canvas ring, LeakyReLU, then decode.2's 27 taps
+// E[u] = sum_ci W2[u][ci] d0[ci].  Lane l owns channels 2l, 2l+1.
+__global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__ DecArgs a) {
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
+  const long g = (long)blockIdx.x * 8 + warp;
+  if (g >= (long)a.frames * NB) {
+    pdl_wait();
+    return;
+  }
+  const int f = (int)(g / NB), bi = (int)(g - (long)f * NB);
+  int y, x;
+  if (bi < W) { y = 0; x = bi; }
+  else if (bi < 2 * W) { y = H - 1; x = bi - W; }
+  else if (bi < 2 * W + H - 2) { y = bi - 2 * W + 1; x = 0; }
+  else { y = bi - 2 * W - (H - 2) + 1; x = W - 1; }
+  const int co = 2 * lane;
+  const float* dk = a.dk;
+  const int PC = a.Cc + 2, PR = a.R + 2;
+  pdl_wait();
+  const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
+  // sum_ci K[ci][co, co+1] tok(ty, tx)[ci] over the warp (token channels broadcast by shuffle)
+  auto gemv = [&](const float* k, int ty, int tx, float2& acc) {
+    const __half2 tp = reinterpret_cast<const __half2*>(tokf + ((size_t)(ty + 1) * PC + (tx + 1)) * 64)[lane];
+    const float2 tv = __half22float2(tp);
+#pragma unroll 8
+    for (int c2 = 0; c2 < 32; ++c2) {
+      const float t0 = __shfl_sync(0xffffffffu, tv.x, c2), t1 = __shfl_sync(0xffffffffu, tv.y, c2);
+      const float2 w0 = __ldg(reinterpret_cast<const float2*>(k + (size_t)(2 * c2) * 64 + co));
+      const float2 w1 = __ldg(reinterpret_cast<const float2*>(k + (size_t)(2 * c2 + 1) * 64 + co));
+      acc.x = fmaf(w0.x, t0, fmaf(w1.x, t1, acc.x));
+      acc.y = fmaf(w0.y, t0, fmaf(w1.y, t1, acc.y));
+    }
+  };
+  float2 corr = make_float2(0.f, 0.f);
+  const bool e[4] = {y == 0, y == H - 1, x == 0, x == W - 1};
+  for (int ed = 0; ed < 4; ++ed) {
+    if (!e[ed]) continue;
+    const float2 eb = __ldg(reinterpret_cast<const float2*>(dk + DK_EB + ed * 64 + co));
+    corr.x += eb.x;
+    corr.y += eb.y;
+    const bool along_x = ed < 2;
+    const int pos = along_x ? x : y;
+    const int line = ed == 0 ? 0 : (ed == 1 ? a.R - 1 : (ed == 2 ? 0 : a.Cc - 1));
+    const int nlim = along_x ? a.Cc : a.R;
+    for (int t = pos / 8 - 1; t <= pos / 8 + 1; ++t) {
+      const int v = pos - 8 * t;
+      if (v < -2 || v > 9 || t < 0 || t >= nlim) continue;
+      gemv(dk + DK_EDGE + (size_t)(ed * 12 + v + 2) * 4096, along_x ? line : t, along_x ? t : line, corr);
+    }
+  }
+  for (int c4 = 0; c4 < 4; ++c4) {                      // doubly removed corner taps
+    const bool top = c4 < 2, left = (c4 & 1) == 0;
+    if (!((top ? e[0] : e[1]) && (left ? e[2] : e[3]))) continue;
+    float2 cs = __ldg(reinterpret_cast<const float2*>(dk + DK_CB + c4 * 64 + co));
+    gemv(dk + DK_CORNER + (size_t)c4 * 4096, top ? 0 : a.R - 1, left ? 0 : a.Cc - 1, cs);
+    corr.x -= cs.x;
+    corr.y -= cs.y;
+  }
+  const float2 pre = reinterpret_cast<const float2*>(a.bd0 + ((size_t)f * NB + bi) * 64)[lane];
+  float d0 = pre.x - corr.x, d1 = pre.y - corr.y;
+  d0 = d0 >= 0.f ? d0 : 0.2f * d0;
+  d1 = d1 >= 0.f ? d1 : 0.2f * d1;
+  // decode.0's output is fp16 on the tensor-core path: round the same way
+  d0 = __half2float(__float2half_rn(d0));
+  d1 = __half2float(__float2half_rn(d1));
+  float* out = a.be + ((size_t)f * NB + bi) * 27;
+  for (int u = 0; u < 27; ++u) {
+    const float2 w = __ldg(reinterpret_cast<const float2*>(a.w2f + u * 64 + co));
+    float s = fmaf(w.x, d0, w.y * d1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[u] = s;
+  }
+}
+
+// The pixels dec_fused left: the sum of the partial planes of every tile whose 1-pixel-
+// expanded area holds the pixel (<= 4 tiles, one parity plane each, over the phase groups,
+// a fixed order), plus the image-border sources' E, then the tail.  The last CTA mirrors
+// the flags (host path).
+__global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ DecArgs a) {
+  pdl_trigger();
+  const int f = blockIdx.y;
+  const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
+  const int nr = a.n_fix_rows, nc = a.n_fix_cols;
+  const long n_pix = a.groups > 1 ? (long)H * W : (long)nr * W + (long)(H - nr) * nc;
+  float b2[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) b2[c] = __ldg(a.b2 + c);
+  pdl_wait();
+  const size_t plane = (size_t)H * W;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pix; i += (long)gridDim.x * blockDim.x) {
+    int y, x;
+    if (a.groups > 1) {
+      y = (int)(i / W);
+      x = (int)(i - (long)y * W);
+    } else if (i < (long)nr * W) {
+      const int r = (int)(i / W);
+      y = a.fix_rows[r];
+      x = (int)(i - (long)r * W);
+    } else {
+      const long j = i - (long)nr * W;
+      int yy = (int)(j / nc);
+      x = a.fix_cols[(int)(j - (long)yy * nc)];
+      for (int k = 0; k < nr; ++k)                      // the yy-th row not in fix_rows
+        if (yy >= a.fix_rows[k]) ++yy;
+      y = yy;
+    }
+    const int ty_a = max(0, y - 1) / TPY, ty_b = min(H - 1, y + 1) / TPY;
+    const int tx_a = max(0, x - 1) / TPX, tx_b = min(W - 1, x + 1) / TPX;
+    float o[3] = {b2[0], b2[1], b2[2]};
+    for (int g = 0; g < a.groups; ++g)
+      for (int ty = ty_a; ty <= ty_b; ++ty)
+        for (int tx = tx_a; tx <= tx_b; ++tx) {
+          const int par = ((ty & 1) << 1) | (tx & 1);
+          const float* part = a.part + ((size_t)(g * 4 + par) * a.frames + f) * 3 * plane;
+#pragma unroll
+          for (int co = 0; co < 3; ++co) o[co] += part[co * plane + (size_t)y * W + x];
+        }
+    if (y <= 1 || x <= 1 || y >= H - 2 || x >= W - 2) {
+      // image-border sources p = (y + ky - 1, x + kx - 1), tap (ky, kx)
+      for (int ky = 0; ky < 3; ++ky)
+        for (int kx = 0; kx < 3; ++kx) {
+          const int py = y + ky - 1, px = x + kx - 1;
+          if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
+          const float* e = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
+#pragma unroll
+          for (int co = 0; co < 3; ++co) o[co] += e[co];
+        }
+    }
+    float alr, srcf[3];
+    uint8_t src8[3];
+    dec_inputs(a.tail, f, y, x, &alr, srcf, src8);
+    dec_emit(a.tail, f, y, x, o, alr, srcf, src8);
+  }
+  // flags mirror (host path): the last CTA to finish publishes the frames' flags
+  const ConvTcArgs& t = a.tail;
+  if (t.flags_mirror || t.mirror_after_spans) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+      if (atomicAdd(t.done, 1u) == total - 1) {
+        __threadfence();
+        int* fm = t.flags_mirror;
+        if (t.mirror_after_spans) {
+          const int4 sp = t.spans[t.H - 1];
+          const size_t n = (size_t)sp.z + 3 * (size_t)(sp.y - sp.x);
+          fm = reinterpret_cast<int*>(t.packed + ((n + 3) & ~(size_t)3));
+        }
+        for (int k = 0; k < t.frames; ++k) fm[k] = atomicOr(t.flags + k, 0);
+        if (t.rgb_flag) *t.rgb_flag = 0;
+        *t.done = 0;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t dec_border_table_floats() { return DK_TOTAL; }
+int dec_border_pixels(int H, int W) { return 2 * W + 2 * (H - 2); }
+
+// Phase groups per tile: enough CTAs for about one wave at small batch (4 at one 512^2
+// frame: 32 tiles).
+int dec_groups(int frames, int H, int W, int sms) {
+  const int tiles = frames * ((H + TPY - 1) / TPY) * ((W + TPX - 1) / TPX);
+  if (tiles >= sms) return 1;
+  if (2 * tiles >= sms) return 2;
+  return 4;
+}
+
+void dec_fix_lines(DecArgs& a) {
+  std::vector<int> rows = {0, 1, a.H - 2, a.H - 1}, cols = {0, 1, a.W - 2, a.W - 1};
+  for (int k = TPY; k < a.H; k += TPY) { rows.push_back(k - 1); rows.push_back(k); }
+  for (int k = TPX; k < a.W; k += TPX) { cols.push_back(k - 1); cols.push_back(k); }
+  auto finish = [](std::vector<int>& v, int n, short* out, int* cnt) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    v.erase(std::remove_if(v.begin(), v.end(), [n](int e) { return e < 0 || e >= n; }), v.end());
+    *cnt = (int)std::min<size_t>(v.size(), DEC_MAX_FIX);
+    for (int i = 0; i < *cnt; ++i) out[i] = (short)v[i];
+  };
+  finish(rows, a.H, a.fix_rows, &a.n_fix_rows);
+  finish(cols, a.W, a.fix_cols, &a.n_fix_cols);
+}
+
+#ifdef DR_TRACE
+std::vector<std::vector<unsigned long long>>& dec_trace_store() {
+  static std::vector<std::vector<unsigned long long>> v;
+  return v;
+}
+#endif
+
+void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s) {
+  static unsigned long long init = 0;
+  const int smem = (int)sizeof(DecSmem) + 1024;
+  once_per_device(init, [&] {
+    cudaFuncSetAttribute(dec_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  const dim3 grid((a.W + TPX - 1) / TPX, ((a.H + TPY - 1) / TPY) * a.groups, a.frames);
+  launch_pdl(dec_fused_kernel, grid, dim3(THREADS), smem, s, tok4d, a);
+#ifdef DR_TRACE
+  if (dec_trace_store().size() < 4) {
+    cudaStreamSynchronize(s);
+    const int n = std::min(4096, (int)(grid.x * grid.y * grid.z));
+    std::vector<unsigned long long> h((size_t)n * 16);
+    cudaMemcpyFromSymbol(h.data(), g_dec_trace, h.size() * sizeof(unsigned long long));
+    dec_trace_store().push_back(std::move(h));
+  }
+#endif
+}
+
+void launch_dec_border(const DecArgs& a, cudaStream_t s) {
+  const long warps = (long)a.frames * dec_border_pixels(a.H, a.W);
+  launch_pdl(dec_border_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, a);
+}
+
+void launch_dec_fixup(const DecArgs& a, cudaStream_t s) {
+  const long n_pix = a.groups > 1 ? (long)a.H * a.W
+                                  : (long)a.n_fix_rows * a.W + (long)(a.H - a.n_fix_rows) * a.n_fix_cols;
+  const int blocks = (int)std::max<long>(1, std::min<long>((n_pix + 255) / 256, 1024));
+  launch_pdl(dec_fixup_kernel, dim3(blocks, a.frames), dim3(256), 0, s, a);
+}
+
+}  // namespace dr
+
+#ifdef DR_TRACE
+extern "C" int dr_debug_dec_trace(int idx, unsigned long long* host, int n) {
+  auto& v = dr::dec_trace_store();
+  if (idx < 0 || idx >= (int)v.size()) return -1;
+  const int k = std::min(n, (int)v[idx].size());
+  for (int i = 0; i < k; ++i) host[i] = v[idx][i];
+  return k;
+}
+#endif

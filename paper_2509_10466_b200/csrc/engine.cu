@@ -357,16 +357,18 @@ struct dr_engine {
   uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We + be, then per block
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
-  // combined Vec2Patch o decode.0 (DR_V2P_COMB): 144 taps of the 12x12 kernel, combined
-  // bias, fp32 Vec2Patch / decode.0 weights for the border corrections
-  bool comb = false;
+  // fused decoder (dec_fused.cu): 144 taps of the combined 12x12 Vec2Patch o decode.0
+  // kernel, combined bias, border-correction tables; DR_DEC_FUSED=0 selects the unfused
+  // Vec2Patch -> decode.0 (+ E planes) -> decode.2 gather sequence (A/B only)
+  int dec_fused = 1;
   uint8_t* wcomb = nullptr;
   float* bcomb = nullptr;
-  float* wv32 = nullptr;
-  float* wc32 = nullptr;
-  float* canv_ring = nullptr;        // Vec2Patch canvas just outside the image
-  float* bdelta = nullptr;           // decode.0 border corrections
-  CUtensorMap map_rows{};
+  float* dk = nullptr;
+  float* part = nullptr;             // dec_fused partial sums (workspace)
+  float* bord_d0 = nullptr;          // border pixels' combined pre-activation (workspace)
+  float* bord_e = nullptr;           // border pixels' decode.2 taps (workspace)
+  float* w2f = nullptr;              // decode.2 weights fp32 [27][64]
+  CUtensorMap map_tok4{};
   size_t wtc_v2p = 0;                // byte offset of the Vec2Patch image
   size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
   CUtensorMap map_raster{}, map_tok{};
@@ -515,12 +517,15 @@ struct dr_engine {
     const size_t o_q = take(tok * C * 2), o_k = take(tok * C * 2), o_v = take(tok * C * 2);
     const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
     const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
-    const size_t o_ras = take(px * C * 2), o_ep = take(px * 27 * 2);
+    const size_t o_ras = take(dec_fused ? 0 : px * C * 2), o_ep = take(dec_fused ? 0 : px * 27 * 2);
+    size_t part_frames = 0;            // max over batches <= frames of groups x frames
+    for (int b = 1; b <= frames; ++b)
+      part_frames = std::max(part_frames, (size_t)dec_groups(b, H, W, sm_count()) * b);
+    const size_t o_part = take(dec_fused ? part_frames * 4 * frame_px() * 3 * 4 : 0);
+    const size_t nbp = (size_t)frames * dec_border_pixels(H, W);
+    const size_t o_bd0 = take(dec_fused ? nbp * 64 * 4 : 0), o_be = take(dec_fused ? nbp * 27 * 4 : 0);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
-    const size_t n_ring = (size_t)frames * (2 * (W + 2) + 2 * H) * 64;
-    const size_t n_delta = (size_t)frames * (2 * W + 2 * (H - 2)) * 64;
-    const size_t o_ring = take(comb ? n_ring * 4 : 0), o_delta = take(comb ? n_delta * 4 : 0);
     CUDA_TRY(cudaMalloc(&ws, off));
     uint8_t* b = static_cast<uint8_t*>(ws);
     bits0 = (uint32_t*)(b + o_b0); bits1 = (uint32_t*)(b + o_b1);
@@ -531,17 +536,32 @@ struct dr_engine {
     attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
     raster = (__half*)(b + o_ras); eplanes = (__half*)(b + o_ep);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
-    canv_ring = comb ? (float*)(b + o_ring) : nullptr;
-    bdelta = comb ? (float*)(b + o_delta) : nullptr;
+    part = dec_fused ? (float*)(b + o_part) : nullptr;
+    bord_d0 = dec_fused ? (float*)(b + o_bd0) : nullptr;
+    bord_e = dec_fused ? (float*)(b + o_be) : nullptr;
     cap = frames;
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
+    if (dec_fused) return make_token_map4(&map_tok4, tok16, frames, R + 2, Cc + 2);
     int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
     if (rc) return rc;
-    if (comb) {
-      rc = make_nhwc_map(&map_rows, raster, frames, H, W, 1, 128);
-      if (rc) return rc;
-    }
     return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
+  }
+
+  // 4-D TMA view of the padded token grid [frames][rows][cols][64] for the fused decoder:
+  // box = 64 ch x 10 columns x 18 rows (a 16 x 8 token tile with its 1-token halo)
+  int make_token_map4(CUtensorMap* map, void* base, int frames, int rows, int cols) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[4] = {64, (cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames};
+    const cuuint64_t strides[3] = {128, (cuuint64_t)cols * 128, (cuuint64_t)rows * cols * 128};
+    const cuuint32_t box[4] = {64, 10, 18, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled (token tile) failed: " + std::to_string((int)r));
+    return DR_OK;
   }
 
 
@@ -709,20 +729,21 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
             }
   }
 
-#ifndef DR_V2P_COMB
-#define DR_V2P_COMB 0
-#endif
-  // Vec2Patch o decode.0 as one transposed convolution: Wcomb[co][ci][u][v]
-  // = sum_{dy,dx,c'} Wc[co][c'][dy][dx] Wv[ci][c'][u+dy][v+dx], u, v in [-2, 9], packed like
-  // the Vec2Patch taps; bcomb = bc + sum Wc bv (double accumulation)
-  std::vector<uint16_t> combimg;
-  std::vector<float> bcomb;
-  // (the combined taps need a token window of 128 + 2 (Cc + 2) + 2 rows <= 3 x 128: W <= 1000)
-  if (DR_V2P_COMB && kk == 10 && c == 64 && 2 * (e->Cc + 2) + 130 <= 384) {
-    e->comb = true;
-    const float* wv = weights[tb];
-    const float* wc = weights[tb + 2];
-    combimg.resize((size_t)144 * 64 * 64);
+  // Fused decoder (dec_fused.cu): Vec2Patch o decode.0 as one transposed convolution,
+  // Wcomb[co][ci][u][v] = sum_{dy,dx,c'} Wc[co][c'][dy][dx] Wv[ci][c'][u+dy][v+dx], u, v in
+  // [-2, 9], 144 tap images [(u+2)*12 + (v+2)][k-chunk][co][8 ci] fp16; bcomb = bc + sum
+  // Wc bv; and the border-correction tables (float64 accumulation).
+  if (const char* df = std::getenv("DR_DEC_FUSED")) e->dec_fused = std::atoi(df) != 0;
+  std::vector<uint16_t> combimg((size_t)144 * 64 * 64);
+  std::vector<float> bcomb(64);
+  std::vector<float> dkt(dec_border_table_floats(), 0.f);
+  {
+    const float* wv = weights[tb];                       // [ci][c'][10][10]
+    const float* wc = weights[tb + 2];                   // [co][c'][3][3]
+    const float* bv = weights[tb + 1];
+    const float* bc = weights[tb + 3];
+    auto WC = [&](int co, int cp, int ky, int kx) { return (double)wc[((size_t)co * 64 + cp) * 9 + ky * 3 + kx]; };
+    auto WV = [&](int ci, int cp, int a, int b) { return (double)wv[(((size_t)ci * 64 + cp) * 10 + a) * 10 + b]; };
     WorkPool::get().run([&](int part, int parts) {
       std::vector<double> acc((size_t)64 * 64);
       for (int tap = part; tap < 144; tap += parts) {
@@ -734,9 +755,8 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
             if (ay < 0 || ay >= 10 || ax < 0 || ax >= 10) continue;
             for (int co = 0; co < 64; ++co)
               for (int cp = 0; cp < 64; ++cp) {
-                const double wcv = wc[((size_t)co * 64 + cp) * 9 + dy * 3 + dx];
-                for (int ci = 0; ci < 64; ++ci)
-                  acc[(size_t)co * 64 + ci] += wcv * wv[(((size_t)ci * 64 + cp) * 10 + ay) * 10 + ax];
+                const double wcv = WC(co, cp, dy, dx);
+                for (int ci = 0; ci < 64; ++ci) acc[(size_t)co * 64 + ci] += wcv * WV(ci, cp, ay, ax);
               }
           }
         uint16_t* dst = combimg.data() + (size_t)tap * 64 * 64;    // [k-chunk][co][8 ci]
@@ -748,35 +768,81 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
             }
       }
     });
-    const float* bv = weights[tb + 1];
-    const float* bc = weights[tb + 3];
-    bcomb.resize(64);
     for (int co = 0; co < 64; ++co) {
       double b = bc[co];
       for (int cp = 0; cp < 64; ++cp)
         for (int t = 0; t < 9; ++t) b += (double)wc[((size_t)co * 64 + cp) * 9 + t] * bv[cp];
       bcomb[co] = (float)b;
     }
-    // border-correction weights, output channel fastest (coalesced across threads):
-    // Vec2Patch [ky][kx][ci][c'], decode.0 [tap][c'][co]
-    std::vector<float> wvt((size_t)100 * 64 * 64), wct((size_t)9 * 64 * 64);
-    for (int ci = 0; ci < 64; ++ci)
-      for (int cp = 0; cp < 64; ++cp)
-        for (int k = 0; k < 100; ++k) wvt[((size_t)k * 64 + ci) * 64 + cp] = wv[((size_t)ci * 64 + cp) * 100 + k];
-    for (int co = 0; co < 64; ++co)
-      for (int cp = 0; cp < 64; ++cp)
-        for (int t = 0; t < 9; ++t) wct[((size_t)t * 64 + cp) * 64 + co] = wc[((size_t)co * 64 + cp) * 9 + t];
-    if (cudaMalloc(&e->wcomb, combimg.size() * 2) != cudaSuccess ||
-        cudaMalloc(&e->bcomb, 64 * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&e->wv32, (size_t)64 * 64 * 100 * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&e->wc32, (size_t)64 * 64 * 9 * sizeof(float)) != cudaSuccess ||
-        cudaMemcpy(e->wcomb, combimg.data(), combimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(e->bcomb, bcomb.data(), 64 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(e->wv32, wvt.data(), wvt.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(e->wc32, wct.data(), wct.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
-      dr_destroy(e);
-      return fail(DR_ERR_CUDA, "combined decoder weight upload failed");
+    // Border corrections (subtracted from the combined pre-activation on the image
+    // border): decode.0 taps (ky, kx) that read the canvas ring outside the crop.  Edge e
+    // (0 top: ky 0 / canvas row 0 <- a 0; 1 bottom: ky 2 <- a 9; 2 left: kx 0 <- b 0;
+    // 3 right: kx 2 <- b 9), tap v in [-2, 9] along the edge:
+    //   dK[e][v][ci][co] = sum_d sum_c' Wc[co][c'][ky][kx] Wv[ci][c'][a][b]
+    // with d the position along the edge; corners add back the doubly removed tap.
+    const size_t EB = (size_t)4 * 12 * 4096, CK = EB + 256, CB = CK + (size_t)4 * 4096;
+    for (int edge = 0; edge < 4; ++edge)
+      for (int v = -2; v <= 9; ++v)
+        for (int d = -1; d <= 1; ++d) {
+          int ky, kx, a, b;
+          if (edge == 0) { ky = 0; kx = d + 1; a = 0; b = v + d + 1; }
+          else if (edge == 1) { ky = 2; kx = d + 1; a = 9; b = v + d + 1; }
+          else if (edge == 2) { ky = d + 1; kx = 0; a = v + d + 1; b = 0; }
+          else { ky = d + 1; kx = 2; a = v + d + 1; b = 9; }
+          if (a < 0 || a >= 10 || b < 0 || b >= 10) continue;
+          float* dst = dkt.data() + ((size_t)(edge * 12 + v + 2) * 64) * 64;
+          for (int ci = 0; ci < 64; ++ci)
+            for (int co = 0; co < 64; ++co) {
+              double sacc = 0.0;
+              for (int cp = 0; cp < 64; ++cp) sacc += WC(co, cp, ky, kx) * WV(ci, cp, a, b);
+              dst[ci * 64 + co] += (float)sacc;
+            }
+        }
+    for (int edge = 0; edge < 4; ++edge)
+      for (int d = -1; d <= 1; ++d) {
+        const int ky = edge == 0 ? 0 : (edge == 1 ? 2 : d + 1);
+        const int kx = edge == 2 ? 0 : (edge == 3 ? 2 : d + 1);
+        for (int co = 0; co < 64; ++co) {
+          double sacc = 0.0;
+          for (int cp = 0; cp < 64; ++cp) sacc += WC(co, cp, ky, kx) * bv[cp];
+          dkt[EB + edge * 64 + co] += (float)sacc;
+        }
+      }
+    const int cky[4] = {0, 0, 2, 2}, ckx[4] = {0, 2, 0, 2}, ca[4] = {0, 0, 9, 9}, cb[4] = {0, 9, 0, 9};
+    for (int c4 = 0; c4 < 4; ++c4) {
+      for (int ci = 0; ci < 64; ++ci)
+        for (int co = 0; co < 64; ++co) {
+          double sacc = 0.0;
+          for (int cp = 0; cp < 64; ++cp) sacc += WC(co, cp, cky[c4], ckx[c4]) * WV(ci, cp, ca[c4], cb[c4]);
+          dkt[CK + (size_t)c4 * 4096 + ci * 64 + co] = (float)sacc;
+        }
+      for (int co = 0; co < 64; ++co) {
+        double sacc = 0.0;
+        for (int cp = 0; cp < 64; ++cp) sacc += WC(co, cp, cky[c4], ckx[c4]) * bv[cp];
+        dkt[CB + c4 * 64 + co] = (float)sacc;
+      }
     }
+  }
+  std::vector<float> w2f((size_t)27 * 64);
+  {
+    const float* w2 = weights[tb + 4];                   // [3][c][3][3]
+    for (int co = 0; co < 3; ++co)
+      for (int ci = 0; ci < 64; ++ci)
+        for (int tap = 0; tap < 9; ++tap) w2f[(size_t)(3 * tap + co) * 64 + ci] = w2[((size_t)co * 64 + ci) * 9 + tap];
+  }
+  if (cudaMalloc(&e->w2f, w2f.size() * sizeof(float)) != cudaSuccess ||
+      cudaMemcpy(e->w2f, w2f.data(), w2f.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+    dr_destroy(e);
+    return fail(DR_ERR_CUDA, "decode.2 weight upload failed");
+  }
+  if (cudaMalloc(&e->wcomb, combimg.size() * 2) != cudaSuccess ||
+      cudaMalloc(&e->bcomb, 64 * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&e->dk, dkt.size() * sizeof(float)) != cudaSuccess ||
+      cudaMemcpy(e->wcomb, combimg.data(), combimg.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(e->bcomb, bcomb.data(), 64 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(e->dk, dkt.data(), dkt.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+    dr_destroy(e);
+    return fail(DR_ERR_CUDA, "fused decoder weight upload failed");
   }
 
   std::vector<double> fw = feather_taps(cfg->mask_feather_sigma);
@@ -819,8 +885,8 @@ void dr_destroy(dr_engine* e) {
   cudaFree(e->fparams);
   cudaFree(e->wcomb);
   cudaFree(e->bcomb);
-  cudaFree(e->wv32);
-  cudaFree(e->wc32);
+  cudaFree(e->dk);
+  cudaFree(e->w2f);
   cudaFree(e->feather_w);
   cudaFree(e->wtc);
   cudaFree(e->timg);
@@ -1068,42 +1134,9 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   }
 
   // 5. decoder tail
-  V2pArgs vp{};
-  vp.frames = B; vp.H = e->H; vp.W = e->W; vp.R = e->R; vp.Cc = e->Cc;
-  vp.w = e->wtc + e->wtc_v2p; vp.bias = e->fparams + e->bv2p; vp.raster = e->raster;
-  if (e->comb) {
-    // Vec2Patch o decode.0 in one transposed convolution (raster = LeakyReLU(decode.0)),
-    // after the border corrections, then decode.2's tap-expanded GEMM alone
-    BorderArgs ba{};
-    ba.frames = B; ba.H = e->H; ba.W = e->W; ba.R = e->R; ba.Cc = e->Cc;
-    ba.tok16 = e->tok16; ba.wv = e->wv32; ba.bv = e->fparams + e->bv2p; ba.wc = e->wc32;
-    ba.ring = e->canv_ring; ba.delta = e->bdelta;
-    DR_STOP_CHECK();
-    DR_L(launch_border_corrections(ba, s));
-    vp.comb = 1; vp.w = e->wcomb; vp.bias = e->bcomb; vp.delta = e->bdelta;
-    DR_STOP_CHECK();
-    DR_L(launch_v2p_tc(e->map_tok, vp, s));
-    DR_L(e->mark(6, s));
-    DR_STOP_CHECK();
-    DR_L(launch_e_only(e->map_rows, nullptr, e->timg + e->te_d2, e->eplanes, B, e->H, e->W, s));
-    DR_L(e->mark(7, s));
-  } else {
-  DR_STOP_CHECK();
-  DR_L(launch_v2p_tc(e->map_tok, vp, s));
-  DR_L(e->mark(6, s));
-  // decode.0 with decode.2's tap-expanded GEMM fused into its epilogue (E planes), then
-  // the decode.2 gather + tanh + composite
-  ConvTcArgs cv{};
-  cv.frames = B; cv.H = e->H; cv.W = e->W;
-  cv.w = e->wtc; cv.bias = e->fparams + e->bd0;
-  cv.e_planes = e->eplanes; cv.w2 = e->timg + e->te_d2;
-  DR_STOP_CHECK();
-  DR_L(launch_conv3x3_tc(64, e->map_raster, cv, s));
-  DR_L(e->mark(7, s));
-  }
   ConvTcArgs c2{};
   c2.frames = B; c2.H = e->H; c2.W = e->W;
-  c2.bias = e->fparams + e->bd2; c2.e_planes = e->eplanes;
+  c2.bias = e->fparams + e->bd2;
   c2.alpha = alpha; c2.rgb_f32 = io->rgb_f32; c2.rgb_u8 = io->rgb_u8;
   c2.fill = io->fill; c2.out_f32 = io->out_f32; c2.out_u8 = io->out_u8; c2.flags = flags;
   c2.flags_mirror = e->flags_mirror; c2.done = e->d_done;
@@ -1111,10 +1144,46 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     c2.spans = e->pack_spans; c2.packed = e->pack_out; c2.mirror_after_spans = 1;
     c2.rgb_flag = e->rgb_flag;
   }
-  DR_STOP_CHECK();
-  DR_L(launch_dec2_gather(c2, s));
-  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0) + (e->comb ? 2 : 0);
-  DR_L(e->mark(8, s));
+  if (e->dec_fused) {
+    // Vec2Patch o decode.0 o decode.2 + composite per tile, then the seams
+    DecArgs da{};
+    da.frames = B; da.H = e->H; da.W = e->W; da.R = e->R; da.Cc = e->Cc;
+    da.groups = dec_groups(B, e->H, e->W, e->sm_count());
+    da.wcomb = e->wcomb; da.bcomb = e->bcomb; da.w2 = e->timg + e->te_d2; da.w2f = e->w2f;
+    da.b2 = e->fparams + e->bd2; da.dk = e->dk; da.tok16 = e->tok16;
+    da.part = e->part; da.bd0 = e->bord_d0; da.be = e->bord_e;
+    dec_fix_lines(da);
+    da.tail = c2;
+    DR_STOP_CHECK();
+    DR_L(launch_dec_fused(e->map_tok4, da, s));
+    DR_L(e->mark(9, s));
+    DR_STOP_CHECK();
+    DR_L(launch_dec_border(da, s));
+    DR_STOP_CHECK();
+    DR_L(launch_dec_fixup(da, s));
+    DR_L(e->mark(10, s));
+  } else {
+    V2pArgs vp{};
+    vp.frames = B; vp.H = e->H; vp.W = e->W; vp.R = e->R; vp.Cc = e->Cc;
+    vp.w = e->wtc + e->wtc_v2p; vp.bias = e->fparams + e->bv2p; vp.raster = e->raster;
+    DR_STOP_CHECK();
+    DR_L(launch_v2p_tc(e->map_tok, vp, s));
+    DR_L(e->mark(6, s));
+    // decode.0 with decode.2's tap-expanded GEMM fused into its epilogue (E planes), then
+    // the decode.2 gather + tanh + composite
+    ConvTcArgs cv{};
+    cv.frames = B; cv.H = e->H; cv.W = e->W;
+    cv.w = e->wtc; cv.bias = e->fparams + e->bd0;
+    cv.e_planes = e->eplanes; cv.w2 = e->timg + e->te_d2;
+    DR_STOP_CHECK();
+    DR_L(launch_conv3x3_tc(64, e->map_raster, cv, s));
+    DR_L(e->mark(7, s));
+    c2.e_planes = e->eplanes;
+    DR_STOP_CHECK();
+    DR_L(launch_dec2_gather(c2, s));
+    DR_L(e->mark(8, s));
+  }
+  e->last_launches = 1 + n_slotkv + 1 + 2 * e->nb + 3 + (split ? 1 : 0);
   e->sig = {B, split, (intptr_t)io->rgb_u8, (intptr_t)io->rgb_f32, (intptr_t)io->mask_m0,
             (intptr_t)io->slot0, (intptr_t)io->slot1, (intptr_t)io->new_slot,
             (intptr_t)io->slot_batched, (intptr_t)flags, (intptr_t)tv, (intptr_t)alpha,
@@ -1122,7 +1191,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
             (intptr_t)io->out_f32, (intptr_t)e->pack_spans, (intptr_t)e->pack_out,
             (intptr_t)e->flags_mirror, (intptr_t)e->rgb_ready, (intptr_t)e->rgb_flag,
             ent[0], ent[1], kv_computed,
-            en_fill, e->comb};
+            en_fill, e->dec_fused};
 #undef DR_L
 #undef DR_STOP_CHECK
   CUDA_TRY(cudaGetLastError());

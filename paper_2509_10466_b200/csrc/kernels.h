@@ -184,6 +184,43 @@ void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaS
 // decode.2 gather + tail over the E planes the fused decode.0 wrote (conv_tc.cu)
 void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- fused decoder
+// (dec_fused.cu) Vec2Patch o decode.0 as one stride-8 transposed convolution with a 12x12
+// kernel, LeakyReLU, decode.2's tap-expanded GEMM and the 3x3 gather in shared memory,
+// tanh and the composite -- per tile of 16 x 8 tokens (128 x 64 px), no 64-channel raster.
+// The combined form is exact off the image border; border pixels (decode.0 reads zero
+// padding there, the combined form the cropped canvas ring) are redone by dec_border from
+// the tile pass's pre-activations, and every pixel next to another tile (or within one
+// pixel of the image border) is finished by dec_fixup from per-tile partial sums; with
+// `groups` > 1 the 64 phases of a tile are split over that many CTAs and every pixel is
+// finished there.
+constexpr int DEC_MAX_FIX = 128;
+struct DecArgs {
+  int frames, H, W, R, Cc;
+  int groups;                // phase groups per tile: 1, 2 or 4
+  const void* wcomb;         // 144 tap images [(u+2)*12 + (v+2)][k-chunk 8][co 64][8 ci] fp16
+  const float* bcomb;        // [64] combined bias
+  const void* w2;            // decode.2 tap-expanded weights, K-major SW128 [32 u][64 ci]
+  const float* w2f;          // decode.2 weights fp32 [27 u][64 ci] (u = 3*(3*ky+kx)+co)
+  const float* b2;           // [3]
+  const float* dk;           // border-correction tables (engine.cu, dec_border_table_floats)
+  const __half* tok16;       // padded token grid [frames][R+2][Cc+2][64]
+  float* part;               // partial sums [groups * 4][frames][3][H][W]
+  float* bd0;                // border pixels' combined pre-activation [frames][NB][64]
+  float* be;                 // border pixels' decode.2 taps E [frames][NB][27]
+  // rows / columns dec_fixup finishes (seams and the 2-pixel image border band), sorted
+  int n_fix_rows, n_fix_cols;
+  short fix_rows[DEC_MAX_FIX], fix_cols[DEC_MAX_FIX];
+  ConvTcArgs tail;           // composite / output / flags fields (alpha .. packed)
+};
+size_t dec_border_table_floats();
+int dec_groups(int frames, int H, int W, int sms);
+int dec_border_pixels(int H, int W);                 // 2W + 2(H-2)
+void dec_fix_lines(DecArgs& a);                      // fills n_fix_rows/cols, fix_rows/cols
+void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s);
+void launch_dec_border(const DecArgs& a, cudaStream_t s);
+void launch_dec_fixup(const DecArgs& a, cudaStream_t s);   // fix pixels + flags mirror
+
 // ---------------------------------------------------------------- frame byte kernels
 // (frame_ops.cu): display composite / upscale2x, merge + redact, point-cloud pack.
 struct DisplayArgs {

@@ -99,8 +99,9 @@ def test_c3_eight_streams_batched_warm_memory_vs_oracle():
             ref_slots[s] = (ref_slots[s][1], ref["slot"][0])
             check_img(out[s:s + 1], ref["out"], f"C3 stream {s} frame {t}")
     # 1 mask + slot K/V (2 temporal blocks per uncached slot) + embed + 8 block kernels +
-    # 3 decoder: frames 0 and 1 project the (shared) zero slot, frame 2 nothing (both slots
-    # were filled inside the previous forwards' last blocks)
+    # 3 decoder (fused tile pass, image border, seams): frames 0 and 1 project the (shared)
+    # zero slot, frame 2 nothing (both slots were filled inside the previous forwards' last
+    # blocks)
     base = 1 + 1 + 8 + 3
     assert launches == [base + 2, base + 2, base], launches
 

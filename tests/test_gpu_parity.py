@@ -285,8 +285,8 @@ def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
     # every frame projects its newest slot's K/V (2 temporal blocks) at the start, next to
     # the mask stage; the older slot is cached from the previous frame:
     # 1 mask + 2 slot K/V + 1 embed + 2 x 4 blocks + 3 decoder (frame 1 also projects the
-    # second zero slot of the cold memory); +2 with the combined decoder (DR_V2P_COMB)
-    assert launches in ([15, 17, 15, 15, 15], [17, 19, 17, 17, 17])
+    # second zero slot of the cold memory)
+    assert launches == [15, 17, 15, 15, 15]
     mem_b = eng.zero_memory()
     for t in range(5):                           # stream B: clones, always recomputed
         rb = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]),
@@ -311,10 +311,13 @@ def test_batch_invariance_and_determinism_512():
     out_b, slot_b = eng.forward(cuda(imgs), cuda(masks), slots)
     out_b2, _ = eng.forward(cuda(imgs), cuda(masks), slots)
     assert torch.equal(out_b, out_b2), "non-deterministic"
+    # batch invariance: the token path is bit-identical; the fused decoder splits a tile's
+    # 64 phases over 1-4 CTAs by batch size (dec_groups), which only reorders fp32 sums
     for i in range(3):
         o, s = eng.forward(cuda(imgs[i:i + 1]), cuda(masks[i:i + 1]),
                            [sl[i:i + 1] for sl in slots])
-        assert torch.equal(o[0], out_b[i]) and torch.equal(s[0], slot_b[i])
+        assert torch.equal(s[0], slot_b[i])
+        assert float((o[0] - out_b[i]).abs().max()) <= 1e-5
     # composite guarantee: alpha == 0 pixels are the input frame bit-exactly
     res = eng.run(cuda(imgs), cuda(masks), slots, want_masks=True)
     a = res["alpha"].cpu().numpy()
