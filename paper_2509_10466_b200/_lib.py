@@ -83,7 +83,7 @@ SIGNATURES = {
 
 STAGE_NAMES = {0: "mask_stage", 1: "slot_kv", 2: "embed_qkv", 3: "attn_spatial",
                4: "attn_temporal", 5: "mlp_qkv", 6: "vec2patch", 7: "decode0",
-               8: "decode2_composite", 9: "decoder_fused", 10: "border_seam_fixup"}
+               8: "decode2_composite", 9: "decoder_fused", 10: "seam_fixup", 11: "dec_border"}
 
 _lib = None
 

@@ -70,7 +70,7 @@ struct __align__(1024) DecSmem {
   alignas(1024) uint8_t w2[32 * 128];            // SW128 [32][64] fp16
   alignas(1024) uint8_t w[NSLOT][TAP_BYTES];
   float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + 1]
-  float bias[64];
+  alignas(16) float bias[64];
   float b2[4];
   uint64_t tok_full, w_full[NSLOT], w_empty[NSLOT];
   uint64_t d_full[NB4], d_empty[NB4], a2_full[NB4], a2_empty[NB4], e_full[NB4], e_empty[NB4];
@@ -122,6 +122,21 @@ DR_DEV int acc_col(int r, int c) {
 constexpr size_t DK_EDGE = 0, DK_EB = (size_t)4 * 12 * 4096, DK_CORNER = DK_EB + 256,
                  DK_CB = DK_CORNER + (size_t)4 * 4096, DK_TOTAL = DK_CB + 256;
 
+DR_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+DR_DEV uint32_t map_rank(uint32_t local_saddr, int rank) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_saddr), "r"(rank));
+  return remote;
+}
+// (not volatile: read only after a cluster barrier, so the loads may be scheduled freely)
+DR_DEV float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 DR_DEV bool on_border(int y, int x, int H, int W) { return y == 0 || x == 0 || y == H - 1 || x == W - 1; }
 // index of an image-border pixel: top row, bottom row, left column, right column
 DR_DEV int border_index(int y, int x, int H, int W) {
@@ -137,6 +152,10 @@ DR_DEV int border_index(int y, int x, int H, int W) {
 // d_empty, 4 E-warp a2_full, 5 E-warp e_empty, 6 epi1 d_full, 8 epi1 a2_empty, 9 epi2
 // e_full, 10 epi2 phase barrier; 14 SM id
 __device__ unsigned long long g_dec_trace[4096 * 16];
+// per-phase timeline of CTA 0 (clock64): [0] D MMAs committed, [1] epilogue 1 done (set 0/1),
+// [2] E MMAs committed, [3] epilogue 2 done; [4][0] kernel start
+__device__ long long g_dec_tl[5][64];
+#define DT_TL(k, i) do { if (DT_CTA == 0 && (i) < 64) g_dec_tl[k][i] = clock64(); } while (0)
 #define DT_CTA (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z))
 #define DT_SET(slot, v) do { if (DT_CTA < 4096) g_dec_trace[DT_CTA * 16 + (slot)] = (v); } while (0)
 #define DT_WAIT(slot, stmt) do { const long long t0_ = clock64(); stmt; \
@@ -149,6 +168,7 @@ DR_DEV unsigned long long dt_ns() {
 #else
 #define DT_SET(slot, v) do {} while (0)
 #define DT_WAIT(slot, stmt) stmt
+#define DT_TL(k, i) do {} while (0)
 #endif
 
 }  // namespace
@@ -242,6 +262,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   __syncthreads();
   if (threadIdx.x == 0) {
     DT_SET(0, dt_ns());
+    DT_TL(4, 0);
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     DT_SET(14, smid);
@@ -255,8 +276,8 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     }
     for (int i = 0; i < NB4; ++i) {
       tc::mbar_init(&sm.d_full[i], 1);
-      tc::mbar_init(&sm.d_empty[i], 8);
-      tc::mbar_init(&sm.a2_full[i], 8);
+      tc::mbar_init(&sm.d_empty[i], 4);
+      tc::mbar_init(&sm.a2_full[i], 4);
       tc::mbar_init(&sm.a2_empty[i], 1);
       tc::mbar_init(&sm.e_full[i], 1);
       tc::mbar_init(&sm.e_empty[i], 8);
@@ -338,6 +359,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         tc::mma_commit_warp(&sm.w_empty[sl]);
       }
       tc::mma_commit_warp(&sm.d_full[b]);
+      if (lane == 0) DT_TL(0, i);
     }
   } else if (warp == W_EMMA) {
     // --------------------------------------------------------------- E = A2 x W2te
@@ -355,55 +377,68 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
                             bw2 + (uint64_t)(2 * ks), idesc2, ks != 0);
       tc::mma_commit_warp(&sm.e_full[b]);
       tc::mma_commit_warp(&sm.a2_empty[b]);
+      if (lane == 0) DT_TL(2, i);
     }
   } else if (warp < W_EPI2) {
     // --------------------------------------------------------------- epilogue 1
-    const int q = warp & 3, h = (warp - W_EPI1) >> 2;    // lane quarter, column half
+    // two sets of 4 warps (one per TMEM lane quarter) take alternate phases, all 64
+    // channels each, so two phases' TMEM round trips are in flight at once
+    const int q = warp & 3, set = (warp - W_EPI1) >> 2;
     const int row = 32 * q + lane;                        // token position in the tile
     const int tyl = row >> 3, txl = row & 7;
     const uint32_t lrow = (uint32_t)(32 * q) << 16;
-    float bias[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) bias[c] = sm.bias[32 * h + c];
-    for (int i = 0; i < nph; ++i) {
+    for (int i = set; i < nph; i += 2) {
       int py, px;
       phase_of(k0 + i, &py, &px);
       const int b = i % NB4;
       const int y = y0 + 8 * tyl + py, x = x0 + 8 * txl + px;
       DT_WAIT(6, tc::mbar_wait(&sm.d_full[b], (uint32_t)(i / NB4) & 1u));
       tc::fence_after();
-      uint32_t v[32];
-      DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * h, v);
-      DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * h + 16, (v + 16));
-      tc::tmem_wait_ld();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
-#pragma unroll
-      for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) + bias[c]);
-      if (y < H && x < W && on_border(y, x, H, W)) {
-        // image border: the combined pre-activation is redone by dec_border
-        float4* dst = reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 32 * h);
-#pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
-          dst[c4] = make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
-                                __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
-      }
-      uint32_t pk[16];
-#pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const float u0 = __uint_as_float(v[c]), u1 = __uint_as_float(v[c + 1]);
-        pk[c / 2] = pack_half2(fmaxf(u0, 0.2f * u0), fmaxf(u1, 0.2f * u1));   // LeakyReLU(0.2)
-      }
+      const bool brd = y < H && x < W && on_border(y, x, H, W);
+      float4* bdst = brd ? reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64) : nullptr;
       if (i >= NB4) {
         DT_WAIT(8, tc::mbar_wait(&sm.a2_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
         tc::fence_after();
       }
-      DR_TMEM_ST16(tbase + lrow + TM_A2 + 32 * b + 16 * h, pk);
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {                    // 32 channels at a time
+        uint32_t v[32];
+        DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * hc, v);
+        DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * hc + 16, (v + 16));
+        tc::tmem_wait_ld();
+        if (hc == 1) {                                    // D(b) fully read
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
+        }
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {                  // bias: 128-bit broadcast loads
+          const float4 bb = reinterpret_cast<const float4*>(sm.bias)[8 * hc + c4];
+          v[4 * c4] = __float_as_uint(__uint_as_float(v[4 * c4]) + bb.x);
+          v[4 * c4 + 1] = __float_as_uint(__uint_as_float(v[4 * c4 + 1]) + bb.y);
+          v[4 * c4 + 2] = __float_as_uint(__uint_as_float(v[4 * c4 + 2]) + bb.z);
+          v[4 * c4 + 3] = __float_as_uint(__uint_as_float(v[4 * c4 + 3]) + bb.w);
+        }
+        if (brd) {
+          // image border: the combined pre-activation is redone by dec_border
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            bdst[8 * hc + c4] = make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
+                                            __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float u0 = __uint_as_float(v[c]), u1 = __uint_as_float(v[c + 1]);
+          pk[c / 2] = pack_half2(fmaxf(u0, 0.2f * u0), fmaxf(u1, 0.2f * u1));   // LeakyReLU(0.2)
+        }
+        DR_TMEM_ST16(tbase + lrow + TM_A2 + 32 * b + 16 * hc, pk);
+      }
       tc::tmem_wait_st();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.a2_full[b]);
+      if (lane == 0 && q == 0) DT_TL(1, i);
     }
   } else {
     // --------------------------------------------------------------- epilogue 2
@@ -413,73 +448,121 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     const int row = 32 * q + lane;
     const int tyl = row >> 3, txl = row & 7;
     const uint32_t lrow = (uint32_t)(32 * q) << 16;
+    // E of phase i + 1 is loaded from TMEM while this warp waits at phase i's barrier
+    uint32_t ev[32];
+    if (nph > 0) {
+      DT_WAIT(9, tc::mbar_wait(&sm.e_full[0], 0));
+      tc::fence_after();
+      DR_TMEM_LD16(tbase + lrow + TM_E, ev);
+      DR_TMEM_LD16(tbase + lrow + TM_E + 16, (ev + 16));
+    }
     for (int i = 0; i < nph; ++i) {
       int py, px;
       phase_of(k0 + i, &py, &px);
       const int b = i % NB4;
-      DT_WAIT(9, tc::mbar_wait(&sm.e_full[b], (uint32_t)(i / NB4) & 1u));
-      tc::fence_after();
-      uint32_t ev[32];
-      DR_TMEM_LD16(tbase + lrow + TM_E + 32 * b, ev);
-      DR_TMEM_LD16(tbase + lrow + TM_E + 32 * b + 16, (ev + 16));
       tc::tmem_wait_ld();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.e_empty[b]);
+      uint32_t cur[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) cur[c] = ev[c];
       const int yl = 8 * tyl + py, xl = 8 * txl + px;      // source pixel in the tile
       const int y = y0 + yl, x = x0 + xl;
       if (y < H && x < W && !on_border(y, x, H, W)) {
-        if (hh) epi2_rmw<5, 4>(sm, ev, yl, xl);
-        else epi2_rmw<0, 5>(sm, ev, yl, xl);
+        if (hh) epi2_rmw<5, 4>(sm, cur, yl, xl);
+        else epi2_rmw<0, 5>(sm, cur, yl, xl);
+      }
+      if (i + 1 < nph) {
+        const int bn = (i + 1) % NB4;
+        DT_WAIT(9, tc::mbar_wait(&sm.e_full[bn], (uint32_t)((i + 1) / NB4) & 1u));
+        tc::fence_after();
+        DR_TMEM_LD16(tbase + lrow + TM_E + 32 * bn, ev);
+        DR_TMEM_LD16(tbase + lrow + TM_E + 32 * bn + 16, (ev + 16));
       }
       DT_WAIT(10, asm volatile("bar.sync 2, 256;\n" ::: "memory"));   // phase order of the RMWs
+      if (lane == 0 && warp == W_EPI2) DT_TL(3, i);
     }
   }
 
   // ------------------------------------------------------------------- finish the tile
+  // With G > 1 the G CTAs of a tile form a cluster: after a cluster barrier each finishes
+  // 1/G of the tile's rows, summing the G accumulators (distributed shared memory, rank
+  // order: deterministic); a second barrier keeps every accumulator alive until all reads
+  // are done.
   tc::fence_before();
   __syncthreads();
 #ifdef DR_TRACE
   if (threadIdx.x == 0) DT_SET(12, dt_ns());
 #endif
   if (warp == W_MMA) tc::tmem_dealloc<TM_COLS>(tbase);
+  if (G > 1) cluster_sync_all();
   const int ye = min(TPY, H - y0), xe = min(TPX, W - x0);
+  const int rows_per = TPY / G, rbeg = grp * rows_per, rend = min(ye, rbeg + rows_per);
   const bool nb_up = y0 > 0, nb_dn = y0 + TPY < H, nb_l = x0 > 0, nb_r = x0 + TPX < W;
   const int par = ((tile_y & 1) << 1) | (tile_x & 1);
   const size_t plane = (size_t)H * W;
-  float* part = a.part + ((size_t)(grp * 4 + par) * a.frames + f) * 3 * plane;
-  // pixel of the tile (+ ring) that dec_fixup finishes: next to another tile, within one
-  // pixel of the image border, or every pixel when the phases are split over CTAs
+  float* part = a.part + ((size_t)par * a.frames + f) * 3 * plane;
+  // accumulator value summed over the cluster's ranks (in rank order)
+  uint32_t acc_rank[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (G > 1 && q < G) acc_rank[q] = map_rank(tc::smem_u32(&sm.acc[0][0][0]), q);
+  auto accv = [&](int co, int r, int c) -> float {
+    if (G == 1) return sm.acc[co][r][c];
+    const uint32_t off = (uint32_t)(((co * ACC_ROWS + r) * ACC_RS + c) * 4);
+    float p[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) p[q] = q < G ? ld_dsmem_f32(acc_rank[q] + off) : 0.f;
+    float v = p[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q) if (q < G) v += p[q];
+    return v;
+  };
+  // pixel of the tile (+ ring) that dec_fixup finishes: next to another tile or within one
+  // pixel of the image border
   auto is_fix = [&](int yl, int xl, int y, int x) {
-    return G > 1 || (yl == 0 && nb_up) || (yl == TPY - 1 && nb_dn) || (xl == 0 && nb_l) ||
+    return (yl == 0 && nb_up) || (yl == TPY - 1 && nb_dn) || (xl == 0 && nb_l) ||
            (xl == TPX - 1 && nb_r) || y <= 1 || x <= 1 || y >= H - 2 || x >= W - 2;
   };
   // interior pixels in runs of 4 along x (vector loads / stores), two runs per thread per
   // pass with the inputs loaded up front; runs holding a dec_fixup pixel go pixel by pixel
   const int nq = xe >> 2;                                  // runs per row (xe % 8 == 0)
+  const int nrun = max(0, rend - rbeg) * nq;
   const ConvTcArgs& t = a.tail;
-  for (int idx = threadIdx.x; idx < ye * nq; idx += 2 * THREADS) {
+  for (int idx = threadIdx.x; idx < nrun; idx += 2 * THREADS) {
     int yy[2], xx[2];
-    bool act[2], fast[2];
+    bool act[2], fast[2], need[2];
     float4 al[2], rf[2][3];
     uint32_t r8[2][3];
+    // inputs of both runs first (vector loads), then the tails
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int id = idx + j * THREADS;
-      act[j] = id < ye * nq;
-      const int yl = act[j] ? id / nq : 0, xl = act[j] ? 4 * (id - yl * nq) : 0;
+      act[j] = id < nrun;
+      const int yl = act[j] ? rbeg + id / nq : 0, xl = act[j] ? 4 * (id % nq) : 0;
       yy[j] = y0 + yl;
       xx[j] = x0 + xl;
-      fast[j] = act[j] && !is_fix(yl, xl, yy[j], xx[j]) && !is_fix(yl, xl + 3, yy[j], xx[j] + 3) &&
-                !t.packed;
-      if (fast[j]) {
+      const bool f0 = is_fix(yl, xl, yy[j], xx[j]), f3 = is_fix(yl, xl + 3, yy[j], xx[j] + 3);
+      // is_fix is monotone inside a run except at its ends: only x = tile / image edges
+      need[j] = act[j] && !(f0 && f3 && is_fix(yl, xl + 1, yy[j], xx[j] + 1) && is_fix(yl, xl + 2, yy[j], xx[j] + 2));
+      fast[j] = act[j] && !f0 && !f3 && !t.packed;
+#ifdef DR_DEC_NOLOAD
+      if (need[j]) {                                      // diagnostic: no input loads
+        al[j] = make_float4(0.5f, 0.5f, 0.5f, 0.5f);
+        for (int ch = 0; ch < 3; ++ch) { rf[j][ch] = make_float4(0.f, 0.f, 0.f, 0.f); r8[j][ch] = 0; }
+      }
+      if (false) {
+#else
+      if (need[j]) {
+#endif
         const size_t pix = (size_t)yy[j] * W + xx[j];
         al[j] = t.alpha ? __ldg(reinterpret_cast<const float4*>(t.alpha + (size_t)f * plane + pix))
                         : make_float4(1.f, 1.f, 1.f, 1.f);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
           if (t.out_f32) rf[j][ch] = __ldg(reinterpret_cast<const float4*>(t.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix));
-          if (t.out_u8) r8[j][ch] = __ldg(reinterpret_cast<const uint32_t*>(t.rgb_u8 + ((size_t)f * plane + pix) * 3) + ch);
+          if (t.rgb_u8) r8[j][ch] = __ldg(reinterpret_cast<const uint32_t*>(t.rgb_u8 + ((size_t)f * plane + pix) * 3) + ch);
         }
       }
     }
@@ -488,21 +571,28 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       if (!act[j]) continue;
       const int r = yy[j] - y0 + 1;
       if (!fast[j]) {
+        // pixel by pixel: partial sums for dec_fixup's pixels, the tail (preloaded inputs)
+        const float alv[4] = {al[j].x, al[j].y, al[j].z, al[j].w};
+        uint8_t src[12];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) *reinterpret_cast<uint32_t*>(src + 4 * ch) = r8[j][ch];
+#pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int x = xx[j] + e, cc = acc_col(r, x - x0 + 1);
           float o[3];
 #pragma unroll
-          for (int co = 0; co < 3; ++co) o[co] = sm.acc[co][r][cc];
+          for (int co = 0; co < 3; ++co) o[co] = accv(co, r, cc);
           if (is_fix(yy[j] - y0, x - x0, yy[j], x)) {
 #pragma unroll
             for (int co = 0; co < 3; ++co) part[co * plane + (size_t)yy[j] * W + x] = o[co];
           } else {
 #pragma unroll
             for (int co = 0; co < 3; ++co) o[co] += sm.b2[co];
-            float alr, srcf[3];
-            uint8_t src8[3];
-            dec_inputs(t, f, yy[j], x, &alr, srcf, src8);
-            dec_emit(t, f, yy[j], x, o, alr, srcf, src8);
+            const float rfe[4][3] = {{rf[j][0].x, rf[j][1].x, rf[j][2].x}, {rf[j][0].y, rf[j][1].y, rf[j][2].y},
+                                     {rf[j][0].z, rf[j][1].z, rf[j][2].z}, {rf[j][0].w, rf[j][1].w, rf[j][2].w}};
+            const float srcf[3] = {rfe[e][0], rfe[e][1], rfe[e][2]};
+            const uint8_t src8[3] = {src[3 * e], src[3 * e + 1], src[3 * e + 2]};
+            dec_emit(t, f, yy[j], x, o, alv[e], srcf, src8);
           }
         }
         continue;
@@ -516,7 +606,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         const int cc = acc_col(r, xx[j] + e - x0 + 1);
 #pragma unroll
         for (int co = 0; co < 3; ++co) {
-          out01[co][e] = (tanhf(sm.acc[co][r][cc] + sm.b2[co]) + 1.0f) * 0.5f;
+          out01[co][e] = (tanhf(accv(co, r, cc) + sm.b2[co]) + 1.0f) * 0.5f;
           bad |= !isfinite(out01[co][e]);
         }
       }
@@ -559,19 +649,32 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       if (bad) atomicOr(t.flags + f, 1);
     }
   }
-  // the outer ring (contributions to the neighbouring tiles' pixels)
-  for (int idx = threadIdx.x; idx < 2 * (TPX + 2) + 2 * TPY; idx += THREADS) {
+#ifdef DR_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) DT_SET(11, dt_ns());
+#endif
+  // the outer ring (contributions to the neighbouring tiles' pixels): the top ring row with
+  // the first row block, the bottom one with the last, the side columns with each block
+  for (int idx = threadIdx.x; idx < 2 * (TPX + 2) + 2 * rows_per; idx += THREADS) {
     int yl, xl;
-    if (idx < TPX + 2) { yl = -1; xl = idx - 1; }
-    else if (idx < 2 * (TPX + 2)) { yl = TPY; xl = idx - (TPX + 2) - 1; }
-    else if (idx < 2 * (TPX + 2) + TPY) { yl = idx - 2 * (TPX + 2); xl = -1; }
-    else { yl = idx - 2 * (TPX + 2) - TPY; xl = TPX; }
+    if (idx < TPX + 2) {
+      if (grp != 0) continue;
+      yl = -1; xl = idx - 1;
+    } else if (idx < 2 * (TPX + 2)) {
+      if (grp != G - 1) continue;
+      yl = TPY; xl = idx - (TPX + 2) - 1;
+    } else if (idx < 2 * (TPX + 2) + rows_per) {
+      yl = rbeg + idx - 2 * (TPX + 2); xl = -1;
+    } else {
+      yl = rbeg + idx - 2 * (TPX + 2) - rows_per; xl = TPX;
+    }
     const int y = y0 + yl, x = x0 + xl;
     if (y < 0 || x < 0 || y >= H || x >= W) continue;
     const int r = yl + 1, cc = acc_col(r, xl + 1);
 #pragma unroll
-    for (int co = 0; co < 3; ++co) part[co * plane + (size_t)y * W + x] = sm.acc[co][r][cc];
+    for (int co = 0; co < 3; ++co) part[co * plane + (size_t)y * W + x] = accv(co, r, cc);
   }
+  if (G > 1) cluster_sync_all();                           // the ranks' reads are done
 #ifdef DR_TRACE
   __syncthreads();
   if (threadIdx.x == 0) DT_SET(13, dt_ns());
@@ -605,7 +708,7 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   auto gemv = [&](const float* k, int ty, int tx, float2& acc) {
     const __half2 tp = reinterpret_cast<const __half2*>(tokf + ((size_t)(ty + 1) * PC + (tx + 1)) * 64)[lane];
     const float2 tv = __half22float2(tp);
-#pragma unroll 8
+#pragma unroll
     for (int c2 = 0; c2 < 32; ++c2) {
       const float t0 = __shfl_sync(0xffffffffu, tv.x, c2), t1 = __shfl_sync(0xffffffffu, tv.y, c2);
       const float2 w0 = __ldg(reinterpret_cast<const float2*>(k + (size_t)(2 * c2) * 64 + co));
@@ -615,9 +718,10 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
     }
   };
   float2 corr = make_float2(0.f, 0.f);
-  const bool e[4] = {y == 0, y == H - 1, x == 0, x == W - 1};
+  const bool e_t = y == 0, e_b = y == H - 1, e_l = x == 0, e_r = x == W - 1;
+#pragma unroll
   for (int ed = 0; ed < 4; ++ed) {
-    if (!e[ed]) continue;
+    if (!(ed == 0 ? e_t : (ed == 1 ? e_b : (ed == 2 ? e_l : e_r)))) continue;
     const float2 eb = __ldg(reinterpret_cast<const float2*>(dk + DK_EB + ed * 64 + co));
     corr.x += eb.x;
     corr.y += eb.y;
@@ -633,12 +737,15 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   }
   for (int c4 = 0; c4 < 4; ++c4) {                      // doubly removed corner taps
     const bool top = c4 < 2, left = (c4 & 1) == 0;
-    if (!((top ? e[0] : e[1]) && (left ? e[2] : e[3]))) continue;
+    if (!((top ? e_t : e_b) && (left ? e_l : e_r))) continue;
     float2 cs = __ldg(reinterpret_cast<const float2*>(dk + DK_CB + c4 * 64 + co));
     gemv(dk + DK_CORNER + (size_t)c4 * 4096, top ? 0 : a.R - 1, left ? 0 : a.Cc - 1, cs);
     corr.x -= cs.x;
     corr.y -= cs.y;
   }
+  float2 w2v[27];                                       // decode.2 weights of this lane's channels
+#pragma unroll
+  for (int u = 0; u < 27; ++u) w2v[u] = __ldg(reinterpret_cast<const float2*>(a.w2f + u * 64 + co));
   const float2 pre = reinterpret_cast<const float2*>(a.bd0 + ((size_t)f * NB + bi) * 64)[lane];
   float d0 = pre.x - corr.x, d1 = pre.y - corr.y;
   d0 = d0 >= 0.f ? d0 : 0.2f * d0;
@@ -647,13 +754,15 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   d0 = __half2float(__float2half_rn(d0));
   d1 = __half2float(__float2half_rn(d1));
   float* out = a.be + ((size_t)f * NB + bi) * 27;
+  float es = 0.f;                                       // lane u < 27 ends with E[u]
+#pragma unroll
   for (int u = 0; u < 27; ++u) {
-    const float2 w = __ldg(reinterpret_cast<const float2*>(a.w2f + u * 64 + co));
-    float s = fmaf(w.x, d0, w.y * d1);
+    float s = fmaf(w2v[u].x, d0, w2v[u].y * d1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[u] = s;
+    if (lane == u) es = s;
   }
+  if (lane < 27) out[lane] = es;
 }
 
 // The pixels dec_fused left: the sum of the partial planes of every tile whose 1-pixel-
@@ -665,55 +774,76 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
   const int f = blockIdx.y;
   const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
   const int nr = a.n_fix_rows, nc = a.n_fix_cols;
-  const long n_pix = a.groups > 1 ? (long)H * W : (long)nr * W + (long)(H - nr) * nc;
+  const long n_runs = (long)nr * (W / 4);                // fix rows, in runs of 4
+  const long n_items = n_runs + (long)(H - nr) * nc;
   float b2[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) b2[c] = __ldg(a.b2 + c);
   pdl_wait();
   const size_t plane = (size_t)H * W;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pix; i += (long)gridDim.x * blockDim.x) {
-    int y, x;
-    if (a.groups > 1) {
-      y = (int)(i / W);
-      x = (int)(i - (long)y * W);
-    } else if (i < (long)nr * W) {
-      const int r = (int)(i / W);
+  const ConvTcArgs& tl = a.tail;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += (long)gridDim.x * blockDim.x) {
+    int y, x, n;
+    if (i < n_runs) {                                   // 4 pixels of a finished row
+      const int r = (int)(i / (W / 4));
       y = a.fix_rows[r];
-      x = (int)(i - (long)r * W);
-    } else {
-      const long j = i - (long)nr * W;
+      x = 4 * (int)(i - (long)r * (W / 4));
+      n = 4;
+    } else {                                            // a fix column of another row
+      const long j = i - n_runs;
       int yy = (int)(j / nc);
       x = a.fix_cols[(int)(j - (long)yy * nc)];
       for (int k = 0; k < nr; ++k)                      // the yy-th row not in fix_rows
         if (yy >= a.fix_rows[k]) ++yy;
       y = yy;
+      n = 1;
     }
     const int ty_a = max(0, y - 1) / TPY, ty_b = min(H - 1, y + 1) / TPY;
-    const int tx_a = max(0, x - 1) / TPX, tx_b = min(W - 1, x + 1) / TPX;
-    float o[3] = {b2[0], b2[1], b2[2]};
-    for (int g = 0; g < a.groups; ++g)
-      for (int ty = ty_a; ty <= ty_b; ++ty)
+    const int tx_a = max(0, x - 1) / TPX, tx_b = min(W - 1, x + n) / TPX;
+    float o[4][3];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int co = 0; co < 3; ++co) o[e][co] = b2[co];
+    // partial planes: tile (ty, tx) holds pixel x' iff x' in [TPX tx - 1, TPX (tx + 1)]
+    for (int ty = ty_a; ty <= ty_b; ++ty)
         for (int tx = tx_a; tx <= tx_b; ++tx) {
           const int par = ((ty & 1) << 1) | (tx & 1);
-          const float* part = a.part + ((size_t)(g * 4 + par) * a.frames + f) * 3 * plane;
+          const float* part = a.part + ((size_t)par * a.frames + f) * 3 * plane + (size_t)y * W + x;
+          const int lo = TPX * tx - 1, hi = TPX * (tx + 1);
+          if (n == 4) {
 #pragma unroll
-          for (int co = 0; co < 3; ++co) o[co] += part[co * plane + (size_t)y * W + x];
-        }
-    if (y <= 1 || x <= 1 || y >= H - 2 || x >= W - 2) {
-      // image-border sources p = (y + ky - 1, x + kx - 1), tap (ky, kx)
-      for (int ky = 0; ky < 3; ++ky)
-        for (int kx = 0; kx < 3; ++kx) {
-          const int py = y + ky - 1, px = x + kx - 1;
-          if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
-          const float* e = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
+            for (int co = 0; co < 3; ++co) {
+              const float4 v = *reinterpret_cast<const float4*>(part + co * plane);
+              const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int co = 0; co < 3; ++co) o[co] += e[co];
+              for (int e = 0; e < 4; ++e)
+                if (x + e >= lo && x + e <= hi) o[e][co] += vv[e];
+            }
+          } else {
+#pragma unroll
+            for (int co = 0; co < 3; ++co) o[0][co] += part[co * plane];
+          }
         }
+    for (int e = 0; e < n; ++e) {
+      const int xe = x + e;
+      float oo[3] = {o[e][0], o[e][1], o[e][2]};
+      if (y <= 1 || xe <= 1 || y >= H - 2 || xe >= W - 2) {
+        // image-border sources p = (y + ky - 1, xe + kx - 1), tap (ky, kx)
+        for (int ky = 0; ky < 3; ++ky)
+          for (int kx = 0; kx < 3; ++kx) {
+            const int py = y + ky - 1, px = xe + kx - 1;
+            if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
+            const float* ev = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
+#pragma unroll
+            for (int co = 0; co < 3; ++co) oo[co] += ev[co];
+          }
+      }
+      float alr, srcf[3];
+      uint8_t src8[3];
+      dec_inputs(tl, f, y, xe, &alr, srcf, src8);
+      dec_emit(tl, f, y, xe, oo, alr, srcf, src8);
     }
-    float alr, srcf[3];
-    uint8_t src8[3];
-    dec_inputs(a.tail, f, y, x, &alr, srcf, src8);
-    dec_emit(a.tail, f, y, x, o, alr, srcf, src8);
   }
   // flags mirror (host path): the last CTA to finish publishes the frames' flags
   const ConvTcArgs& t = a.tail;
@@ -781,7 +911,21 @@ void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s
     cudaFuncSetAttribute(dec_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
   const dim3 grid((a.W + TPX - 1) / TPX, ((a.H + TPY - 1) / TPY) * a.groups, a.frames);
-  launch_pdl(dec_fused_kernel, grid, dim3(THREADS), smem, s, tok4d, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;         // the G phase groups of a tile
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = a.groups;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, dec_fused_kernel, tok4d, a);
 #ifdef DR_TRACE
   if (dec_trace_store().size() < 4) {
     cudaStreamSynchronize(s);
@@ -789,6 +933,9 @@ void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s
     std::vector<unsigned long long> h((size_t)n * 16);
     cudaMemcpyFromSymbol(h.data(), g_dec_trace, h.size() * sizeof(unsigned long long));
     dec_trace_store().push_back(std::move(h));
+    std::vector<unsigned long long> tl(5 * 64);
+    cudaMemcpyFromSymbol(tl.data(), g_dec_tl, tl.size() * sizeof(long long));
+    dec_trace_store().push_back(std::move(tl));
   }
 #endif
 }
@@ -799,9 +946,8 @@ void launch_dec_border(const DecArgs& a, cudaStream_t s) {
 }
 
 void launch_dec_fixup(const DecArgs& a, cudaStream_t s) {
-  const long n_pix = a.groups > 1 ? (long)a.H * a.W
-                                  : (long)a.n_fix_rows * a.W + (long)(a.H - a.n_fix_rows) * a.n_fix_cols;
-  const int blocks = (int)std::max<long>(1, std::min<long>((n_pix + 255) / 256, 1024));
+  const long n_items = (long)a.n_fix_rows * (a.W / 4) + (long)(a.H - a.n_fix_rows) * a.n_fix_cols;
+  const int blocks = (int)std::max<long>(1, std::min<long>((n_items + 255) / 256, 1024));
   launch_pdl(dec_fixup_kernel, dim3(blocks, a.frames), dim3(256), 0, s, a);
 }
 

@@ -357,14 +357,20 @@ struct dr_engine {
   uint8_t* timg = nullptr;           // tcgen05 token-GEMM images: We + be, then per block
   double* feather_w = nullptr;
   uint8_t* wtc = nullptr;            // tcgen05 conv weight images: decode.0 then decode.2
-  // fused decoder (dec_fused.cu): 144 taps of the combined 12x12 Vec2Patch o decode.0
-  // kernel, combined bias, border-correction tables; DR_DEC_FUSED=0 selects the unfused
-  // Vec2Patch -> decode.0 (+ E planes) -> decode.2 gather sequence (A/B only)
-  int dec_fused = 1;
+  // Decoder: the fused tile pass (dec_fused.cu: 144 taps of the combined 12x12 Vec2Patch o
+  // decode.0 kernel, combined bias, border-correction tables) for batches that fill the
+  // GPU with tiles, else Vec2Patch -> decode.0 (+ decode.2's E planes) -> decode.2 gather,
+  // whose finer grids suit one frame.  DR_DEC_FUSED=1 / 0 forces one (tests, A/B).
+  int dec_force = -1;
+  static constexpr int kUnfusedMaxFrames = 2;        // auto: unfused up to this batch
+  bool use_fused(int frames) const {
+    return dec_force >= 0 ? dec_force != 0 : frames > kUnfusedMaxFrames;
+  }
   uint8_t* wcomb = nullptr;
   float* bcomb = nullptr;
   float* dk = nullptr;
   float* part = nullptr;             // dec_fused partial sums (workspace)
+  int unf_frames = 0;                // frames the unfused decoder's buffers hold
   float* bord_d0 = nullptr;          // border pixels' combined pre-activation (workspace)
   float* bord_e = nullptr;           // border pixels' decode.2 taps (workspace)
   float* w2f = nullptr;              // decode.2 weights fp32 [27][64]
@@ -517,13 +523,14 @@ struct dr_engine {
     const size_t o_q = take(tok * C * 2), o_k = take(tok * C * 2), o_v = take(tok * C * 2);
     const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
     const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
-    const size_t o_ras = take(dec_fused ? 0 : px * C * 2), o_ep = take(dec_fused ? 0 : px * 27 * 2);
-    size_t part_frames = 0;            // max over batches <= frames of groups x frames
-    for (int b = 1; b <= frames; ++b)
-      part_frames = std::max(part_frames, (size_t)dec_groups(b, H, W, sm_count()) * b);
-    const size_t o_part = take(dec_fused ? part_frames * 4 * frame_px() * 3 * 4 : 0);
+    // unfused decoder buffers for the batches it runs (<= unf frames), fused ones likewise
+    const int unf = use_fused(1) ? 0 : (dec_force == 0 ? frames : std::min(frames, kUnfusedMaxFrames));
+    const bool fus = use_fused(frames);
+    const size_t upx = frame_px() * unf;
+    const size_t o_ras = take(upx * C * 2), o_ep = take(upx * 27 * 2);
+    const size_t o_part = take(fus ? (size_t)frames * 4 * frame_px() * 3 * 4 : 0);
     const size_t nbp = (size_t)frames * dec_border_pixels(H, W);
-    const size_t o_bd0 = take(dec_fused ? nbp * 64 * 4 : 0), o_be = take(dec_fused ? nbp * 27 * 4 : 0);
+    const size_t o_bd0 = take(fus ? nbp * 64 * 4 : 0), o_be = take(fus ? nbp * 27 * 4 : 0);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
     const size_t o_fl = take((size_t)frames * 4);
     CUDA_TRY(cudaMalloc(&ws, off));
@@ -536,15 +543,23 @@ struct dr_engine {
     attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
     raster = (__half*)(b + o_ras); eplanes = (__half*)(b + o_ep);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
-    part = dec_fused ? (float*)(b + o_part) : nullptr;
-    bord_d0 = dec_fused ? (float*)(b + o_bd0) : nullptr;
-    bord_e = dec_fused ? (float*)(b + o_be) : nullptr;
+    part = fus ? (float*)(b + o_part) : nullptr;
+    bord_d0 = fus ? (float*)(b + o_bd0) : nullptr;
+    bord_e = fus ? (float*)(b + o_be) : nullptr;
+    unf_frames = unf;
     cap = frames;
     CUDA_TRY(cudaMemset(tok16, 0, npad * C * 2));    // the grid padding stays zero
-    if (dec_fused) return make_token_map4(&map_tok4, tok16, frames, R + 2, Cc + 2);
-    int rc = make_nhwc_map(&map_raster, raster, frames, H, W, conv_tc_rows(64) + 2);
-    if (rc) return rc;
-    return make_token_map(&map_tok, tok16, frames, (R + 2) * (Cc + 2));
+    if (fus) {
+      const int rc = make_token_map4(&map_tok4, tok16, frames, R + 2, Cc + 2);
+      if (rc) return rc;
+    }
+    if (unf > 0) {
+      int rc = make_nhwc_map(&map_raster, raster, unf, H, W, conv_tc_rows(64) + 2);
+      if (rc) return rc;
+      rc = make_token_map(&map_tok, tok16, unf, (R + 2) * (Cc + 2));
+      if (rc) return rc;
+    }
+    return DR_OK;
   }
 
   // 4-D TMA view of the padded token grid [frames][rows][cols][64] for the fused decoder:
@@ -733,7 +748,7 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
   // Wcomb[co][ci][u][v] = sum_{dy,dx,c'} Wc[co][c'][dy][dx] Wv[ci][c'][u+dy][v+dx], u, v in
   // [-2, 9], 144 tap images [(u+2)*12 + (v+2)][k-chunk][co][8 ci] fp16; bcomb = bc + sum
   // Wc bv; and the border-correction tables (float64 accumulation).
-  if (const char* df = std::getenv("DR_DEC_FUSED")) e->dec_fused = std::atoi(df) != 0;
+  if (const char* df = std::getenv("DR_DEC_FUSED")) e->dec_force = std::atoi(df) != 0 ? 1 : 0;
   std::vector<uint16_t> combimg((size_t)144 * 64 * 64);
   std::vector<float> bcomb(64);
   std::vector<float> dkt(dec_border_table_floats(), 0.f);
@@ -1144,7 +1159,8 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     c2.spans = e->pack_spans; c2.packed = e->pack_out; c2.mirror_after_spans = 1;
     c2.rgb_flag = e->rgb_flag;
   }
-  if (e->dec_fused) {
+  const bool fused = e->use_fused(B);
+  if (fused) {
     // Vec2Patch o decode.0 o decode.2 + composite per tile, then the seams
     DecArgs da{};
     da.frames = B; da.H = e->H; da.W = e->W; da.R = e->R; da.Cc = e->Cc;
@@ -1159,6 +1175,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     DR_L(e->mark(9, s));
     DR_STOP_CHECK();
     DR_L(launch_dec_border(da, s));
+    DR_L(e->mark(11, s));
     DR_STOP_CHECK();
     DR_L(launch_dec_fixup(da, s));
     DR_L(e->mark(10, s));
@@ -1191,7 +1208,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
             (intptr_t)io->out_f32, (intptr_t)e->pack_spans, (intptr_t)e->pack_out,
             (intptr_t)e->flags_mirror, (intptr_t)e->rgb_ready, (intptr_t)e->rgb_flag,
             ent[0], ent[1], kv_computed,
-            en_fill, e->dec_fused};
+            en_fill, fused};
 #undef DR_L
 #undef DR_STOP_CHECK
   CUDA_TRY(cudaGetLastError());

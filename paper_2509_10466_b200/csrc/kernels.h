@@ -192,8 +192,8 @@ void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s);
 // padding there, the combined form the cropped canvas ring) are redone by dec_border from
 // the tile pass's pre-activations, and every pixel next to another tile (or within one
 // pixel of the image border) is finished by dec_fixup from per-tile partial sums; with
-// `groups` > 1 the 64 phases of a tile are split over that many CTAs and every pixel is
-// finished there.
+// `groups` > 1 the 64 phases of a tile are split over a cluster of that many CTAs, whose
+// accumulators are summed through distributed shared memory.
 constexpr int DEC_MAX_FIX = 128;
 struct DecArgs {
   int frames, H, W, R, Cc;
@@ -205,7 +205,7 @@ struct DecArgs {
   const float* b2;           // [3]
   const float* dk;           // border-correction tables (engine.cu, dec_border_table_floats)
   const __half* tok16;       // padded token grid [frames][R+2][Cc+2][64]
-  float* part;               // partial sums [groups * 4][frames][3][H][W]
+  float* part;               // seam partial sums, tile parity planes [4][frames][3][H][W]
   float* bd0;                // border pixels' combined pre-activation [frames][NB][64]
   float* be;                 // border pixels' decode.2 taps E [frames][NB][27]
   // rows / columns dec_fixup finishes (seams and the 2-pixel image border band), sorted

@@ -22,7 +22,8 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="C2")
     args = p.parse_args()
-    _lib.LIB_PATH = _lib.LIB_PATH.parent.parent / "_build_trace" / _lib.LIB_PATH.name
+    import os
+    _lib.LIB_PATH = _lib.LIB_PATH.parent.parent / os.environ.get("DEC_TRACE_BUILD", "_build_trace") / _lib.LIB_PATH.name
     import torch
 
     import bench
@@ -46,6 +47,14 @@ def main():
     print("  start            ", pct((t[:, 0] - t0) / 1e3))
     print("  main loop (us)   ", pct((t[:, 12] - t[:, 0]) / 1e3))
     print("  finish pass (us) ", pct((t[:, 13] - t[:, 12]) / 1e3))
+    print("   of which pixels", pct((t[:, 11] - t[:, 12]) / 1e3))
+    tl = (ctypes.c_ulonglong * 320)()
+    if fn(1, tl, 320) == 320:
+        v = np.frombuffer(tl, dtype=np.uint64).reshape(5, 64).astype(np.int64)
+        st = v[4, 0]
+        print("  CTA 0 timeline (us from start): phase: D committed / epi1 done / E committed / epi2 done")
+        for i in list(range(0, 8)) + list(range(8, 64, 8)):
+            print("    %2d: %7.2f %7.2f %7.2f %7.2f" % ((i,) + tuple((v[k, i] - st) / 1965.0 for k in range(4))))
     for s, n in NAMES.items():
         per_warp = 1 if s <= 5 else 8
         print(f"  {n:18s}", pct(us(t[:, s] / per_warp)))

@@ -152,3 +152,27 @@ def test_forced_128_rows_carried_memory_matches_oracle_and_small_tiles(monkeypat
         ref_slots = (ref_slots[1], ref["slot"][0])
         check_img(rb["out"].cpu().numpy(), ref["out"], f"128-row frame {t}")
         check_img(rb["out"].cpu().numpy(), rs["out"].cpu().numpy(), f"128 vs small {t}")
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_both_decoders_on_reference_golden_and_small_frames(monkeypatch, fused):
+    """The fused decoder (tile pass + border + seams) and the unfused sequence (Vec2Patch,
+    decode.0 with decode.2's taps, gather) are both product paths (chosen by batch size,
+    DR_DEC_FUSED forces one): each against the reference forward golden (64^2, B=2, all
+    four image borders inside one tile) and the oracle at 128^2 (seams)."""
+    monkeypatch.setenv("DR_DEC_FUSED", fused)
+    g = golden("forward_b64.npz")
+    cfg = cfg_from(g["cfg"])
+    w = perturb_1d(seed_parameters(cfg, int(g["weight_seed"])), int(g["perturb_seed"]))
+    eng = DsttEngine.from_arrays(cfg, w)
+    fill, _ = eng.model_forward(cuda(g["rgb"]), cuda(g["mask"]),
+                                (cuda(g["warm0"]), cuda(g["warm1"])))
+    check_img(fill.cpu().numpy(), g["out_warm"], f"decoder {fused} golden")
+    cfg = DsttConfig.baseline(128, mask_dilate=3, mask_feather_sigma=2.0)
+    eng = DsttEngine(cfg, seed=0)
+    imgs, masks = synth.frame_pool("C1", 2, size=128)
+    res = eng.run(cuda(imgs), cuda(masks), None, want_fill=True)
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    ref = O.inpaint_path(cfg, seed_parameters(cfg, 0), imgs, masks, (zero, zero))
+    check_img(res["fill"].cpu().numpy(), ref["fill"], f"decoder {fused} 128^2 fill")
+    check_img(res["out"].cpu().numpy(), ref["out"], f"decoder {fused} 128^2 composite")
