@@ -43,7 +43,6 @@ extern "C" {
 /* per-frame status bits written to dr_frame_io.flags */
 #define DR_FLAG_NONFINITE 1    /* network output not finite  -> EngineNumericError */
 #define DR_FLAG_UNREDACTED 2   /* u8 input nonzero inside m0 -> InputError         */
-#define DR_FLAG_UPLOAD_TIMEOUT 4 /* host path: rgb upload never signalled (200 ms)  */
 
 /* DsttConfig (inpaint/dstt.py:35-86) plus the mask-stage fields. */
 typedef struct dr_config {

@@ -342,7 +342,6 @@ DR_DEV void mirror_flags(const ConvTcArgs& a) {
         fm = reinterpret_cast<int*>(a.packed + ((n + 3) & ~(size_t)3));
       }
       for (int i = 0; i < a.frames; ++i) fm[i] = atomicOr(a.flags + i, 0);
-      if (a.rgb_flag) *a.rgb_flag = 0;
       *a.done = 0;
     }
   }
@@ -576,85 +575,8 @@ size_t conv_tc_weight_bytes(int n) { return (size_t)9 * 8 * n * 16; }
 
 int conv_tc_rows(int n) { return n == 64 ? 2 : 4; }   // decode.0 tiles: 2 output rows
 
-// decode.2's tap-expanded GEMM alone, for the combined Vec2Patch o decode.0 path where the
-// raster already holds LeakyReLU(decode.0): per 128-pixel row segment, TMA the 128 x 64 fp16
-// A tile (SWIZZLE_128B), E = A x W2^T (4 x tcgen05.mma 128x32x16) into 32 TMEM columns, and
-// the 27 E columns out as fp16 planes.  One tile per CTA; many CTAs per SM hide latency.
-struct __align__(1024) EOnlySmem {
-  uint8_t a[128 * 128];
-  uint8_t w2[32 * 128];
-  uint64_t full, mma;
-  uint32_t tmem_base;
-};
-__global__ void __launch_bounds__(128) e_only_kernel(const __grid_constant__ CUtensorMap d0_rows,
-                                                      const void* w2, __half* e_planes, int H, int W) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  EOnlySmem& sm = *reinterpret_cast<EOnlySmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                                ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int x0 = blockIdx.x * 128, y = blockIdx.y, f = blockIdx.z;
-  pdl_trigger();
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&sm.full, 1);
-    tc::mbar_init(&sm.mma, 1);
-    tc::fence_barrier_init();
-    tc::mbar_arrive_expect_tx(&sm.full, 32 * 128 + 128 * 128);
-    tc::bulk_load(sm.w2, w2, 32 * 128, &sm.full);        // constant: before the wait
-  }
-  __syncthreads();
-  pdl_wait();
-  if (threadIdx.x == 0) tc::tma_load_4d(sm.a, &d0_rows, &sm.full, 0, x0, y, f);
-  if (warp == 0) tc::tmem_alloc<32>(&sm.tmem_base);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tbase = sm.tmem_base;
-  if (warp == 0) {
-    tc::mbar_wait(&sm.full, 0);
-    tc::fence_after();
-    constexpr uint32_t idesc = tc::idesc_f16(128, 32);
-    const uint64_t ad = tc::sdesc_sw128(tc::smem_u32(sm.a), 0);
-    const uint64_t bd = tc::sdesc_sw128(tc::smem_u32(sm.w2), 0);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-      tc::mma_f16_warp(tbase, ad + (uint64_t)(2 * ks), bd + (uint64_t)(2 * ks), idesc, ks != 0);
-    tc::mma_commit_warp(&sm.mma);
-  }
-  tc::mbar_wait(&sm.mma, 0);
-  tc::fence_after();
-  uint32_t ev[32];
-  const uint32_t eaddr = tbase + ((uint32_t)(32 * warp) << 16);
-  tc::tmem_ld16(eaddr, ev);
-  tc::tmem_ld16(eaddr + 16, ev + 16);
-  tc::tmem_wait_ld();
-  const int x = x0 + 32 * warp + lane;
-  if (x < W) {
-    const size_t plane = (size_t)H * W;
-    __half* ep = e_planes + (size_t)f * 27 * plane + (size_t)y * W + x;
-#pragma unroll
-    for (int u = 0; u < 27; ++u) ep[(size_t)u * plane] = __float2half_rn(__uint_as_float(ev[u]));
-  }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<32>(tbase);
-}
-
-void launch_e_only(const CUtensorMap& d0_rows, const __half*, const void* w2, __half* e_planes,
-                   int frames, int H, int W, cudaStream_t s) {
-  static unsigned long long init = 0;
-  const int smem = (int)sizeof(EOnlySmem) + 1024;
-  once_per_device(init, [&] {
-    cudaFuncSetAttribute(e_only_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
-  launch_pdl(e_only_kernel, dim3((W + 127) / 128, H, frames), dim3(128), smem, s, d0_rows, w2,
-             e_planes, H, W);
-}
-
 void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s) {
-#ifndef DR_GATHER_PX
-#define DR_GATHER_PX 4
-#endif
-  constexpr int PX = DR_GATHER_PX, TPB = 256 / (PX / 2) > 256 ? 256 : 512 / PX;
+  constexpr int PX = 4, TPB = 128;               // 4 pixels per thread, vector loads / stores
   if (a.W % PX == 0) {
     dim3 grid((a.W / PX + TPB - 1) / TPB, a.H, a.frames);
     launch_pdl(dec2_gather_vec_kernel<PX, TPB>, grid, dim3(TPB), 0, s, a);

@@ -153,8 +153,8 @@ DR_DEV int border_index(int y, int x, int H, int W) {
 // e_full, 10 epi2 phase barrier; 14 SM id
 __device__ unsigned long long g_dec_trace[4096 * 16];
 // per-phase timeline of CTA 0 (clock64): [0] D MMAs committed, [1] epilogue 1 done (set 0/1),
-// [2] E MMAs committed, [3] epilogue 2 done; [4][0] kernel start
-__device__ long long g_dec_tl[5][64];
+// [2] E MMAs committed, [3] epilogue 2 done; [4][0] kernel start; [5] D MMAs begin
+__device__ long long g_dec_tl[6][64];
 #define DT_TL(k, i) do { if (DT_CTA == 0 && (i) < 64) g_dec_tl[k][i] = clock64(); } while (0)
 #define DT_CTA (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z))
 #define DT_SET(slot, v) do { if (DT_CTA < 4096) g_dec_trace[DT_CTA * 16 + (slot)] = (v); } while (0)
@@ -347,6 +347,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       const int b = i % NB4;
       if (i >= NB4) DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
       tc::fence_after();
+      if (lane == 0) DT_TL(5, i);
       for (int t = 0; t < n; ++t, ++kk) {
         const int sl = kk % NSLOT;
         DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(kk / NSLOT) & 1u));
@@ -528,7 +529,34 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   // interior pixels in runs of 4 along x (vector loads / stores), two runs per thread per
   // pass with the inputs loaded up front; runs holding a dec_fixup pixel go pixel by pixel
   const int nq = xe >> 2;                                  // runs per row (xe % 8 == 0)
+  // Runs without any dec_fixup pixel form a rectangle [ra, rb) x [ca, cb) of the block
+  // (fixup rows / columns only occur at its edges); they come first so that warps do not
+  // diverge between the vector path and the pixel-by-pixel one.
+  const int ra = min(rend, max(rbeg, y0 == 0 ? 2 : (nb_up ? 1 : 0)));
+  const int rb = max(ra, min(rend, nb_dn ? TPY - 1 : H - 2 - y0));
+  const int ca = (nb_l || x0 == 0) ? 1 : 0, cb = max(ca, (nb_r || x0 + xe >= W) ? nq - 1 : nq);
+  const int n_clean = (rb - ra) * (cb - ca);
+  const int n_top = (ra - rbeg) * nq, n_mid = (rb - ra) * (ca + nq - cb);
   const int nrun = max(0, rend - rbeg) * nq;
+  auto run_at = [&](int id, int* yl, int* xl) {
+    if (id < n_clean) {
+      *yl = ra + id / (cb - ca);
+      *xl = 4 * (ca + id % (cb - ca));
+      return;
+    }
+    id -= n_clean;
+    if (id < n_top) { *yl = rbeg + id / nq; *xl = 4 * (id % nq); return; }
+    id -= n_top;
+    if (id < n_mid) {
+      const int w = ca + nq - cb, c = id % w;
+      *yl = ra + id / w;
+      *xl = 4 * (c < ca ? c : cb + (c - ca));
+      return;
+    }
+    id -= n_mid;
+    *yl = rb + id / nq;
+    *xl = 4 * (id % nq);
+  };
   const ConvTcArgs& t = a.tail;
   for (int idx = threadIdx.x; idx < nrun; idx += 2 * THREADS) {
     int yy[2], xx[2];
@@ -540,22 +568,15 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     for (int j = 0; j < 2; ++j) {
       const int id = idx + j * THREADS;
       act[j] = id < nrun;
-      const int yl = act[j] ? rbeg + id / nq : 0, xl = act[j] ? 4 * (id % nq) : 0;
+      int yl = 0, xl = 0;
+      if (act[j]) run_at(id, &yl, &xl);
       yy[j] = y0 + yl;
       xx[j] = x0 + xl;
       const bool f0 = is_fix(yl, xl, yy[j], xx[j]), f3 = is_fix(yl, xl + 3, yy[j], xx[j] + 3);
       // is_fix is monotone inside a run except at its ends: only x = tile / image edges
       need[j] = act[j] && !(f0 && f3 && is_fix(yl, xl + 1, yy[j], xx[j] + 1) && is_fix(yl, xl + 2, yy[j], xx[j] + 2));
       fast[j] = act[j] && !f0 && !f3 && !t.packed;
-#ifdef DR_DEC_NOLOAD
-      if (need[j]) {                                      // diagnostic: no input loads
-        al[j] = make_float4(0.5f, 0.5f, 0.5f, 0.5f);
-        for (int ch = 0; ch < 3; ++ch) { rf[j][ch] = make_float4(0.f, 0.f, 0.f, 0.f); r8[j][ch] = 0; }
-      }
-      if (false) {
-#else
       if (need[j]) {
-#endif
         const size_t pix = (size_t)yy[j] * W + xx[j];
         al[j] = t.alpha ? __ldg(reinterpret_cast<const float4*>(t.alpha + (size_t)f * plane + pix))
                         : make_float4(1.f, 1.f, 1.f, 1.f);
@@ -861,7 +882,6 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
           fm = reinterpret_cast<int*>(t.packed + ((n + 3) & ~(size_t)3));
         }
         for (int k = 0; k < t.frames; ++k) fm[k] = atomicOr(t.flags + k, 0);
-        if (t.rgb_flag) *t.rgb_flag = 0;
         *t.done = 0;
       }
     }
@@ -933,7 +953,7 @@ void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s
     std::vector<unsigned long long> h((size_t)n * 16);
     cudaMemcpyFromSymbol(h.data(), g_dec_trace, h.size() * sizeof(unsigned long long));
     dec_trace_store().push_back(std::move(h));
-    std::vector<unsigned long long> tl(5 * 64);
+    std::vector<unsigned long long> tl(6 * 64);
     cudaMemcpyFromSymbol(tl.data(), g_dec_tl, tl.size() * sizeof(long long));
     dec_trace_store().push_back(std::move(tl));
   }

@@ -409,9 +409,6 @@ struct dr_engine {
   // K/V cache decisions, so each distinct signature is captured once and replayed
   bool dry = false;                  // dr_forward: host-side decisions only, no launches
   bool capturing = false;            // dr_forward under host-path graph capture
-  unsigned* rgb_flag = nullptr;      // host path: set by the copy stream after the rgb upload
-  int use_rgb_flag = 0;              // DR_RGB_FLAG=1: pack spins on a device flag (launch first)
-  int rgb_chunks = 1;                // DR_RGB_CHUNKS: host-path rgb staging/upload pieces
   std::vector<intptr_t> sig;         // dr_forward: what its launches depended on
   struct HostGraph { std::vector<intptr_t> key; cudaGraphExec_t exec; };
   std::vector<HostGraph> hgraphs;
@@ -868,9 +865,6 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
     const int r = std::atoi(tr);
     e->tok_rows = (r == 32 || r == 64 || r == 128) ? r : 0;
   }
-  if (const char* rf = std::getenv("DR_RGB_FLAG")) e->use_rgb_flag = std::atoi(rf);
-  if (const char* rcn = std::getenv("DR_RGB_CHUNKS"))
-    e->rgb_chunks = std::min(8, std::max(1, std::atoi(rcn)));
 
   auto cleanup = [&](int code) { dr_destroy(e); return code; };
   if (cudaMalloc(&e->fparams, fp.size() * sizeof(float)) != cudaSuccess ||
@@ -1009,7 +1003,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   float* alpha = io->alpha ? io->alpha : e->alpha;
   fill_mask_args(e, m, B, io->mask_m0, io->dilated, alpha, tv, flags);
   m.rgb_f32 = io->rgb_f32; m.rgb_u8 = io->rgb_u8; m.xin = e->xin;
-  const bool split = (e->rgb_ready != nullptr || e->rgb_flag != nullptr) && io->rgb_u8 != nullptr;
+  const bool split = e->rgb_ready != nullptr && io->rgb_u8 != nullptr;
   if (split) {
     // host path, split uploads: the stage runs on the mask alone while the rgb is still in
     // flight on the copy stream; the input pack follows once it has landed
@@ -1018,11 +1012,9 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     if (!mo.m1) mo.m1 = e->m1;
     DR_STOP_CHECK();
     DR_L(launch_mask_stage(mo, s));
-    if (!e->rgb_flag)
-      DR_L(CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, e->capturing ? cudaEventWaitExternal : 0)));
+    DR_L(CUDA_TRY(cudaStreamWaitEvent(s, e->rgb_ready, e->capturing ? cudaEventWaitExternal : 0)));
     MaskArgs pk = m;
     pk.m1 = mo.m1;
-    pk.rgb_flag = e->rgb_flag;
     DR_L(launch_pack_input(pk, s));
   } else {
     DR_STOP_CHECK();
@@ -1157,7 +1149,6 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   c2.flags_mirror = e->flags_mirror; c2.done = e->d_done;
   if (B == 1 && e->pack_spans) {
     c2.spans = e->pack_spans; c2.packed = e->pack_out; c2.mirror_after_spans = 1;
-    c2.rgb_flag = e->rgb_flag;
   }
   const bool fused = e->use_fused(B);
   if (fused) {
@@ -1206,7 +1197,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
             (intptr_t)io->slot_batched, (intptr_t)flags, (intptr_t)tv, (intptr_t)alpha,
             (intptr_t)io->dilated, (intptr_t)io->fill, (intptr_t)io->out_u8,
             (intptr_t)io->out_f32, (intptr_t)e->pack_spans, (intptr_t)e->pack_out,
-            (intptr_t)e->flags_mirror, (intptr_t)e->rgb_ready, (intptr_t)e->rgb_flag,
+            (intptr_t)e->flags_mirror, (intptr_t)e->rgb_ready,
             ent[0], ent[1], kv_computed,
             en_fill, fused};
 #undef DR_L
@@ -1321,8 +1312,8 @@ int host_inpaint(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
     CUDA_TRY(cudaMalloc(&e->h_rgb, in_bytes));
     e->h_m0 = e->h_rgb + px * 3;
     CUDA_TRY(cudaMalloc(&e->h_out, out_cap));
-    CUDA_TRY(cudaMalloc(&e->d_done, 2 * sizeof(unsigned)));      // [counter, rgb flag]
-    CUDA_TRY(cudaMemset(e->d_done, 0, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaMalloc(&e->d_done, sizeof(unsigned)));          // finished-CTA counter
+    CUDA_TRY(cudaMemset(e->d_done, 0, sizeof(unsigned)));
     CUDA_TRY(cudaMallocHost(&e->pin, in_bytes + out_cap));
     int rc = dr_reset_memory(e);
     if (rc) return rc;
@@ -1398,39 +1389,23 @@ int host_inpaint(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
   struct Restore {
     dr_engine* e;
     ~Restore() {
-      e->pack_spans = nullptr; e->pack_out = nullptr; e->rgb_ready = nullptr; e->rgb_flag = nullptr;
+      e->pack_spans = nullptr; e->pack_out = nullptr; e->rgb_ready = nullptr;
       e->dry = false; e->capturing = false;
     }
   } restore{e};
-  // uploads: mask + span table on s first, then the rgb on the copy stream (in chunks, each
-  // sent as soon as it is staged).  The mask stage runs while the rgb crosses PCIe.  Flag
-  // mode (DR_RGB_FLAG=1): the launch sequence is enqueued right after the mask upload, before
-  // the rgb is even staged, and the input pack spins on a device word the copy stream sets
-  // after the rgb upload (the gather's last CTA re-arms it); event mode: launched after the
-  // staging, the pack joins the rgb event.
+  // uploads: mask + span table on s first, then the rgb on the copy stream; the mask stage
+  // runs while the rgb crosses PCIe and the input pack joins the rgb event.
   const bool graphed = e->host_graph && !e->profiling && e->stop_after < 0;
-  const bool flag_mode = e->use_rgb_flag != 0;
-  if (flag_mode) { e->rgb_flag = e->d_done + 1; e->rgb_ready = nullptr; }
   int rc = DR_OK;
-  auto stage_rgb = [&]() -> int {
-    for (int c = 0; c < e->rgb_chunks; ++c) {
-      const size_t b0 = (px * 3 * c / e->rgb_chunks) & ~(size_t)63;
-      const size_t b1 = c + 1 == e->rgb_chunks ? px * 3 : (px * 3 * (c + 1) / e->rgb_chunks) & ~(size_t)63;
-      par_memcpy(p_rgb + b0, rgb_hwc + b0, b1 - b0, CP_NT);
-      CUDA_TRY(cudaMemcpyAsync(e->h_rgb + b0, p_rgb + b0, b1 - b0, cudaMemcpyHostToDevice,
-                               e->copy_stream));
-    }
-    if (flag_mode) CUDA_TRY(cudaMemsetAsync(e->rgb_flag, 1, sizeof(unsigned), e->copy_stream));
-    else CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
-    return DR_OK;
-  };
   if (tr.on) cudaEventRecord(tr.ev[0], s);
   par_memcpy(p_m0, mask_hw, px, CP_NT);
   CUDA_TRY(cudaMemcpyAsync(e->h_m0, p_m0, in_bytes - px * 3, cudaMemcpyHostToDevice, s));
   // the copy stream follows s up to here (never past the launches: the pack waits on it)
   CUDA_TRY(cudaEventRecord(e->fork_ev, s));
   CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->fork_ev, 0));
-  if (!flag_mode && (rc = stage_rgb())) return rc;
+  par_memcpy(p_rgb, rgb_hwc, px * 3, CP_NT);
+  CUDA_TRY(cudaMemcpyAsync(e->h_rgb, p_rgb, px * 3, cudaMemcpyHostToDevice, e->copy_stream));
+  CUDA_TRY(cudaEventRecord(e->rgb_event, e->copy_stream));
   if (tr.on) tt[1] = now_us();
   if (!graphed) {
     if (tr.on) cudaEventRecord(tr.ev[1], s);
@@ -1476,7 +1451,6 @@ int host_inpaint(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
     }
     CUDA_TRY(cudaGraphLaunch(exec, s));
   }
-  if (flag_mode && (rc = stage_rgb())) return rc;
   if (tr.on) {
     cudaEventRecord(tr.ev[2], s);
     tt[2] = now_us();
@@ -1490,11 +1464,6 @@ int host_inpaint(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask_hw,
   if (tr.on) tt[4] = now_us();
   int fl;
   std::memcpy(&fl, p_out + mirror, sizeof(int));
-  if (fl & DR_FLAG_UPLOAD_TIMEOUT) {
-    CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
-    CUDA_TRY(cudaMemset(e->d_done + 1, 0, sizeof(unsigned)));      // re-arm
-    return fail(DR_ERR_CUDA, "rgb upload was not signalled within 200 ms");
-  }
   if (fl & DR_FLAG_UNREDACTED)
     return fail(DR_ERR_INPUT, "input is not redacted: nonzero pixels inside mask");
   if (fl & DR_FLAG_NONFINITE) return fail(DR_ERR_NUMERIC, "model produced non-finite output");

@@ -96,10 +96,6 @@ struct MaskArgs {
   uint8_t* token_valid;      // [frames][T] out
   __half* xin;               // [frames][T][4*p*p] out (optional)
   int* flags;                // [frames] out: bit1 = input not redacted inside m0
-  // input pack (host path): spin until the copy stream sets this word after the rgb upload
-  // (so the launch sequence can be enqueued before the rgb is even staged); bounded wait,
-  // bit2 of flags on timeout
-  unsigned* rgb_flag;
 };
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s);
 // xin + redaction check alone, from u8 rgb, m0 and the stage's m1 bytes
@@ -137,7 +133,6 @@ struct ConvTcArgs {
   // align4(spans[H-1].z + 3 * (spans[H-1].y - spans[H-1].x)) (fixed kernel arguments, so
   // the host path's launch sequence can be replayed from a CUDA graph)
   int mirror_after_spans;
-  unsigned* rgb_flag;        // host path: re-armed (zeroed) by the last CTA
   // decode.2 gather (optional, one frame): also write the u8 composite of the pixels in
   // row y's span [spans[y].x, spans[y].y) to packed + spans[y].z + 3 * (x - x0)
   const int4* spans;
@@ -157,29 +152,9 @@ struct V2pArgs {
   const void* w;
   const float* bias;
   __half* raster;            // [frames][H][W][64]
-  // combined mode (Vec2Patch o decode.0, see v2p_tc.cu): w = 144 taps of the 12x12
-  // combined kernel, bias = combined bias, output = LeakyReLU(decode.0 pre-activation);
-  // delta = border corrections [frames][2W + 2(H-2)][64] (border_corrections)
-  int comb;
-  const float* delta;
 };
 size_t v2p_tc_weight_bytes();
 void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s);
-// Border corrections of the combined Vec2Patch o decode.0: the canvas ring outside the
-// image (Vec2Patch output incl. bias) and, per border pixel, the decode.0 taps that read it
-struct BorderArgs {
-  int frames, H, W, R, Cc;
-  const __half* tok16;       // padded token grid (as Vec2Patch reads it)
-  const float* wv;           // Vec2Patch weight fp32 [ky][kx][ci][c']
-  const float* bv;           // Vec2Patch bias [c']
-  const float* wc;           // decode.0 weight fp32 [dy][dx][c'][co]
-  float* ring;               // [frames][2(W+2) + 2H][64]
-  float* delta;              // [frames][2W + 2(H-2)][64]
-};
-void launch_border_corrections(const BorderArgs& a, cudaStream_t s);
-// decode.2's tap-expanded GEMM alone over an activated d0 raster: E planes (fp16)
-void launch_e_only(const CUtensorMap& d0_rows, const __half* dummy, const void* w2,
-                   __half* e_planes, int frames, int H, int W, cudaStream_t s);
 void launch_conv3x3_tc(int n, const CUtensorMap& tin, const ConvTcArgs& a, cudaStream_t s);
 // decode.2 gather + tail over the E planes the fused decode.0 wrote (conv_tc.cu)
 void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s);

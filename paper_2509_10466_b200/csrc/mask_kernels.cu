@@ -445,25 +445,6 @@ __global__ void __launch_bounds__(256) pack_input_kernel(MaskArgs a) {
   const long gtok = (long)blockIdx.x * 8 + (threadIdx.x >> 5);
   pdl_trigger();
   pdl_wait();
-  if (a.rgb_flag) {
-    if (threadIdx.x == 0) {
-      unsigned long long t0, t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      for (;;) {
-        unsigned v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.rgb_flag) : "memory");
-        if (v) break;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 200000000ull) {                  // 200 ms: report, do not hang
-          if (blockIdx.x == 0 && a.flags)
-            for (int i = 0; i < a.frames; ++i) atomicOr(a.flags + i, 4);
-          break;
-        }
-        __nanosleep(100);
-      }
-    }
-    __syncthreads();
-  }
   if (gtok >= (long)a.frames * T) return;
   const int f = (int)(gtok / T), tok = (int)(gtok - (long)f * T);
   const int i = tok / Cc, j = tok - i * Cc;

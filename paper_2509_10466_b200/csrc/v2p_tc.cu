@@ -65,34 +65,6 @@ DR_DEV int phase_taps(int py, int px, int PC, int* img, int* off) {
   return n;
 }
 
-// Combined mode (Vec2Patch o decode.0): raster pixel (8 i0 + py, 8 j0 + px) of token (i0, j0)
-// = sum over tokens (i0 + di, j0 + dj) of Wcomb[py - 8 di][px - 8 dj], kernel index in
-// [-2, 9]: di = 0 always, di = -1 if py <= 1 (index py + 8), di = +1 if py >= 6 (py - 8).
-// Image index (u + 2) * 12 + (v + 2); window base = run start - (PC + 1), so token offset
-// (di, dj) is window row PC + 1 + di * PC + dj.
-DR_DEV int phase_taps12(int py, int px, int PC, int* img, int* off) {
-  int du[2], uu[2], nu = 0, dv[2], vv[2], nv = 0;
-  du[nu] = 0; uu[nu++] = py;
-  if (py <= 1) { du[nu] = -1; uu[nu++] = py + 8; }
-  if (py >= 6) { du[nu] = 1; uu[nu++] = py - 8; }
-  dv[nv] = 0; vv[nv++] = px;
-  if (px <= 1) { dv[nv] = -1; vv[nv++] = px + 8; }
-  if (px >= 6) { dv[nv] = 1; vv[nv++] = px - 8; }
-  int n = 0;
-  for (int a = 0; a < nu; ++a)
-    for (int b = 0; b < nv; ++b) {
-      img[n] = (uu[a] + 2) * 12 + (vv[b] + 2);
-      off[n++] = PC + 1 + du[a] * PC + dv[b];
-    }
-  return n;
-}
-template <bool COMB>
-DR_DEV int taps_of(int py, int px, int PC, int* img, int* off) {
-  if constexpr (COMB) return phase_taps12(py, px, PC, img, off);
-  else return phase_taps(py, px, PC, img, off);
-}
-
-template <bool COMB>
 __global__ void __launch_bounds__(THREADS, 2)
 v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -102,7 +74,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
   const int P0 = blockIdx.x * M, py = blockIdx.y, f = blockIdx.z;
   const int PC = a.Cc + 2;                              // padded row length
   const int NP = (a.R + 2) * PC;
-  const int win_rows = COMB ? M + 2 * PC + 2 : M + PC + 1;
+  const int win_rows = M + PC + 1;
   const int n_chunks = (win_rows + M - 1) / M;
 
   if (threadIdx.x == 0) VT(0);
@@ -121,7 +93,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
     int k = 0;
     for (int px = 0; px < 8 && k < NSLOT; ++px) {
       int img[4], off[4];
-      const int n = taps_of<COMB>(py, px, PC, img, off);
+      const int n = phase_taps(py, px, PC, img, off);
       for (int t = 0; t < n && k < NSLOT; ++t, ++k) {
         tc::mbar_arrive_expect_tx(&sm.w_full[k], TAP_BYTES);
         tc::bulk_load(sm.w[k], reinterpret_cast<const uint8_t*>(a.w) + (size_t)img[t] * TAP_BYTES,
@@ -145,7 +117,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       int k = 0;                                       // tap ring, taps NSLOT.. of the CTA
       for (int px = 0; px < 8; ++px) {
         int img[4], off[4];
-        const int n = taps_of<COMB>(py, px, PC, img, off);
+        const int n = phase_taps(py, px, PC, img, off);
         for (int t = 0; t < n; ++t, ++k) {
           if (k < NSLOT) continue;                     // issued in the prologue
           const int sl = k % NSLOT;
@@ -172,7 +144,7 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
         if (px >= NBUF) tc::mbar_wait(&sm.tmem_empty[buf], 0);   // epilogue drained px-4
         const uint32_t d = tbase + (uint32_t)(buf * 64);
         int img[4], off[4];
-        const int n = taps_of<COMB>(py, px, PC, img, off);
+        const int n = phase_taps(py, px, PC, img, off);
         for (int t = 0; t < n; ++t) {
           const int sl = (k + t) % NSLOT;
           tc::mbar_wait(&sm.w_full[sl], (uint32_t)((k + t) / NSLOT) & 1u);
@@ -198,16 +170,10 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
     for (int it = 0; it < 8; ++it) {
       const int Pp = P0 + 32 * q + 4 * it + (lane >> 3);
       const int ip = Pp / PC, jp = Pp - ip * PC;
-      if constexpr (COMB) {                              // raster = token phase grid
-        const bool ok = Pp < NP && ip >= 1 && ip <= a.R && jp >= 1 && jp <= a.Cc;
-        ys[it] = ok ? 8 * (ip - 1) + py : -1;
-        xb[it] = 8 * (jp - 1);
-      } else {                                           // raster = canvas - 1
-        const int yp = 8 * (ip - 1) + py - 1;
-        const bool ok = Pp < NP && yp >= 0 && yp < a.H && jp >= 1;
-        ys[it] = ok ? yp : -1;
-        xb[it] = 8 * (jp - 1) - 1;
-      }
+      const int yp = 8 * (ip - 1) + py - 1;
+      const bool ok = Pp < NP && yp >= 0 && yp < a.H && jp >= 1;
+      ys[it] = ok ? yp : -1;
+      xb[it] = 8 * (jp - 1) - 1;
     }
     // bias via shared memory (broadcast reads): 64 registers back for the epilogue
     if (warp == 2) {
@@ -232,43 +198,13 @@ v2p_tc_kernel(const __grid_constant__ CUtensorMap tok, V2pArgs a) {
       // pixel slot p at p*128 + ((c ^ (p & 7)) << 4)), then 8 lanes per pixel write its
       // 128 B: each store instruction covers 4 whole lines instead of 32 half-sectors
       uint8_t* st = sm.stage[q];
-      if constexpr (COMB) {
-        // this lane's TMEM row = run position P0 + 32q + lane -> raster pixel; border pixels
-        // subtract the decode.0 taps that read outside the image (zero padding)
-        const int Pp = P0 + 32 * q + lane;
-        const int ip = Pp / PC, jp = Pp - ip * PC;
-        const int y = 8 * (ip - 1) + py, x = 8 * (jp - 1) + px;
-        int b = -1;
-        if (Pp < NP && ip >= 1 && ip <= a.R && jp >= 1 && jp <= a.Cc) {
-          if (y == 0) b = x;
-          else if (y == a.H - 1) b = a.W + x;
-          else if (x == 0) b = 2 * a.W + (y - 1);
-          else if (x == a.W - 1) b = 2 * a.W + (a.H - 2) + (y - 1);
-        }
-        if (b >= 0) {
-          const float4* dl = reinterpret_cast<const float4*>(
-              a.delta + ((size_t)f * (2 * a.W + 2 * (a.H - 2)) + b) * 64);
-#pragma unroll
-          for (int c4 = 0; c4 < 16; ++c4) {
-            const float4 d = __ldg(dl + c4);
-            v[4 * c4] = __float_as_uint(__uint_as_float(v[4 * c4]) - d.x);
-            v[4 * c4 + 1] = __float_as_uint(__uint_as_float(v[4 * c4 + 1]) - d.y);
-            v[4 * c4 + 2] = __float_as_uint(__uint_as_float(v[4 * c4 + 2]) - d.z);
-            v[4 * c4 + 3] = __float_as_uint(__uint_as_float(v[4 * c4 + 3]) - d.w);
-          }
-        }
-      }
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = c8 * 8 + 2 * e;
-          float u0 = __uint_as_float(v[c]) + bias[c], u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
-          if constexpr (COMB) {                          // decode.0's LeakyReLU(0.2)
-            u0 = u0 >= 0.f ? u0 : 0.2f * u0;
-            u1 = u1 >= 0.f ? u1 : 0.2f * u1;
-          }
+          const float u0 = __uint_as_float(v[c]) + bias[c], u1 = __uint_as_float(v[c + 1]) + bias[c + 1];
           pk[e] = pack_half2(u0, u1);
         }
         *reinterpret_cast<uint4*>(st + lane * 128 + ((c8 ^ (lane & 7)) << 4)) =
@@ -302,90 +238,11 @@ void launch_v2p_tc(const CUtensorMap& tok, const V2pArgs& a, cudaStream_t s) {
   static unsigned long long init = 0;
   const int smem = (int)sizeof(V2pSmem) + 1024;
   once_per_device(init, [&] {
-    cudaFuncSetAttribute(v2p_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(v2p_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(v2p_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
   const int NP = (a.R + 2) * (a.Cc + 2);
   dim3 grid((NP + M - 1) / M, 8, a.frames);
-  if (a.comb) launch_pdl(v2p_tc_kernel<true>, grid, dim3(THREADS), smem, s, tok, a);
-  else launch_pdl(v2p_tc_kernel<false>, grid, dim3(THREADS), smem, s, tok, a);
-}
-
-// ---------------------------------------------------------------- border corrections
-// ring position r (raster coordinates outside the image): top row y = -1, x = r - 1 (W + 2);
-// bottom y = H; left x = -1, y in [0, H); right x = W.  Value = Vec2Patch canvas at
-// (y + 1, x + 1) incl. bias, from the fp16 tokens Vec2Patch reads.  256 threads per
-// position: 64 output channels x 4 input-channel quarters (unrolled loads, smem reduction).
-__global__ void __launch_bounds__(256) ring_kernel(BorderArgs a) {
-  __shared__ float part[4][64];
-  const int r = blockIdx.x, f = blockIdx.y, cp = threadIdx.x & 63, qg = threadIdx.x >> 6;
-  const int NR = 2 * (a.W + 2) + 2 * a.H;
-  pdl_trigger();
-  pdl_wait();
-  int y, x;
-  if (r < a.W + 2) { y = -1; x = r - 1; }
-  else if (r < 2 * (a.W + 2)) { y = a.H; x = r - (a.W + 2) - 1; }
-  else if (r < 2 * (a.W + 2) + a.H) { x = -1; y = r - 2 * (a.W + 2); }
-  else { x = a.W; y = r - 2 * (a.W + 2) - a.H; }
-  const int Y = y + 1, X = x + 1, PC = a.Cc + 2;
-  float acc = 0.f;
-  for (int i = max(0, (Y - 9 + 7) / 8); i <= min(a.R - 1, Y / 8); ++i) {
-    const int ky = Y - 8 * i;
-    if (ky < 0 || ky > 9) continue;
-    for (int j = max(0, (X - 9 + 7) / 8); j <= min(a.Cc - 1, X / 8); ++j) {
-      const int kx = X - 8 * j;
-      if (kx < 0 || kx > 9) continue;
-      const __half* t = a.tok16 + ((size_t)f * (a.R + 2) * PC + (size_t)(i + 1) * PC + (j + 1)) * 64 + 16 * qg;
-      const float* w = a.wv + ((size_t)(ky * 10 + kx) * 64 + 16 * qg) * 64 + cp;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc = fmaf(__half2float(t[c]), __ldg(w + (size_t)c * 64), acc);
-    }
-  }
-  part[qg][cp] = acc;
-  __syncthreads();
-  if (qg == 0)
-    a.ring[((size_t)f * NR + r) * 64 + cp] =
-        a.bv[cp] + ((part[0][cp] + part[1][cp]) + (part[2][cp] + part[3][cp]));
-}
-
-// border pixel b: top y = 0 (x = b), bottom y = H - 1, left x = 0 (y in [1, H-1)), right;
-// 64 output channels x 4 quarters of the 64 canvas channels per out-of-image neighbour
-__global__ void __launch_bounds__(256) delta_kernel(BorderArgs a) {
-  __shared__ float part[4][64];
-  const int b = blockIdx.x, f = blockIdx.y, co = threadIdx.x & 63, qg = threadIdx.x >> 6;
-  const int NB = 2 * a.W + 2 * (a.H - 2), NR = 2 * (a.W + 2) + 2 * a.H;
-  pdl_trigger();
-  pdl_wait();
-  int y, x;
-  if (b < a.W) { y = 0; x = b; }
-  else if (b < 2 * a.W) { y = a.H - 1; x = b - a.W; }
-  else if (b < 2 * a.W + a.H - 2) { x = 0; y = b - 2 * a.W + 1; }
-  else { x = a.W - 1; y = b - 2 * a.W - (a.H - 2) + 1; }
-  float acc = 0.f;
-  for (int dy = 0; dy < 3; ++dy)
-    for (int dx = 0; dx < 3; ++dx) {
-      const int ny = y + dy - 1, nx = x + dx - 1;
-      if (ny >= 0 && ny < a.H && nx >= 0 && nx < a.W) continue;
-      int r;
-      if (ny == -1) r = nx + 1;
-      else if (ny == a.H) r = (a.W + 2) + nx + 1;
-      else if (nx == -1) r = 2 * (a.W + 2) + ny;
-      else r = 2 * (a.W + 2) + a.H + ny;
-      const float* rv = a.ring + ((size_t)f * NR + r) * 64 + 16 * qg;
-      const float* w = a.wc + ((size_t)(dy * 3 + dx) * 64 + 16 * qg) * 64 + co;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc = fmaf(__ldg(w + (size_t)c * 64), rv[c], acc);
-    }
-  part[qg][co] = acc;
-  __syncthreads();
-  if (qg == 0)
-    a.delta[((size_t)f * NB + b) * 64 + co] = (part[0][co] + part[1][co]) + (part[2][co] + part[3][co]);
-}
-
-void launch_border_corrections(const BorderArgs& a, cudaStream_t s) {
-  const int NR = 2 * (a.W + 2) + 2 * a.H, NB = 2 * a.W + 2 * (a.H - 2);
-  launch_pdl(ring_kernel, dim3(NR, a.frames), dim3(256), 0, s, a);
-  launch_pdl(delta_kernel, dim3(NB, a.frames), dim3(256), 0, s, a);
+  launch_pdl(v2p_tc_kernel, grid, dim3(THREADS), smem, s, tok, a);
 }
 
 }  // namespace dr

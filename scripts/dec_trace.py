@@ -48,13 +48,13 @@ def main():
     print("  main loop (us)   ", pct((t[:, 12] - t[:, 0]) / 1e3))
     print("  finish pass (us) ", pct((t[:, 13] - t[:, 12]) / 1e3))
     print("   of which pixels", pct((t[:, 11] - t[:, 12]) / 1e3))
-    tl = (ctypes.c_ulonglong * 320)()
-    if fn(1, tl, 320) == 320:
-        v = np.frombuffer(tl, dtype=np.uint64).reshape(5, 64).astype(np.int64)
+    tl = (ctypes.c_ulonglong * 384)()
+    if fn(1, tl, 384) == 384:
+        v = np.frombuffer(tl, dtype=np.uint64).reshape(6, 64).astype(np.int64)
         st = v[4, 0]
-        print("  CTA 0 timeline (us from start): phase: D committed / epi1 done / E committed / epi2 done")
-        for i in list(range(0, 8)) + list(range(8, 64, 8)):
-            print("    %2d: %7.2f %7.2f %7.2f %7.2f" % ((i,) + tuple((v[k, i] - st) / 1965.0 for k in range(4))))
+        print("  CTA 0 timeline (us from start): phase: MMA issue start / D committed / epi1 done / E committed / epi2 done")
+        for i in list(range(0, 12)) + list(range(12, 64, 8)):
+            print("    %2d: %7.2f %7.2f %7.2f %7.2f %7.2f" % ((i,) + tuple((v[k, i] - st) / 1965.0 for k in (5, 0, 1, 2, 3))))
     for s, n in NAMES.items():
         per_warp = 1 if s <= 5 else 8
         print(f"  {n:18s}", pct(us(t[:, s] / per_warp)))

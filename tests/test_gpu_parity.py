@@ -221,16 +221,14 @@ def test_memory_fifo_and_memory_changes_output(rng):
     assert not np.array_equal(cold.rgb, warm.rgb)
 
 
-@pytest.mark.parametrize("graphed,rgb_flag", [("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")])
-def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed, rgb_flag):
+@pytest.mark.parametrize("graphed", ["1", "0"])
+def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed):
     """dr_inpaint_u8_host (engine-held memory) == engine.inpaint with carried memory.  Nine
     frames: the host path's CUDA graphs (one per ring / slot K/V-cache signature) are
     captured on the first cycle and replayed after, with masks of different areas (so the
     flags word lands at a different offset of the packed read-back every frame).  Graphed
-    and direct launches; the input pack waiting on the rgb upload by device flag (launch
-    before staging) or by event join."""
+    and direct launches."""
     monkeypatch.setenv("DR_HOST_GRAPH", graphed)       # read at engine creation
-    monkeypatch.setenv("DR_RGB_FLAG", rgb_flag)
     cfg = DsttConfig.baseline(64, mask_dilate=2, mask_feather_sigma=1.5)
     eng = DsttEngine(cfg, seed=4)
     mem = eng.zero_memory()
