@@ -130,8 +130,10 @@ def config_dict(name, world, batch, size):
             "l2": "inputs staged from an HBM pool, L2 flushed (256 MiB write) between steps"}
 
 
-def stage_flops(cfg):
-    """Dense algorithmic FLOPs per frame of each kernel class (per launch)."""
+def stage_flops(cfg, kv_bands=3):
+    """Dense algorithmic FLOPs per frame of each kernel class (per launch).  kv_bands: key
+    bands a temporal query attends explicitly -- 3 with warm memory, 1 when both slots are
+    the zero slot (their keys are one constant, dr_b200.h)."""
     T, C, H, W = cfg.tokens, cfg.channels, cfg.height, cfg.width
     g = cfg.temporal_groups
     tg = T // g
@@ -141,7 +143,7 @@ def stage_flops(cfg):
         "embed_qkv": 2 * T * (4 * cfg.patch ** 2) * C + qkv,
         "slot_kv": 2 * T * C * 2 * C,
         "attn_spatial": 2 * 2 * cfg.heads * T * T * dh,
-        "attn_temporal": 2 * 2 * cfg.heads * g * tg * (3 * tg) * dh,
+        "attn_temporal": 2 * 2 * cfg.heads * g * tg * (kv_bands * tg) * dh,
         "mlp_qkv": 2 * T * (C * C + C * 2 * C + 2 * C * C) + qkv,
         "vec2patch": 2 * T * C * C * cfg.kernel ** 2,
         "decode0": 2 * H * W * C * C * 9,
@@ -150,11 +152,12 @@ def stage_flops(cfg):
     }
 
 
-def stage_exps(cfg):
-    """Softmax exponentials per frame per attention launch (dense, all keys)."""
+def stage_exps(cfg, kv_bands=3):
+    """Softmax exponentials per frame per attention launch (keys attended explicitly)."""
     T, g = cfg.tokens, cfg.temporal_groups
     tg = T // g
-    return {"attn_spatial": cfg.heads * T * T, "attn_temporal": cfg.heads * g * tg * 3 * tg}
+    return {"attn_spatial": cfg.heads * T * T,
+            "attn_temporal": cfg.heads * g * tg * kv_bands * tg}
 
 
 def frame_flops_reference(cfg):
@@ -469,12 +472,13 @@ def run_ours(args):
     x_img = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev)   # graph inputs
     x_msk = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
     ring = [torch.zeros((B, T, C), dtype=torch.float32, device=dev) for _ in range(3)]
-    zero = torch.zeros((B, T, C), dtype=torch.float32, device=dev)
     out = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def slots_for(k):
-        """Memory FIFO over a 3-buffer ring: step k reads (k-2, k-1), writes k."""
+    def slots_for(k, e=None):
+        """Memory FIFO over a 3-buffer ring: step k reads (k-2, k-1), writes k.  Cold slots
+        are engine e's zero slot (InpaintMemory.from_zero_slot, memory.py:32-34)."""
+        zero = (e or eng).zero_memory().slots[0]     # [T][C], shared by every frame
         if not carried:
             return zero, zero, ring[0]
         s0 = zero if k < 2 else ring[(k - 2) % 3]
@@ -487,7 +491,7 @@ def run_ours(args):
     stage.inputs = (x_img, x_msk)
 
     def launch(e, k, o=None, ns=None, clone=False):
-        s0, s1, w = slots_for(k)
+        s0, s1, w = slots_for(k, e)
         if clone:
             s0, s1 = s0.clone(), s1.clone()
         e.run(x_img, x_msk, (s0, s1), out={"out": out if o is None else o,
@@ -547,7 +551,9 @@ def run_ours(args):
     p50 = statistics.median(step_ms)
     p99 = float(np.percentile(step_ms, 99))
     k_last = Wm + K - 1
-    last = [t.clone() for t in slots_for(k_last)] + [out.clone()]    # s0, s1, new slot, out
+    # s0, s1 (None = the zero slot), new slot, out
+    z = eng.zero_memory().slots[0]
+    last = [None if t is z else t.clone() for t in slots_for(k_last)] + [out.clone()]
 
     # ---- per-stage times inside a CUDA graph (second engine, event nodes per stage)
     lib = _lib.load()
@@ -572,7 +578,8 @@ def run_ours(args):
                 name = _lib.STAGE_NAMES.get(kinds[j], str(kinds[j]))
                 acc.setdefault(name, []).append(msb[j])
     lib.dr_profile(eng_p.handle, 0)
-    flops = stage_flops(cfg)
+    kv_bands = 3 if carried else 1           # cold memory: both slots are the zero slot
+    flops = stage_flops(cfg, kv_bands)
     stages = {}
     prof_step = statistics.mean(prof_ms) if prof_ms else 0.0
     for name, v in acc.items():
@@ -598,7 +605,7 @@ def run_ours(args):
         if dom.startswith("attn_"):
             # head_dim 16: the binding unit is MUFU ex2 (16/clk/SM measured,
             # profiles/r01/pipe_microbench_b200.txt), not the tensor pipe
-            exps = stage_exps(cfg)[dom] * B
+            exps = stage_exps(cfg, kv_bands)[dom] * B
             clk_hz = 1e6 * (clk["sm_mhz"] if clk and clk.get("sm_mhz") else 1965.0)
             mufu_peak = 16 * 148 * clk_hz
             roof["mufu"] = {"exps_per_launch": exps,
@@ -658,17 +665,18 @@ def run_ours(args):
 
 def check_parity(eng2, cfg, B, stage, k_last, last, imgs, masks, P, rank, dev, stream):
     """Re-run the last timed step eagerly on a second engine with copies of its memory
-    slots (fresh slot K/V projections, no graph): composite and new slot must be bit-equal
-    to the graph replay.  Then frame 0 of that step against the CPU oracle (2e-2 max-abs,
-    40 dB) given the same memory."""
+    slots (fresh slot K/V projections, no graph; a zero slot stays that engine's zero
+    slot): composite and new slot must be bit-equal to the graph replay.  Then frame 0 of
+    that step against the CPU oracle (2e-2 max-abs, 40 dB) given the same memory."""
     import torch
     s0, s1, last_slot, last_out = last
     out2 = torch.empty_like(last_out)
     ns2 = torch.empty_like(last_slot)
+    zero = eng2.zero_memory().slots[0]
+    mem = tuple(zero if s is None else s.clone() for s in (s0, s1))
     with torch.cuda.stream(stream):
         stage(k_last)
-        eng2.run(*_inputs_of(stage), (s0.clone(), s1.clone()), out={"out": out2, "slot": ns2},
-                 sync=False)
+        eng2.run(*_inputs_of(stage), mem, out={"out": out2, "slot": ns2}, sync=False)
     torch.cuda.synchronize(dev)
     bit_out = bool(torch.equal(out2, last_out))
     bit_slot = bool(torch.equal(ns2, last_slot))
@@ -676,7 +684,7 @@ def check_parity(eng2, cfg, B, stage, k_last, last, imgs, masks, P, rank, dev, s
     if rank == 0:
         from oracle import dstt_oracle as O
         from paper_2509_10466_b200.weights import seed_parameters
-        sl = (s0[0].cpu().numpy(), s1[0].cpu().numpy())
+        sl = tuple((s if s.dim() == 2 else s[0]).cpu().numpy() for s in mem)
         i = (k_last % P) * B
         t0 = time.perf_counter()
         ref = O.inpaint_path(cfg, seed_parameters(cfg, 0), imgs[i:i + 1], masks[i:i + 1], sl)

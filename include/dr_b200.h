@@ -61,8 +61,8 @@ typedef struct dr_frame_io {
   const float* rgb_f32;          /* [B][3][H][W] in [0,1], or NULL                   */
   const uint8_t* rgb_u8;         /* [B][H][W][3], or NULL (exactly one rgb input)    */
   const uint8_t* mask_m0;        /* [B][H][W], nonzero = private                     */
-  const float* slot0;            /* memory, oldest first: [B][T][C] or [T][C]        */
-  const float* slot1;
+  const float* slot0;            /* memory, oldest first: [B][T][C] or [T][C], or    */
+  const float* slot1;            /* NULL = the all-zero slot (InpaintMemory.zero)    */
   int32_t slot_batched;          /* 1: slots are [B][T][C]; 0: one [T][C] for all    */
   float* new_slot;               /* [B][T][C] out: post-block tokens (required)      */
   float* out_f32;                /* [B][3][H][W] composite (float API), or NULL      */
@@ -78,6 +78,11 @@ typedef struct dr_frame_io {
    * computes them (correct for any slot contents). */
   int32_t slot_kv_reuse;
 } dr_frame_io;
+
+/* A NULL slot is the cold memory slot (all zeros, InpaintMemory.from_zero_slot, memory.py:32-34).  Its tokens are
+ * identical, so its keys are one constant per temporal block: no slot K/V projection is
+ * launched, and attention takes its `band` equal keys as one key of that multiplicity --
+ * the same softmax, without the 2 x band redundant scores per query. */
 
 /* Build an engine on `device` from the 72 DRWT tensors in state_dict order (host fp32
  * pointers, element counts checked against cfg).  Weights are repacked once into
@@ -114,7 +119,7 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
 /* dr_inpaint_u8_host with the memory passed explicitly, the reference signature
  * InpaintEngine.inpaint(rgb, mask, memory) (base.py:52-89, called by
  * LocalEngineClient.inpaint_frame, service.py:198-204): slot0 / slot1 are the memory's
- * two device fp32 [T][C] slots (oldest first), new_slot receives the post-block tokens
+ * two device fp32 [T][C] slots (oldest first; NULL = zero slot), new_slot receives the post-block tokens
  * (the caller pushes it: memory.py:40-45).  Bit i of slot_kv_reuse may be set only if
  * slot i is unchanged since this engine wrote it as a new_slot (its cached K/V are
  * reused).  Same staging, graphs and errors as dr_inpaint_u8_host. */

@@ -521,6 +521,7 @@ __launch_bounds__(attn_threads<QT>(), attn_ctas_per_sm<QT>()) attn_tc_kernel(Att
         for (int r1 = 0; r1 < KSPLIT - 1; ++r1) M = fmaxf(M, sm.mrg[r1][row][0]);
         const float b = M == -INFINITY ? 0.f : M;
         const float a0 = ex2(m - b);
+        m = b;                                          // o, l are relative to b now
         l *= a0;
 #pragma unroll
         for (int d = 0; d < 16; ++d) o[d] *= a0;
@@ -543,6 +544,24 @@ __launch_bounds__(attn_threads<QT>(), attn_ctas_per_sm<QT>()) attn_tc_kernel(Att
     }
     DR_TRACE_T(4);
     if (crank == 0 && q0 + row < a.band) {
+      if (a.const_mult > 0) {
+        // the zero slots' keys: one key k0 of multiplicity const_mult, value v0.  q row in
+        // the SW32 layout: logical 16-byte chunk c at chunk c ^ ((row >> 2) & 1).
+        const __half* qr = &sm.q[t][32 * q + lane][0];
+        const int sw = (lane >> 2) & 1;
+        const float* k0 = a.const_kv + h * DH;
+        float dot = 0.f;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) dot = fmaf(__half2float(qr[(((d >> 3) ^ sw) << 3) | (d & 7)]), __ldg(k0 + d), dot);
+        const float s0 = dot * sl2;
+        const float ob = m == -INFINITY ? 0.f : m;    // base of o and l
+        const float nb2 = fmaxf(ob, s0);
+        const float f = ex2(ob - nb2), w0 = (float)a.const_mult * ex2(s0 - nb2);
+        const float* v0 = a.const_kv + C + h * DH;
+        l = l * f + w0;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) o[d] = fmaf(o[d], f, w0 * __ldg(v0 + d));
+      }
       const float inv = l > 0.f ? 1.f / l : 0.f;
       uint32_t outp[8];
 #pragma unroll

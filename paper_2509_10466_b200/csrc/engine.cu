@@ -283,7 +283,10 @@ void append_f32(const float* v, int64_t n, std::vector<uint8_t>& out) {
 struct Blk {
   size_t img;                                               // tcgen05 image byte offset
   bool temporal;
+  size_t zkv = 0;            // temporal: fparams offset of the zero slot's [k0 | v0]
 };
+
+inline float round_half(float x) { return __half2float(__float2half_rn(x)); }
 
 // scipy.ndimage._filters._gaussian_kernel1d (order 0) in float64, radius int(4 sigma + 0.5)
 std::vector<double> feather_taps(double sigma) {
@@ -392,6 +395,7 @@ struct dr_engine {
   float* ring[3] = {nullptr, nullptr, nullptr};
   int mem0 = 0, mem1 = 0;                                        // ring index of slots
   bool ring_own[3] = {false, false, false};                      // written by dr_forward
+  bool ring_zero[3] = {true, true, true};                        // still the zero slot
   int last_launches = 0;                                         // kernels of the last call
   size_t last_d2h = 0;                                           // host path: D2H bytes
   int stop_after = -1;               // DR_STOP_AFTER=k (diagnostics): launch only k kernels
@@ -699,7 +703,23 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
       dr_destroy(e);
       return fail(DR_ERR_CONFIG, "internal: token image size mismatch");
     }
-    if (b.temporal) e->n_temporal++;
+    if (b.temporal) {
+      // K / V of an all-zero memory slot: LN1(0) = beta (dstt.py:186-190), so every slot
+      // token projects to k0 = Wk beta + bk, v0 = Wv beta + bv (fp16 operands, as the
+      // slot K/V kernel computes them, rounded to fp16 like its stores)
+      b.zkv = fp.size();
+      const float* beta = weights[base + 1];
+      for (int which = 0; which < 2; ++which) {
+        const float* w = weights[base + 4 + 2 * which];
+        const float* bias = weights[base + 5 + 2 * which];
+        for (int co = 0; co < c; ++co) {
+          double acc = 0.0;
+          for (int j = 0; j < c; ++j) acc += (double)round_half(beta[j]) * round_half(w[(size_t)co * c + j]);
+          fp.push_back(round_half((float)(acc + bias[co])));
+        }
+      }
+      e->n_temporal++;
+    }
     if (e->n_temporal > MAX_TEMPORAL) {
       dr_destroy(e);
       return fail(DR_ERR_CONFIG, "B200 engine supports at most 4 temporal blocks");
@@ -977,8 +997,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   if (B <= 0) return fail(DR_ERR_INPUT, "frames must be positive");
   if ((io->rgb_f32 == nullptr) == (io->rgb_u8 == nullptr))
     return fail(DR_ERR_INPUT, "exactly one of rgb_f32 / rgb_u8 is required");
-  if (!io->mask_m0 || !io->slot0 || !io->slot1 || !io->new_slot)
-    return fail(DR_ERR_INPUT, "mask, both memory slots and new_slot are required");
+  if (!io->mask_m0 || !io->new_slot) return fail(DR_ERR_INPUT, "mask and new_slot are required");
   if (io->out_u8 && !io->rgb_u8) return fail(DR_ERR_INPUT, "out_u8 needs the u8 input");
   if (io->out_f32 && !io->rgb_f32) return fail(DR_ERR_INPUT, "out_f32 needs the f32 input");
   CUDA_TRY(cudaSetDevice(e->device));
@@ -1033,6 +1052,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     const float* sp[2] = {io->slot0, io->slot1};
     for (int sl = 0; sl < 2; ++sl) {
       ent[sl] = -1;
+      if (!sp[sl]) continue;                              // zero slot: constant K/V
       if (sl == 1 && sp[1] == sp[0]) { ent[1] = ent[0]; continue; }
       if ((io->slot_kv_reuse >> sl) & 1) ent[sl] = e->kv_find(sp[sl], fs, io->slot_batched);
       if (ent[sl] >= 0) continue;
@@ -1086,10 +1106,20 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
     at.k[0] = e->k; at.v[0] = e->v; at.seg_frame_stride[0] = 1;
     at.key_valid = tv; at.mask_mode = mode;
     if (temporal) {
-      at.n_seg = 3; at.groups = e->cfg.temporal_groups; at.band = T / at.groups;
-      at.k[1] = e->kv_ptr(ent[0], ti, 0); at.v[1] = e->kv_ptr(ent[0], ti, 1);
-      at.k[2] = e->kv_ptr(ent[1], ti, 0); at.v[2] = e->kv_ptr(ent[1], ti, 1);
-      at.seg_frame_stride[1] = at.seg_frame_stride[2] = io->slot_batched ? 1 : 0;
+      at.groups = e->cfg.temporal_groups; at.band = T / at.groups;
+      // key segments: current band, then each non-zero slot's band; the zero slots' keys
+      // (all equal) enter as one constant key of multiplicity band per zero slot
+      at.n_seg = 1;
+      for (int sl = 0; sl < 2; ++sl) {
+        if (ent[sl] < 0) {
+          at.const_mult += at.band;
+          continue;
+        }
+        at.k[at.n_seg] = e->kv_ptr(ent[sl], ti, 0); at.v[at.n_seg] = e->kv_ptr(ent[sl], ti, 1);
+        at.seg_frame_stride[at.n_seg] = io->slot_batched ? 1 : 0;
+        ++at.n_seg;
+      }
+      if (at.const_mult) at.const_kv = e->fparams + e->blk[i].zkv;
       ++ti;
       seen_t = true;
     } else {
@@ -1264,6 +1294,7 @@ int dr_reset_memory(dr_engine* e) {
   e->mem0 = 0;
   e->mem1 = 0;                       // cold start: both slots are the same zero tensor
   for (bool& o : e->ring_own) o = false;
+  for (bool& z : e->ring_zero) z = true;
   return DR_OK;
 }
 
@@ -1512,8 +1543,11 @@ int dr_inpaint_u8_host(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* mask
   while (fresh == e->mem0 || fresh == e->mem1) ++fresh;
   const int reuse = (e->ring_own[e->mem0] ? 1 : 0) | (e->ring_own[e->mem1] ? 2 : 0);
   e->ring_own[fresh] = false;
-  const int rc = host_inpaint(e, rgb_hwc, mask_hw, out_hwc, e->ring[e->mem0], e->ring[e->mem1],
-                              e->ring[fresh], reuse, stream);
+  e->ring_zero[fresh] = false;
+  // a slot still at its reset value goes in as the zero slot (NULL: constant K/V)
+  const float* s0 = e->ring_zero[e->mem0] ? nullptr : e->ring[e->mem0];
+  const float* s1 = e->ring_zero[e->mem1] ? nullptr : e->ring[e->mem1];
+  const int rc = host_inpaint(e, rgb_hwc, mask_hw, out_hwc, s0, s1, e->ring[fresh], reuse, stream);
   if (rc == DR_OK || rc == DR_ERR_INPUT || rc == DR_ERR_NUMERIC) {
     // the launches ran: contents and slot K/V cache entry of `fresh` agree
     e->ring_own[fresh] = true;
@@ -1528,8 +1562,7 @@ int dr_inpaint_u8_host_mem(dr_engine* e, const uint8_t* rgb_hwc, const uint8_t* 
                            uint8_t* out_hwc, const float* slot0, const float* slot1,
                            float* new_slot, int32_t slot_kv_reuse, void* stream) {
   if (!e || !rgb_hwc || !mask_hw || !out_hwc) return fail(DR_ERR_INPUT, "null argument");
-  if (!slot0 || !slot1 || !new_slot)
-    return fail(DR_ERR_INPUT, "both memory slots and new_slot are required");
+  if (!new_slot) return fail(DR_ERR_INPUT, "new_slot is required");
   if (new_slot == slot0 || new_slot == slot1)
     return fail(DR_ERR_INPUT, "new_slot must not alias a memory slot");
   return host_inpaint(e, rgb_hwc, mask_hw, out_hwc, slot0, slot1, new_slot, slot_kv_reuse & 3,

@@ -75,6 +75,12 @@ struct AttnArgs {
                              // 3 temporal collapsed (mask iff frame has no valid token)
   // key split: CTAs (one cluster) per query tile, 1..4; 0 = chosen by attention_ksplit
   int ksplit;
+  // all-zero memory slots (temporal blocks): LN1(0) = beta, so every key of such a slot is
+  // the same k0 = Wk beta + bk with value v0 = Wv beta + bv.  Their `const_mult` (band per
+  // zero slot) identical keys enter the softmax as one key of that multiplicity:
+  // const_kv = [k0 (64) | v0 (64)] fp32 (fp16-rounded values), 0 = none.
+  const float* const_kv;
+  int const_mult;
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 int attention_ksplit(const AttnArgs& a);

@@ -138,9 +138,23 @@ class DsttEngine(InpaintEngine):
         return self._native.handle
 
     def zero_memory(self) -> InpaintMemory:
+        """Cold memory (memory.py:32-34).  Both slots are one engine-held zero tensor; while
+        it is unmodified (same storage, version counter unchanged) the launches receive
+        it as the NULL zero slot, whose keys are a per-block constant (dr_b200.h)."""
         import torch
-        zero = torch.zeros(self.config.tokens, self.config.channels, device=self.device)
-        return InpaintMemory.from_zero_slot(zero)
+        z = self.__dict__.get("_zero")
+        if z is None or z._version != self._zero_version:
+            z = torch.zeros(self.config.tokens, self.config.channels, device=self.device)
+            self._zero, self._zero_version = z, z._version
+        return InpaintMemory.from_zero_slot(z)
+
+    def _is_zero_slot(self, s) -> bool:
+        import torch
+        z = self.__dict__.get("_zero")
+        return (z is not None and isinstance(s, torch.Tensor) and s.is_cuda
+                and s.data_ptr() == z.data_ptr() and z._version == self._zero_version
+                and s._version == self._zero_version and s.dtype == torch.float32
+                and tuple(s.shape) in {tuple(z.shape), (1,) + tuple(z.shape)})
 
     def save_weights(self, path) -> None:
         save_weights(self._arrays, path)
@@ -223,6 +237,7 @@ class DsttEngine(InpaintEngine):
                                   f"({T}, {C})")
             slots.append(t)
         reuse = sum(1 << i for i, s in enumerate(memory.slots) if self._is_own_slot(s))
+        ptrs = [0 if self._is_zero_slot(s) else t.data_ptr() for s, t in zip(memory.slots, slots)]
         new = self._fresh_slot(slots)
         bits = np.ascontiguousarray(mask.bits)
         if bits.dtype != np.uint8:
@@ -232,7 +247,7 @@ class DsttEngine(InpaintEngine):
         t0 = time.perf_counter()
         _lib.check(self._native.lib.dr_inpaint_u8_host_mem(
             self.handle, frame.ctypes.data, bits.ctypes.data, out.ctypes.data,
-            slots[0].data_ptr(), slots[1].data_ptr(), new.data_ptr(), reuse,
+            ptrs[0], ptrs[1], new.data_ptr(), reuse,
             torch.cuda.current_stream(self.device).cuda_stream))
         ms = (time.perf_counter() - t0) * 1e3
         self._register_slot(new)
@@ -306,20 +321,23 @@ class DsttEngine(InpaintEngine):
         if memory is None:
             memory = self.zero_memory().slots
         reuse = sum(1 << i for i, s in enumerate(memory) if self._is_own_slot(s))
+        zero = [self._is_zero_slot(s) for s in memory]
         slots = [self._slot(s) for s in memory]
         T, C = cfg.tokens, cfg.channels
-        shapes = {tuple(s.shape) for s in slots}
-        if len(shapes) != 1:
+        # the zero slot (passed as NULL) broadcasts to any batch
+        shapes = {tuple(s.shape) for s, z in zip(slots, zero) if not z}
+        if len(shapes) > 1:
             raise ConfigError("memory slots must share one shape")
-        shape = shapes.pop()
+        shape = shapes.pop() if shapes else tuple(slots[0].shape)
         if shape[-2:] != (T, C):
             raise ConfigError(f"memory slot shape {shape} does not match tokens ({T}, {C})")
         if len(shape) == 3 and shape[0] != B:
             if shape[0] == 1:
-                slots = [s[0] for s in slots]
+                slots = [s if z else s[0] for s, z in zip(slots, zero)]
+                shape = shape[1:]
             else:
                 raise ConfigError(f"memory slot batch {shape[0]} does not match {B} frames")
-        batched = int(slots[0].dim() == 3)
+        batched = int(len(shape) == 3)
         o = out or {}
         new_slot = o.get("slot")
         if new_slot is None:
@@ -328,7 +346,7 @@ class DsttEngine(InpaintEngine):
         io = _lib.DrFrameIO()
         io.frames = B
         io.mask_m0 = mask.data_ptr()
-        io.slot0, io.slot1 = slots[0].data_ptr(), slots[1].data_ptr()
+        io.slot0, io.slot1 = (0 if z else s.data_ptr() for z, s in zip(zero, slots))
         io.slot_batched = batched
         io.new_slot = new_slot.data_ptr()
         if u8:

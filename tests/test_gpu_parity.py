@@ -282,13 +282,13 @@ def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
         mem_a = mem_a.push(ra["slot"][0])
     # every frame projects its newest slot's K/V (2 temporal blocks) at the start, next to
     # the mask stage; the older slot is cached from the previous frame:
-    # 1 mask + 2 slot K/V + 1 embed + 2 x 4 blocks + 3 decoder (frame 1 also projects the
-    # second zero slot of the cold memory)
-    assert launches == [15, 17, 15, 15, 15]
+    # 1 mask + 2 slot K/V + 1 embed + 2 x 4 blocks + 3 decoder; frame 0 reads only the zero
+    # slot (constant keys, no projection)
+    assert launches == [13, 15, 15, 15, 15]
     mem_b = eng.zero_memory()
     for t in range(5):                           # stream B: clones, always recomputed
         rb = eng.run(cuda(imgs[t:t + 1]), cuda(masks[t:t + 1]),
-                     [s.clone() for s in mem_b.slots])
+                     [s if eng._is_zero_slot(s) else s.clone() for s in mem_b.slots])
         assert torch.equal(outs_a[t][0], rb["out"]) and torch.equal(outs_a[t][1], rb["slot"])
         mem_b = mem_b.push(rb["slot"][0])
     # an in-place edit of a carried slot must not reuse stale K/V
@@ -300,6 +300,47 @@ def test_slot_kv_cache_is_exact_and_invalidated_by_inplace_edits():
 
 
 # ------------------------------------------------------------------ full-size properties
+def test_zero_slot_constant_keys_vs_explicit_zeros_and_oracle():
+    """The engine's zero slot (NULL at the C-ABI) enters temporal attention as one constant
+    key of multiplicity band (dr_b200.h); a user-made zeros tensor takes the explicit path
+    (slot K/V projection, 3 key bands).  Cold, half-cold (zero + warm slot) and mask-aware:
+    both paths against the oracle, and against each other well inside the tolerance."""
+    cfg = DsttConfig.baseline(512, mask_dilate=5, mask_feather_sigma=3.0)
+    eng = DsttEngine(cfg, seed=0)
+    imgs, masks = synth.frame_pool("C2", 2)
+    w = seed_parameters(cfg, 0)
+    T, C = cfg.tokens, cfg.channels
+    zero_e = eng.zero_memory().slots[0]
+    zero_x = torch.zeros(T, C, device="cuda")
+    warm = torch.from_numpy(np.random.default_rng(1).normal(0, 1, (T, C)).astype(np.float32))
+    z = np.zeros((T, C), np.float32)
+    # slot K/V launches (2 temporal blocks per distinct non-zero slot pointer)
+    for mem_e, mem_x, ref_mem, n_e, n_x in (((zero_e, zero_e), (zero_x, zero_x), (z, z), 0, 2),
+                                            ((zero_e, warm.cuda()), (zero_x, warm.cuda()),
+                                             (z, warm.numpy()), 2, 4)):
+        re = eng.run(cuda(imgs), cuda(masks), mem_e)
+        assert eng.kernels_per_forward() == 1 + n_e + 1 + 8 + 3
+        rx = eng.run(cuda(imgs), cuda(masks), mem_x)
+        assert eng.kernels_per_forward() == 1 + n_x + 1 + 8 + 3
+        oe, ox = re["out"].cpu().numpy(), rx["out"].cpu().numpy()
+        assert np.max(np.abs(oe - ox)) <= 4e-3
+        assert np.max(np.abs(re["slot"].cpu().numpy() - rx["slot"].cpu().numpy())) < 2e-2
+        for i in range(2):
+            ref = O.inpaint_path(cfg, w, imgs[i:i + 1], masks[i:i + 1], ref_mem)
+            assert_close_img(oe[i:i + 1], ref["out"], f"zero-slot frame {i}")
+    # mask-aware attention (modes 2 / 3 on the temporal blocks) with the zero slot
+    cfg_m = DsttConfig.baseline(128, mask_dilate=2, mask_feather_sigma=1.5,
+                                mask_aware_attention=True)
+    eng_m = DsttEngine(cfg_m, seed=2)
+    imgs, masks = synth.frame_pool("C1", 2, size=128)
+    z = np.zeros((cfg_m.tokens, cfg_m.channels), np.float32)
+    res = eng_m.run(cuda(imgs), cuda(masks), None)
+    for i in range(2):
+        ref = O.inpaint_path(cfg_m, seed_parameters(cfg_m, 2), imgs[i:i + 1], masks[i:i + 1],
+                             (z, z))
+        assert_close_img(res["out"][i:i + 1].cpu().numpy(), ref["out"], f"mask-aware {i}")
+
+
 def test_batch_invariance_and_determinism_512():
     cfg = DsttConfig.baseline(512, mask_dilate=5, mask_feather_sigma=3.0)
     eng = DsttEngine(cfg, seed=0)
