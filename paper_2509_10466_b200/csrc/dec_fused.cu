@@ -56,50 +56,41 @@ namespace {
 constexpr int TY = 16, TX = 8;                   // token cells per tile (M = 128)
 constexpr int TPY = 8 * TY, TPX = 8 * TX;        // 128 x 64 pixels
 constexpr int HTY = TY + 2, HTX = TX + 2;        // halo'd token tile
-constexpr int TAP_BYTES = 64 * 64 * 2;           // [k-chunk 8][co 64][8 ci] fp16
-constexpr int NSLOT = 8;                         // weight tap ring
-constexpr int NB4 = 4;                           // D / A2 / E buffers in TMEM
+constexpr int SLOT_BYTES = 2 * 256 * 16;         // one K step of an offset block: 8 KB
+constexpr int NSLOT = 8;                         // weight ring (K-step slots)
+constexpr int NBUF = 2;                          // quad buffers in TMEM (256 columns each)
 constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
 constexpr int NWARP = 19;
 constexpr int THREADS = 32 * NWARP;
 constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 18;
-constexpr uint32_t TM_D = 0, TM_A2 = 256, TM_E = 384, TM_COLS = 512;
+constexpr uint32_t TM_COLS = 512;
 
 struct __align__(1024) DecSmem {
   uint8_t tok[HTY * HTX * 128];                  // 23040 B, SW128 rows (one token per row)
   alignas(1024) uint8_t w2[32 * 128];            // SW128 [32][64] fp16
-  alignas(1024) uint8_t w[NSLOT][TAP_BYTES];
+  alignas(1024) uint8_t w[NSLOT][SLOT_BYTES];
   float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + 1]
   alignas(16) float bias[64];
   float b2[4];
   uint64_t tok_full, w_full[NSLOT], w_empty[NSLOT];
-  uint64_t d_full[NB4], d_empty[NB4], a2_full[NB4], a2_empty[NB4], e_full[NB4], e_empty[NB4];
+  uint64_t d_full[NBUF], d_empty[NBUF], a2_full[NBUF][4], e_full[NBUF][4];
   uint32_t tmem_base;
 };
 static_assert(sizeof(DecSmem) + 1024 <= 227 * 1024, "fused decoder shared memory");
 
-// 64 phases, row-major
-DR_DEV void phase_of(int k, int* py, int* px) {
-  *py = k >> 3;
-  *px = k & 7;
-}
+// token-tile row offset of the A operand for token offset (du, dv)
+DR_DEV int tok_off(int du, int dv) { return (1 + du) * HTX + (1 + dv); }
 
-// taps of phase (py, px): (image index, token-tile row offset of the A operand)
-DR_DEV int phase_taps(int py, int px, int* img, int* off) {
-  int du[2], uu[2], nu = 0, dv[2], vv[2], nv = 0;
-  du[nu] = 0; uu[nu++] = py;
-  if (py <= 1) { du[nu] = -1; uu[nu++] = py + 8; }
-  if (py >= 6) { du[nu] = 1; uu[nu++] = py - 8; }
-  dv[nv] = 0; vv[nv++] = px;
-  if (px <= 1) { dv[nv] = -1; vv[nv++] = px + 8; }
-  if (px >= 6) { dv[nv] = 1; vv[nv++] = px - 8; }
-  int n = 0;
-  for (int a = 0; a < nu; ++a)
-    for (int b = 0; b < nv; ++b) {
-      img[n] = (uu[a] + 2) * 12 + (vv[b] + 2);
-      off[n++] = (1 + du[a]) * HTX + (1 + dv[b]);
-    }
-  return n;
+// Seam partial sums of a tile (the pixels dec_fixup finishes): its accumulator on the band
+// of tile rows -1..1 and ye-2..ye (full width -1..xe) and columns -1..1, xe-2..xe of the
+// rows between (ye x xe = the tile's extent in the image); [3 channels][DEC_BAND] fp32 per
+// tile, contiguous, so dec_fixup's reads are compact.
+constexpr int DEC_BAND = 6 * (TPX + 2) + 6 * (TPY - 4);
+DR_DEV int band_idx(int yl, int xl, int ye, int xe) {
+  const int w2 = xe + 2;
+  if (yl <= 1) return (yl + 1) * w2 + xl + 1;
+  if (yl >= ye - 2) return (yl - ye + 5) * w2 + xl + 1;
+  return 6 * w2 + (yl - 2) * 6 + (xl <= 1 ? xl + 1 : xl - xe + 5);
 }
 
 // K-major SWIZZLE_128B descriptor with an explicit stride between 8-row groups
@@ -251,8 +242,9 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   const int f = blockIdx.z;
   const int ty0 = tile_y * TY, tx0 = tile_x * TX;          // first token cell
   const int y0 = 8 * ty0, x0 = 8 * tx0;                    // first pixel
-  const int k0 = grp * 64 / G, k1 = (grp + 1) * 64 / G;   // this CTA's phases
-  const int nph = k1 - k0;
+  const int g0 = grp * 16 / G, g1 = (grp + 1) * 16 / G;   // this CTA's phase quads
+  const int nq4 = g1 - g0;
+  const int c0 = 4 * dec_quad_first(g0), nchunk = 4 * dec_quad_first(g1) - c0;   // K-step slots
   const int H = a.H, W = a.W;
   const int NB = 2 * W + 2 * (H - 2);
 
@@ -274,13 +266,13 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       tc::mbar_init(&sm.w_full[i], 1);
       tc::mbar_init(&sm.w_empty[i], 1);
     }
-    for (int i = 0; i < NB4; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       tc::mbar_init(&sm.d_full[i], 1);
-      tc::mbar_init(&sm.d_empty[i], 4);
-      tc::mbar_init(&sm.a2_full[i], 4);
-      tc::mbar_init(&sm.a2_empty[i], 1);
-      tc::mbar_init(&sm.e_full[i], 1);
-      tc::mbar_init(&sm.e_empty[i], 8);
+      tc::mbar_init(&sm.d_empty[i], 8);
+      for (int p = 0; p < 4; ++p) {
+        tc::mbar_init(&sm.a2_full[i][p], 8);
+        tc::mbar_init(&sm.e_full[i][p], 1);
+      }
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tokmap);
@@ -288,16 +280,10 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     // predecessor grid
     tc::mbar_arrive_expect_tx(&sm.tok_full, (uint32_t)(HTY * HTX * 128 + 32 * 128));
     tc::bulk_load(sm.w2, a.w2, 32 * 128, &sm.tok_full);
-    int kk = 0;
-    for (int k = k0; k < k1 && kk < NSLOT; ++k) {
-      int py, px, img[4], off[4];
-      phase_of(k, &py, &px);
-      const int n = phase_taps(py, px, img, off);
-      for (int t = 0; t < n && kk < NSLOT; ++t, ++kk) {
-        tc::mbar_arrive_expect_tx(&sm.w_full[kk], TAP_BYTES);
-        tc::bulk_load(sm.w[kk], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)img[t] * TAP_BYTES,
-                      TAP_BYTES, &sm.w_full[kk]);
-      }
+    for (int kk = 0; kk < NSLOT && kk < nchunk; ++kk) {
+      tc::mbar_arrive_expect_tx(&sm.w_full[kk], SLOT_BYTES);
+      tc::bulk_load(sm.w[kk], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + kk) * SLOT_BYTES,
+                    SLOT_BYTES, &sm.w_full[kk]);
     }
   }
   // zero the accumulator (the ring included), biases to smem
@@ -314,51 +300,47 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   tc::fence_after();
   const uint32_t tbase = sm.tmem_base;
 
+  // TMEM: quad buffer b = columns [256 b, 256 b + 256); phase p of the quad owns columns
+  // 256 b + 64 p .. +63: D (fp32, pre-filled with the combined bias), then in place its
+  // LeakyReLU'd fp16 A2 (first 32 columns) and decode.2's E (last 32)
+  auto qcol = [&](int b, int p) { return tbase + (uint32_t)(256 * b + 64 * p); };
   if (warp == W_LOAD) {
     if (lane == 0) {                                       // ------------------- loads
       tc::tma_load_4d(sm.tok, &tokmap, &sm.tok_full, 0, tx0, ty0, f);
-      int kk = 0;
-      for (int k = k0; k < k1; ++k) {
-        int py, px, img[4], off[4];
-        phase_of(k, &py, &px);
-        const int n = phase_taps(py, px, img, off);
-        for (int t = 0; t < n; ++t, ++kk) {
-          if (kk < NSLOT) continue;                        // issued in the prologue
-          const int sl = kk % NSLOT;
-          tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(kk / NSLOT - 1) & 1u);
-          tc::mbar_arrive_expect_tx(&sm.w_full[sl], TAP_BYTES);
-          tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)img[t] * TAP_BYTES,
-                        TAP_BYTES, &sm.w_full[sl]);
-        }
+      for (int kk = NSLOT; kk < nchunk; ++kk) {            // the first NSLOT: prologue
+        const int sl = kk % NSLOT;
+        tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(kk / NSLOT - 1) & 1u);
+        tc::mbar_arrive_expect_tx(&sm.w_full[sl], SLOT_BYTES);
+        tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + kk) * SLOT_BYTES,
+                      SLOT_BYTES, &sm.w_full[sl]);
       }
     }
   } else if (warp == W_MMA) {
-    // --------------------------------------------------------------- D = tokens x Wcomb
-    constexpr uint32_t idesc = tc::idesc_f16(128, 64);
+    // ------------------------------------------- D(quad) += tokens(offset) x Wcomb(quad, offset)
+    constexpr uint32_t idesc = tc::idesc_f16(128, 256);
     tc::mbar_wait(&sm.tok_full, 0);
     tc::fence_after();
     const uint64_t a0 = sdesc_sw128_sbo(tc::smem_u32(sm.tok), HTX * 128);
-    const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 1024, 128);
+    const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 256 * 16, 128);
     int kk = 0;
-    for (int i = 0; i < nph; ++i) {
-      int py, px, img[4], off[4];
-      phase_of(k0 + i, &py, &px);
-      const int n = phase_taps(py, px, img, off);
-      const int b = i % NB4;
-      if (i >= NB4) DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
+    for (int i = 0; i < nq4; ++i) {
+      const int g = g0 + i, gy = g >> 2, gx = g & 3, b = i & 1;
+      DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i >> 1) & 1u));   // bias pre-filled
       tc::fence_after();
       if (lane == 0) DT_TL(5, i);
-      for (int t = 0; t < n; ++t, ++kk) {
-        const int sl = kk % NSLOT;
-        DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(kk / NSLOT) & 1u));
-        tc::fence_after();
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc::mma_f16_warp(tbase + TM_D + 64 * b, a0 + (uint64_t)(off[t] * 8 + ks * 2),
-                           b0 + (uint64_t)(sl * (TAP_BYTES / 16) + ks * 128), idesc,
-                           (t | ks) != 0);
-        tc::mma_commit_warp(&sm.w_empty[sl]);
-      }
+      for (int ia = 0; ia < dec_quad_noff(gy); ++ia)
+        for (int ib = 0; ib < dec_quad_noff(gx); ++ib) {
+          const int off = tok_off(dec_quad_off(gy, ia), dec_quad_off(gx, ib));
+#pragma unroll 1
+          for (int ks = 0; ks < 4; ++ks, ++kk) {
+            const int sl = kk % NSLOT;
+            DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(kk / NSLOT) & 1u));
+            tc::fence_after();
+            tc::mma_f16_warp(qcol(b, 0), a0 + (uint64_t)(off * 8 + ks * 2),
+                             b0 + (uint64_t)(sl * (SLOT_BYTES / 16)), idesc, 1u);
+            tc::mma_commit_warp(&sm.w_empty[sl]);
+          }
+        }
       tc::mma_commit_warp(&sm.d_full[b]);
       if (lane == 0) DT_TL(0, i);
     }
@@ -367,121 +349,134 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     constexpr uint32_t idesc2 = tc::idesc_f16(128, 32);
     tc::mbar_wait(&sm.tok_full, 0);                        // w2 landed with the tokens
     const uint64_t bw2 = tc::sdesc_sw128(tc::smem_u32(sm.w2), 0);
-    for (int i = 0; i < nph; ++i) {
-      const int b = i % NB4;
-      DT_WAIT(4, tc::mbar_wait(&sm.a2_full[b], (uint32_t)(i / NB4) & 1u));
-      if (i >= NB4) DT_WAIT(5, tc::mbar_wait(&sm.e_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
-      tc::fence_after();
+    for (int i = 0; i < nq4; ++i) {
+      const int b = i & 1;
+      for (int p = 0; p < 4; ++p) {
+        DT_WAIT(4, tc::mbar_wait(&sm.a2_full[b][p], (uint32_t)(i >> 1) & 1u));
+        tc::fence_after();
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
-        tc::mma_ts_f16_warp(tbase + TM_E + 32 * b, tbase + TM_A2 + 32 * b + 8 * ks,
-                            bw2 + (uint64_t)(2 * ks), idesc2, ks != 0);
-      tc::mma_commit_warp(&sm.e_full[b]);
-      tc::mma_commit_warp(&sm.a2_empty[b]);
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_ts_f16_warp(qcol(b, p) + 32, qcol(b, p) + 8 * ks, bw2 + (uint64_t)(2 * ks), idesc2,
+                              ks != 0);
+        tc::mma_commit_warp(&sm.e_full[b][p]);
+      }
       if (lane == 0) DT_TL(2, i);
     }
   } else if (warp < W_EPI2) {
     // --------------------------------------------------------------- epilogue 1
-    // two sets of 4 warps (one per TMEM lane quarter) take alternate phases, all 64
-    // channels each, so two phases' TMEM round trips are in flight at once
+    // two sets of 4 warps (one per TMEM lane quarter); set s takes channels 32 s .. 32 s + 31
+    // of every phase, in phase order (phase p's A2 is complete after 8 arrivals): D (bias
+    // included) -> LeakyReLU -> fp16 A2 in place.  The next phase's D is loaded from TMEM
+    // while this one is converted.
     const int q = warp & 3, set = (warp - W_EPI1) >> 2;
     const int row = 32 * q + lane;                        // token position in the tile
     const int tyl = row >> 3, txl = row & 7;
-    const uint32_t lrow = (uint32_t)(32 * q) << 16;
-    for (int i = set; i < nph; i += 2) {
-      int py, px;
-      phase_of(k0 + i, &py, &px);
-      const int b = i % NB4;
-      const int y = y0 + 8 * tyl + py, x = x0 + 8 * txl + px;
-      DT_WAIT(6, tc::mbar_wait(&sm.d_full[b], (uint32_t)(i / NB4) & 1u));
+    const uint32_t lrow = ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * set);
+    const __half2 slope = __float2half2_rn(0.2f);
+    for (int i = 0; i < nq4; ++i) {
+      const int g = g0 + i, b = i & 1;
+      DT_WAIT(6, tc::mbar_wait(&sm.d_full[b], (uint32_t)(i >> 1) & 1u));
       tc::fence_after();
-      const bool brd = y < H && x < W && on_border(y, x, H, W);
-      float4* bdst = brd ? reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64) : nullptr;
-      if (i >= NB4) {
-        DT_WAIT(8, tc::mbar_wait(&sm.a2_empty[b], (uint32_t)(i / NB4 - 1) & 1u));
-        tc::fence_after();
-      }
+      uint32_t v[2][32];
+      DR_TMEM_LD16(qcol(b, 0) + lrow, v[0]);
+      DR_TMEM_LD16(qcol(b, 0) + lrow + 16, (v[0] + 16));
 #pragma unroll
-      for (int hc = 0; hc < 2; ++hc) {                    // 32 channels at a time
-        uint32_t v[32];
-        DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * hc, v);
-        DR_TMEM_LD16(tbase + lrow + TM_D + 64 * b + 32 * hc + 16, (v + 16));
+      for (int p = 0; p < 4; ++p) {
+        const int py = 2 * (g >> 2) + (p >> 1), px = 2 * (g & 3) + (p & 1);
+        const int y = y0 + 8 * tyl + py, x = x0 + 8 * txl + px;
         tc::tmem_wait_ld();
-        if (hc == 1) {                                    // D(b) fully read
-          tc::fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
+        // both sets of this lane quarter hold their D(p) before either overwrites the
+        // columns with A2 (set 1's A2 lands in set 0's channel columns 16 .. 31)
+        asm volatile("bar.sync %0, 64;\n" :: "r"(3 + q) : "memory");
+        if (p < 3) {
+          DR_TMEM_LD16(qcol(b, p + 1) + lrow, v[(p + 1) & 1]);
+          DR_TMEM_LD16(qcol(b, p + 1) + lrow + 16, (v[(p + 1) & 1] + 16));
         }
-#pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {                  // bias: 128-bit broadcast loads
-          const float4 bb = reinterpret_cast<const float4*>(sm.bias)[8 * hc + c4];
-          v[4 * c4] = __float_as_uint(__uint_as_float(v[4 * c4]) + bb.x);
-          v[4 * c4 + 1] = __float_as_uint(__uint_as_float(v[4 * c4 + 1]) + bb.y);
-          v[4 * c4 + 2] = __float_as_uint(__uint_as_float(v[4 * c4 + 2]) + bb.z);
-          v[4 * c4 + 3] = __float_as_uint(__uint_as_float(v[4 * c4 + 3]) + bb.w);
-        }
-        if (brd) {
+        const uint32_t* vp = v[p & 1];
+        if (y < H && x < W && on_border(y, x, H, W)) {
           // image border: the combined pre-activation is redone by dec_border
+          float4* bdst = reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 32 * set);
 #pragma unroll
           for (int c4 = 0; c4 < 8; ++c4)
-            bdst[8 * hc + c4] = make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
-                                            __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
+            bdst[c4] = make_float4(__uint_as_float(vp[4 * c4]), __uint_as_float(vp[4 * c4 + 1]),
+                                   __uint_as_float(vp[4 * c4 + 2]), __uint_as_float(vp[4 * c4 + 3]));
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float u0 = __uint_as_float(v[c]), u1 = __uint_as_float(v[c + 1]);
-          pk[c / 2] = pack_half2(fmaxf(u0, 0.2f * u0), fmaxf(u1, 0.2f * u1));   // LeakyReLU(0.2)
+        for (int c = 0; c < 16; ++c) {                    // LeakyReLU(0.2) on fp16 pairs
+          const uint32_t h = pack_half2(__uint_as_float(vp[2 * c]), __uint_as_float(vp[2 * c + 1]));
+          const __half2 hv = *reinterpret_cast<const __half2*>(&h);
+          const __half2 r = __hmax2(hv, __hmul2(hv, slope));
+          pk[c] = *reinterpret_cast<const uint32_t*>(&r);
         }
-        DR_TMEM_ST16(tbase + lrow + TM_A2 + 32 * b + 16 * hc, pk);
+        // A2 columns of channels 32 set .. : 16 fp16 pairs at column 64 p + 16 set
+        DR_TMEM_ST16(qcol(b, p) + (lrow - (uint32_t)(32 * set)) + (uint32_t)(16 * set), pk);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sm.a2_full[b][p]);
       }
-      tc::tmem_wait_st();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.a2_full[b]);
       if (lane == 0 && q == 0) DT_TL(1, i);
     }
   } else {
     // --------------------------------------------------------------- epilogue 2
     // two warps per lane quarter: decode.2 taps 0-4 / 5-8 of the same pixels (distinct
-    // targets within a phase), one barrier per phase orders the read-modify-writes
+    // targets within a phase), one barrier per phase orders the read-modify-writes; then
+    // each warp re-fills its half of the phase's columns with the combined bias for the
+    // quad two steps on (the first two quads: filled up front)
     const int q = warp & 3, hh = (warp - W_EPI2) >> 2;
     const int row = 32 * q + lane;
     const int tyl = row >> 3, txl = row & 7;
     const uint32_t lrow = (uint32_t)(32 * q) << 16;
-    // E of phase i + 1 is loaded from TMEM while this warp waits at phase i's barrier
-    uint32_t ev[32];
-    if (nph > 0) {
-      DT_WAIT(9, tc::mbar_wait(&sm.e_full[0], 0));
-      tc::fence_after();
-      DR_TMEM_LD16(tbase + lrow + TM_E, ev);
-      DR_TMEM_LD16(tbase + lrow + TM_E + 16, (ev + 16));
-    }
-    for (int i = 0; i < nph; ++i) {
-      int py, px;
-      phase_of(k0 + i, &py, &px);
-      const int b = i % NB4;
-      tc::tmem_wait_ld();
+    uint32_t bias_h[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) bias_h[c] = __float_as_uint(sm.bias[32 * hh + c]);
+    auto fill_bias = [&](int b, int p) {
+      DR_TMEM_ST16(qcol(b, p) + lrow + 32 * hh, bias_h);
+      DR_TMEM_ST16(qcol(b, p) + lrow + 32 * hh + 16, (bias_h + 16));
+    };
+    auto release = [&](int b) {                           // buffer b: bias in, free for D
+      tc::tmem_wait_st();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sm.e_empty[b]);
-      uint32_t cur[32];
+      if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
+    };
+    for (int b = 0; b < NBUF; ++b) {
+      for (int p = 0; p < 4; ++p) fill_bias(b, p);
+      release(b);
+    }
+    for (int i = 0; i < nq4; ++i) {
+      const int g = g0 + i, b = i & 1;
+      // E of phase p + 1 is loaded from TMEM while this warp waits at phase p's barrier
+      uint32_t ev[32];
+      DT_WAIT(9, tc::mbar_wait(&sm.e_full[b][0], (uint32_t)(i >> 1) & 1u));
+      tc::fence_after();
+      DR_TMEM_LD16(qcol(b, 0) + lrow + 32, ev);
+      DR_TMEM_LD16(qcol(b, 0) + lrow + 48, (ev + 16));
+#pragma unroll 1
+      for (int p = 0; p < 4; ++p) {
+        const int py = 2 * (g >> 2) + (p >> 1), px = 2 * (g & 3) + (p & 1);
+        tc::tmem_wait_ld();
+        uint32_t cur[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) cur[c] = ev[c];
-      const int yl = 8 * tyl + py, xl = 8 * txl + px;      // source pixel in the tile
-      const int y = y0 + yl, x = x0 + xl;
-      if (y < H && x < W && !on_border(y, x, H, W)) {
-        if (hh) epi2_rmw<5, 4>(sm, cur, yl, xl);
-        else epi2_rmw<0, 5>(sm, cur, yl, xl);
+        for (int c = 0; c < 32; ++c) cur[c] = ev[c];
+        const int yl = 8 * tyl + py, xl = 8 * txl + px;    // source pixel in the tile
+        const int y = y0 + yl, x = x0 + xl;
+        if (y < H && x < W && !on_border(y, x, H, W)) {
+          if (hh) epi2_rmw<5, 4>(sm, cur, yl, xl);
+          else epi2_rmw<0, 5>(sm, cur, yl, xl);
+        }
+        if (p < 3) {
+          DT_WAIT(9, tc::mbar_wait(&sm.e_full[b][p + 1], (uint32_t)(i >> 1) & 1u));
+          tc::fence_after();
+          DR_TMEM_LD16(qcol(b, p + 1) + lrow + 32, ev);
+          DR_TMEM_LD16(qcol(b, p + 1) + lrow + 48, (ev + 16));
+        }
+        // phase order of the RMWs; also both warps of the quarter have read E
+        DT_WAIT(10, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
+        if (i + 2 < nq4) fill_bias(b, p);
       }
-      if (i + 1 < nph) {
-        const int bn = (i + 1) % NB4;
-        DT_WAIT(9, tc::mbar_wait(&sm.e_full[bn], (uint32_t)((i + 1) / NB4) & 1u));
-        tc::fence_after();
-        DR_TMEM_LD16(tbase + lrow + TM_E + 32 * bn, ev);
-        DR_TMEM_LD16(tbase + lrow + TM_E + 32 * bn + 16, (ev + 16));
-      }
-      DT_WAIT(10, asm volatile("bar.sync 2, 256;\n" ::: "memory"));   // phase order of the RMWs
+      if (i + 2 < nq4) release(b);
       if (lane == 0 && warp == W_EPI2) DT_TL(3, i);
     }
   }
@@ -501,9 +496,9 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   const int ye = min(TPY, H - y0), xe = min(TPX, W - x0);
   const int rows_per = TPY / G, rbeg = grp * rows_per, rend = min(ye, rbeg + rows_per);
   const bool nb_up = y0 > 0, nb_dn = y0 + TPY < H, nb_l = x0 > 0, nb_r = x0 + TPX < W;
-  const int par = ((tile_y & 1) << 1) | (tile_x & 1);
   const size_t plane = (size_t)H * W;
-  float* part = a.part + ((size_t)par * a.frames + f) * 3 * plane;
+  const int ntx = (W + TPX - 1) / TPX, nty = (H + TPY - 1) / TPY;
+  float* band = a.part + ((size_t)(f * nty + tile_y) * ntx + tile_x) * 3 * DEC_BAND;
   // accumulator value summed over the cluster's ranks (in rank order)
   uint32_t acc_rank[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -604,8 +599,9 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 #pragma unroll
           for (int co = 0; co < 3; ++co) o[co] = accv(co, r, cc);
           if (is_fix(yy[j] - y0, x - x0, yy[j], x)) {
+            const int bi = band_idx(yy[j] - y0, x - x0, ye, xe);
 #pragma unroll
-            for (int co = 0; co < 3; ++co) part[co * plane + (size_t)yy[j] * W + x] = o[co];
+            for (int co = 0; co < 3; ++co) band[co * DEC_BAND + bi] = o[co];
           } else {
 #pragma unroll
             for (int co = 0; co < 3; ++co) o[co] += sm.b2[co];
@@ -691,9 +687,9 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     }
     const int y = y0 + yl, x = x0 + xl;
     if (y < 0 || x < 0 || y >= H || x >= W) continue;
-    const int r = yl + 1, cc = acc_col(r, xl + 1);
+    const int r = yl + 1, cc = acc_col(r, xl + 1), bi = band_idx(yl, xl, ye, xe);
 #pragma unroll
-    for (int co = 0; co < 3; ++co) part[co * plane + (size_t)y * W + x] = accv(co, r, cc);
+    for (int co = 0; co < 3; ++co) band[co * DEC_BAND + bi] = accv(co, r, cc);
   }
   if (G > 1) cluster_sync_all();                           // the ranks' reads are done
 #ifdef DR_TRACE
@@ -702,28 +698,16 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 #endif
 }
 
-// One warp per image-border pixel: pre-activation = combined (stored by dec_fused) minus
-// the decode.0 taps reading the canvas ring, LeakyReLU, then decode.2's 27 taps
-// E[u] = sum_ci W2[u][ci] d0[ci].  Lane l owns channels 2l, 2l+1.
-__global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__ DecArgs a) {
-  pdl_trigger();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Image-border pixel (y, x) by one warp (used for the 4 corners): pre-activation =
+// combined (stored by dec_fused) minus the decode.0 taps reading the canvas ring,
+// LeakyReLU, then decode.2's 27 taps E[u] = sum_ci W2[u][ci] d0[ci].  Lane l owns channels
+// 2l, 2l+1.
+DR_DEV void border_pixel_warp(const DecArgs& a, int f, int y, int x, int lane) {
   const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
-  const long g = (long)blockIdx.x * 8 + warp;
-  if (g >= (long)a.frames * NB) {
-    pdl_wait();
-    return;
-  }
-  const int f = (int)(g / NB), bi = (int)(g - (long)f * NB);
-  int y, x;
-  if (bi < W) { y = 0; x = bi; }
-  else if (bi < 2 * W) { y = H - 1; x = bi - W; }
-  else if (bi < 2 * W + H - 2) { y = bi - 2 * W + 1; x = 0; }
-  else { y = bi - 2 * W - (H - 2) + 1; x = W - 1; }
+  const int bi = border_index(y, x, H, W);
   const int co = 2 * lane;
   const float* dk = a.dk;
   const int PC = a.Cc + 2, PR = a.R + 2;
-  pdl_wait();
   const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
   // sum_ci K[ci][co, co+1] tok(ty, tx)[ci] over the warp (token channels broadcast by shuffle)
   auto gemv = [&](const float* k, int ty, int tx, float2& acc) {
@@ -786,10 +770,112 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   if (lane < 27) out[lane] = es;
 }
 
-// The pixels dec_fused left: the sum of the partial planes of every tile whose 1-pixel-
-// expanded area holds the pixel (<= 4 tiles, one parity plane each, over the phase groups,
-// a fixed order), plus the image-border sources' E, then the tail.  The last CTA mirrors
-// the flags (host path).
+
+// The other border pixels, one CTA per (frame, edge, phase r = position mod 8) for the
+// edge's pixels at positions r + 8k (corners excluded): they share the 1-2 correction
+// matrices dK[edge][v] (v = r, and r + 8 for r <= 1 / r - 8 for r >= 6), staged in shared
+// memory with the edge's token row; per 64 pixels a [64 px x 64 ci] x [64 ci x 64 co]
+// product per tap, LeakyReLU, fp16 rounding, then the 27 decode.2 taps.
+struct BorderSmem {
+  float k[2][64][64];                            // [tap][ci][co]
+  float tok[66][68];                             // tokens k0-1 .. k0+64 of the edge line
+  float d0[64][65];
+  float w2[27][65];                              // padded: lanes of one column hit 27 banks
+  float eb[64];
+};
+
+__global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__ DecArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  BorderSmem& sm = *reinterpret_cast<BorderSmem*>(smem_raw);
+  pdl_trigger();
+  const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
+  const int tid = threadIdx.x;
+  const int nmain = a.frames * 32;
+  if ((int)blockIdx.x >= nmain) {                        // corners: one warp each
+    pdl_wait();
+    const int c = ((int)blockIdx.x - nmain) * 8 + (tid >> 5);
+    if (c >= 4 * a.frames) return;
+    const int f = c >> 2, k = c & 3;
+    border_pixel_warp(a, f, (k & 2) ? H - 1 : 0, (k & 1) ? W - 1 : 0, tid & 31);
+    return;
+  }
+  const int f = blockIdx.x / 32, ed = (blockIdx.x >> 3) & 3, r = blockIdx.x & 7;
+  const bool along_x = ed < 2;
+  const int len = along_x ? W : H;
+  const int line = ed == 0 ? 0 : (ed == 1 ? a.R - 1 : (ed == 2 ? 0 : a.Cc - 1));
+  const int nlim = along_x ? a.Cc : a.R;
+  const int nt = (r <= 1 || r >= 6) ? 2 : 1, dt1 = r <= 1 ? -1 : 1;   // tap 1: token k + dt1
+  // constants first (before the predecessor grid completes)
+  for (int t = 0; t < nt; ++t) {
+    const int v = t == 0 ? r : r - 8 * dt1;
+    const float4* src = reinterpret_cast<const float4*>(a.dk + DK_EDGE + (size_t)(ed * 12 + v + 2) * 4096);
+    float4* dst = reinterpret_cast<float4*>(&sm.k[t][0][0]);
+    for (int i = tid; i < 1024; i += 256) dst[i] = __ldg(src + i);
+  }
+  for (int i = tid; i < 27 * 64; i += 256) sm.w2[i >> 6][i & 63] = __ldg(a.w2f + i);
+  if (tid < 64) sm.eb[tid] = __ldg(a.dk + DK_EB + ed * 64 + tid);
+  const int k_lo = r == 0 ? 1 : 0, k_hi = (len - 2 - r) >= 0 ? (len - 2 - r) / 8 : -1;
+  const int PC = a.Cc + 2, PR = a.R + 2;
+  pdl_wait();
+  const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
+  const int co = tid & 63, pg = tid >> 6;
+  for (int kb = k_lo; kb <= k_hi; kb += 64) {
+    __syncthreads();
+    for (int i = tid; i < 66 * 32; i += 256) {          // tokens kb-1 .. kb+64, half2 pairs
+      const int j = i >> 5, c2 = i & 31, t = kb - 1 + j;
+      float2 v = make_float2(0.f, 0.f);
+      if (t >= 0 && t < nlim) {
+        const int ty = along_x ? line : t, tx = along_x ? t : line;
+        v = __half22float2(reinterpret_cast<const __half2*>(tokf + ((size_t)(ty + 1) * PC + (tx + 1)) * 64)[c2]);
+      }
+      sm.tok[j][2 * c2] = v.x;
+      sm.tok[j][2 * c2 + 1] = v.y;
+    }
+    __syncthreads();
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = sm.eb[co];
+    for (int t = 0; t < nt; ++t) {
+      const int o = 1 + (t == 0 ? 0 : dt1);              // token row of pixel j: j + o
+#pragma unroll 2
+      for (int c4 = 0; c4 < 16; ++c4) {
+        const float w0 = sm.k[t][4 * c4][co], w1 = sm.k[t][4 * c4 + 1][co];
+        const float w2 = sm.k[t][4 * c4 + 2][co], w3 = sm.k[t][4 * c4 + 3][co];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[16 * pg + i + o][4 * c4]);
+          acc[i] = fmaf(tv.x, w0, fmaf(tv.y, w1, fmaf(tv.z, w2, fmaf(tv.w, w3, acc[i]))));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int j = 16 * pg + i, k = kb + j, pos = r + 8 * k;
+      float d = 0.f;
+      if (k <= k_hi) {
+        const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
+        d = a.bd0[((size_t)f * NB + border_index(y, x, H, W)) * 64 + co] - acc[i];
+        d = d >= 0.f ? d : 0.2f * d;
+        d = __half2float(__float2half_rn(d));             // decode.0's output is fp16
+      }
+      sm.d0[j][co] = d;
+    }
+    __syncthreads();
+    for (int i = tid; i < 64 * 27; i += 256) {
+      const int j = i / 27, u = i - 27 * j, k = kb + j, pos = r + 8 * k;
+      if (k > k_hi) continue;
+      float e = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < 64; ++c) e = fmaf(sm.w2[u][c], sm.d0[j][c], e);
+      const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
+      a.be[((size_t)f * NB + border_index(y, x, H, W)) * 27 + u] = e;
+    }
+  }
+}
+
+// The pixels dec_fused left: the sum of the band partials of every tile whose 1-pixel-
+// expanded area holds the pixel (<= 4 tiles, a fixed order), plus the image-border
+// sources' E, then the tail.  The last CTA mirrors the flags (host path).
 __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ DecArgs a) {
   pdl_trigger();
   const int f = blockIdx.y;
@@ -801,7 +887,7 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
 #pragma unroll
   for (int c = 0; c < 3; ++c) b2[c] = __ldg(a.b2 + c);
   pdl_wait();
-  const size_t plane = (size_t)H * W;
+  const int ntx = (W + TPX - 1) / TPX, nty = (H + TPY - 1) / TPY;
   const ConvTcArgs& tl = a.tail;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += (long)gridDim.x * blockDim.x) {
     int y, x, n;
@@ -826,26 +912,23 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
     for (int e = 0; e < 4; ++e)
 #pragma unroll
       for (int co = 0; co < 3; ++co) o[e][co] = b2[co];
-    // partial planes: tile (ty, tx) holds pixel x' iff x' in [TPX tx - 1, TPX (tx + 1)]
-    for (int ty = ty_a; ty <= ty_b; ++ty)
-        for (int tx = tx_a; tx <= tx_b; ++tx) {
-          const int par = ((ty & 1) << 1) | (tx & 1);
-          const float* part = a.part + ((size_t)par * a.frames + f) * 3 * plane + (size_t)y * W + x;
-          const int lo = TPX * tx - 1, hi = TPX * (tx + 1);
-          if (n == 4) {
+    // tile (ty, tx) holds pixel (y, x') iff y - y0 in [-1, ye] and x' - x0 in [-1, xe]
+    for (int ty = ty_a; ty <= ty_b; ++ty) {
+      const int yl = y - TPY * ty, ye = min(TPY, H - TPY * ty);
+      if (yl < -1 || yl > ye) continue;
+      for (int tx = tx_a; tx <= tx_b; ++tx) {
+        const int xe = min(TPX, W - TPX * tx);
+        const float* bp = a.part + ((size_t)(f * nty + ty) * ntx + tx) * 3 * DEC_BAND;
 #pragma unroll
-            for (int co = 0; co < 3; ++co) {
-              const float4 v = *reinterpret_cast<const float4*>(part + co * plane);
-              const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int e = 0; e < 4; ++e) {
+          const int xl = x + e - TPX * tx;
+          if (e >= n || xl < -1 || xl > xe) continue;
+          const int bi = band_idx(yl, xl, ye, xe);
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (x + e >= lo && x + e <= hi) o[e][co] += vv[e];
-            }
-          } else {
-#pragma unroll
-            for (int co = 0; co < 3; ++co) o[0][co] += part[co * plane];
-          }
+          for (int co = 0; co < 3; ++co) o[e][co] += __ldg(bp + co * DEC_BAND + bi);
         }
+      }
+    }
     for (int e = 0; e < n; ++e) {
       const int xe = x + e;
       float oo[3] = {o[e][0], o[e][1], o[e][2]};
@@ -891,6 +974,9 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
 }  // namespace
 
 size_t dec_border_table_floats() { return DK_TOTAL; }
+size_t dec_part_floats(int frames, int H, int W) {
+  return (size_t)frames * ((H + TPY - 1) / TPY) * ((W + TPX - 1) / TPX) * 3 * DEC_BAND;
+}
 int dec_border_pixels(int H, int W) { return 2 * W + 2 * (H - 2); }
 
 // Phase groups per tile: enough CTAs for about one wave at small batch (4 at one 512^2
@@ -961,8 +1047,14 @@ void launch_dec_fused(const CUtensorMap& tok4d, const DecArgs& a, cudaStream_t s
 }
 
 void launch_dec_border(const DecArgs& a, cudaStream_t s) {
-  const long warps = (long)a.frames * dec_border_pixels(a.H, a.W);
-  launch_pdl(dec_border_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, s, a);
+  static unsigned long long init = 0;
+  const int smem = (int)sizeof(BorderSmem);
+  once_per_device(init, [&] {
+    cudaFuncSetAttribute(dec_border_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  // frames x 4 edges x 8 phases, then the corners (8 per CTA)
+  const int blocks = a.frames * 32 + (4 * a.frames + 7) / 8;
+  launch_pdl(dec_border_kernel, dim3(blocks), dim3(256), smem, s, a);
 }
 
 void launch_dec_fixup(const DecArgs& a, cudaStream_t s) {

@@ -529,7 +529,7 @@ struct dr_engine {
     const bool fus = use_fused(frames);
     const size_t upx = frame_px() * unf;
     const size_t o_ras = take(upx * C * 2), o_ep = take(upx * 27 * 2);
-    const size_t o_part = take(fus ? (size_t)frames * 4 * frame_px() * 3 * 4 : 0);
+    const size_t o_part = take(fus ? dec_part_floats(frames, H, W) * 4 : 0);
     const size_t nbp = (size_t)frames * dec_border_pixels(H, W);
     const size_t o_bd0 = take(fus ? nbp * 64 * 4 : 0), o_be = take(fus ? nbp * 27 * 4 : 0);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
@@ -800,6 +800,28 @@ int dr_create(const dr_config* cfg, const float* const* weights, const int64_t* 
             }
       }
     });
+    // regroup the tap images into the kernel's stream order: per phase quad and token
+    // offset one [k-chunk 8][4 phases x 64 co][8 ci] block (kernels.h dec_quad_*)
+    {
+      std::vector<uint16_t> grp(combimg.size());
+      size_t blk = 0;
+      for (int g = 0; g < 16; ++g) {
+        const int gy = g >> 2, gx = g & 3;
+        for (int ia = 0; ia < dec_quad_noff(gy); ++ia)
+          for (int ib = 0; ib < dec_quad_noff(gx); ++ib, ++blk) {
+            const int du = dec_quad_off(gy, ia), dv = dec_quad_off(gx, ib);
+            uint16_t* dst = grp.data() + blk * 256 * 64;
+            for (int q = 0; q < 4; ++q) {
+              const int py = 2 * gy + (q >> 1), px = 2 * gx + (q & 1);
+              const int tap = (py - 8 * du + 2) * 12 + (px - 8 * dv + 2);
+              const uint16_t* src = combimg.data() + (size_t)tap * 64 * 64;
+              for (int ch = 0; ch < 8; ++ch)
+                std::memcpy(dst + ((size_t)ch * 256 + q * 64) * 8, src + (size_t)ch * 64 * 8, 64 * 8 * 2);
+            }
+          }
+      }
+      combimg.swap(grp);
+    }
     for (int co = 0; co < 64; ++co) {
       double b = bc[co];
       for (int cp = 0; cp < 64; ++cp)

@@ -176,17 +176,30 @@ void launch_dec2_gather(const ConvTcArgs& a, cudaStream_t s);
 // `groups` > 1 the 64 phases of a tile are split over a cluster of that many CTAs, whose
 // accumulators are summed through distributed shared memory.
 constexpr int DEC_MAX_FIX = 128;
+// Phase quads of the fused decoder: quad g = (gy, gx) of a 4 x 4 grid holds the phases
+// py in {2gy, 2gy+1}, px in {2gx, 2gx+1}, which read the same token offsets: du in {0},
+// plus -1 (tap u = py + 8) for gy = 0 and +1 (u = py - 8) for gy = 3; likewise dv.  One
+// MMA with N = 256 (4 phases x 64 channels) per offset and K step.
+__host__ __device__ inline int dec_quad_noff(int gq) { return (gq == 0 || gq == 3) ? 2 : 1; }
+__host__ __device__ inline int dec_quad_off(int gq, int i) { return i == 0 ? 0 : (gq == 0 ? -1 : 1); }
+__host__ __device__ inline int dec_quad_first(int g) {     // offset blocks before quad g
+  int n = 0;
+  for (int k = 0; k < g; ++k) n += dec_quad_noff(k >> 2) * dec_quad_noff(k & 3);
+  return n;
+}
 struct DecArgs {
   int frames, H, W, R, Cc;
-  int groups;                // phase groups per tile: 1, 2 or 4
-  const void* wcomb;         // 144 tap images [(u+2)*12 + (v+2)][k-chunk 8][co 64][8 ci] fp16
+  int groups;                // parts per tile (cluster size): 1, 2 or 4; each takes 16 / groups quads
+  // 36 offset blocks in quad order, offsets du-major: [k-chunk 8][4 phases x 64 co][8 ci]
+  // fp16 (phase p = 2 (py & 1) + (px & 1) of the quad)
+  const void* wcomb;
   const float* bcomb;        // [64] combined bias
   const void* w2;            // decode.2 tap-expanded weights, K-major SW128 [32 u][64 ci]
   const float* w2f;          // decode.2 weights fp32 [27 u][64 ci] (u = 3*(3*ky+kx)+co)
   const float* b2;           // [3]
   const float* dk;           // border-correction tables (engine.cu, dec_border_table_floats)
   const __half* tok16;       // padded token grid [frames][R+2][Cc+2][64]
-  float* part;               // seam partial sums, tile parity planes [4][frames][3][H][W]
+  float* part;               // seam partial sums [frames][tile][3][band] (dec_part_floats)
   float* bd0;                // border pixels' combined pre-activation [frames][NB][64]
   float* be;                 // border pixels' decode.2 taps E [frames][NB][27]
   // rows / columns dec_fixup finishes (seams and the 2-pixel image border band), sorted
@@ -195,6 +208,7 @@ struct DecArgs {
   ConvTcArgs tail;           // composite / output / flags fields (alpha .. packed)
 };
 size_t dec_border_table_floats();
+size_t dec_part_floats(int frames, int H, int W);
 int dec_groups(int frames, int H, int W, int sms);
 int dec_border_pixels(int H, int W);                 // 2W + 2(H-2)
 void dec_fix_lines(DecArgs& a);                      // fills n_fix_rows/cols, fix_rows/cols

@@ -243,11 +243,17 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   t.cg = t.warp >> 2;
   t.lane_base = (uint32_t)(32 * (t.warp & 3)) << 16;
   const int rows = a.tile_rows;                           // 32, 64 or 128 tokens per CTA
-  t.n = blockIdx.x * rows + t.row;
   t.nact = CG * rows;
-  t.valid = t.row < rows && t.n < a.n_tok;
-  t.f = t.n / a.T;
-  t.tk = t.n - t.f * a.T;
+  // 128-token tiles: persistent, the CTA walks tiles blockIdx.x, + gridDim.x, ... with the
+  // block weights loaded once (smaller tiles: one tile per CTA, gridDim = tiles)
+  const int n_tiles = (a.n_tok + rows - 1) / rows;
+  auto set_tile = [&](int tile) {
+    t.n = tile * rows + t.row;
+    t.valid = t.row < rows && t.n < a.n_tok;
+    t.f = t.n / a.T;
+    t.tk = t.n - t.f * a.T;
+  };
+  set_tile(blockIdx.x);
   uint8_t* sa = sm + OFF_A;
   uint8_t* big = sm + OFF_BIG;
   constexpr int big_bytes = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
@@ -319,6 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   uint32_t phase = 0;
   float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // residual: 8 of 64 channels
   const int c0 = 8 * t.cg;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  set_tile(tile);
   auto store_resid = [&]() {
     if (!t.valid) return;
     float4* dst = reinterpret_cast<float4*>(a.resid_out + (size_t)t.n * C + c0);
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
       }
     }
   }
+  }  // tiles
   tc::fence_before();
   sync_act(t);
   TT();
@@ -905,6 +914,7 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
   if (a.tile_rows != 32 && a.tile_rows != 64 && a.tile_rows != 128)
     a.tile_rows = token_tc_tile_rows(a.n_tok, sms);
   dim3 grid((a.n_tok + a.tile_rows - 1) / a.tile_rows), block(THREADS);
+  const dim3 grid_tc(a.tile_rows == 128 ? std::min<unsigned>(grid.x, (unsigned)sms) : grid.x);
   if (a.tile_rows < 128 && a.kin == (mode == TOK_EMBED ? 256 : a.kin)) {
     const int smem = mode == TOK_EMBED ? smem_bytes<TOK_EMBED>(a)
                    : (mode == TOK_POST ? smem_bytes<TOK_POST>(a) : smem_bytes<TOK_SLOTKV>(a));
@@ -925,13 +935,13 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
   }
   switch (mode) {
     case TOK_EMBED:
-      launch_pdl(token_tc_kernel<TOK_EMBED>, grid, block, smem_bytes<TOK_EMBED>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_EMBED>, grid_tc, block, smem_bytes<TOK_EMBED>(a), s, a);
       break;
     case TOK_POST:
-      launch_pdl(token_tc_kernel<TOK_POST>, grid, block, smem_bytes<TOK_POST>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_POST>, grid_tc, block, smem_bytes<TOK_POST>(a), s, a);
       break;
     default:
-      launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid, block, smem_bytes<TOK_SLOTKV>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid_tc, block, smem_bytes<TOK_SLOTKV>(a), s, a);
       break;
   }
 #ifdef DR_TRACE

@@ -52,8 +52,8 @@ def main():
     if fn(1, tl, 384) == 384:
         v = np.frombuffer(tl, dtype=np.uint64).reshape(6, 64).astype(np.int64)
         st = v[4, 0]
-        print("  CTA 0 timeline (us from start): phase: MMA issue start / D committed / epi1 done / E committed / epi2 done")
-        for i in list(range(0, 12)) + list(range(12, 64, 8)):
+        print("  CTA 0 timeline (us from start): quad: MMA issue start / D committed / epi1 done / E committed / epi2 done")
+        for i in range(16):
             print("    %2d: %7.2f %7.2f %7.2f %7.2f %7.2f" % ((i,) + tuple((v[k, i] - st) / 1965.0 for k in (5, 0, 1, 2, 3))))
     for s, n in NAMES.items():
         per_warp = 1 if s <= 5 else 8

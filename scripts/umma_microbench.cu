@@ -43,11 +43,12 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
   tc::fence_after();
   const uint32_t d = tmem;
   __shared__ uint64_t lbar;
-  if (MODE == 4 && threadIdx.x == 32) {
+  if ((MODE == 4 || MODE == 8) && threadIdx.x == 32) {
     tc::mbar_init(&lbar, 1);
     tc::fence_barrier_init();
     uint8_t* dst = b + 4 * 8 * N * 16;
-    for (int k = 0; k < ITERS / 16; ++k) {       // one 8 KB tap per 4 MMAs x 4
+    // MODE 4: one 8 KB tap per 4 MMAs x 4; MODE 8: 8 KB per MMA (the N = 256 decoder rate)
+    for (int k = 0; k < (MODE == 8 ? ITERS : ITERS / 16); ++k) {
       tc::mbar_arrive_expect_tx(&lbar, 8192);
       tc::bulk_load(dst, gsrc + (size_t)(k % 144) * 8192, 8192, &lbar);
       tc::mbar_wait(&lbar, (uint32_t)k & 1u);
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
 template <int N, int MODE = 0>
 void run(int sms, unsigned long long* d_out) {
   const int smem = 180 * 128 + 1024 + 4 * 8 * N * 16 + 8192 + 2048;
+  if (smem > 227 * 1024) { printf("mode %d N=%d: smem %d too large\n", MODE, N, smem); return; }
   cudaFuncSetAttribute(umma_bench<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   static uint8_t* gsrc = nullptr;
   if (!gsrc) { cudaMalloc(&gsrc, 144 * 8192); cudaMemset(gsrc, 0, 144 * 8192); }
@@ -127,6 +129,11 @@ int main() {
   run<64, 4>(sms, d_out);
   run<64, 6>(sms, d_out);
   run<64, 7>(sms, d_out);
+  run<256, 1>(sms, d_out);
+  run<256, 2>(sms, d_out);
+  run<256, 4>(sms, d_out);
+  run<256, 8>(sms, d_out);
+  run<128, 8>(sms, d_out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error: %s\n", cudaGetErrorString(e));
   return 0;
