@@ -60,9 +60,9 @@ constexpr int SLOT_BYTES = 2 * 256 * 16;         // one K step of an offset bloc
 constexpr int NSLOT = 8;                         // weight ring (K-step slots)
 constexpr int NBUF = 2;                          // quad buffers in TMEM (256 columns each)
 constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
-constexpr int NWARP = 19;
+constexpr int NWARP = 15;
 constexpr int THREADS = 32 * NWARP;
-constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 18;
+constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 14;
 constexpr uint32_t TM_COLS = 512;
 
 struct __align__(1024) DecSmem {
@@ -268,7 +268,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     }
     for (int i = 0; i < NBUF; ++i) {
       tc::mbar_init(&sm.d_full[i], 1);
-      tc::mbar_init(&sm.d_empty[i], 8);
+      tc::mbar_init(&sm.d_empty[i], 4);
       for (int p = 0; p < 4; ++p) {
         tc::mbar_init(&sm.a2_full[i][p], 8);
         tc::mbar_init(&sm.e_full[i][p], 1);
@@ -420,20 +420,25 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     }
   } else {
     // --------------------------------------------------------------- epilogue 2
-    // two warps per lane quarter: decode.2 taps 0-4 / 5-8 of the same pixels (distinct
-    // targets within a phase), one barrier per phase orders the read-modify-writes; then
-    // each warp re-fills its half of the phase's columns with the combined bias for the
-    // quad two steps on (the first two quads: filled up front)
-    const int q = warp & 3, hh = (warp - W_EPI2) >> 2;
+    // one warp per lane quarter scatters all 27 E values of its pixels.  Within a quad no
+    // two lanes hit the same accumulator (a phase's sources are 8 pixels apart and the
+    // quad's phases differ by at most one pixel), so only program order per lane and one
+    // barrier per quad (the wrap from px / py 6, 7 to 0, 1 of the next cell) order the
+    // read-modify-writes.  Then the warp re-fills the quad's columns with the combined
+    // bias for the quad two steps on (the first two quads: filled up front).
+    const int q = warp & 3;
     const int row = 32 * q + lane;
     const int tyl = row >> 3, txl = row & 7;
     const uint32_t lrow = (uint32_t)(32 * q) << 16;
-    uint32_t bias_h[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) bias_h[c] = __float_as_uint(sm.bias[32 * hh + c]);
     auto fill_bias = [&](int b, int p) {
-      DR_TMEM_ST16(qcol(b, p) + lrow + 32 * hh, bias_h);
-      DR_TMEM_ST16(qcol(b, p) + lrow + 32 * hh + 16, (bias_h + 16));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t bias_h[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) bias_h[c] = __float_as_uint(sm.bias[32 * h + c]);
+        DR_TMEM_ST16(qcol(b, p) + lrow + 32 * h, bias_h);
+        DR_TMEM_ST16(qcol(b, p) + lrow + 32 * h + 16, (bias_h + 16));
+      }
     };
     auto release = [&](int b) {                           // buffer b: bias in, free for D
       tc::tmem_wait_st();
@@ -446,37 +451,54 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       release(b);
     }
     for (int i = 0; i < nq4; ++i) {
-      const int g = g0 + i, b = i & 1;
-      // E of phase p + 1 is loaded from TMEM while this warp waits at phase p's barrier
-      uint32_t ev[32];
-      DT_WAIT(9, tc::mbar_wait(&sm.e_full[b][0], (uint32_t)(i >> 1) & 1u));
-      tc::fence_after();
-      DR_TMEM_LD16(qcol(b, 0) + lrow + 32, ev);
-      DR_TMEM_LD16(qcol(b, 0) + lrow + 48, (ev + 16));
-#pragma unroll 1
-      for (int p = 0; p < 4; ++p) {
-        const int py = 2 * (g >> 2) + (p >> 1), px = 2 * (g & 3) + (p & 1);
-        tc::tmem_wait_ld();
-        uint32_t cur[32];
+      const int g = g0 + i, b = i & 1, gy = g >> 2, gx = g & 3;
+      // The quad's 4 phases x 9 taps land on the 4 x 4 pixel block at (2 gy - 1, 2 gx - 1)
+      // of the lane's cell: summed in registers, then one read-modify-write per pixel.
+      float blk[3][4][4];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) cur[c] = ev[c];
-        const int yl = 8 * tyl + py, xl = 8 * txl + px;    // source pixel in the tile
-        const int y = y0 + yl, x = x0 + xl;
+      for (int co = 0; co < 3; ++co)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) blk[co][u][v] = 0.f;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int dy = p >> 1, dx = p & 1;
+        uint32_t ev[1][32];
+        DT_WAIT(9, tc::mbar_wait(&sm.e_full[b][p], (uint32_t)(i >> 1) & 1u));
+        tc::fence_after();
+        DR_TMEM_LD16(qcol(b, p) + lrow + 32, ev[0]);
+        DR_TMEM_LD16(qcol(b, p) + lrow + 48, (ev[0] + 16));
+        tc::tmem_wait_ld();
+        const int y = y0 + 8 * tyl + 2 * gy + dy, x = x0 + 8 * txl + 2 * gx + dx;   // source
         if (y < H && x < W && !on_border(y, x, H, W)) {
-          if (hh) epi2_rmw<5, 4>(sm, cur, yl, xl);
-          else epi2_rmw<0, 5>(sm, cur, yl, xl);
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+              for (int co = 0; co < 3; ++co)
+                blk[co][dy - ky + 2][dx - kx + 2] += __uint_as_float(ev[0][3 * (3 * ky + kx) + co]);
         }
-        if (p < 3) {
-          DT_WAIT(9, tc::mbar_wait(&sm.e_full[b][p + 1], (uint32_t)(i >> 1) & 1u));
-          tc::fence_after();
-          DR_TMEM_LD16(qcol(b, p + 1) + lrow + 32, ev);
-          DR_TMEM_LD16(qcol(b, p + 1) + lrow + 48, (ev + 16));
-        }
-        // phase order of the RMWs; also both warps of the quarter have read E
-        DT_WAIT(10, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
-        if (i + 2 < nq4) fill_bias(b, p);
       }
-      if (i + 2 < nq4) release(b);
+      {
+        const int r0 = 8 * tyl + 2 * gy, c0 = 8 * txl + 2 * gx;   // accumulator row / column
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int r = r0 + u, cc = acc_col(r, c0 + v);
+#pragma unroll
+            for (int co = 0; co < 3; ++co) sm.acc[co][r][cc] += blk[co][u][v];
+          }
+      }
+      __syncwarp();
+      if (i + 2 < nq4) {
+#pragma unroll 1
+        for (int p = 0; p < 4; ++p) fill_bias(b, p);
+        release(b);
+      }
+      DT_WAIT(10, asm volatile("bar.sync 2, 128;\n" ::: "memory"));   // quad order
       if (lane == 0 && warp == W_EPI2) DT_TL(3, i);
     }
   }

@@ -54,6 +54,13 @@ struct Smem {
   int dirty;
 };
 
+// bit i = (byte i of w != 0), i < 4: byte flags to 0x01 each, then the multiply by
+// 2^28 + 2^21 + 2^14 + 2^7 moves byte i's flag to bit 28 + i (all cross terms land on
+// distinct bits below 28 or above 31: no carries)
+DR_DEV uint32_t nibble4(uint32_t w) {
+  return ((__vcmpne4(w, 0u) & 0x01010101u) * 0x10204080u) >> 28;
+}
+
 DR_DEV void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
   uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   int n = valid ? 4 : 0;
@@ -146,11 +153,17 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   }
   MT(2);
 
-  // 1. m0 -> bits (one warp per 32-pixel word, bytes from smem)
-  for (int e = warp; e < NR0 * NW; e += NWARP) {
+  // 1. m0 -> bits: one thread per 32-pixel word (two 16-byte smem loads; per 4 bytes a
+  //    SIMD byte compare, then a multiply gathers the 4 flags into a nibble)
+  for (int e = tid; e < NR0 * NW; e += NT) {
     const int row = e / NW, w = e - row * NW;
-    const uint32_t word = __ballot_sync(0xffffffffu, sm.m0[row][32 * w + lane] != 0);
-    if (lane == 0) sm.b0[row][w] = word;
+    const uint4* src = reinterpret_cast<const uint4*>(&sm.m0[row][32 * w]);
+    const uint4 q0 = src[0], q1 = src[1];
+    const uint32_t wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) word |= nibble4(wd[k]) << (4 * k);
+    sm.b0[row][w] = word;
   }
   __syncthreads();
   MT(3);
@@ -254,6 +267,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   };
 
   // outputs: m1 bytes (+ binary alpha)
+  if (a.m1 || (R == 0 && a.alpha))
   for (int e = tid; e < TH * TW; e += NT) {
     const int ty = e / TW, tx = e - ty * TW;
     const int y = y0 + ty, x = x0 + tx;
@@ -271,22 +285,25 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     const int NR1c = TH + 2 * R;
     // 3a. column words by warp-ballot bit transposes: task (word w, 32-row chunk c); lane i
     //     holds row y0-R+32c+i (clamped 'nearest'), ballot b yields window column 32w+b
+    //     (a 32 x 32 bit transpose in 5 shuffle stages: each swaps the off-diagonal
+    //     j x j blocks)
     for (int task = warp; task < NW * CW; task += NWARP) {
       const int w = task % NW, c = task / NW;
       const int j = 32 * c + lane;
-      uint32_t word = 0u;
+      uint32_t x = 0u;
       if (j < NR1c) {
         int yy = y0 - R + j;
         yy = yy < 0 ? 0 : (yy >= a.H ? a.H - 1 : yy);
-        word = sm.b1[yy - (y0 - R)][w];
+        x = sm.b1[yy - (y0 - R)][w];
       }
-      uint32_t mine = 0u;
 #pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        const uint32_t v = __ballot_sync(0xffffffffu, (word >> b) & 1u);
-        if (lane == b) mine = v;
+      for (int st = 16; st >= 1; st >>= 1) {
+        const uint32_t lo = st == 16 ? 0x0000FFFFu : (st == 8 ? 0x00FF00FFu : (st == 4 ? 0x0F0F0F0Fu
+                            : (st == 2 ? 0x33333333u : 0x55555555u)));
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, x, st);
+        x = (lane & st) ? ((x & ~lo) | ((o & ~lo) >> st)) : ((x & lo) | ((o & lo) << st));
       }
-      sm.col[c][32 * w + lane] = mine;
+      sm.col[c][32 * w + lane] = x;
     }
     __syncthreads();
     MT(5);
@@ -371,12 +388,12 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
       const int c = lane / P, ky = lane % P;
       const int y = i * P + ky, xl = j * P;
       uint32_t mb = 0, m0b = 0;
-      if (active) {
-        for (int kx = 0; kx < P; ++kx) {
-          mb |= m1bit(y, xl + kx) << kx;
-          const int px = xl + kx - xs, row = y - (y0 - Hd);
-          m0b |= (uint32_t)(sm.m0[row][px] != 0) << kx;   // raw m0 bytes (b0 is dilated in place)
-        }
+      if (active) {                       // the patch row: P bits of one m1 word (in frame)
+        const int px = xl - xs;
+        mb = (sm.b1[y - (y0 - R)][px >> 5] >> (px & 31)) & ((1u << P) - 1u);
+        const uint32_t* m0w = reinterpret_cast<const uint32_t*>(&sm.m0[y - (y0 - Hd)][px]);
+        m0b = nibble4(m0w[0]);            // raw m0 bytes (b0 is dilated in place)
+        if (P == 8) m0b |= nibble4(m0w[1]) << 4;
       }
       const bool any_unmasked = __any_sync(0xffffffffu, active && mb != ((1u << P) - 1u));
       if (lane == 0) a.token_valid[(size_t)f * T + tok] = any_unmasked ? 1 : 0;

@@ -56,7 +56,7 @@ def main():
         for i in range(16):
             print("    %2d: %7.2f %7.2f %7.2f %7.2f %7.2f" % ((i,) + tuple((v[k, i] - st) / 1965.0 for k in (5, 0, 1, 2, 3))))
     for s, n in NAMES.items():
-        per_warp = 1 if s <= 5 else 8
+        per_warp = 1 if s <= 5 else (4 if s >= 9 else 8)
         print(f"  {n:18s}", pct(us(t[:, s] / per_warp)))
 
 

@@ -54,6 +54,19 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
       tc::mbar_wait(&lbar, (uint32_t)k & 1u);
     }
   }
+  __shared__ uint64_t rbar[8];
+  if (MODE == 9 && threadIdx.x == 32) {             // 8 KB per MMA, 8 copies in flight
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&rbar[i], 1);
+    tc::fence_barrier_init();
+    uint8_t* dst = b + 4 * 8 * N * 16;              // 8 slots of 8 KB after the B ring
+    for (int k = 0; k < ITERS; ++k) {
+      const int sl = k & 7;
+      if (k >= 8) tc::mbar_wait(&rbar[sl], (uint32_t)((k >> 3) - 1) & 1u);
+      tc::mbar_arrive_expect_tx(&rbar[sl], 8192);
+      tc::bulk_load(dst + sl * 8192, gsrc + (size_t)(k % 144) * 8192, 8192, &rbar[sl]);
+    }
+    for (int sl = 0; sl < 8; ++sl) tc::mbar_wait(&rbar[sl], (uint32_t)((ITERS >> 3) - 1) & 1u);
+  }
   __shared__ uint64_t done;
   if (threadIdx.x == 0) { tc::mbar_init(&done, 1); tc::fence_barrier_init(); }
   __syncthreads();
@@ -96,12 +109,12 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
 
 template <int N, int MODE = 0>
 void run(int sms, unsigned long long* d_out) {
-  const int smem = 180 * 128 + 1024 + 4 * 8 * N * 16 + 8192 + 2048;
+  const int smem = 180 * 128 + 1024 + 4 * 8 * N * 16 + (MODE == 9 ? 8 * 8192 : 8192) + 2048;
   if (smem > 227 * 1024) { printf("mode %d N=%d: smem %d too large\n", MODE, N, smem); return; }
   cudaFuncSetAttribute(umma_bench<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   static uint8_t* gsrc = nullptr;
   if (!gsrc) { cudaMalloc(&gsrc, 144 * 8192); cudaMemset(gsrc, 0, 144 * 8192); }
-  const int thr = MODE == 6 ? 640 : 128;  // (MODE 7: warp 1 issues the TS MMAs)
+  const int thr = MODE == 6 ? 640 : 128;  // (MODE 9: warp 1 streams the copies)  // (MODE 7: warp 1 issues the TS MMAs)
   umma_bench<N, MODE><<<sms, thr, smem>>>(d_out, gsrc);
   umma_bench<N, MODE><<<sms, thr, smem>>>(d_out, gsrc);
   cudaDeviceSynchronize();
@@ -134,6 +147,9 @@ int main() {
   run<256, 4>(sms, d_out);
   run<256, 8>(sms, d_out);
   run<128, 8>(sms, d_out);
+  run<256, 9>(sms, d_out);
+  run<128, 9>(sms, d_out);
+  run<64, 9>(sms, d_out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error: %s\n", cudaGetErrorString(e));
   return 0;
