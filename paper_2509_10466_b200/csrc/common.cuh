@@ -63,6 +63,14 @@ DR_DEV float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
+
+// (tanh(x) + 1) / 2 = 1 / (1 + 2^(-2 x log2 e)): decode.2's output map (dstt.py:267) as one
+// ex2 and one reciprocal (MUFU, relative error ~1e-7; saturates to 0 / 1, NaN stays NaN)
+DR_DEV float tanh01(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + ex2(-2.8853900817779268f * x)));
+  return r;
+}
 // 2^x on the FMA/ALU pipes (no MUFU), for x <= ~16: x clamped at -125 (-> ~0; the
 // exponent-field add must not underflow, 2^f < 1 has biased exponent 126), split as
 // x = j + f with j = round(x) via the 1.5*2^23 magic add, f in [-0.5, 0.5]; 2^f by a

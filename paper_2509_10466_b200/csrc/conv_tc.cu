@@ -373,7 +373,7 @@ DR_DEV void gather_pixel(const ConvTcArgs& a, const float (&bias)[3], int x, int
   bool bad = false;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    const float out01 = (tanhf(o[ch]) + 1.0f) * 0.5f;
+    const float out01 = tanh01(o[ch]);
     bad |= !isfinite(out01);
     const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
     if (a.fill) a.fill[pl] = out01;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
       float out01[PX];
 #pragma unroll
       for (int i = 0; i < PX; ++i) {
-        out01[i] = (tanhf(o[ch][i]) + 1.0f) * 0.5f;
+        out01[i] = tanh01(o[ch][i]);
         bad |= !isfinite(out01[i]);
       }
       const size_t pl = ((size_t)f * 3 + ch) * plane + pix0;

@@ -57,7 +57,8 @@ constexpr int TY = 16, TX = 8;                   // token cells per tile (M = 12
 constexpr int TPY = 8 * TY, TPX = 8 * TX;        // 128 x 64 pixels
 constexpr int HTY = TY + 2, HTX = TX + 2;        // halo'd token tile
 constexpr int SLOT_BYTES = 2 * 256 * 16;         // one K step of an offset block: 8 KB
-constexpr int NSLOT = 8;                         // weight ring (K-step slots)
+constexpr int BLK_BYTES = 4 * SLOT_BYTES;        // one offset block (4 K steps): 32 KB
+constexpr int NBLK = 2;                          // weight ring (offset blocks)
 constexpr int NBUF = 2;                          // quad buffers in TMEM (256 columns each)
 constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
 constexpr int NWARP = 15;
@@ -68,11 +69,11 @@ constexpr uint32_t TM_COLS = 512;
 struct __align__(1024) DecSmem {
   uint8_t tok[HTY * HTX * 128];                  // 23040 B, SW128 rows (one token per row)
   alignas(1024) uint8_t w2[32 * 128];            // SW128 [32][64] fp16
-  alignas(1024) uint8_t w[NSLOT][SLOT_BYTES];
+  alignas(1024) uint8_t w[NBLK][BLK_BYTES];
   float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + 1]
   alignas(16) float bias[64];
   float b2[4];
-  uint64_t tok_full, w_full[NSLOT], w_empty[NSLOT];
+  uint64_t tok_full, w_full[NBLK], w_empty[NBLK];
   uint64_t d_full[NBUF], d_empty[NBUF], a2_full[NBUF][4], e_full[NBUF][4];
   uint32_t tmem_base;
 };
@@ -176,7 +177,7 @@ DR_DEV void dec_emit(const ConvTcArgs& a, int f, int y, int x, const float (&o)[
   bool bad = false;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    const float out01 = (tanhf(o[ch]) + 1.0f) * 0.5f;
+    const float out01 = tanh01(o[ch]);
     bad |= !isfinite(out01);
     const size_t pl = ((size_t)f * 3 + ch) * plane + pix;
     if (a.fill) a.fill[pl] = out01;
@@ -244,7 +245,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   const int y0 = 8 * ty0, x0 = 8 * tx0;                    // first pixel
   const int g0 = grp * 16 / G, g1 = (grp + 1) * 16 / G;   // this CTA's phase quads
   const int nq4 = g1 - g0;
-  const int c0 = 4 * dec_quad_first(g0), nchunk = 4 * dec_quad_first(g1) - c0;   // K-step slots
+  const int c0 = dec_quad_first(g0), nblk = dec_quad_first(g1) - c0;   // offset blocks
   const int H = a.H, W = a.W;
   const int NB = 2 * W + 2 * (H - 2);
 
@@ -262,7 +263,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 #endif
   if (threadIdx.x == 0) {
     tc::mbar_init(&sm.tok_full, 1);
-    for (int i = 0; i < NSLOT; ++i) {
+    for (int i = 0; i < NBLK; ++i) {
       tc::mbar_init(&sm.w_full[i], 1);
       tc::mbar_init(&sm.w_empty[i], 1);
     }
@@ -280,10 +281,10 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     // predecessor grid
     tc::mbar_arrive_expect_tx(&sm.tok_full, (uint32_t)(HTY * HTX * 128 + 32 * 128));
     tc::bulk_load(sm.w2, a.w2, 32 * 128, &sm.tok_full);
-    for (int kk = 0; kk < NSLOT && kk < nchunk; ++kk) {
-      tc::mbar_arrive_expect_tx(&sm.w_full[kk], SLOT_BYTES);
-      tc::bulk_load(sm.w[kk], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + kk) * SLOT_BYTES,
-                    SLOT_BYTES, &sm.w_full[kk]);
+    for (int k = 0; k < NBLK && k < nblk; ++k) {
+      tc::mbar_arrive_expect_tx(&sm.w_full[k], BLK_BYTES);
+      tc::bulk_load(sm.w[k], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + k) * BLK_BYTES,
+                    BLK_BYTES, &sm.w_full[k]);
     }
   }
   // zero the accumulator (the ring included), biases to smem
@@ -294,6 +295,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     if (threadIdx.x < 3) sm.b2[threadIdx.x] = __ldg(a.b2 + threadIdx.x);
   }
   pdl_wait();                    // predecessor complete: tokens written, its TMEM free
+  if (threadIdx.x == 0) tc::tma_load_4d(sm.tok, &tokmap, &sm.tok_full, 0, tx0, ty0, f);
   if (warp == W_MMA) tc::tmem_alloc<TM_COLS>(&sm.tmem_base);
   tc::fence_before();
   __syncthreads();
@@ -306,13 +308,12 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   auto qcol = [&](int b, int p) { return tbase + (uint32_t)(256 * b + 64 * p); };
   if (warp == W_LOAD) {
     if (lane == 0) {                                       // ------------------- loads
-      tc::tma_load_4d(sm.tok, &tokmap, &sm.tok_full, 0, tx0, ty0, f);
-      for (int kk = NSLOT; kk < nchunk; ++kk) {            // the first NSLOT: prologue
-        const int sl = kk % NSLOT;
-        tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(kk / NSLOT - 1) & 1u);
-        tc::mbar_arrive_expect_tx(&sm.w_full[sl], SLOT_BYTES);
-        tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + kk) * SLOT_BYTES,
-                      SLOT_BYTES, &sm.w_full[sl]);
+      for (int k = NBLK; k < nblk; ++k) {                 // the first NBLK: prologue
+        const int sl = k % NBLK;
+        tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(k / NBLK - 1) & 1u);
+        tc::mbar_arrive_expect_tx(&sm.w_full[sl], BLK_BYTES);
+        tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + k) * BLK_BYTES,
+                      BLK_BYTES, &sm.w_full[sl]);
       }
     }
   } else if (warp == W_MMA) {
@@ -322,24 +323,25 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     tc::fence_after();
     const uint64_t a0 = sdesc_sw128_sbo(tc::smem_u32(sm.tok), HTX * 128);
     const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 256 * 16, 128);
-    int kk = 0;
+    int k = 0;                                             // offset block
     for (int i = 0; i < nq4; ++i) {
       const int g = g0 + i, gy = g >> 2, gx = g & 3, b = i & 1;
-      DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i >> 1) & 1u));   // bias pre-filled
+      DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i >> 1) & 1u));   // E of quad i-2 read
       tc::fence_after();
       if (lane == 0) DT_TL(5, i);
       for (int ia = 0; ia < dec_quad_noff(gy); ++ia)
-        for (int ib = 0; ib < dec_quad_noff(gx); ++ib) {
+        for (int ib = 0; ib < dec_quad_noff(gx); ++ib, ++k) {
+          const uint32_t first = ia == 0 && ib == 0;        // first block: overwrite D
           const int off = tok_off(dec_quad_off(gy, ia), dec_quad_off(gx, ib));
-#pragma unroll 1
-          for (int ks = 0; ks < 4; ++ks, ++kk) {
-            const int sl = kk % NSLOT;
-            DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(kk / NSLOT) & 1u));
-            tc::fence_after();
+          const int sl = k % NBLK;
+          DT_WAIT(2, tc::mbar_wait(&sm.w_full[sl], (uint32_t)(k / NBLK) & 1u));
+          tc::fence_after();
+          const uint64_t bb = b0 + (uint64_t)(sl * (BLK_BYTES / 16));
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
             tc::mma_f16_warp(qcol(b, 0), a0 + (uint64_t)(off * 8 + ks * 2),
-                             b0 + (uint64_t)(sl * (SLOT_BYTES / 16)), idesc, 1u);
-            tc::mma_commit_warp(&sm.w_empty[sl]);
-          }
+                             bb + (uint64_t)(ks * (SLOT_BYTES / 16)), idesc, (first && ks == 0) ? 0u : 1u);
+          tc::mma_commit_warp(&sm.w_empty[sl]);
         }
       tc::mma_commit_warp(&sm.d_full[b]);
       if (lane == 0) DT_TL(0, i);
@@ -392,7 +394,15 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
           DR_TMEM_LD16(qcol(b, p + 1) + lrow, v[(p + 1) & 1]);
           DR_TMEM_LD16(qcol(b, p + 1) + lrow + 16, (v[(p + 1) & 1] + 16));
         }
-        const uint32_t* vp = v[p & 1];
+        uint32_t* vp = v[p & 1];
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {                  // combined bias: 128-bit broadcasts
+          const float4 bb = reinterpret_cast<const float4*>(sm.bias)[8 * set + c4];
+          vp[4 * c4] = __float_as_uint(__uint_as_float(vp[4 * c4]) + bb.x);
+          vp[4 * c4 + 1] = __float_as_uint(__uint_as_float(vp[4 * c4 + 1]) + bb.y);
+          vp[4 * c4 + 2] = __float_as_uint(__uint_as_float(vp[4 * c4 + 2]) + bb.z);
+          vp[4 * c4 + 3] = __float_as_uint(__uint_as_float(vp[4 * c4 + 3]) + bb.w);
+        }
         if (y < H && x < W && on_border(y, x, H, W)) {
           // image border: the combined pre-activation is redone by dec_border
           float4* bdst = reinterpret_cast<float4*>(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 32 * set);
@@ -424,43 +434,33 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     // two lanes hit the same accumulator (a phase's sources are 8 pixels apart and the
     // quad's phases differ by at most one pixel), so only program order per lane and one
     // barrier per quad (the wrap from px / py 6, 7 to 0, 1 of the next cell) order the
-    // read-modify-writes.  Then the warp re-fills the quad's columns with the combined
-    // bias for the quad two steps on (the first two quads: filled up front).
+    // read-modify-writes.  The quad's TMEM buffer is released as soon as its last E is in
+    // registers.
     const int q = warp & 3;
     const int row = 32 * q + lane;
     const int tyl = row >> 3, txl = row & 7;
     const uint32_t lrow = (uint32_t)(32 * q) << 16;
-    auto fill_bias = [&](int b, int p) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t bias_h[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) bias_h[c] = __float_as_uint(sm.bias[32 * h + c]);
-        DR_TMEM_ST16(qcol(b, p) + lrow + 32 * h, bias_h);
-        DR_TMEM_ST16(qcol(b, p) + lrow + 32 * h + 16, (bias_h + 16));
-      }
-    };
-    auto release = [&](int b) {                           // buffer b: bias in, free for D
-      tc::tmem_wait_st();
+    auto release = [&](int b) {                           // buffer b free for D
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.d_empty[b]);
     };
-    for (int b = 0; b < NBUF; ++b) {
-      for (int p = 0; p < 4; ++p) fill_bias(b, p);
-      release(b);
-    }
+    for (int b = 0; b < NBUF; ++b) release(b);
+    // The quad's 4 phases x 9 taps land on the 4 x 4 pixel block at (2 gy - 1, 2 gx - 1)
+    // of the lane's cell: summed in registers.  Along a quad row (gx = 0..3; a CTA's quads
+    // are whole rows) the next block shares two columns, which stay in registers: per quad
+    // one read-modify-write per pixel of the two columns left behind (all four at gx = 3).
+    float blk[3][4][4];
     for (int i = 0; i < nq4; ++i) {
       const int g = g0 + i, b = i & 1, gy = g >> 2, gx = g & 3;
-      // The quad's 4 phases x 9 taps land on the 4 x 4 pixel block at (2 gy - 1, 2 gx - 1)
-      // of the lane's cell: summed in registers, then one read-modify-write per pixel.
-      float blk[3][4][4];
 #pragma unroll
       for (int co = 0; co < 3; ++co)
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) blk[co][u][v] = 0.f;
+        for (int u = 0; u < 4; ++u) {
+          blk[co][u][0] = gx ? blk[co][u][2] : 0.f;
+          blk[co][u][1] = gx ? blk[co][u][3] : 0.f;
+          blk[co][u][2] = blk[co][u][3] = 0.f;
+        }
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         const int dy = p >> 1, dx = p & 1;
@@ -470,6 +470,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         DR_TMEM_LD16(qcol(b, p) + lrow + 32, ev[0]);
         DR_TMEM_LD16(qcol(b, p) + lrow + 48, (ev[0] + 16));
         tc::tmem_wait_ld();
+        if (p == 3 && i + 2 < nq4) release(b);
         const int y = y0 + 8 * tyl + 2 * gy + dy, x = x0 + 8 * txl + 2 * gx + dx;   // source
         if (y < H && x < W && !on_border(y, x, H, W)) {
 #pragma unroll
@@ -487,17 +488,13 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
+            if (v >= 2 && gx != 3) continue;
             const int r = r0 + u, cc = acc_col(r, c0 + v);
 #pragma unroll
             for (int co = 0; co < 3; ++co) sm.acc[co][r][cc] += blk[co][u][v];
           }
       }
       __syncwarp();
-      if (i + 2 < nq4) {
-#pragma unroll 1
-        for (int p = 0; p < 4; ++p) fill_bias(b, p);
-        release(b);
-      }
       DT_WAIT(10, asm volatile("bar.sync 2, 128;\n" ::: "memory"));   // quad order
       if (lane == 0 && warp == W_EPI2) DT_TL(3, i);
     }
@@ -645,7 +642,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         const int cc = acc_col(r, xx[j] + e - x0 + 1);
 #pragma unroll
         for (int co = 0; co < 3; ++co) {
-          out01[co][e] = (tanhf(accv(co, r, cc) + sm.b2[co]) + 1.0f) * 0.5f;
+          out01[co][e] = tanh01(accv(co, r, cc) + sm.b2[co]);
           bad |= !isfinite(out01[co][e]);
         }
       }

@@ -1,9 +1,9 @@
 """Per-CTA phase timeline of the tcgen05 token-chain kernels (diagnostic build, -DDR_TRACE).
 
     python -m paper_2509_10466_b200.build --trace
-    python scripts/token_trace.py
+    python scripts/token_trace.py [--config C5]
 
-One un-graphed C2 frame; for each token launch prints the median (over CTAs) time of every
+One un-graphed frame batch (C2 default); for each token launch prints the median (over CTAs) time of every
 phase between consecutive stamps of thread 0 (clock64, per SM; us at 1965 MHz).
 """
 import ctypes
@@ -20,13 +20,17 @@ NAMES = {0: "EMBED", 1: "POST", 2: "SLOTKV"}
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    args = ap.parse_args()
     _lib.LIB_PATH = TRACE_LIB
     import torch
 
     import bench
     from paper_2509_10466_b200 import DsttEngine
-    cfg, B, carried, _ = bench.workload("C2")
-    imgs, masks = bench.make_pool("C2", B, 0, cfg.width)
+    cfg, B, carried, _ = bench.workload(args.config)
+    imgs, masks = bench.make_pool(args.config, B, 0, cfg.width)
     eng = DsttEngine(cfg, seed=0)
     img = torch.from_numpy(imgs).cuda()
     msk = torch.from_numpy(masks.astype(np.uint8)).cuda()

@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
     }
   }
   __shared__ uint64_t rbar[8];
+  if (MODE == 10 && threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&rbar[i], 1);
+    tc::fence_barrier_init();
+  }
   if (MODE == 9 && threadIdx.x == 32) {             // 8 KB per MMA, 8 copies in flight
     for (int i = 0; i < 8; ++i) tc::mbar_init(&rbar[i], 1);
     tc::fence_barrier_init();
@@ -85,6 +89,10 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
     for (int i = 0; i < ITERS; ++i) {
       const int tap = (i >> 2) & 3, ks = i & 3;
       const uint64_t aa = MODE == 0 ? ad + (uint64_t)(ks * 2) : ad + (uint64_t)(offs[tap] * 8 + ks * 2);
+      if (MODE == 11) {                                   // wait + fence before EVERY MMA
+        tc::mbar_wait(&bar2, 0u ^ 1u);
+        tc::fence_after();
+      }
       if (MODE == 5 && ks == 0) {
         tc::mbar_wait(&bar2, 0u ^ 1u);                 // a completed phase: returns at once
         tc::fence_after();
@@ -94,7 +102,8 @@ __global__ void __launch_bounds__(640, 1) umma_bench(unsigned long long* out, co
         tc::mma_ts_f16_warp(d, d + 128 + (uint32_t)(8 * ks), bb, idesc, i != 0);
       else
         tc::mma_f16_warp(d, aa, bb, idesc, i != 0);
-      if (MODE >= 2 && MODE != 3 && ks == 3) tc::mma_commit_warp(&bar2);
+      if (MODE >= 2 && MODE != 3 && MODE != 10 && ks == 3) tc::mma_commit_warp(&bar2);
+      if (MODE == 10) tc::mma_commit_warp(&rbar[i & 7]);   // a commit after every MMA
     }
     tc::mma_commit_warp(&bar);
     tc::mbar_wait(&bar, 0);
@@ -150,6 +159,10 @@ int main() {
   run<256, 9>(sms, d_out);
   run<128, 9>(sms, d_out);
   run<64, 9>(sms, d_out);
+  run<256, 10>(sms, d_out);
+  run<256, 5>(sms, d_out);
+  run<256, 11>(sms, d_out);
+  run<128, 10>(sms, d_out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error: %s\n", cudaGetErrorString(e));
   return 0;

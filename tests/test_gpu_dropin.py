@@ -121,3 +121,45 @@ def test_dropin_errors_propagate_through_the_reference_client():
     rgb[bits] = 0
     call = client.inpaint_frame(1, rgb, RefBinaryMask(bits))
     assert client.memory.pushes == 1 and call.rgb.shape == rgb.shape
+
+
+def test_integration_md_ctypes_stub_runs_with_reference_classes():
+    """INTEGRATION.md §B is executable: its ctypes binding, loaded as a module of the
+    reference package (`dimreal.inpaint.b200`, relative imports of the reference's errors,
+    base and memory), builds an engine from the reference DsttEngine's state_dict and is
+    driven by the reference LocalEngineClient with real memory (NULL zero slot, pushed
+    device slots).  Its frames equal this repository's DsttEngine.inpaint bit for bit."""
+    import importlib.util
+    import re
+
+    from dimreal.inpaint import dstt as ref_dstt
+
+    from paper_2509_10466_b200 import _lib
+    text = (Path(__file__).resolve().parents[1] / "INTEGRATION.md").read_text()
+    sec = text[text.index("## B. Bind the C-ABI directly"):text.index("## C.")]
+    code = re.search(r"```python\n(.*?)```", sec, re.S).group(1)
+    code = code.replace('ctypes.CDLL("libdrb200.so")', f'ctypes.CDLL("{_lib.LIB_PATH}")')
+    spec = importlib.util.spec_from_loader("dimreal.inpaint.b200", loader=None)
+    mod = importlib.util.module_from_spec(spec)
+    mod.__package__ = "dimreal.inpaint"
+    exec(compile(code, "INTEGRATION.md#B", "exec"), mod.__dict__)
+
+    ref_cfg = ref_dstt.DsttConfig(width=64, height=64, temporal_groups=4)
+    stub = mod.B200DsttEngine(ref_dstt.DsttEngine(ref_cfg, seed=0), mask_dilate=3,
+                              feather_sigma=2.0)
+    ours = DsttEngine(DsttConfig.baseline(64, mask_dilate=3, mask_feather_sigma=2.0), seed=0)
+    client = LocalEngineClient(stub)
+    mem = ours.zero_memory()
+    for i, (rgb, bits) in enumerate(_frames(5, 64, seed=7)):
+        call = client.inpaint_frame(i, rgb, RefBinaryMask(bits))
+        r = ours.inpaint(rgb, RefBinaryMask(bits), mem)
+        mem = r.memory
+        assert np.array_equal(call.rgb, r.rgb), f"frame {i}"
+        assert client.memory.pushes == i + 1
+        assert torch.equal(client.memory.slots[1], r.memory.slots[1])
+    rgb, bits = _frames(1, 64, seed=8)[0]
+    rgb[bits] = 5
+    if bits.any():
+        with pytest.raises(Exception) as ei:
+            stub.inpaint(rgb, RefBinaryMask(bits), stub.zero_memory())
+        assert "redacted" in str(ei.value)
