@@ -47,6 +47,10 @@ constexpr int PRM_BYTES = 704 * 4;           // fp32 params of one block (Prm)
 constexpr int OFF_A = 0;
 constexpr int OFF_BIG = ATOM_A;
 
+// cp.async staging of a 128-token tile's inputs, chunk-major so that a warp's 32 rows are
+// contiguous: attn [8 chunks][128 rows][16 B], residual [8 chunk pairs][128 rows][32 B]
+constexpr int STAGE_ATTN = 8 * 128 * 16, STAGE_BYTES = STAGE_ATTN + 8 * 128 * 32;
+
 struct Ctl {
   float red[2][CG][M];                       // LayerNorm partial sums per column group
   uint64_t w_bar, mma_bar;
@@ -128,30 +132,41 @@ DR_DEV uint4 pack8(const float* v, const float* bias) {
                     pack_half2(v[4] + bias[4], v[5] + bias[5]), pack_half2(v[6] + bias[6], v[7] + bias[7]));
 }
 
-// Row LayerNorm (eps 1e-5, biased variance) over 64 channels split in CG groups of 8.
-// Writes this thread's 8 normalised values (one fp16 chunk) into the A atom.
+// Row LayerNorm (eps 1e-5, biased variance) over 64 channels split in CG groups of 8, with
+// one CTA barrier: every group publishes its mean and sum of squared deviations, which
+// combine exactly (Chan et al.: M2 = sum M2_g + 8 sum (m_g - mu)^2).  Writes this thread's
+// 8 normalised values (one fp16 chunk) into the A atom.  (ctl.red is rewritten only after
+// a later publish barrier, so one barrier per LayerNorm suffices.)
 DR_DEV void layer_norm_to_a(const float (&x)[8], const float* w, const float* b, uint8_t* sa,
                             Ctl& ctl, const Thr& t) {
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i) s += x[i];
-  ctl.red[0][t.cg][t.row] = s;
-  sync_act(t);
-  float mu = 0.f;
-#pragma unroll
-  for (int g = 0; g < CG; ++g) mu += ctl.red[0][g][t.row];
-  mu *= 1.f / 64.f;
+  const float mg = s * 0.125f;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float d = x[i] - mu;
+    const float d = x[i] - mg;
     q += d * d;
   }
+  ctl.red[0][t.cg][t.row] = mg;
   ctl.red[1][t.cg][t.row] = q;
   sync_act(t);
-  float var = 0.f;
+  float m[CG], mu = 0.f;
 #pragma unroll
-  for (int g = 0; g < CG; ++g) var += ctl.red[1][g][t.row];
+  for (int g = 0; g < CG; ++g) {
+    m[g] = ctl.red[0][g][t.row];
+    mu += m[g];
+  }
+  mu *= 1.f / CG;
+  float var = 0.f, dm = 0.f;
+#pragma unroll
+  for (int g = 0; g < CG; ++g) {
+    var += ctl.red[1][g][t.row];
+    const float e = m[g] - mu;
+    dm += e * e;
+  }
+  var = fmaf(8.f, dm, var);
   const float rs = rsqrtf(var * (1.f / 64.f) + 1e-5f);
   const int c = 8 * t.cg;
   float y[8];
@@ -325,8 +340,37 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   uint32_t phase = 0;
   float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // residual: 8 of 64 channels
   const int c0 = 8 * t.cg;
+  // Inputs of tile `tile` for this thread, started with cp.async (no registers held):
+  // EMBED straight into the swizzled xin operand (free once the embed GEMM has read it),
+  // POST / SLOTKV into the staging area (the residual, POST also the attention row chunk).
+  uint8_t* stage = reinterpret_cast<uint8_t*>(gscr);
+  const bool staged = rows == 128;
+  auto prefetch = [&](int tile) {
+    const int n = tile * rows + t.row;
+    const bool v = t.row < rows && n < a.n_tok;
+    const int nn = v ? n : 0;
+    if constexpr (MODE == TOK_EMBED) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.xin + (size_t)nn * a.kin) + 4 * t.cg;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ch = 4 * t.cg + c;
+        cp_async16_zfill(big + (ch >> 3) * ATOM_A + sw128(t.row, ch & 7), src + c, v);
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(a.resid_in + (size_t)nn * C + c0);
+      uint8_t* dr = stage + STAGE_ATTN + (t.cg * 128 + t.row) * 32;
+      cp_async16_zfill(dr, src, v);
+      cp_async16_zfill(dr + 16, src + 1, v);
+      if constexpr (MODE == TOK_POST)
+        cp_async16_zfill(stage + (t.cg * 128 + t.row) * 16,
+                         reinterpret_cast<const uint4*>(a.attn + (size_t)nn * C) + t.cg, v);
+    }
+    cp_async_commit();
+  };
+  if (staged) prefetch(blockIdx.x);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
   set_tile(tile);
+  const int next_tile = tile + gridDim.x;
   auto store_resid = [&]() {
     if (!t.valid) return;
     float4* dst = reinterpret_cast<float4*>(a.resid_out + (size_t)t.n * C + c0);
@@ -343,28 +387,44 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   // ------------------------------------------------------------ stage 0: first GEMM input
   if constexpr (MODE == TOK_EMBED) {
     // xin row: 256 halves = 4 K-atoms of 8 chunks; this thread copies chunks 4cg..4cg+3
-    const uint4* src = reinterpret_cast<const uint4*>(a.xin + (size_t)t.n * a.kin) + 4 * t.cg;
-    uint4 r[4];
+    if (staged) {
+      cp_async_wait<0>();
+    } else {
+      const uint4* src = reinterpret_cast<const uint4*>(a.xin + (size_t)t.n * a.kin) + 4 * t.cg;
+      uint4 r[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) r[c] = t.valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < 4; ++c) r[c] = t.valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int ch = 4 * t.cg + c;
-      *reinterpret_cast<uint4*>(big + (ch >> 3) * ATOM_A + sw128(t.row, ch & 7)) = r[c];
+      for (int c = 0; c < 4; ++c) {
+        const int ch = 4 * t.cg + c;
+        *reinterpret_cast<uint4*>(big + (ch >> 3) * ATOM_A + sw128(t.row, ch & 7)) = r[c];
+      }
     }
     publish(t);
     tc::mbar_wait(&ctl.w_bar, 0);
     tc::fence_after();
     if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(big), tc::smem_u32(sw), 64, 4, &ctl.mma_bar);
     wait_mma(ctl, phase);
+    if (staged && next_tile < n_tiles) prefetch(next_tile);   // xin operand read: refill
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = 0.f;
     add_d64(0, prm);
     store_resid();
   } else {
-    const float4* src = reinterpret_cast<const float4*>(a.resid_in + (size_t)t.n * C + c0);
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 f0 = t.valid ? __ldg(src) : z, f1 = t.valid ? __ldg(src + 1) : z;
+    float4 f0, f1;
+    if (staged) {
+      cp_async_wait<0>();
+      TT();
+      const float4* st = reinterpret_cast<const float4*>(stage + STAGE_ATTN + (t.cg * 128 + t.row) * 32);
+      f0 = st[0];
+      f1 = st[1];
+      if (MODE == TOK_SLOTKV && next_tile < n_tiles) prefetch(next_tile);
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(a.resid_in + (size_t)t.n * C + c0);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      f0 = t.valid ? __ldg(src) : z;
+      f1 = t.valid ? __ldg(src + 1) : z;
+    }
     x[0] = f0.x; x[1] = f0.y; x[2] = f0.z; x[3] = f0.w;
     x[4] = f1.x; x[5] = f1.y; x[6] = f1.z; x[7] = f1.w;
   }
@@ -372,10 +432,16 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   if constexpr (MODE == TOK_POST) {
     // ---------------------------------------------------------- out-proj + residual
     {
-      const uint4* src = reinterpret_cast<const uint4*>(a.attn + (size_t)t.n * C) + t.cg;
-      const uint4 r0 = t.valid ? __ldg(src) : make_uint4(0, 0, 0, 0);
+      uint4 r0;
+      if (staged) {
+        r0 = *reinterpret_cast<const uint4*>(stage + (t.cg * 128 + t.row) * 16);
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(a.attn + (size_t)t.n * C) + t.cg;
+        r0 = t.valid ? __ldg(src) : make_uint4(0, 0, 0, 0);
+      }
       *reinterpret_cast<uint4*>(sa + sw128(t.row, t.cg)) = r0;
     }
+    if (staged && next_tile < n_tiles) prefetch(next_tile);   // staging consumed: refill
     publish(t);
     tc::mbar_wait(&ctl.w_bar, 0);
     tc::fence_after();
@@ -448,6 +514,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
       __half* dst = which == 0 ? a.q : (which == 1 ? a.k : a.v);
       store_chunk(v, pn + Prm::bqkv + 8 * u, dst, a.T, t, h, u & 1);
     }
+    TT();
   } else {
     // k|v only: SLOTKV (one block) or the last block's slot K/V for every temporal block
     const int n_kv = MODE == TOK_SLOTKV ? 1 : a.n_kv;
@@ -875,7 +942,8 @@ template <int MODE>
 int smem_bytes(const TokenArgs& a) {
   constexpr int big = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
   // small tiles: the fp32 accumulator dump (rows x (192 + 4)); large: none
-  const int scratch = a.tile_rows < 128 ? a.tile_rows * 196 * 4 : 0;
+  // 128-token tiles: the next tile's attn / residual rows staged by cp.async (token_tc_kernel)
+  const int scratch = a.tile_rows < 128 ? a.tile_rows * 196 * 4 : (MODE == TOK_EMBED ? 0 : STAGE_BYTES);
   return ATOM_A + big + wlayout<MODE>(a).total() + (((int)sizeof(Ctl) + 15) & ~15) + scratch + 1024;
 }
 
