@@ -160,15 +160,17 @@ def stage_exps(cfg, kv_bands=3):
             "attn_temporal": cfg.heads * g * tg * kv_bands * tg}
 
 
-def frame_flops_reference(cfg):
+def frame_flops_reference(cfg, kv_bands=3):
     """Reference FlopCounterMode count per frame: the forward's dense
-    contractions; attention counts QK^T and PV, linear layers once."""
-    f = stage_flops(cfg)
+    contractions; attention counts QK^T and PV, linear layers once.  kv_bands=1: what runs
+    with cold memory here (the zero slots' keys are one constant: no slot K/V projection,
+    one key band per temporal query)."""
+    f = stage_flops(cfg, kv_bands)
     T, C = cfg.tokens, cfg.channels
     n_s = sum(b == "S" for b in cfg.blocks)
     n_t = len(cfg.blocks) - n_s
     per_block_lin = 2 * T * (4 * C * C + 4 * C * C)     # q,k,v,out + ffn (64x128 x2)
-    t_extra = 2 * 2 * T * 2 * C * C                     # k,v over both slots
+    t_extra = 2 * 2 * T * 2 * C * C if kv_bands == 3 else 0   # k,v over both slots
     return (2 * T * 4 * cfg.patch ** 2 * C + len(cfg.blocks) * per_block_lin
             + n_s * f["attn_spatial"] + n_t * (f["attn_temporal"] + t_extra)
             + f["vec2patch"] + f["decode0"] + f["decode2_composite"])
