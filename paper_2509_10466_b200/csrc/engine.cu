@@ -381,6 +381,9 @@ struct dr_engine {
   size_t wtc_v2p = 0;                // byte offset of the Vec2Patch image
   size_t te_d2 = 0;                  // decode.2 tap-expanded image (in timg)
   CUtensorMap map_raster{}, map_tok{};
+  // 128-token tile inputs of the token chains (2-D, rows of the workspace buffers)
+  CUtensorMap map_xin{}, map_attn{}, map_res[2]{};
+  bool tok_maps = false;
   // workspace
   int cap = 0;
   void* ws = nullptr;
@@ -461,7 +464,14 @@ struct dr_engine {
   void launch_tok(int mode, const TokenArgs& a_in, cudaStream_t s) const {
     TokenArgs a = a_in;
     if (tok_rows) a.tile_rows = tok_rows;
-    launch_token_tc(mode, a, s);
+    const CUtensorMap* mi = nullptr;
+    const CUtensorMap* mr = nullptr;
+    if (tok_maps && mode == TOK_EMBED && a.xin == xin) mi = &map_xin;
+    if (tok_maps && mode == TOK_POST && a.attn == attn) {
+      mi = &map_attn;
+      mr = a.resid_in == resid[0] ? &map_res[0] : (a.resid_in == resid[1] ? &map_res[1] : nullptr);
+    }
+    launch_token_tc(mode, a, s, mi, mr);
   }
 
   // Slot K/V cache: KV_ENTRIES entries (3 per memory stream: slot0, slot1, new slot),
@@ -554,12 +564,40 @@ struct dr_engine {
       const int rc = make_token_map4(&map_tok4, tok16, frames, R + 2, Cc + 2);
       if (rc) return rc;
     }
+    {   // token-chain inputs: 128-row boxes, 128B-swizzled
+      const cuuint64_t n = (cuuint64_t)frames * T;
+      int rc = make_rows_map(&map_xin, xin, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4 * cfg.patch * cfg.patch, n, 64);
+      if (!rc) rc = make_rows_map(&map_attn, attn, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, C, n, 64);
+      if (!rc) rc = make_rows_map(&map_res[0], resid[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, C, n, 32);
+      if (!rc) rc = make_rows_map(&map_res[1], resid[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, C, n, 32);
+      if (rc) return rc;
+      tok_maps = true;
+    }
     if (unf > 0) {
       int rc = make_nhwc_map(&map_raster, raster, unf, H, W, conv_tc_rows(64) + 2);
       if (rc) return rc;
       rc = make_token_map(&map_tok, tok16, unf, (R + 2) * (Cc + 2));
       if (rc) return rc;
     }
+    return DR_OK;
+  }
+
+  // 2-D TMA view of a row-major [n][width] buffer: box = `box` elements (128 B) x 128 rows,
+  // 128B swizzle (the UMMA K-major layout)
+  int make_rows_map(CUtensorMap* map, void* base, CUtensorMapDataType dt, int width,
+                    cuuint64_t n, int box) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode) return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const int esz = dt == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
+    const cuuint64_t dims[2] = {(cuuint64_t)width, n};
+    const cuuint64_t strides[1] = {(cuuint64_t)width * esz};
+    const cuuint32_t bx[2] = {(cuuint32_t)box, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, dt, 2, base, dims, strides, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(DR_ERR_CUDA, "cuTensorMapEncodeTiled (token rows) failed: " + std::to_string((int)r));
     return DR_OK;
   }
 

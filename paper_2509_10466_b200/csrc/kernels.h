@@ -1,5 +1,6 @@
 // Internal kernel interfaces of libdrb200 (not part of the C-ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -51,7 +52,11 @@ constexpr int MAX_TEMPORAL = 4;
 
 enum TokenMode { TOK_EMBED = 0, TOK_POST = 1, TOK_SLOTKV = 2 };
 
-void launch_token_tc(int mode, const TokenArgs& a, cudaStream_t s);   // tcgen05 + TMEM
+// tcgen05 + TMEM.  128-token tiles take their inputs by TMA when the maps are given
+// (2-D, 128B-swizzled, box 128 rows: m_in = xin [n][256] fp16 (EMBED) / attn [n][64] fp16
+// (POST), box 64 halves; m_res = residual [n][64] fp32, box 32 floats), else by cp.async.
+void launch_token_tc(int mode, const TokenArgs& a, cudaStream_t s,
+                     const CUtensorMap* m_in = nullptr, const CUtensorMap* m_res = nullptr);
 size_t token_tc_block_image_bytes();   // per block: weights + 704 fp32 params
 size_t token_tc_embed_image_bytes();   // We + be
 int token_tc_tile_rows(int n_tok, int sms);   // tokens per CTA the token kernels use

@@ -53,7 +53,7 @@ constexpr int STAGE_ATTN = 8 * 128 * 16, STAGE_BYTES = STAGE_ATTN + 8 * 128 * 32
 
 struct Ctl {
   float red[2][CG][M];                       // LayerNorm partial sums per column group
-  uint64_t w_bar, mma_bar;
+  uint64_t w_bar, mma_bar, in_bar;
   uint32_t tmem_base;
 };
 
@@ -243,7 +243,9 @@ __device__ unsigned long long g_tok_trace[1024 * TT_SLOTS];
 #endif
 
 template <int MODE>
-__global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(
+    const __grid_constant__ TokenArgs a, const __grid_constant__ CUtensorMap m_in,
+    const __grid_constant__ CUtensorMap m_res, int tma) {
 #ifdef DR_TRACE
   int tt_i = 0;
 #endif
@@ -284,7 +286,12 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   if (threadIdx.x == 0) {
     tc::mbar_init(&ctl.w_bar, 1);
     tc::mbar_init(&ctl.mma_bar, 1);
+    tc::mbar_init(&ctl.in_bar, 1);
     tc::fence_barrier_init();
+    if (tma) {
+      tc::tma_prefetch(&m_in);
+      if (MODE != TOK_EMBED) tc::tma_prefetch(&m_res);
+    }
   }
   __syncthreads();
   if (t.row >= rows) {                                     // idle lane quarter (small tiles)
@@ -343,8 +350,24 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
   // Inputs of tile `tile` for this thread, started with cp.async (no registers held):
   // EMBED straight into the swizzled xin operand (free once the embed GEMM has read it),
   // POST / SLOTKV into the staging area (the residual, POST also the attention row chunk).
-  uint8_t* stage = reinterpret_cast<uint8_t*>(gscr);
-  const bool staged = rows == 128;
+  uint8_t* stage = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gscr) + 1023) & ~uintptr_t(1023));
+  const bool staged = rows == 128 && !tma;
+  // TMA path (128-token tiles, maps given): thread 0 loads a tile's rows as 128B-swizzled
+  // boxes -- EMBED into the xin operand, POST the attention rows (= the out-proj A operand)
+  // and the residual's two 32-float boxes into the staging area; completion on in_bar
+  auto tma_fetch = [&](int tile) {
+    const int r0 = tile * rows;
+    if constexpr (MODE == TOK_EMBED) {
+      tc::mbar_arrive_expect_tx(&ctl.in_bar, 4u * ATOM_A);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tc::tma_load_2d(big + j * ATOM_A, &m_in, &ctl.in_bar, 64 * j, r0);
+    } else {
+      tc::mbar_arrive_expect_tx(&ctl.in_bar, (MODE == TOK_POST ? 3u : 2u) * ATOM_A);
+      if constexpr (MODE == TOK_POST) tc::tma_load_2d(stage, &m_in, &ctl.in_bar, 0, r0);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) tc::tma_load_2d(stage + (1 + j) * ATOM_A, &m_res, &ctl.in_bar, 32 * j, r0);
+    }
+  };
   auto prefetch = [&](int tile) {
     const int n = tile * rows + t.row;
     const bool v = t.row < rows && n < a.n_tok;
@@ -368,9 +391,15 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     cp_async_commit();
   };
   if (staged) prefetch(blockIdx.x);
+  if (tma && threadIdx.x == 0) tma_fetch(blockIdx.x);
+  uint32_t in_phase = 0;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
   set_tile(tile);
   const int next_tile = tile + gridDim.x;
+  if (tma) {
+    tc::mbar_wait(&ctl.in_bar, in_phase);
+    in_phase ^= 1u;
+  }
   auto store_resid = [&]() {
     if (!t.valid) return;
     float4* dst = reinterpret_cast<float4*>(a.resid_out + (size_t)t.n * C + c0);
@@ -389,7 +418,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     // xin row: 256 halves = 4 K-atoms of 8 chunks; this thread copies chunks 4cg..4cg+3
     if (staged) {
       cp_async_wait<0>();
-    } else {
+    } else if (!tma) {
       const uint4* src = reinterpret_cast<const uint4*>(a.xin + (size_t)t.n * a.kin) + 4 * t.cg;
       uint4 r[4];
 #pragma unroll
@@ -406,13 +435,22 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(big), tc::smem_u32(sw), 64, 4, &ctl.mma_bar);
     wait_mma(ctl, phase);
     if (staged && next_tile < n_tiles) prefetch(next_tile);   // xin operand read: refill
+    if (tma && threadIdx.x == 0 && next_tile < n_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tma_fetch(next_tile);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = 0.f;
     add_d64(0, prm);
     store_resid();
   } else {
     float4 f0, f1;
-    if (staged) {
+    if (tma) {
+      const uint8_t* bx = stage + (1 + (t.cg >> 2)) * ATOM_A + t.row * 128;
+      const int c = 2 * (t.cg & 3), sw = t.row & 7;
+      f0 = *reinterpret_cast<const float4*>(bx + ((c ^ sw) << 4));
+      f1 = *reinterpret_cast<const float4*>(bx + (((c + 1) ^ sw) << 4));
+    } else if (staged) {
       cp_async_wait<0>();
       TT();
       const float4* st = reinterpret_cast<const float4*>(stage + STAGE_ATTN + (t.cg * 128 + t.row) * 32);
@@ -431,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
 
   if constexpr (MODE == TOK_POST) {
     // ---------------------------------------------------------- out-proj + residual
-    {
+    if (!tma) {
       uint4 r0;
       if (staged) {
         r0 = *reinterpret_cast<const uint4*>(stage + (t.cg * 128 + t.row) * 16);
@@ -446,8 +484,12 @@ __global__ void __launch_bounds__(THREADS, 1) token_tc_kernel(TokenArgs a) {
     tc::mbar_wait(&ctl.w_bar, 0);
     tc::fence_after();
     const uint32_t wo = tc::smem_u32(sw), w1 = wo + (IMG_1 - IMG_O), w2 = wo + (IMG_2 - IMG_O);
-    if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(sa), wo, 64, 1, &ctl.mma_bar);
+    if (t.warp == 0) gemm_issue(tbase, tc::smem_u32(tma ? stage : sa), wo, 64, 1, &ctl.mma_bar);
     wait_mma(ctl, phase);
+    if (tma && threadIdx.x == 0 && next_tile < n_tiles) {   // attn operand + residual read
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tma_fetch(next_tile);
+    }
     add_d64(0, prm + Prm::bo);
     TT();
     // ---------------------------------------------------------- LN2 -> FFN1 -> GELU
@@ -943,7 +985,7 @@ int smem_bytes(const TokenArgs& a) {
   constexpr int big = MODE == TOK_EMBED ? 4 * ATOM_A : (MODE == TOK_POST ? 2 * ATOM_A : 0);
   // small tiles: the fp32 accumulator dump (rows x (192 + 4)); large: none
   // 128-token tiles: the next tile's attn / residual rows staged by cp.async (token_tc_kernel)
-  const int scratch = a.tile_rows < 128 ? a.tile_rows * 196 * 4 : (MODE == TOK_EMBED ? 0 : STAGE_BYTES);
+  const int scratch = a.tile_rows < 128 ? a.tile_rows * 196 * 4 : (MODE == TOK_EMBED ? 0 : STAGE_BYTES + 1024);
   return ATOM_A + big + wlayout<MODE>(a).total() + (((int)sizeof(Ctl) + 15) & ~15) + scratch + 1024;
 }
 
@@ -963,7 +1005,8 @@ int token_tc_tile_rows(int n_tok, int sms) {
 void tok_trace_snapshot(cudaStream_t s, int n_cta, int mode);
 #endif
 
-void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
+void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s, const CUtensorMap* m_in,
+                     const CUtensorMap* m_res) {
   static unsigned long long init = 0;
   once_per_device(init, [] {
     const int mx = 227 * 1024;
@@ -1001,15 +1044,20 @@ void launch_token_tc(int mode, const TokenArgs& a_in, cudaStream_t s) {
 #endif
     return;
   }
+  // TMA inputs: 128-token tiles with the maps this mode needs
+  const int tma = a.tile_rows == 128 && m_in && (mode == TOK_EMBED || m_res) && mode != TOK_SLOTKV;
+  CUtensorMap zin{}, zres{};
+  const CUtensorMap& mi = tma ? *m_in : zin;
+  const CUtensorMap& mr = (tma && m_res) ? *m_res : zres;
   switch (mode) {
     case TOK_EMBED:
-      launch_pdl(token_tc_kernel<TOK_EMBED>, grid_tc, block, smem_bytes<TOK_EMBED>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_EMBED>, grid_tc, block, smem_bytes<TOK_EMBED>(a), s, a, mi, mr, tma);
       break;
     case TOK_POST:
-      launch_pdl(token_tc_kernel<TOK_POST>, grid_tc, block, smem_bytes<TOK_POST>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_POST>, grid_tc, block, smem_bytes<TOK_POST>(a), s, a, mi, mr, tma);
       break;
     default:
-      launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid_tc, block, smem_bytes<TOK_SLOTKV>(a), s, a);
+      launch_pdl(token_tc_kernel<TOK_SLOTKV>, grid_tc, block, smem_bytes<TOK_SLOTKV>(a), s, a, mi, mr, tma);
       break;
   }
 #ifdef DR_TRACE
