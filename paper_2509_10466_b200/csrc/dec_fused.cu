@@ -61,6 +61,7 @@ constexpr int BLK_BYTES = 4 * SLOT_BYTES;        // one offset block (4 K steps)
 constexpr int NBLK = 2;                          // weight ring (offset blocks)
 constexpr int NBUF = 2;                          // quad buffers in TMEM (256 columns each)
 constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
+constexpr int ACC_C0 = 4;                        // column of tile pixel 0 (ring at 3 and 68)
 constexpr int NWARP = 15;
 constexpr int THREADS = 32 * NWARP;
 constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 14;
@@ -70,7 +71,7 @@ struct __align__(1024) DecSmem {
   uint8_t tok[HTY * HTX * 128];                  // 23040 B, SW128 rows (one token per row)
   alignas(1024) uint8_t w2[32 * 128];            // SW128 [32][64] fp16
   alignas(1024) uint8_t w[NBLK][BLK_BYTES];
-  float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + 1]
+  float acc[3][ACC_ROWS][ACC_RS];                // [co][qy + 1][swizzled qx + ACC_C0]
   alignas(16) float bias[64];
   float b2[4];
   uint64_t tok_full, w_full[NBLK], w_empty[NBLK];
@@ -100,13 +101,12 @@ DR_DEV uint64_t sdesc_sw128_sbo(uint32_t saddr, uint32_t sbo) {
          (1ull << 46) | (2ull << 61);
 }
 
-// accumulator column of tile pixel column c = qx + 1 (0..65) in row r = qy + 1: 8-column
-// blocks XOR-swizzled by the token row within 4 and the 32-pixel half, so the 32 lanes of
-// an epilogue-2 warp (4 token rows x 8 token columns, same phase) hit 32 banks
-DR_DEV int acc_col(int r, int c) {
-  const int g = ((r >> 3) & 3) | (((c >> 5) & 1) << 2);
-  return c ^ g;
-}
+// accumulator column of tile pixel column qx (-1..64) at c = qx + ACC_C0 in row r = qy + 1:
+// 8-column blocks XOR-swizzled by the token row within 4 and the 32-pixel half, so the 32
+// lanes of an epilogue-2 warp (4 token rows x 8 token columns, same phase) hit 32 banks.
+// A run of 4 pixels from a multiple of 4 stays one 16-byte group (acc_vec4).
+DR_DEV int acc_swz(int r, int c) { return ((r >> 3) & 3) | (((c >> 5) & 1) << 2); }
+DR_DEV int acc_col(int r, int c) { return c ^ acc_swz(r, c); }
 
 // border-correction table layout (floats): edges [4][12][64 ci][64 co], edge bias [4][64],
 // corners [4][64 ci][64 co], corner bias [4][64]; edges 0 top, 1 bottom, 2 left, 3 right;
@@ -126,6 +126,12 @@ DR_DEV uint32_t map_rank(uint32_t local_saddr, int rank) {
 DR_DEV float ld_dsmem_f32(uint32_t addr) {
   float v;
   asm("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+DR_DEV float4 ld_dsmem_f32x4(uint32_t addr) {
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
 
@@ -210,27 +216,6 @@ DR_DEV void dec_inputs(const ConvTcArgs& a, int f, int y, int x, float* alr, flo
 }
 
 namespace {
-
-// decode.2 taps TAP0 .. TAP0+NTAP-1 of source pixel (yl, xl) into the accumulator; the
-// targets are distinct, so load all, add, store all
-template <int TAP0, int NTAP>
-DR_DEV void epi2_rmw(DecSmem& sm, const uint32_t (&ev)[32], int yl, int xl) {
-  float cur[3 * NTAP];
-  int rr[NTAP], cc[NTAP];
-#pragma unroll
-  for (int k = 0; k < NTAP; ++k) {
-    const int tap = TAP0 + k, ky = tap / 3, kx = tap % 3;
-    rr[k] = yl - (ky - 1) + 1;
-    cc[k] = acc_col(rr[k], xl - (kx - 1) + 1);
-#pragma unroll
-    for (int co = 0; co < 3; ++co) cur[3 * k + co] = sm.acc[co][rr[k]][cc[k]];
-  }
-#pragma unroll
-  for (int k = 0; k < NTAP; ++k)
-#pragma unroll
-    for (int co = 0; co < 3; ++co)
-      sm.acc[co][rr[k]][cc[k]] = cur[3 * k + co] + __uint_as_float(ev[3 * (TAP0 + k) + co]);
-}
 
 __global__ void __launch_bounds__(THREADS, 1)
 dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_constant__ DecArgs a) {
@@ -483,7 +468,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         }
       }
       {
-        const int r0 = 8 * tyl + 2 * gy, c0 = 8 * txl + 2 * gx;   // accumulator row / column
+        const int r0 = 8 * tyl + 2 * gy, c0 = 8 * txl + 2 * gx - 1 + ACC_C0;   // block origin
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -533,6 +518,27 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 #pragma unroll
     for (int q = 1; q < 4; ++q) if (q < G) v += p[q];
     return v;
+  };
+  // the 4 pixels xl .. xl+3 (xl % 4 == 0) of row r, channel co: one 16-byte group (every
+  // rank's, summed in rank order), un-permuted
+  auto acc_run = [&](int co, int r, int xl, float (&o)[4]) {
+    const int c = xl + ACC_C0, g = acc_swz(r, c), base = c ^ (g & 4);
+    float4 v;
+    if (G == 1) {
+      v = *reinterpret_cast<const float4*>(&sm.acc[co][r][base]);
+    } else {
+      const uint32_t off = (uint32_t)(((co * ACC_ROWS + r) * ACC_RS + base) * 4);
+      v = ld_dsmem_f32x4(acc_rank[0] + off);
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (q < G) {
+          const float4 w = ld_dsmem_f32x4(acc_rank[q] + off);
+          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+        }
+    }
+    const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = e4[e ^ (g & 3)];
   };
   // pixel of the tile (+ ring) that dec_fixup finishes: next to another tile or within one
   // pixel of the image border
@@ -611,12 +617,13 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         uint8_t src[12];
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) *reinterpret_cast<uint32_t*>(src + 4 * ch) = r8[j][ch];
+        float run[3][4];
+#pragma unroll
+        for (int co = 0; co < 3; ++co) acc_run(co, r, xx[j] - x0, run[co]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int x = xx[j] + e, cc = acc_col(r, x - x0 + 1);
-          float o[3];
-#pragma unroll
-          for (int co = 0; co < 3; ++co) o[co] = accv(co, r, cc);
+          const int x = xx[j] + e;
+          float o[3] = {run[0][e], run[1][e], run[2][e]};
           if (is_fix(yy[j] - y0, x - x0, yy[j], x)) {
             const int bi = band_idx(yy[j] - y0, x - x0, ye, xe);
 #pragma unroll
@@ -638,11 +645,12 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       float out01[3][4];
       bool bad = false;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int cc = acc_col(r, xx[j] + e - x0 + 1);
+      for (int co = 0; co < 3; ++co) {
+        float run[4];
+        acc_run(co, r, xx[j] - x0, run);
 #pragma unroll
-        for (int co = 0; co < 3; ++co) {
-          out01[co][e] = tanh01(accv(co, r, cc) + sm.b2[co]);
+        for (int e = 0; e < 4; ++e) {
+          out01[co][e] = tanh01(run[e] + sm.b2[co]);
           bad |= !isfinite(out01[co][e]);
         }
       }
@@ -706,7 +714,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     }
     const int y = y0 + yl, x = x0 + xl;
     if (y < 0 || x < 0 || y >= H || x >= W) continue;
-    const int r = yl + 1, cc = acc_col(r, xl + 1), bi = band_idx(yl, xl, ye, xe);
+    const int r = yl + 1, cc = acc_col(r, xl + ACC_C0), bi = band_idx(yl, xl, ye, xe);
 #pragma unroll
     for (int co = 0; co < 3; ++co) band[co * DEC_BAND + bi] = accv(co, r, cc);
   }
@@ -809,7 +817,8 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   pdl_trigger();
   const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
   const int tid = threadIdx.x;
-  const int nmain = a.frames * 32;
+  const int sp = a.border_split;                        // CTAs per (frame, edge, phase)
+  const int nmain = a.frames * 32 * sp;
   if ((int)blockIdx.x >= nmain) {                        // corners: one warp each
     pdl_wait();
     const int c = ((int)blockIdx.x - nmain) * 8 + (tid >> 5);
@@ -818,7 +827,8 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
     border_pixel_warp(a, f, (k & 2) ? H - 1 : 0, (k & 1) ? W - 1 : 0, tid & 31);
     return;
   }
-  const int f = blockIdx.x / 32, ed = (blockIdx.x >> 3) & 3, r = blockIdx.x & 7;
+  const int bq = blockIdx.x / sp, part = blockIdx.x - bq * sp;
+  const int f = bq / 32, ed = (bq >> 3) & 3, r = bq & 7;
   const bool along_x = ed < 2;
   const int len = along_x ? W : H;
   const int line = ed == 0 ? 0 : (ed == 1 ? a.R - 1 : (ed == 2 ? 0 : a.Cc - 1));
@@ -833,7 +843,10 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   }
   for (int i = tid; i < 27 * 64; i += 256) sm.w2[i >> 6][i & 63] = __ldg(a.w2f + i);
   if (tid < 64) sm.eb[tid] = __ldg(a.dk + DK_EB + ed * 64 + tid);
-  const int k_lo = r == 0 ? 1 : 0, k_hi = (len - 2 - r) >= 0 ? (len - 2 - r) / 8 : -1;
+  // this CTA's share of the edge pixels r + 8k, k in [k_lo, k_hi]
+  const int k_first = r == 0 ? 1 : 0, k_last = (len - 2 - r) >= 0 ? (len - 2 - r) / 8 : -1;
+  const int nk = k_last - k_first + 1, per = (nk + sp - 1) / sp;
+  const int k_lo = k_first + part * per, k_hi = min(k_last, k_lo + per - 1);
   const int PC = a.Cc + 2, PR = a.R + 2;
   pdl_wait();
   const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
@@ -926,16 +939,28 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
     }
     const int ty_a = max(0, y - 1) / TPY, ty_b = min(H - 1, y + 1) / TPY;
     const int tx_a = max(0, x - 1) / TPX, tx_b = min(W - 1, x + n) / TPX;
+    // every load of the item is issued before any is used (one memory round trip): the
+    // pixels' inputs, the partial sums of the <= 2 x 2 tiles holding them, border E
+    float alr[4], srcf[4][3];
+    uint8_t src8[4][3];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (e < n) dec_inputs(tl, f, y, x + e, &alr[e], srcf[e], src8[e]);
     float o[4][3];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
 #pragma unroll
       for (int co = 0; co < 3; ++co) o[e][co] = b2[co];
     // tile (ty, tx) holds pixel (y, x') iff y - y0 in [-1, ye] and x' - x0 in [-1, xe]
-    for (int ty = ty_a; ty <= ty_b; ++ty) {
+#pragma unroll
+    for (int dty = 0; dty < 2; ++dty) {
+      const int ty = ty_a + dty;
       const int yl = y - TPY * ty, ye = min(TPY, H - TPY * ty);
-      if (yl < -1 || yl > ye) continue;
-      for (int tx = tx_a; tx <= tx_b; ++tx) {
+      if (ty > ty_b || yl < -1 || yl > ye) continue;
+#pragma unroll
+      for (int dtx = 0; dtx < 2; ++dtx) {
+        const int tx = tx_a + dtx;
+        if (tx > tx_b) continue;
         const int xe = min(TPX, W - TPX * tx);
         const float* bp = a.part + ((size_t)(f * nty + ty) * ntx + tx) * 3 * DEC_BAND;
 #pragma unroll
@@ -948,25 +973,27 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
         }
       }
     }
-    for (int e = 0; e < n; ++e) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (e >= n) continue;
       const int xe = x + e;
-      float oo[3] = {o[e][0], o[e][1], o[e][2]};
       if (y <= 1 || xe <= 1 || y >= H - 2 || xe >= W - 2) {
         // image-border sources p = (y + ky - 1, xe + kx - 1), tap (ky, kx)
+#pragma unroll
         for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
           for (int kx = 0; kx < 3; ++kx) {
             const int py = y + ky - 1, px = xe + kx - 1;
             if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
             const float* ev = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
 #pragma unroll
-            for (int co = 0; co < 3; ++co) oo[co] += ev[co];
+            for (int co = 0; co < 3; ++co) o[e][co] += __ldg(ev + co);
           }
       }
-      float alr, srcf[3];
-      uint8_t src8[3];
-      dec_inputs(tl, f, y, xe, &alr, srcf, src8);
-      dec_emit(tl, f, y, xe, oo, alr, srcf, src8);
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (e < n) dec_emit(tl, f, y, x + e, o[e], alr[e], srcf[e], src8[e]);
   }
   // flags mirror (host path): the last CTA to finish publishes the frames' flags
   const ConvTcArgs& t = a.tail;
@@ -1071,9 +1098,12 @@ void launch_dec_border(const DecArgs& a, cudaStream_t s) {
   once_per_device(init, [&] {
     cudaFuncSetAttribute(dec_border_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
-  // frames x 4 edges x 8 phases, then the corners (8 per CTA)
-  const int blocks = a.frames * 32 + (4 * a.frames + 7) / 8;
-  launch_pdl(dec_border_kernel, dim3(blocks), dim3(256), smem, s, a);
+  // frames x 4 edges x 8 phases (x split: about two CTAs per SM at small batches), then the
+  // corners (8 per CTA)
+  DecArgs b = a;
+  b.border_split = std::min(8, std::max(1, (2 * device_sms() + a.frames * 32 - 1) / (a.frames * 32)));
+  const int blocks = a.frames * 32 * b.border_split + (4 * a.frames + 7) / 8;
+  launch_pdl(dec_border_kernel, dim3(blocks), dim3(256), smem, s, b);
 }
 
 void launch_dec_fixup(const DecArgs& a, cudaStream_t s) {

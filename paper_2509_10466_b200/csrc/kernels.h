@@ -195,6 +195,7 @@ __host__ __device__ inline int dec_quad_first(int g) {     // offset blocks befo
 struct DecArgs {
   int frames, H, W, R, Cc;
   int groups;                // parts per tile (cluster size): 1, 2 or 4; each takes 16 / groups quads
+  int border_split;          // dec_border CTAs per (frame, edge, phase) (set by its launcher)
   // 36 offset blocks in quad order, offsets du-major: [k-chunk 8][4 phases x 64 co][8 ci]
   // fp16 (phase p = 2 (py & 1) + (px & 1) of the quad)
   const void* wcomb;
