@@ -44,6 +44,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.h"
@@ -79,6 +80,13 @@ struct __align__(1024) DecSmem {
   uint32_t tmem_base;
 };
 static_assert(sizeof(DecSmem) + 1024 <= 227 * 1024, "fused decoder shared memory");
+
+// The i-th phase quad of cluster rank `grp` of `G`: whole quad rows, 16 / G quads each.
+// (Anti-diagonal classes (gy + gx) % G balance the offset blocks better, 9 / 8 / 9 / 8 vs
+// 12 / 6 / 6 / 12 at G = 4, but lose epilogue 2's row carry: measured slower.)
+DR_DEV int quad_at(int grp, int G, int i) { return grp * (16 / G) + i; }
+// global offset block of this CTA's kk-th weight block (the prologue's first blocks)
+DR_DEV int block_at(int grp, int G, int kk) { return dec_quad_first(quad_at(grp, G, 0)) + kk; }
 
 // token-tile row offset of the A operand for token offset (du, dv)
 DR_DEV int tok_off(int du, int dv) { return (1 + du) * HTX + (1 + dv); }
@@ -228,9 +236,12 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   const int f = blockIdx.z;
   const int ty0 = tile_y * TY, tx0 = tile_x * TX;          // first token cell
   const int y0 = 8 * ty0, x0 = 8 * tx0;                    // first pixel
-  const int g0 = grp * 16 / G, g1 = (grp + 1) * 16 / G;   // this CTA's phase quads
-  const int nq4 = g1 - g0;
-  const int c0 = dec_quad_first(g0), nblk = dec_quad_first(g1) - c0;   // offset blocks
+  const int nq4 = 16 / G;                                   // this CTA's phase quads
+  int nblk = 0;                                              // ... and their offset blocks
+  for (int i = 0; i < nq4; ++i) {
+    const int g = quad_at(grp, G, i);
+    nblk += dec_quad_noff(g >> 2) * dec_quad_noff(g & 3);
+  }
   const int H = a.H, W = a.W;
   const int NB = 2 * W + 2 * (H - 2);
 
@@ -268,7 +279,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     tc::bulk_load(sm.w2, a.w2, 32 * 128, &sm.tok_full);
     for (int k = 0; k < NBLK && k < nblk; ++k) {
       tc::mbar_arrive_expect_tx(&sm.w_full[k], BLK_BYTES);
-      tc::bulk_load(sm.w[k], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + k) * BLK_BYTES,
+      tc::bulk_load(sm.w[k], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)block_at(grp, G, k) * BLK_BYTES,
                     BLK_BYTES, &sm.w_full[k]);
     }
   }
@@ -293,12 +304,18 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
   auto qcol = [&](int b, int p) { return tbase + (uint32_t)(256 * b + 64 * p); };
   if (warp == W_LOAD) {
     if (lane == 0) {                                       // ------------------- loads
-      for (int k = NBLK; k < nblk; ++k) {                 // the first NBLK: prologue
-        const int sl = k % NBLK;
-        tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(k / NBLK - 1) & 1u);
-        tc::mbar_arrive_expect_tx(&sm.w_full[sl], BLK_BYTES);
-        tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(c0 + k) * BLK_BYTES,
-                      BLK_BYTES, &sm.w_full[sl]);
+      int k = 0;                                           // this CTA's offset blocks in order
+      for (int i = 0; i < nq4; ++i) {
+        const int g = quad_at(grp, G, i), gb = dec_quad_first(g);
+        const int n = dec_quad_noff(g >> 2) * dec_quad_noff(g & 3);
+        for (int bo = 0; bo < n; ++bo, ++k) {
+          if (k < NBLK) continue;                          // issued in the prologue
+          const int sl = k % NBLK;
+          tc::mbar_wait(&sm.w_empty[sl], (uint32_t)(k / NBLK - 1) & 1u);
+          tc::mbar_arrive_expect_tx(&sm.w_full[sl], BLK_BYTES);
+          tc::bulk_load(sm.w[sl], reinterpret_cast<const uint8_t*>(a.wcomb) + (size_t)(gb + bo) * BLK_BYTES,
+                        BLK_BYTES, &sm.w_full[sl]);
+        }
       }
     }
   } else if (warp == W_MMA) {
@@ -310,7 +327,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     const uint64_t b0 = tc::sdesc(tc::smem_u32(sm.w[0]), 256 * 16, 128);
     int k = 0;                                             // offset block
     for (int i = 0; i < nq4; ++i) {
-      const int g = g0 + i, gy = g >> 2, gx = g & 3, b = i & 1;
+      const int g = quad_at(grp, G, i), gy = g >> 2, gx = g & 3, b = i & 1;
       DT_WAIT(3, tc::mbar_wait(&sm.d_empty[b], (uint32_t)(i >> 1) & 1u));   // E of quad i-2 read
       tc::fence_after();
       if (lane == 0) DT_TL(5, i);
@@ -361,7 +378,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     const uint32_t lrow = ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * set);
     const __half2 slope = __float2half2_rn(0.2f);
     for (int i = 0; i < nq4; ++i) {
-      const int g = g0 + i, b = i & 1;
+      const int g = quad_at(grp, G, i), b = i & 1;
       DT_WAIT(6, tc::mbar_wait(&sm.d_full[b], (uint32_t)(i >> 1) & 1u));
       tc::fence_after();
       uint32_t v[2][32];
@@ -437,13 +454,14 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     // one read-modify-write per pixel of the two columns left behind (all four at gx = 3).
     float blk[3][4][4];
     for (int i = 0; i < nq4; ++i) {
-      const int g = g0 + i, b = i & 1, gy = g >> 2, gx = g & 3;
+      const int g = quad_at(grp, G, i), b = i & 1, gy = g >> 2, gx = g & 3;
+      const bool carry = gx > 0;                          // previous quad: same row, gx - 1
 #pragma unroll
       for (int co = 0; co < 3; ++co)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          blk[co][u][0] = gx ? blk[co][u][2] : 0.f;
-          blk[co][u][1] = gx ? blk[co][u][3] : 0.f;
+          blk[co][u][0] = carry ? blk[co][u][2] : 0.f;
+          blk[co][u][1] = carry ? blk[co][u][3] : 0.f;
           blk[co][u][2] = blk[co][u][3] = 0.f;
         }
 #pragma unroll
@@ -473,7 +491,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            if (v >= 2 && gx != 3) continue;
+            if (v >= 2 && gx != 3) continue;                // (carried to gx + 1)
             const int r = r0 + u, cc = acc_col(r, c0 + v);
 #pragma unroll
             for (int co = 0; co < 3; ++co) sm.acc[co][r][cc] += blk[co][u][v];
@@ -725,81 +743,10 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 #endif
 }
 
-// Image-border pixel (y, x) by one warp (used for the 4 corners): pre-activation =
-// combined (stored by dec_fused) minus the decode.0 taps reading the canvas ring,
-// LeakyReLU, then decode.2's 27 taps E[u] = sum_ci W2[u][ci] d0[ci].  Lane l owns channels
-// 2l, 2l+1.
-DR_DEV void border_pixel_warp(const DecArgs& a, int f, int y, int x, int lane) {
-  const int H = a.H, W = a.W, NB = 2 * W + 2 * (H - 2);
-  const int bi = border_index(y, x, H, W);
-  const int co = 2 * lane;
-  const float* dk = a.dk;
-  const int PC = a.Cc + 2, PR = a.R + 2;
-  const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
-  // sum_ci K[ci][co, co+1] tok(ty, tx)[ci] over the warp (token channels broadcast by shuffle)
-  auto gemv = [&](const float* k, int ty, int tx, float2& acc) {
-    const __half2 tp = reinterpret_cast<const __half2*>(tokf + ((size_t)(ty + 1) * PC + (tx + 1)) * 64)[lane];
-    const float2 tv = __half22float2(tp);
-#pragma unroll
-    for (int c2 = 0; c2 < 32; ++c2) {
-      const float t0 = __shfl_sync(0xffffffffu, tv.x, c2), t1 = __shfl_sync(0xffffffffu, tv.y, c2);
-      const float2 w0 = __ldg(reinterpret_cast<const float2*>(k + (size_t)(2 * c2) * 64 + co));
-      const float2 w1 = __ldg(reinterpret_cast<const float2*>(k + (size_t)(2 * c2 + 1) * 64 + co));
-      acc.x = fmaf(w0.x, t0, fmaf(w1.x, t1, acc.x));
-      acc.y = fmaf(w0.y, t0, fmaf(w1.y, t1, acc.y));
-    }
-  };
-  float2 corr = make_float2(0.f, 0.f);
-  const bool e_t = y == 0, e_b = y == H - 1, e_l = x == 0, e_r = x == W - 1;
-#pragma unroll
-  for (int ed = 0; ed < 4; ++ed) {
-    if (!(ed == 0 ? e_t : (ed == 1 ? e_b : (ed == 2 ? e_l : e_r)))) continue;
-    const float2 eb = __ldg(reinterpret_cast<const float2*>(dk + DK_EB + ed * 64 + co));
-    corr.x += eb.x;
-    corr.y += eb.y;
-    const bool along_x = ed < 2;
-    const int pos = along_x ? x : y;
-    const int line = ed == 0 ? 0 : (ed == 1 ? a.R - 1 : (ed == 2 ? 0 : a.Cc - 1));
-    const int nlim = along_x ? a.Cc : a.R;
-    for (int t = pos / 8 - 1; t <= pos / 8 + 1; ++t) {
-      const int v = pos - 8 * t;
-      if (v < -2 || v > 9 || t < 0 || t >= nlim) continue;
-      gemv(dk + DK_EDGE + (size_t)(ed * 12 + v + 2) * 4096, along_x ? line : t, along_x ? t : line, corr);
-    }
-  }
-  for (int c4 = 0; c4 < 4; ++c4) {                      // doubly removed corner taps
-    const bool top = c4 < 2, left = (c4 & 1) == 0;
-    if (!((top ? e_t : e_b) && (left ? e_l : e_r))) continue;
-    float2 cs = __ldg(reinterpret_cast<const float2*>(dk + DK_CB + c4 * 64 + co));
-    gemv(dk + DK_CORNER + (size_t)c4 * 4096, top ? 0 : a.R - 1, left ? 0 : a.Cc - 1, cs);
-    corr.x -= cs.x;
-    corr.y -= cs.y;
-  }
-  float2 w2v[27];                                       // decode.2 weights of this lane's channels
-#pragma unroll
-  for (int u = 0; u < 27; ++u) w2v[u] = __ldg(reinterpret_cast<const float2*>(a.w2f + u * 64 + co));
-  const float2 pre = reinterpret_cast<const float2*>(a.bd0 + ((size_t)f * NB + bi) * 64)[lane];
-  float d0 = pre.x - corr.x, d1 = pre.y - corr.y;
-  d0 = d0 >= 0.f ? d0 : 0.2f * d0;
-  d1 = d1 >= 0.f ? d1 : 0.2f * d1;
-  // decode.0's output is fp16 on the tensor-core path: round the same way
-  d0 = __half2float(__float2half_rn(d0));
-  d1 = __half2float(__float2half_rn(d1));
-  float* out = a.be + ((size_t)f * NB + bi) * 27;
-  float es = 0.f;                                       // lane u < 27 ends with E[u]
-#pragma unroll
-  for (int u = 0; u < 27; ++u) {
-    float s = fmaf(w2v[u].x, d0, w2v[u].y * d1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == u) es = s;
-  }
-  if (lane < 27) out[lane] = es;
-}
-
-
-// The other border pixels, one CTA per (frame, edge, phase r = position mod 8) for the
-// edge's pixels at positions r + 8k (corners excluded): they share the 1-2 correction
+// Image-border pixels: pre-activation = the combined one (stored by dec_fused) minus the
+// decode.0 taps reading the canvas ring, LeakyReLU, fp16, then decode.2's 27 taps.  One CTA
+// per (frame, edge, phase r = position mod 8) for the edge's pixels at positions r + 8k
+// (corners excluded; one CTA per corner below): they share the 1-2 correction
 // matrices dK[edge][v] (v = r, and r + 8 for r <= 1 / r - 8 for r >= 6), staged in shared
 // memory with the edge's token row; per 64 pixels a [64 px x 64 ci] x [64 ci x 64 co]
 // product per tap, LeakyReLU, fp16 rounding, then the 27 decode.2 taps.
@@ -819,12 +766,60 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   const int tid = threadIdx.x;
   const int sp = a.border_split;                        // CTAs per (frame, edge, phase)
   const int nmain = a.frames * 32 * sp;
-  if ((int)blockIdx.x >= nmain) {                        // corners: one warp each
+  if ((int)blockIdx.x >= nmain) {
+    // one CTA per image corner: thread (co, q) sums a quarter (16 ci) of every correction
+    // gemv of the pixel (its two edges' taps, minus the corner table), reduced in smem
+    const int c = (int)blockIdx.x - nmain, f = c >> 2, k = c & 3;
+    const int y = (k & 2) ? H - 1 : 0, x = (k & 1) ? W - 1 : 0;
+    const int co = tid & 63, q = tid >> 6;
+    const int PC = a.Cc + 2, PR = a.R + 2;
     pdl_wait();
-    const int c = ((int)blockIdx.x - nmain) * 8 + (tid >> 5);
-    if (c >= 4 * a.frames) return;
-    const int f = c >> 2, k = c & 3;
-    border_pixel_warp(a, f, (k & 2) ? H - 1 : 0, (k & 1) ? W - 1 : 0, tid & 31);
+    const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
+    auto part16 = [&](const float* kmat, int ty, int tx) {  // sum over ci in [16q, 16q+16)
+      const __half* tp = tokf + ((size_t)(ty + 1) * PC + (tx + 1)) * 64 + 16 * q;
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc = fmaf(__half2float(tp[i]), __ldg(kmat + (size_t)(16 * q + i) * 64 + co), acc);
+      return acc;
+    };
+    float corr = 0.f;
+#pragma unroll
+    for (int ed = 0; ed < 4; ++ed) {
+      const bool on = ed == 0 ? y == 0 : (ed == 1 ? y == H - 1 : (ed == 2 ? x == 0 : x == W - 1));
+      if (!on) continue;
+      if (q == 0) corr += __ldg(a.dk + DK_EB + ed * 64 + co);
+      const bool along_x = ed < 2;
+      const int pos = along_x ? x : y;
+      const int line = ed == 0 ? 0 : (ed == 1 ? a.R - 1 : (ed == 2 ? 0 : a.Cc - 1));
+      const int nlim = along_x ? a.Cc : a.R;
+      for (int t = pos / 8 - 1; t <= pos / 8 + 1; ++t) {
+        const int v = pos - 8 * t;
+        if (v < -2 || v > 9 || t < 0 || t >= nlim) continue;
+        corr += part16(a.dk + DK_EDGE + (size_t)(ed * 12 + v + 2) * 4096, along_x ? line : t, along_x ? t : line);
+      }
+    }
+    {   // the doubly removed corner tap
+      const bool top = (k & 2) == 0, left = (k & 1) == 0;
+      const int c4 = (top ? 0 : 2) + (left ? 0 : 1);
+      corr -= part16(a.dk + DK_CORNER + (size_t)c4 * 4096, top ? 0 : a.R - 1, left ? 0 : a.Cc - 1);
+      if (q == 0) corr -= __ldg(a.dk + DK_CB + c4 * 64 + co);
+    }
+    float* red = &sm.d0[0][0];                           // [4][64] partials, then d0
+    red[q * 64 + co] = corr;
+    __syncthreads();
+    const int bi = border_index(y, x, H, W);
+    if (tid < 64) {
+      const float cs = (red[co] + red[64 + co]) + (red[128 + co] + red[192 + co]);
+      float d = a.bd0[((size_t)f * NB + bi) * 64 + co] - cs;
+      d = d >= 0.f ? d : 0.2f * d;
+      sm.w2[0][co] = __half2float(__float2half_rn(d));    // decode.0's output is fp16
+    }
+    __syncthreads();
+    if (tid < 27) {
+      float e = 0.f;
+      for (int cc = 0; cc < 64; ++cc) e = fmaf(__ldg(a.w2f + tid * 64 + cc), sm.w2[0][cc], e);
+      a.be[((size_t)f * NB + bi) * 27 + tid] = e;
+    }
     return;
   }
   const int bq = blockIdx.x / sp, part = blockIdx.x - bq * sp;
@@ -852,6 +847,7 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
   const int co = tid & 63, pg = tid >> 6;
   for (int kb = k_lo; kb <= k_hi; kb += 64) {
+    const int cnt = min(64, k_hi - kb + 1);              // pixels of this pass
     __syncthreads();
     for (int i = tid; i < 66 * 32; i += 256) {          // tokens kb-1 .. kb+64, half2 pairs
       const int j = i >> 5, c2 = i & 31, t = kb - 1 + j;
@@ -864,36 +860,43 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
       sm.tok[j][2 * c2 + 1] = v.y;
     }
     __syncthreads();
-    float acc[16];
+    // thread (co, pg) takes the pixels j = pg + 4i: 16 of them per pass, 4 when the pass
+    // has <= 16 (small batches: a quarter of the FMA chain per thread)
+    auto corr_pass = [&](auto ni_tag) {
+      constexpr int NI = decltype(ni_tag)::value;
+      float acc[NI];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = sm.eb[co];
-    for (int t = 0; t < nt; ++t) {
-      const int o = 1 + (t == 0 ? 0 : dt1);              // token row of pixel j: j + o
+      for (int i = 0; i < NI; ++i) acc[i] = sm.eb[co];
+      for (int t = 0; t < nt; ++t) {
+        const int o = 1 + (t == 0 ? 0 : dt1);            // token row of pixel j: j + o
 #pragma unroll 2
-      for (int c4 = 0; c4 < 16; ++c4) {
-        const float w0 = sm.k[t][4 * c4][co], w1 = sm.k[t][4 * c4 + 1][co];
-        const float w2 = sm.k[t][4 * c4 + 2][co], w3 = sm.k[t][4 * c4 + 3][co];
+        for (int c4 = 0; c4 < 16; ++c4) {
+          const float w0 = sm.k[t][4 * c4][co], w1 = sm.k[t][4 * c4 + 1][co];
+          const float w2 = sm.k[t][4 * c4 + 2][co], w3 = sm.k[t][4 * c4 + 3][co];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[16 * pg + i + o][4 * c4]);
-          acc[i] = fmaf(tv.x, w0, fmaf(tv.y, w1, fmaf(tv.z, w2, fmaf(tv.w, w3, acc[i]))));
+          for (int i = 0; i < NI; ++i) {
+            const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[pg + 4 * i + o][4 * c4]);
+            acc[i] = fmaf(tv.x, w0, fmaf(tv.y, w1, fmaf(tv.z, w2, fmaf(tv.w, w3, acc[i]))));
+          }
         }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int j = 16 * pg + i, k = kb + j, pos = r + 8 * k;
-      float d = 0.f;
-      if (k <= k_hi) {
-        const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
-        d = a.bd0[((size_t)f * NB + border_index(y, x, H, W)) * 64 + co] - acc[i];
-        d = d >= 0.f ? d : 0.2f * d;
-        d = __half2float(__float2half_rn(d));             // decode.0's output is fp16
+      for (int i = 0; i < NI; ++i) {
+        const int j = pg + 4 * i, k = kb + j, pos = r + 8 * k;
+        float d = 0.f;
+        if (k <= k_hi) {
+          const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
+          d = a.bd0[((size_t)f * NB + border_index(y, x, H, W)) * 64 + co] - acc[i];
+          d = d >= 0.f ? d : 0.2f * d;
+          d = __half2float(__float2half_rn(d));           // decode.0's output is fp16
+        }
+        sm.d0[j][co] = d;
       }
-      sm.d0[j][co] = d;
-    }
+    };
+    if (cnt <= 16) corr_pass(std::integral_constant<int, 4>{});
+    else corr_pass(std::integral_constant<int, 16>{});
     __syncthreads();
-    for (int i = tid; i < 64 * 27; i += 256) {
+    for (int i = tid; i < cnt * 27; i += 256) {
       const int j = i / 27, u = i - 27 * j, k = kb + j, pos = r + 8 * k;
       if (k > k_hi) continue;
       float e = 0.f;
@@ -939,28 +942,16 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
     }
     const int ty_a = max(0, y - 1) / TPY, ty_b = min(H - 1, y + 1) / TPY;
     const int tx_a = max(0, x - 1) / TPX, tx_b = min(W - 1, x + n) / TPX;
-    // every load of the item is issued before any is used (one memory round trip): the
-    // pixels' inputs, the partial sums of the <= 2 x 2 tiles holding them, border E
-    float alr[4], srcf[4][3];
-    uint8_t src8[4][3];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (e < n) dec_inputs(tl, f, y, x + e, &alr[e], srcf[e], src8[e]);
     float o[4][3];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
 #pragma unroll
       for (int co = 0; co < 3; ++co) o[e][co] = b2[co];
     // tile (ty, tx) holds pixel (y, x') iff y - y0 in [-1, ye] and x' - x0 in [-1, xe]
-#pragma unroll
-    for (int dty = 0; dty < 2; ++dty) {
-      const int ty = ty_a + dty;
+    for (int ty = ty_a; ty <= ty_b; ++ty) {
       const int yl = y - TPY * ty, ye = min(TPY, H - TPY * ty);
-      if (ty > ty_b || yl < -1 || yl > ye) continue;
-#pragma unroll
-      for (int dtx = 0; dtx < 2; ++dtx) {
-        const int tx = tx_a + dtx;
-        if (tx > tx_b) continue;
+      if (yl < -1 || yl > ye) continue;
+      for (int tx = tx_a; tx <= tx_b; ++tx) {
         const int xe = min(TPX, W - TPX * tx);
         const float* bp = a.part + ((size_t)(f * nty + ty) * ntx + tx) * 3 * DEC_BAND;
 #pragma unroll
@@ -973,27 +964,25 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
         }
       }
     }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (e >= n) continue;
+    for (int e = 0; e < n; ++e) {
       const int xe = x + e;
+      float oo[3] = {o[e][0], o[e][1], o[e][2]};
       if (y <= 1 || xe <= 1 || y >= H - 2 || xe >= W - 2) {
         // image-border sources p = (y + ky - 1, xe + kx - 1), tap (ky, kx)
-#pragma unroll
         for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
           for (int kx = 0; kx < 3; ++kx) {
             const int py = y + ky - 1, px = xe + kx - 1;
             if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
             const float* ev = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
 #pragma unroll
-            for (int co = 0; co < 3; ++co) o[e][co] += __ldg(ev + co);
+            for (int co = 0; co < 3; ++co) oo[co] += ev[co];
           }
       }
+      float alr, srcf[3];
+      uint8_t src8[3];
+      dec_inputs(tl, f, y, xe, &alr, srcf, src8);
+      dec_emit(tl, f, y, xe, oo, alr, srcf, src8);
     }
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (e < n) dec_emit(tl, f, y, x + e, o[e], alr[e], srcf[e], src8[e]);
   }
   // flags mirror (host path): the last CTA to finish publishes the frames' flags
   const ConvTcArgs& t = a.tail;
@@ -1098,11 +1087,11 @@ void launch_dec_border(const DecArgs& a, cudaStream_t s) {
   once_per_device(init, [&] {
     cudaFuncSetAttribute(dec_border_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
-  // frames x 4 edges x 8 phases (x split: about two CTAs per SM at small batches), then the
-  // corners (8 per CTA)
+  // frames x 4 edges x 8 phases (x split: about two CTAs per SM at small batches), then one
+  // CTA per corner
   DecArgs b = a;
-  b.border_split = std::min(8, std::max(1, (2 * device_sms() + a.frames * 32 - 1) / (a.frames * 32)));
-  const int blocks = a.frames * 32 * b.border_split + (4 * a.frames + 7) / 8;
+  b.border_split = std::min(4, std::max(1, (device_sms() + a.frames * 32 - 1) / (a.frames * 32)));
+  const int blocks = a.frames * 32 * b.border_split + 4 * a.frames;
   launch_pdl(dec_border_kernel, dim3(blocks), dim3(256), smem, s, b);
 }
 
