@@ -177,3 +177,36 @@ def test_both_decoders_on_reference_golden_and_small_frames(monkeypatch, fused):
     ref = O.inpaint_path(cfg, seed_parameters(cfg, 0), imgs, masks, (zero, zero))
     check_img(res["fill"].cpu().numpy(), ref["fill"], f"decoder {fused} 128^2 fill")
     check_img(res["out"].cpu().numpy(), ref["out"], f"decoder {fused} 128^2 composite")
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_decoders_on_partial_tiles_256x136(monkeypatch, fused):
+    """A non-square frame whose width is not a multiple of the fused decoder's 64-pixel
+    tile: 256 x 136 (tiles of 128 x 64 px -> a last column of 8-pixel tiles; token grid
+    32 x 17, bands of 136 tokens), batch 3 cold and then warm with per-frame memory, both
+    decoders against the oracle (u8 path: masks bit-exact, frames within the gate)."""
+    monkeypatch.setenv("DR_DEC_FUSED", fused)
+    cfg = DsttConfig(width=136, height=256, temporal_groups=4, mask_dilate=3,
+                     mask_feather_sigma=2.0)
+    eng = DsttEngine(cfg, seed=1)
+    rng = np.random.default_rng(11)
+    imgs = rng.random((3, 3, 256, 136)).astype(np.float32)
+    masks = np.zeros((3, 256, 136), bool)
+    masks[0, 0:40, 100:136] = True                        # touches the right / top border
+    masks[1, 120:140, 60:70] = True                       # straddles the tile seams
+    masks[2, 200:256, 0:30] = True                        # bottom-left corner
+    w = seed_parameters(cfg, 1)
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    res = eng.run(cuda(imgs), cuda(masks), None, want_masks=True)
+    out = res["out"].cpu().numpy()
+    slots = res["slot"]
+    for i in range(3):
+        ref = O.inpaint_path(cfg, w, imgs[i:i + 1], masks[i:i + 1], (zero, zero))
+        assert np.array_equal(res["m1"][i].cpu().numpy().astype(bool), ref["m1"][0])
+        check_img(out[i:i + 1], ref["out"], f"decoder {fused} 256x136 cold frame {i}")
+    warm = torch.from_numpy(rng.normal(0, 1, (3, cfg.tokens, 64)).astype(np.float32)).cuda()
+    res2 = eng.run(cuda(imgs), cuda(masks), (warm, slots))
+    for i in range(3):
+        ref = O.inpaint_path(cfg, w, imgs[i:i + 1], masks[i:i + 1],
+                             (warm[i].cpu().numpy(), slots[i].cpu().numpy()))
+        check_img(res2["out"][i:i + 1].cpu().numpy(), ref["out"], f"decoder {fused} 256x136 warm {i}")
