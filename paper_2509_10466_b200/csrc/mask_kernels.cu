@@ -19,6 +19,8 @@
 //  4. token validity (any pixel of the patch outside m1) and the network input
 //     cat[rgb zeroed in m1, m1] in conv-weight (c, ky, kx) order (dstt.py:253, :314-316;
 //     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79)
+#include <cstddef>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -53,6 +55,11 @@ struct Smem {
   double all_ones;
   int dirty;
 };
+
+// bt, col and vs are contiguous: the dilation's H_k scratch spans all three
+static_assert(offsetof(Smem, col) == offsetof(Smem, bt) + sizeof(Smem::bt) &&
+              offsetof(Smem, vs) == offsetof(Smem, col) + sizeof(Smem::col), "Smem scratch layout");
+constexpr int HS_WORDS = (int)((sizeof(Smem::bt) + sizeof(Smem::col) + sizeof(Smem::vs)) / 4);
 
 // bit i = (byte i of w != 0), i < 4: byte flags to 0x01 each, then the multiply by
 // 2^28 + 2^21 + 2^14 + 2^7 moves byte i's flag to bit 28 + i (all cross terms land on
@@ -174,7 +181,41 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   //    on the way never create in-frame bits a frame-clipped iteration would not (the
   //    Manhattan path between in-frame pixels stays in the frame).  Rows / pixels outside the
   //    frame are cleared when b1 is extracted.
-  if (r <= 8) {
+  // L1-ball form (the r-fold cross = all pixels within Manhattan distance r): phase A, every
+  // thread one (window row, word): the horizontal dilations H_k (k = 0..r) of the word,
+  // from the word and its two neighbours by funnel shifts (outside the window = 0), into
+  // the feather scratch (vs / col / bt, unused until the feather); phase B, every (output
+  // row, word): OR over dy of H_{r-|dy|} of window row + dy.  Two parallel phases instead
+  // of r dependent iterations.  Used when the H_k fit the scratch.
+  uint32_t* hs = &sm.bt[0][0];                                   // [k][row][word] over bt|col|vs
+  if (r >= 1 && r <= 8 && (r + 1) * NR0 * NW <= HS_WORDS) {
+    for (int e = tid; e < NR0 * NW; e += NT) {
+      const int row = e / NW, w = e - row * NW;
+      const uint32_t c = sm.b0[row][w];
+      const uint32_t lo = w > 0 ? sm.b0[row][w - 1] : 0u;        // pixels below (bit 31 side)
+      const uint32_t hi = w + 1 < NW ? sm.b0[row][w + 1] : 0u;   // pixels above
+      uint32_t h = c;
+      hs[row * NW + w] = h;
+      for (int k = 1; k <= r; ++k) {
+        h |= __funnelshift_l(lo, c, k) | __funnelshift_r(c, hi, k);
+        hs[(k * NR0 + row) * NW + w] = h;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < NR1 * NW; e += NT) {
+      const int row = e / NW, w = e - row * NW;
+      const int y = y0 - R + row;
+      uint32_t acc = 0;
+      if (y >= 0 && y < a.H) {
+        const int c0 = row + (Hd - R);                           // window row of the output
+        for (int dy = -r; dy <= r; ++dy) acc |= hs[((r - abs(dy)) * NR0 + c0 + dy) * NW + w];
+        const int xw = xs + 32 * w;                             // clear pixels outside the frame
+        if (xw < 0) acc &= xw + 32 <= 0 ? 0u : (0xffffffffu << (-xw));
+        if (xw + 32 > a.W) acc &= xw >= a.W ? 0u : (0xffffffffu >> (xw + 32 - a.W));
+      }
+      sm.b1[row][w] = acc;
+    }
+  } else if (r <= 8) {
     // small radius: warp-register form, no CTA barriers.  Warp k owns window rows
     // g0 = k*(32-2r) .. g0+31 (one row per lane, NW words in registers); vertical neighbours
     // come from shuffles (0 past the warp's rows), horizontal ones from the adjacent words.
