@@ -753,8 +753,8 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
 struct BorderSmem {
   float k[2][64][64];                            // [tap][ci][co]
   float tok[66][68];                             // tokens k0-1 .. k0+64 of the edge line
-  float d0[64][65];
-  float w2[27][65];                              // padded: lanes of one column hit 27 banks
+  float d0[64][68];                              // rows 16-byte aligned (float4 reads)
+  float w2[27][68];                              // 16-byte rows; a quarter warp's 8 u hit 32 banks
   float eb[64];
 };
 
@@ -899,9 +899,17 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
     for (int i = tid; i < cnt * 27; i += 256) {
       const int j = i / 27, u = i - 27 * j, k = kb + j, pos = r + 8 * k;
       if (k > k_hi) continue;
-      float e = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < 64; ++c) e = fmaf(sm.w2[u][c], sm.d0[j][c], e);
+      float e0 = 0.f, e1 = 0.f;                          // two chains, 128-bit operand loads
+#pragma unroll 4
+      for (int c = 0; c < 64; c += 8) {
+        const float4 wa = *reinterpret_cast<const float4*>(&sm.w2[u][c]);
+        const float4 da = *reinterpret_cast<const float4*>(&sm.d0[j][c]);
+        const float4 wb = *reinterpret_cast<const float4*>(&sm.w2[u][c + 4]);
+        const float4 db = *reinterpret_cast<const float4*>(&sm.d0[j][c + 4]);
+        e0 = fmaf(wa.x, da.x, fmaf(wa.y, da.y, fmaf(wa.z, da.z, fmaf(wa.w, da.w, e0))));
+        e1 = fmaf(wb.x, db.x, fmaf(wb.y, db.y, fmaf(wb.z, db.z, fmaf(wb.w, db.w, e1))));
+      }
+      const float e = e0 + e1;
       const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
       a.be[((size_t)f * NB + border_index(y, x, H, W)) * 27 + u] = e;
     }
