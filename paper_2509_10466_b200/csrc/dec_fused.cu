@@ -864,9 +864,15 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
     // has <= 16 (small batches: a quarter of the FMA chain per thread)
     auto corr_pass = [&](auto ni_tag) {
       constexpr int NI = decltype(ni_tag)::value;
-      float acc[NI];
+      float acc[NI], pre[NI];
 #pragma unroll
-      for (int i = 0; i < NI; ++i) acc[i] = sm.eb[co];
+      for (int i = 0; i < NI; ++i) {
+        acc[i] = sm.eb[co];
+        // the pixels' stored pre-activations, loaded before the products
+        const int k = kb + pg + 4 * i, pos = r + 8 * k;
+        const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
+        pre[i] = k <= k_hi ? __ldg(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + co) : 0.f;
+      }
       for (int t = 0; t < nt; ++t) {
         const int o = 1 + (t == 0 ? 0 : dt1);            // token row of pixel j: j + o
 #pragma unroll 2
@@ -882,11 +888,10 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
       }
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
-        const int j = pg + 4 * i, k = kb + j, pos = r + 8 * k;
+        const int j = pg + 4 * i, k = kb + j;
         float d = 0.f;
         if (k <= k_hi) {
-          const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
-          d = a.bd0[((size_t)f * NB + border_index(y, x, H, W)) * 64 + co] - acc[i];
+          d = pre[i] - acc[i];
           d = d >= 0.f ? d : 0.2f * d;
           d = __half2float(__float2half_rn(d));           // decode.0's output is fp16
         }
@@ -976,15 +981,21 @@ __global__ void __launch_bounds__(256) dec_fixup_kernel(const __grid_constant__ 
       const int xe = x + e;
       float oo[3] = {o[e][0], o[e][1], o[e][2]};
       if (y <= 1 || xe <= 1 || y >= H - 2 || xe >= W - 2) {
-        // image-border sources p = (y + ky - 1, xe + kx - 1), tap (ky, kx)
-        for (int ky = 0; ky < 3; ++ky)
-          for (int kx = 0; kx < 3; ++kx) {
-            const int py = y + ky - 1, px = xe + kx - 1;
-            if (py < 0 || px < 0 || py >= H || px >= W || !on_border(py, px, H, W)) continue;
-            const float* ev = a.be + ((size_t)f * NB + border_index(py, px, H, W)) * 27 + 3 * (3 * ky + kx);
+        // image-border sources p = (y + ky - 1, xe + kx - 1), tap (ky, kx): all nine loads
+        // issued before the sums (fixed tap order)
+        float ev9[9][3];
 #pragma unroll
-            for (int co = 0; co < 3; ++co) oo[co] += ev[co];
-          }
+        for (int t9 = 0; t9 < 9; ++t9) {
+          const int ky = t9 / 3, kx = t9 % 3, py = y + ky - 1, px = xe + kx - 1;
+          const bool src = py >= 0 && px >= 0 && py < H && px < W && on_border(py, px, H, W);
+          const float* ev = a.be + ((size_t)f * NB + (src ? border_index(py, px, H, W) : 0)) * 27 + 3 * t9;
+#pragma unroll
+          for (int co = 0; co < 3; ++co) ev9[t9][co] = src ? __ldg(ev + co) : 0.f;
+        }
+#pragma unroll
+        for (int t9 = 0; t9 < 9; ++t9)
+#pragma unroll
+          for (int co = 0; co < 3; ++co) oo[co] += ev9[t9][co];
       }
       float alr, srcf[3];
       uint8_t src8[3];
