@@ -195,7 +195,8 @@ def make_pool(name, n, rank, size, world=1, procs=None):
     else:
         keys = [rank * 100003 + i for i in range(n)]
     jobs = [(name, k, size) for k in keys]
-    procs = procs or min(len(jobs), max(1, (os.cpu_count() or 2) - 1), 32)
+    # (the ranks of one node generate their pools at the same time: share the host cores)
+    procs = procs or min(len(jobs), max(1, ((os.cpu_count() or 2) - 1) // max(1, world)), 32)
     if procs > 1 and len(jobs) > 2:
         import multiprocessing as mp
         with mp.get_context("fork").Pool(procs) as pool:

@@ -63,6 +63,9 @@ constexpr int NBLK = 2;                          // weight ring (offset blocks)
 constexpr int NBUF = 2;                          // quad buffers in TMEM (256 columns each)
 constexpr int ACC_RS = 72, ACC_ROWS = TPY + 2;   // accumulator row stride / rows (+ring)
 constexpr int ACC_C0 = 4;                        // column of tile pixel 0 (ring at 3 and 68)
+#ifndef DR_DEC_FINISH_RUNS
+#define DR_DEC_FINISH_RUNS 2
+#endif
 constexpr int NWARP = 15;
 constexpr int THREADS = 32 * NWARP;
 constexpr int W_LOAD = 0, W_MMA = 1, W_EPI1 = 2, W_EPI2 = 10, W_EMMA = 14;
@@ -596,14 +599,15 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
     *xl = 4 * (id % nq);
   };
   const ConvTcArgs& t = a.tail;
-  for (int idx = threadIdx.x; idx < nrun; idx += 2 * THREADS) {
-    int yy[2], xx[2];
-    bool act[2], fast[2], need[2];
-    float4 al[2], rf[2][3];
-    uint32_t r8[2][3];
-    // inputs of both runs first (vector loads), then the tails
+  constexpr int NJ = DR_DEC_FINISH_RUNS;                  // runs in flight per thread
+  for (int idx = threadIdx.x; idx < nrun; idx += NJ * THREADS) {
+    int yy[NJ], xx[NJ];
+    bool act[NJ], fast[NJ], need[NJ];
+    float4 al[NJ], rf[NJ][3];
+    uint32_t r8[NJ][3];
+    // inputs of all runs first (vector loads), then the tails
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int id = idx + j * THREADS;
       act[j] = id < nrun;
       int yl = 0, xl = 0;
@@ -626,7 +630,7 @@ dec_fused_kernel(const __grid_constant__ CUtensorMap tokmap, const __grid_consta
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       if (!act[j]) continue;
       const int r = yy[j] - y0 + 1;
       if (!fast[j]) {
