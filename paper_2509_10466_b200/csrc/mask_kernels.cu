@@ -119,7 +119,17 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   //    pieces, zero-filled off-frame; W % 8 == 0 keeps pieces inside a row) and rgb
   {
     const uint8_t* m0f = a.m0 + (size_t)f * plane;
-    if ((a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0) {
+    if ((a.W & 15) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 15) == 0) {
+      // 16-byte pieces (x0 and the halo start are multiples of 32, W of 16: a piece is
+      // entirely inside or outside the frame)
+      const int pieces = NR0 * NW * 2;
+      for (int e = tid; e < pieces; e += NT) {
+        const int row = e / (NW * 2), pc = e - row * (NW * 2);
+        const int y = y0 - Hd + row, x = xs + 16 * pc;
+        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
+        cp_async16_zfill(&sm.m0[row][16 * pc], v ? m0f + (size_t)y * a.W + x : m0f, v);
+      }
+    } else if ((a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0) {
       const int pieces = NR0 * NW * 8;
       for (int e = tid; e < pieces; e += NT) {
         const int row = e / (NW * 8), pc = e - row * (NW * 8);
