@@ -365,9 +365,13 @@ struct dr_engine {
   // GPU with tiles, else Vec2Patch -> decode.0 (+ decode.2's E planes) -> decode.2 gather,
   // whose finer grids suit one frame.  DR_DEC_FUSED=1 / 0 forces one (tests, A/B).
   int dec_force = -1;
-  static constexpr int kUnfusedMaxFrames = 2;        // auto: unfused up to this batch
+  // auto: fused from 96 tiles of 128 x 64 px (512^2: batch >= 3; 1024^2: every frame --
+  // measured at batch 1: 512^2 unfused ahead by ~4 us, 1024^2 fused ahead by 47 us)
+  static constexpr int kFusedMinTiles = 96;
+  int frame_tiles() const { return ((H + 127) / 128) * ((W + 63) / 64); }
+  int unfused_max_frames() const { return (kFusedMinTiles - 1) / frame_tiles(); }
   bool use_fused(int frames) const {
-    return dec_force >= 0 ? dec_force != 0 : frames > kUnfusedMaxFrames;
+    return dec_force >= 0 ? dec_force != 0 : frames > unfused_max_frames();
   }
   uint8_t* wcomb = nullptr;
   float* bcomb = nullptr;
@@ -535,7 +539,7 @@ struct dr_engine {
     const size_t npad = (size_t)frames * (R + 2) * (Cc + 2);
     const size_t o_at = take(tok * C * 2), o_t16 = take(npad * C * 2);
     // unfused decoder buffers for the batches it runs (<= unf frames), fused ones likewise
-    const int unf = use_fused(1) ? 0 : (dec_force == 0 ? frames : std::min(frames, kUnfusedMaxFrames));
+    const int unf = use_fused(1) ? 0 : (dec_force == 0 ? frames : std::min(frames, unfused_max_frames()));
     const bool fus = use_fused(frames);
     const size_t upx = frame_px() * unf;
     const size_t o_ras = take(upx * C * 2), o_ep = take(upx * 27 * 2);

@@ -221,14 +221,15 @@ def test_memory_fifo_and_memory_changes_output(rng):
     assert not np.array_equal(cold.rgb, warm.rgb)
 
 
-@pytest.mark.parametrize("graphed", ["1", "0"])
-def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed):
+@pytest.mark.parametrize("graphed,fused", [("1", "0"), ("0", "0"), ("1", "1")])
+def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed, fused):
     """dr_inpaint_u8_host (engine-held memory) == engine.inpaint with carried memory.  Nine
     frames: the host path's CUDA graphs (one per ring / slot K/V-cache signature) are
     captured on the first cycle and replayed after, with masks of different areas (so the
     flags word lands at a different offset of the packed read-back every frame).  Graphed
-    and direct launches."""
+    and direct launches; the fused decoder's span-packed output too."""
     monkeypatch.setenv("DR_HOST_GRAPH", graphed)       # read at engine creation
+    monkeypatch.setenv("DR_DEC_FUSED", fused)           # both decoders pack the read-back
     cfg = DsttConfig.baseline(64, mask_dilate=2, mask_feather_sigma=1.5)
     eng = DsttEngine(cfg, seed=4)
     mem = eng.zero_memory()
@@ -236,10 +237,13 @@ def test_host_buffer_path_equals_device_path(rng, monkeypatch, graphed):
         rgb, bits = _redacted(rng, 64, 64, 0.2 if i % 3 == 0 else 0.0)
         bits[20:22 + 3 * i, 30:31 + 2 * i] = True
         rgb[bits] = 0
+        dev = eng.run(torch.from_numpy(rgb)[None], torch.from_numpy(bits)[None], mem.slots)
         a = eng.inpaint(rgb, BinaryMask(bits), mem)
         mem = a.memory
         b = eng.inpaint_host(rgb, bits)
         assert np.array_equal(a.rgb, b)
+        # the span-packed read-back reassembles the device path's full u8 composite
+        assert np.array_equal(a.rgb, dev["out"][0].cpu().numpy())
 
 
 def test_host_buffer_path_edges_and_errors(rng):
