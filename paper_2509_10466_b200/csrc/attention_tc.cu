@@ -33,6 +33,8 @@
 // falls back to unmasked attention (per-block mode resolved on the host, engine.cu).
 #include <math.h>
 
+#include <cmath>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -627,9 +629,13 @@ double attn_cost(const AttnArgs& a, int qt, int k) {
   const int n_kb = (a.n_seg * a.band + KB - 1) / KB;
   const double blocks = (n_kb + k - 1) / k;
   const long per_sm = (n_cta + sms - 1) / sms;
+  // In a single wave, two co-resident CTAs overlap each other's fixed phases (measured at
+  // C2: 2 tiles x 4 key parts, 256 CTAs, 5303 frames/s vs 4 x 4, 128 CTAs, 5155)
+  const bool one_wave = per_sm <= res;
   auto wave = [&](long c) {                // c CTAs resident on one SM
     const int tiles = (int)std::min<long>(4, c * qt);
-    return 3.5 + (k > 1 ? 1.5 : 0.0) + blocks * 1.19 * (tiles / 4.0) / eff[tiles];
+    const double fixed = (3.5 + (k > 1 ? 1.5 : 0.0)) / (one_wave ? std::sqrt((double)std::min<long>(c, 2)) : 1.0);
+    return fixed + blocks * 1.19 * (tiles / 4.0) / eff[tiles];
   };
   const long full = per_sm / res, rem = per_sm % res;
   return full * wave(res) + (rem ? wave(rem) : 0.0);
