@@ -152,6 +152,14 @@ def stage_flops(cfg, kv_bands=3):
     }
 
 
+def stage_bytes(cfg):
+    """Algorithmic HBM bytes per frame of the HBM-class stages (device path: f32 rgb in).
+    Mask stage: m0 u8 + rgb f32 in; alpha f32, token validity u8 and the packed fp16
+    network input (4 channels per pixel) out."""
+    T, H, W = cfg.tokens, cfg.height, cfg.width
+    return {"mask_stage": H * W * (1 + 12 + 4 + 8) + T}
+
+
 def stage_exps(cfg, kv_bands=3):
     """Softmax exponentials per frame per attention launch (keys attended explicitly)."""
     T, g = cfg.tokens, cfg.temporal_groups
@@ -591,6 +599,11 @@ def run_ours(args):
         stages[name] = {"ms_per_step": round(per_step, 5), "launches_per_step": len(v) / n_prof,
                         "share": round(per_step / prof_step, 4) if prof_step else None,
                         "tflops": round(flops.get(name, 0) * B / (mean * 1e-3) / 1e12, 2)}
+        nbytes = stage_bytes(cfg).get(name)
+        if nbytes:                       # HBM-class stage: achieved GB/s vs the copy peak
+            gbs = nbytes * B / (mean * 1e-3) / 1e9
+            stages[name].update({"gbs": round(gbs, 1),
+                                 "hbm_frac": round(gbs / peaks()[0]["hbm_gbs"], 4)})
     dom = max(stages, key=lambda s: stages[s]["ms_per_step"]) if stages else None
     pk, pk_src = peaks()
     roof = None

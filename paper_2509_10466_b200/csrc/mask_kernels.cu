@@ -42,9 +42,9 @@ constexpr int SPAN_MAX = TW + 2 * MAXR;   // columns of the vertical pass
 constexpr int CW = 3;                      // column words: TH + 2R <= 78 rows < 96
 
 struct Smem {
-  uint8_t m0[NR_MAX][NW_MAX * 32];         // m0 bytes of tile + halo (cp.async)
   float rgb[3][TH][TW];                    // f32 input tile, or u8 HWC bytes (aliased)
-  uint32_t b0[NR_MAX][NW_MAX];             // m0 bits, rows y0-H.., words from xs
+  uint32_t b0[NR_MAX][NW_MAX];             // m0 bits, rows y0-H.., words from xs (read-only
+                                           // after the load phase)
   uint32_t b1[TH + 2 * MAXR][NW_MAX];      // m1 bits, rows y0-R..
   uint32_t bt[NR_MAX][NW_MAX];             // dilation ping-pong buffer
   uint32_t col[CW][NW_MAX * 32];           // m1 column words of window pixel px: bit j =
@@ -95,7 +95,7 @@ __device__ unsigned long long g_mask_trace[4096 * MT_SLOTS];
 
 // WH = halo words per side (compile time: every word loop is shift/mask, no division)
 template <int P, int WH>
-__global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
+__global__ void __launch_bounds__(NT, 4) mask_fused_kernel(MaskArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];   // keep the shared address space:
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);        // no integer round trip (LDS, not LD)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -115,74 +115,68 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
   pdl_wait();
   MT(1);
 
-  // 0. one async round trip for every input of the tile: m0 bytes (+halo, 4-byte
-  //    pieces, zero-filled off-frame; W % 8 == 0 keeps pieces inside a row) and rgb
+  // 0. rgb tile: cp.async (lands while the mask bits are built); 1. m0 -> bits straight
+  //    from global memory: one thread per 32-pixel word of the tile + halo (two 16-byte
+  //    loads, or 4-byte / byte pieces for narrow-aligned widths; off-frame = 0), per 4 bytes
+  //    a SIMD byte compare, then a multiply gathers the 4 flags into a nibble.  b0 stays
+  //    read-only from here on: the token phase takes the raw m0 bits of the redaction check
+  //    from it.
+  if (a.xin != nullptr && a.rgb_f32) {
+    for (int e = tid; e < 3 * TH * (TW / 4); e += NT) {
+      const int c = e / (TH * TW / 4), rem = e - c * (TH * TW / 4);
+      const int ty = rem / (TW / 4), q = rem - ty * (TW / 4);
+      const int y = y0 + ty, x = x0 + 4 * q;
+      const bool v = y < a.H && x < a.W;
+      const float* src = a.rgb_f32 + ((size_t)f * 3 + c) * plane + (size_t)y * a.W + x;
+      cp_async16_zfill(&sm.rgb[c][ty][4 * q], v ? src : a.rgb_f32, v);
+    }
+  } else if (a.xin != nullptr && a.rgb_u8) {
+    uint8_t* dst = reinterpret_cast<uint8_t*>(&sm.rgb[0][0][0]);  // [TH][TW][3] bytes
+    for (int e = tid; e < TH * TW * 3 / 4; e += NT) {
+      const int ty = e / (TW * 3 / 4), q = e - ty * (TW * 3 / 4);
+      const int y = y0 + ty;
+      const bool v = y < a.H && x0 + (4 * q) / 3 < a.W;
+      const uint8_t* src = a.rgb_u8 + ((size_t)f * plane + (size_t)y * a.W + x0) * 3 + 4 * q;
+      cp_async4_zfill(dst + ty * TW * 3 + 4 * q, v ? src : a.rgb_u8, v);
+    }
+  }
+  cp_async_commit();
   {
     const uint8_t* m0f = a.m0 + (size_t)f * plane;
-    if ((a.W & 15) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 15) == 0) {
-      // 16-byte pieces (x0 and the halo start are multiples of 32, W of 16: a piece is
-      // entirely inside or outside the frame)
-      const int pieces = NR0 * NW * 2;
-      for (int e = tid; e < pieces; e += NT) {
-        const int row = e / (NW * 2), pc = e - row * (NW * 2);
-        const int y = y0 - Hd + row, x = xs + 16 * pc;
-        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
-        cp_async16_zfill(&sm.m0[row][16 * pc], v ? m0f + (size_t)y * a.W + x : m0f, v);
-      }
-    } else if ((a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0) {
-      const int pieces = NR0 * NW * 8;
-      for (int e = tid; e < pieces; e += NT) {
-        const int row = e / (NW * 8), pc = e - row * (NW * 8);
-        const int y = y0 - Hd + row, x = xs + 4 * pc;
-        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
-        cp_async4_zfill(&sm.m0[row][4 * pc], v ? m0f + (size_t)y * a.W + x : m0f, v);
-      }
-    } else {                                      // odd widths (standalone mask stage)
-      for (int e = tid; e < NR0 * NW * 32; e += NT) {
-        const int row = e / (NW * 32), px = e - row * (NW * 32);
-        const int y = y0 - Hd + row, x = xs + px;
-        const bool v = y >= 0 && y < a.H && x >= 0 && x < a.W;
-        sm.m0[row][px] = v ? m0f[(size_t)y * a.W + x] : 0;
-      }
-    }
-    if (a.xin != nullptr && a.rgb_f32) {
-      for (int e = tid; e < 3 * TH * (TW / 4); e += NT) {
-        const int c = e / (TH * TW / 4), rem = e - c * (TH * TW / 4);
-        const int ty = rem / (TW / 4), q = rem - ty * (TW / 4);
-        const int y = y0 + ty, x = x0 + 4 * q;
-        const bool v = y < a.H && x < a.W;
-        const float* src = a.rgb_f32 + ((size_t)f * 3 + c) * plane + (size_t)y * a.W + x;
-        cp_async16_zfill(&sm.rgb[c][ty][4 * q], v ? src : a.rgb_f32, v);
-      }
-    } else if (a.xin != nullptr && a.rgb_u8) {
-      uint8_t* dst = reinterpret_cast<uint8_t*>(&sm.rgb[0][0][0]);  // [TH][TW][3] bytes
-      for (int e = tid; e < TH * TW * 3 / 4; e += NT) {
-        const int ty = e / (TW * 3 / 4), q = e - ty * (TW * 3 / 4);
-        const int y = y0 + ty;
-        const bool v = y < a.H && x0 + (4 * q) / 3 < a.W;
-        const uint8_t* src = a.rgb_u8 + ((size_t)f * plane + (size_t)y * a.W + x0) * 3 + 4 * q;
-        cp_async4_zfill(dst + ty * TW * 3 + 4 * q, v ? src : a.rgb_u8, v);
-      }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-  }
-  MT(2);
-
-  // 1. m0 -> bits: one thread per 32-pixel word (two 16-byte smem loads; per 4 bytes a
-  //    SIMD byte compare, then a multiply gathers the 4 flags into a nibble)
-  for (int e = tid; e < NR0 * NW; e += NT) {
-    const int row = e / NW, w = e - row * NW;
-    const uint4* src = reinterpret_cast<const uint4*>(&sm.m0[row][32 * w]);
-    const uint4 q0 = src[0], q1 = src[1];
-    const uint32_t wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    uint32_t word = 0;
+    const bool v16 = (a.W & 15) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 15) == 0;
+    const bool v4 = (a.W & 3) == 0 && (reinterpret_cast<uintptr_t>(a.m0) & 3) == 0;
+    // one 16-byte piece per thread (a warp reads 4 rows x 128 contiguous bytes), the two
+    // halves of a word joined by a lane shuffle (pieces 2k, 2k+1 sit in lanes 2j, 2j+1)
+    const int npc = NR0 * NW * 2;
+    for (int e = tid; e < ((npc + 31) & ~31); e += NT) {           // warp-uniform trips
+      const int row = e / (NW * 2), pc = e - row * (NW * 2);
+      const int y = y0 - Hd + row, x = xs + 16 * pc;
+      uint32_t h = 0;
+      if (e < npc && y >= 0 && y < a.H && x + 16 > 0 && x < a.W) {
+        const uint8_t* src = m0f + (size_t)y * a.W;
+        if (v16) {                         // W % 16 == 0: the piece is wholly in the frame
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + x));
+          h = nibble4(q.x) | nibble4(q.y) << 4 | nibble4(q.z) << 8 | nibble4(q.w) << 12;
+        } else if (v4) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) word |= nibble4(wd[k]) << (4 * k);
-    sm.b0[row][w] = word;
+          for (int k = 0; k < 4; ++k) {
+            const int xx = x + 4 * k;
+            if (xx >= 0 && xx < a.W) h |= nibble4(__ldg(reinterpret_cast<const uint32_t*>(src + xx))) << (4 * k);
+          }
+        } else {                           // odd widths (standalone mask stage)
+          for (int k = 0; k < 16; ++k) {
+            const int xx = x + k;
+            if (xx >= 0 && xx < a.W && src[xx]) h |= 1u << k;
+          }
+        }
+      }
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, h, 1);
+      if (e < npc && !(e & 1)) sm.b0[row][pc >> 1] = h | (o << 16);
+    }
   }
+  cp_async_wait<0>();
   __syncthreads();
+  MT(2);
   MT(3);
 
   // 2. m1 = r iterations of the 3x3 cross (masks._CROSS) over the whole b0 window, ping-pong
@@ -271,8 +265,12 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
       }
     }
   } else {
+    // b0 stays read-only (raw m0 bits for the token phase): iteration 0 reads b0, later
+    // ones ping-pong between bt and the vertical-pass scratch (unused until the feather)
+    static_assert(sizeof(Smem::vs) >= sizeof(Smem::bt), "dilation ping-pong scratch");
     uint32_t (*cur)[NW_MAX] = sm.b0;
     uint32_t (*nxt)[NW_MAX] = sm.bt;
+    uint32_t (*spare)[NW_MAX] = reinterpret_cast<uint32_t (*)[NW_MAX]>(&sm.vs[0][0]);
     for (int it = 0; it < r; ++it) {
       for (int e = tid; e < NR0 * NW; e += NT) {
         const int row = e / NW, w = e - row * NW;
@@ -284,7 +282,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
         nxt[row][w] = c | up | dn | (c << 1) | (lf >> 31) | (c >> 1) | (rt << 31);
       }
       __syncthreads();
-      uint32_t (*t)[NW_MAX] = cur;
+      uint32_t (*t)[NW_MAX] = cur == sm.b0 ? spare : cur;
       cur = nxt;
       nxt = t;
     }
@@ -359,43 +357,42 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
     __syncthreads();
     MT(5);
     // 3b. vertical pass (float64, scipy order) for the tile rows x span columns; the
-    //     window of row ty is bits ty .. ty+2R of the column word
+    //     window of row ty is bits ty .. ty+2R of the column word.  Warp ty owns row ty
+    //     (NT = 32 TH): one ballot per 32 columns gives the row's nonzero-column mask for
+    //     the horizontal pass's all-zero test
     const uint64_t need = (2 * R + 1 == 64) ? ~0ull : ((1ull << (2 * R + 1)) - 1ull);
-    for (int tx = tid & 31, ty = tid >> 5; tx < span; tx += 32) {   // ty < TH (NT = 32 TH)
-      double acc;
-      if (y0 + ty >= a.H) acc = 0.0;
-      else {
-        int x = x0 + tx - R;
-        x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
-        const int px = x - xs;
-        const uint64_t lo = (uint64_t)sm.col[0][px] | ((uint64_t)sm.col[1][px] << 32);
-        const uint64_t pat = ((lo >> ty) | (ty ? ((uint64_t)sm.col[2][px] << (64 - ty)) : 0ull)) & need;
-        if (pat == 0) acc = 0.0;
-        else if (pat == need) acc = sm.all_ones;
-        else {
-          // four interleaved float64 partial sums (dependency depth R/4 instead of R; the
-          // float64 result rounds to the same float32 as scipy's serial order except in
-          // vanishingly rare ties -- tests gate max-abs 1e-6 and >= 99.9 % bit-identical)
-          double sp[4] = {__dmul_rn((double)((pat >> R) & 1u), wc[0]), 0.0, 0.0, 0.0};
-          for (int jj = -R; jj < 0; ++jj) {
-            const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
-            sp[(jj + 64) & 3] = __fma_rn(pr, wc[jj], sp[(jj + 64) & 3]);
+    {
+      const int ty = warp;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {                                   // span <= 126 < 4 words
+        const int tx = 32 * c + lane;
+        float out = 0.f;
+        if (tx < span && y0 + ty < a.H) {
+          int x = x0 + tx - R;
+          x = x < 0 ? 0 : (x >= a.W ? a.W - 1 : x);
+          const int px = x - xs;
+          const uint64_t lo = (uint64_t)sm.col[0][px] | ((uint64_t)sm.col[1][px] << 32);
+          const uint64_t pat = ((lo >> ty) | (ty ? ((uint64_t)sm.col[2][px] << (64 - ty)) : 0ull)) & need;
+          if (pat == need) out = (float)sm.all_ones;
+          else if (pat != 0) {
+            // four interleaved float64 partial sums (dependency depth R/4 instead of R; the
+            // float64 result rounds to the same float32 as scipy's serial order except in
+            // vanishingly rare ties -- tests gate max-abs 1e-6 and >= 99.9 % bit-identical)
+            double sp[4] = {__dmul_rn((double)((pat >> R) & 1u), wc[0]), 0.0, 0.0, 0.0};
+            for (int jj = -R; jj < 0; ++jj) {
+              const double pr = (double)(((pat >> (R + jj)) & 1u) + ((pat >> (R - jj)) & 1u));
+              sp[(jj + 64) & 3] = __fma_rn(pr, wc[jj], sp[(jj + 64) & 3]);
+            }
+            out = (float)((sp[0] + sp[1]) + (sp[2] + sp[3]));
           }
-          acc = (sp[0] + sp[1]) + (sp[2] + sp[3]);
         }
+        if (tx < span) sm.vs[ty][tx] = out;
+        const uint32_t m = __ballot_sync(0xffffffffu, out != 0.f);
+        if (lane == 0) sm.nzm[ty][c] = m;
       }
-      sm.vs[ty][tx] = (float)acc;
     }
     __syncthreads();
     MT(6);
-    // 3c. nonzero mask of every vertical-pass row (one ballot per 32 columns)
-    for (int e = warp; e < TH * 4; e += NWARP) {
-      const int ty = e >> 2, c = e & 3, tx = 32 * c + lane;   // span <= 126 < 4 words
-      const bool nz = tx < span && sm.vs[ty][tx] != 0.f;
-      const uint32_t m = __ballot_sync(0xffffffffu, nz);
-      if (lane == 0) sm.nzm[ty][c] = m;
-    }
-    __syncthreads();
     // 3d. horizontal pass: alpha = 1 on m1, 0 where the whole window is zero, else sum.
     //     Off-frame columns of sm.vs already hold their clamped ('nearest') values.
     for (int e = tid; e < TH * TW; e += NT) {
@@ -442,9 +439,7 @@ __global__ void __launch_bounds__(NT) mask_fused_kernel(MaskArgs a) {
       if (active) {                       // the patch row: P bits of one m1 word (in frame)
         const int px = xl - xs;
         mb = (sm.b1[y - (y0 - R)][px >> 5] >> (px & 31)) & ((1u << P) - 1u);
-        const uint32_t* m0w = reinterpret_cast<const uint32_t*>(&sm.m0[y - (y0 - Hd)][px]);
-        m0b = nibble4(m0w[0]);            // raw m0 bytes (b0 is dilated in place)
-        if (P == 8) m0b |= nibble4(m0w[1]) << 4;
+        m0b = (sm.b0[y - (y0 - Hd)][px >> 5] >> (px & 31)) & ((1u << P) - 1u);   // raw m0
       }
       const bool any_unmasked = __any_sync(0xffffffffu, active && mb != ((1u << P) - 1u));
       if (lane == 0) a.token_valid[(size_t)f * T + tok] = any_unmasked ? 1 : 0;
