@@ -397,6 +397,8 @@ struct dr_engine {
   __half *xin = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr,
          *tok16 = nullptr, *raster = nullptr, *eplanes = nullptr, *slotkv = nullptr;
   int* flags = nullptr;
+  int* flag_acc = nullptr;           // mask stage's per-frame redaction OR + CTA count
+  unsigned* flag_cnt = nullptr;      // (self-resetting, zeroed at allocation)
   // host-buffer path (dr_inpaint_u8_host): device frame buffers + 3-slot ring
   uint8_t *h_rgb = nullptr, *h_m0 = nullptr, *h_out = nullptr;   // device
   float* ring[3] = {nullptr, nullptr, nullptr};
@@ -552,7 +554,7 @@ struct dr_engine {
     const size_t nbp = (size_t)frames * dec_border_pixels(H, W);
     const size_t o_bd0 = take(fus ? nbp * 64 * 4 : 0), o_be = take(fus ? nbp * 27 * 4 : 0);
     const size_t o_skv = take((size_t)KV_ENTRIES * MAX_TEMPORAL * 2 * tok * C * 2);
-    const size_t o_fl = take((size_t)frames * 4);
+    const size_t o_fl = take((size_t)frames * 4), o_fla = take((size_t)frames * 8);
     CUDA_TRY(cudaMalloc(&ws, off));
     uint8_t* b = static_cast<uint8_t*>(ws);
     bits0 = (uint32_t*)(b + o_b0); bits1 = (uint32_t*)(b + o_b1);
@@ -563,6 +565,8 @@ struct dr_engine {
     attn = (__half*)(b + o_at); tok16 = (__half*)(b + o_t16);
     raster = (__half*)(b + o_ras); eplanes = (__half*)(b + o_ep);
     slotkv = (__half*)(b + o_skv); flags = (int*)(b + o_fl);
+    flag_acc = (int*)(b + o_fla); flag_cnt = (unsigned*)(b + o_fla + (size_t)frames * 4);
+    CUDA_TRY(cudaMemset(flag_acc, 0, (size_t)frames * 8));
     part = fus ? (float*)(b + o_part) : nullptr;
     bord_d0 = fus ? (float*)(b + o_bd0) : nullptr;
     bord_e = fus ? (float*)(b + o_be) : nullptr;
@@ -1036,6 +1040,7 @@ static void fill_mask_args(dr_engine* e, MaskArgs& m, int frames, const uint8_t*
   m.m1 = m1; m.alpha = alpha; m.token_valid = tv;
   m.gtmp = nullptr;
   m.flags = flags;
+  m.flag_acc = e->flag_acc; m.flag_cnt = e->flag_cnt;   // the stage writes flags[f]
 }
 
 int dr_mask_stage(int32_t frames, int32_t height, int32_t width, int32_t patch, int32_t radius,
@@ -1091,7 +1096,7 @@ int dr_forward(dr_engine* e, const dr_frame_io* io, void* stream) {
   // e->dry: every host-side decision (and its state update) without the launches
 #define DR_L(x) do { if (!e->dry) { x; } } while (0)
   DR_L(e->mark(-1, s));
-  DR_L(CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * B, s)));
+  // no flags memset: the mask stage (first launch) writes every frame's flags word
   // diagnostics only (DR_STOP_AFTER): truncate the launch sequence to time graph prefixes
   int n_launched = 0;
 #define DR_STOP_CHECK() \

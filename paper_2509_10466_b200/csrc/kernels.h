@@ -107,6 +107,12 @@ struct MaskArgs {
   uint8_t* token_valid;      // [frames][T] out
   __half* xin;               // [frames][T][4*p*p] out (optional)
   int* flags;                // [frames] out: bit1 = input not redacted inside m0
+  // with flag_acc / flag_cnt (engine-owned, [frames] each, zero between stages) the stage
+  // WRITES flags[f] (no memset before the forward): CTAs OR their redaction bit into
+  // flag_acc[f] and count themselves in flag_cnt[f]; the frame's last CTA moves flag_acc[f]
+  // into flags[f] and resets both words.  Without them it ORs into a zeroed flags word.
+  int* flag_acc;
+  unsigned* flag_cnt;
 };
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s);
 // xin + redaction check alone, from u8 rgb, m0 and the stage's m1 bytes

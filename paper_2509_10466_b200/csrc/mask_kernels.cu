@@ -481,7 +481,20 @@ __global__ void __launch_bounds__(NT, 4) mask_fused_kernel(MaskArgs a) {
   }
   MT(8);
   __syncthreads();
-  if (tid == 0 && sm.dirty && a.flags) atomicOr(a.flags + f, 2);
+  if (tid == 0 && a.flags) {
+    if (a.flag_cnt == nullptr) {
+      if (sm.dirty) atomicOr(a.flags + f, 2);
+    } else {
+      if (sm.dirty) atomicOr(a.flag_acc + f, 2);
+      __threadfence();
+      const unsigned done = atomicAdd(a.flag_cnt + f, 1u);
+      if (done == gridDim.x * gridDim.y - 1) {            // the frame's last CTA
+        __threadfence();
+        a.flags[f] = atomicExch(a.flag_acc + f, 0);
+        a.flag_cnt[f] = 0;
+      }
+    }
+  }
   MT(9);
 }
 
