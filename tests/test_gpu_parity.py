@@ -383,3 +383,23 @@ def test_c4_1024_mask_aware_vs_oracle():
     assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), ref["token_valid"])
     assert (~ref["token_valid"]).any()
     assert_close_img(res["out"].cpu().numpy(), ref["out"], "C4 composite")
+
+
+def test_c4_1024_mask_aware_warm_sequence_vs_oracle():
+    """BASELINE configs[3] with memory carried: two 1024^2 frames, the second with warm
+    (B,T,C) slots (memory keys always valid in mask-aware mode), both vs the oracle."""
+    cfg = DsttConfig.baseline(1024, mask_dilate=5, mask_feather_sigma=3.0,
+                              mask_aware_attention=True)
+    eng = DsttEngine(cfg, seed=0)
+    w = seed_parameters(cfg, 0)
+    zero = np.zeros((cfg.tokens, cfg.channels), np.float32)
+    ref_slots = (zero, zero)
+    mem = eng.zero_memory()
+    for seed in range(2):
+        img, m0 = synth.c4_frame(seed)
+        res = eng.run(cuda(img[None]), cuda(m0[None]), mem.slots, want_masks=True)
+        mem = mem.push(res["slot"][0])
+        ref = O.inpaint_path(cfg, w, img[None], m0[None], ref_slots)
+        ref_slots = (ref_slots[1], ref["slot"][0])
+        assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), ref["token_valid"])
+        assert_close_img(res["out"].cpu().numpy(), ref["out"], f"C4 frame {seed}")
