@@ -5,7 +5,8 @@ Public names follow the reference package (`pkg/src/dimreal/__init__.py:3-18`,
 
     DsttConfig, DsttEngine, InpaintEngine, EngineResult, InpaintMemory, memory_push,
     load_weights, save_weights, BinaryMask, redact, adjust_mask_area,
-    dilate_mask, feather_mask, token_mask (device mask stage, new)
+    dilate_mask, feather_mask, token_mask (device mask stage, new),
+    BatchStreamer (overlapped pinned-host batches, new)
 
 The compute path is `libdrb200.so` (hand-written sm_100a CUDA behind a C-ABI, see
 `include/dr_b200.h`); there is no CPU fallback.
@@ -20,7 +21,7 @@ from .memory import InpaintMemory, memory_push
 from .weights import load_weights, save_weights
 
 __all__ = [
-    "BinaryMask", "ConfigError", "DegenerateMaskError", "DeviceError", "DsttConfig",
+    "BatchStreamer", "BinaryMask", "ConfigError", "DegenerateMaskError", "DeviceError", "DsttConfig",
     "DsttEngine", "EngineNumericError", "EngineResult", "InpaintEngine", "InpaintMemory",
     "InputError", "adjust_mask_area", "dilate_mask", "feather_mask", "load_weights",
     "memory_push", "redact", "save_weights", "token_mask",
@@ -31,4 +32,7 @@ def __getattr__(name):
     if name in ("DsttEngine", "InpaintEngine", "EngineResult"):
         from . import engine
         return getattr(engine, name)
+    if name == "BatchStreamer":
+        from .streaming import BatchStreamer
+        return BatchStreamer
     raise AttributeError(name)

@@ -218,3 +218,16 @@ def test_engine_fails_loudly_without_cuda():
     from paper_2509_10466_b200 import DeviceError, DsttEngine
     with pytest.raises(DeviceError):
         DsttEngine(DsttConfig.baseline(64))
+
+
+def test_batch_streamer_needs_a_gpu_and_is_exported():
+    """The overlapped batch API is public and, like every compute entry point, raises
+    instead of falling back to the CPU."""
+    import paper_2509_10466_b200 as pkg
+    from paper_2509_10466_b200.errors import DeviceError
+    import torch
+    assert "BatchStreamer" in pkg.__all__
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: tests/test_gpu_streaming.py covers it")
+    with pytest.raises(DeviceError):
+        pkg.BatchStreamer(None, 2)
