@@ -1,6 +1,6 @@
 // Mask stage: privacy mask m0 -> dilated m1 -> feathered alpha, token validity, and the
-// packed fp16 network input, fused in ONE kernel over 16 x 64-pixel tiles.  HBM-bound
-// integer/byte work; no tensor cores.  Per tile (NT = 512 threads):
+// packed fp16 network input, fused in ONE kernel over TH x 64-pixel tiles.  HBM-bound
+// integer/byte work; no tensor cores.  Per tile (TH rows x 64 px, NT = 32 TH threads):
 //
 //  1. m0 bytes of the tile plus a halo of r + R pixels -> 32-pixel bit words in smem
 //     (warp ballots over coalesced byte loads; off-frame = 0)
@@ -20,6 +20,7 @@
 //     cat[rgb zeroed in m1, m1] in conv-weight (c, ky, kx) order (dstt.py:253, :314-316;
 //     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79)
 #include <cstddef>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -28,20 +29,19 @@ namespace dr {
 
 namespace {
 
-#ifndef DR_MASK_TH
-#define DR_MASK_TH 16
-#endif
-constexpr int TH = DR_MASK_TH, TW = 64;    // tile (rows x pixels)
-constexpr int NT = 32 * TH, NWARP = NT / 32;   // one warp per tile row (vertical pass)
+constexpr int TW = 64;                     // tile width (pixels); height TH: template
 constexpr int MAXH = 62;                   // max halo r + R (r <= 31, R <= 31)
 constexpr int MAXR = 31;                   // 2R+1 <= 63: a column window fits a uint64
 constexpr int NW_MAX = 2 + 2 * (MAXH / 32);
-constexpr int NR_MAX = TH + 2 * MAXH;
 
 constexpr int SPAN_MAX = TW + 2 * MAXR;   // columns of the vertical pass
 constexpr int CW = 3;                      // column words: TH + 2R <= 78 rows < 96
 
+// Tile of TH rows (TH = 16, or 8 below one wave of 16-row tiles: batch-1 latency), one
+// warp per tile row (NT = 32 TH threads).
+template <int TH>
 struct Smem {
+  static constexpr int NR_MAX = TH + 2 * MAXH;
   float rgb[3][TH][TW];                    // f32 input tile, or u8 HWC bytes (aliased)
   uint32_t b0[NR_MAX][NW_MAX];             // m0 bits, rows y0-H.., words from xs (read-only
                                            // after the load phase)
@@ -55,11 +55,6 @@ struct Smem {
   double all_ones;
   int dirty;
 };
-
-// bt, col and vs are contiguous: the dilation's H_k scratch spans all three
-static_assert(offsetof(Smem, col) == offsetof(Smem, bt) + sizeof(Smem::bt) &&
-              offsetof(Smem, vs) == offsetof(Smem, col) + sizeof(Smem::col), "Smem scratch layout");
-constexpr int HS_WORDS = (int)((sizeof(Smem::bt) + sizeof(Smem::col) + sizeof(Smem::vs)) / 4);
 
 // bit i = (byte i of w != 0), i < 4: byte flags to 0x01 each, then the multiply by
 // 2^28 + 2^21 + 2^14 + 2^7 moves byte i's flag to bit 28 + i (all cross terms land on
@@ -94,10 +89,16 @@ __device__ unsigned long long g_mask_trace[4096 * MT_SLOTS];
 #endif
 
 // WH = halo words per side (compile time: every word loop is shift/mask, no division)
-template <int P, int WH>
-__global__ void __launch_bounds__(NT, 4) mask_fused_kernel(MaskArgs a) {
+template <int P, int WH, int TH>
+__global__ void __launch_bounds__(32 * TH, 64 / TH) mask_fused_kernel(MaskArgs a) {
+  using S = Smem<TH>;
+  constexpr int NT = 32 * TH, NWARP = TH;
+  // bt, col and vs are contiguous: the dilation's H_k scratch spans all three
+  static_assert(offsetof(S, col) == offsetof(S, bt) + sizeof(S::bt) &&
+                offsetof(S, vs) == offsetof(S, col) + sizeof(S::col), "Smem scratch layout");
+  constexpr int HS_WORDS = (int)((sizeof(S::bt) + sizeof(S::col) + sizeof(S::vs)) / 4);
   extern __shared__ __align__(16) uint8_t smem_raw[];   // keep the shared address space:
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);        // no integer round trip (LDS, not LD)
+  S& sm = *reinterpret_cast<S*>(smem_raw);               // no integer round trip (LDS, not LD)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, f = blockIdx.z;
   const int r = a.radius, R = a.feather_radius;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(NT, 4) mask_fused_kernel(MaskArgs a) {
   } else {
     // b0 stays read-only (raw m0 bits for the token phase): iteration 0 reads b0, later
     // ones ping-pong between bt and the vertical-pass scratch (unused until the feather)
-    static_assert(sizeof(Smem::vs) >= sizeof(Smem::bt), "dilation ping-pong scratch");
+    static_assert(sizeof(S::vs) >= sizeof(S::bt), "dilation ping-pong scratch");
     uint32_t (*cur)[NW_MAX] = sm.b0;
     uint32_t (*nxt)[NW_MAX] = sm.bt;
     uint32_t (*spare)[NW_MAX] = reinterpret_cast<uint32_t (*)[NW_MAX]>(&sm.vs[0][0]);
@@ -500,14 +501,27 @@ __global__ void __launch_bounds__(NT, 4) mask_fused_kernel(MaskArgs a) {
 
 }  // namespace
 
-template <int P, int WH>
-void launch_mask_t(const MaskArgs& a, cudaStream_t s, int smem) {
+template <int P, int WH, int TH>
+void launch_mask_t(const MaskArgs& a, cudaStream_t s) {
   static unsigned long long init = 0;
+  constexpr int smem = (int)sizeof(Smem<TH>) + 16;
   once_per_device(init, [&] {
-    cudaFuncSetAttribute(mask_fused_kernel<P, WH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mask_fused_kernel<P, WH, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
   dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, a.frames);
-  launch_pdl(mask_fused_kernel<P, WH>, grid, dim3(NT), smem, s, a);
+  launch_pdl(mask_fused_kernel<P, WH, TH>, grid, dim3(32 * TH), smem, s, a);
+}
+
+template <int TH>
+void launch_mask_th(const MaskArgs& a, cudaStream_t s) {
+  const int wh = (a.radius + a.feather_radius + 31) / 32;   // 0..2 halo words per side
+  if (a.patch == 4) {
+    if (wh <= 1) launch_mask_t<4, 1, TH>(a, s);
+    else launch_mask_t<4, 2, TH>(a, s);
+  } else {
+    if (wh <= 1) launch_mask_t<8, 1, TH>(a, s);
+    else launch_mask_t<8, 2, TH>(a, s);
+  }
 }
 
 // Network input pack on its own (host path with split uploads: the mask stage runs on the
@@ -575,16 +589,17 @@ void launch_pack_input(const MaskArgs& a, cudaStream_t s) {
   else launch_pdl(pack_input_kernel<8>, grid, dim3(256), 0, s, a);
 }
 
+// Tile height by grid size: below one wave of 16-row tiles (4 resident per SM) the stage is
+// latency-bound and 8-row tiles halve each CTA's path (C2 p50 -2 us); above it the halo
+// overhead of short tiles costs throughput (C5 +1.5 % with 16 rows).  DR_MASK_TH=8|16
+// forces one (tests).
 void launch_mask_stage(const MaskArgs& a, cudaStream_t s) {
-  const int smem = (int)sizeof(Smem) + 16;
-  const int wh = (a.radius + a.feather_radius + 31) / 32;   // 0..2 halo words per side
-  if (a.patch == 4) {
-    if (wh <= 1) launch_mask_t<4, 1>(a, s, smem);
-    else launch_mask_t<4, 2>(a, s, smem);
-  } else {
-    if (wh <= 1) launch_mask_t<8, 1>(a, s, smem);
-    else launch_mask_t<8, 2>(a, s, smem);
-  }
+  const char* fe = std::getenv("DR_MASK_TH");
+  const int forced = fe ? std::atoi(fe) : 0;
+  const long tiles16 = (long)((a.W + TW - 1) / TW) * ((a.H + 15) / 16) * a.frames;
+  const bool short_tiles = forced ? forced == 8 : tiles16 < 4L * device_sms();
+  if (short_tiles) launch_mask_th<8>(a, s);
+  else launch_mask_th<16>(a, s);
 }
 
 }  // namespace dr

@@ -45,15 +45,23 @@ def cuda(x):
 
 
 # ------------------------------------------------------------------ mask stage
+@pytest.fixture(params=["8", "16"])
+def mask_th(request, monkeypatch):
+    """Both tile heights of the mask stage (8 rows below one wave of 16-row tiles, else 16;
+    mask_kernels.cu launch_mask_stage), forced per test through DR_MASK_TH."""
+    monkeypatch.setenv("DR_MASK_TH", request.param)
+    return int(request.param)
+
+
 @pytest.mark.parametrize("r", [0, 1, 3, 5])
-def test_dilate_bit_exact_vs_reference(r):
+def test_dilate_bit_exact_vs_reference(r, mask_th):
     g = golden("masks.npz")
     m1 = dilate_mask(cuda(g["m0"].astype(np.uint8)), r).cpu().numpy().astype(bool)
     assert np.array_equal(m1, g[f"dilate_r{r}"])
 
 
 @pytest.mark.parametrize("sigma", [1.5, 3.0])
-def test_feather_vs_reference_scipy(sigma):
+def test_feather_vs_reference_scipy(sigma, mask_th):
     g = golden("masks.npz")
     a = feather_mask(cuda(g["dilate_r3"].astype(np.uint8)), sigma).cpu().numpy()
     ref = g[f"feather_r3_s{sigma}"]
@@ -62,7 +70,7 @@ def test_feather_vs_reference_scipy(sigma):
     assert np.mean(a == ref) > 0.999
 
 
-def test_token_mask_bit_exact_random(rng):
+def test_token_mask_bit_exact_random(rng, mask_th):
     m = rng.random((3, 64, 96)) > 0.3
     m[0, :32, :32] = True
     m[2] = True
@@ -70,7 +78,7 @@ def test_token_mask_bit_exact_random(rng):
     assert np.array_equal(got, O.token_mask(m, 8))
 
 
-def test_mask_stage_large_radius_borders(rng):
+def test_mask_stage_large_radius_borders(rng, mask_th):
     m0 = rng.random((2, 128, 160)) > 0.995
     m0[1, 0, :] = True
     for r in (7, 12, 31):
