@@ -30,8 +30,9 @@ class BatchStreamer:
     submit(rgb, mask, out, memory) enqueues one batch: rgb (B,H,W,3) u8 and mask (B,H,W)
     u8/bool in pinned host memory, out (B,H,W,3) u8 pinned host memory that receives the
     composite.  It returns the batch's new memory slot (device, (B,T,C)) for carried
-    memory.  `out` is complete (and the batch's redaction / non-finite flags checked) once
-    a later submit() has returned two batches on, or after finish()."""
+    memory.  Batch k's `out` is complete (and its redaction / non-finite flags checked) once
+    submit() of batch k+2 has returned, or after finish(); a caller that reads the results
+    rotates three `out` buffers (batch k+3 may reuse batch k's)."""
 
     def __init__(self, engine, batch: int):
         torch = _lib.require_cuda()
