@@ -375,7 +375,8 @@ class DsttEngine(InpaintEngine):
             io.token_valid = res["token_valid"].data_ptr()
         if self._flags.numel() < B:
             self._flags = torch.zeros(B, dtype=torch.int32, device=dev)
-        io.flags = self._flags.data_ptr()
+        fl = o.get("flags")                  # caller-owned int32 [>= B] flags words
+        io.flags = (fl if fl is not None else self._flags).data_ptr()
         io.slot_kv_reuse = reuse
         stream = torch.cuda.current_stream(dev)
         if sync:

@@ -53,6 +53,8 @@ class BatchStreamer:
         self.ev_down = [torch.cuda.Event() for _ in range(2)]
         self.pending = [False, False]
         self.k = 0
+        self.own, self.own_refs = set(), []    # slots made on the compute stream (kept alive
+                                               # so their ids stay unique)
 
     def submit(self, rgb, mask, out, memory=None):
         torch = _lib.require_cuda()
@@ -71,17 +73,21 @@ class BatchStreamer:
                                  non_blocking=True)
             self.ev_up[i].record(self.up)
         self.comp.wait_event(self.ev_up[i])
-        # memory made on the caller's stream (e.g. a zero slot) is complete before the
-        # forward reads it, and stays allocated until the forward is done
-        self.comp.wait_stream(torch.cuda.current_stream(self.engine.device))
-        for t in (memory or ()):
-            if isinstance(t, torch.Tensor) and t.is_cuda:
+        # memory not made by this streamer (e.g. a zero slot on the caller's stream) is
+        # complete before the forward reads it, and stays allocated until it is done
+        foreign = [t for t in (memory or ()) if isinstance(t, torch.Tensor) and t.is_cuda
+                   and id(t) not in self.own]
+        if foreign:
+            self.comp.wait_stream(torch.cuda.current_stream(self.engine.device))
+            for t in foreign:
                 t.record_stream(self.comp)
         with torch.cuda.stream(self.comp):
-            r = self.engine.run(self.d_rgb[i], self.d_mask[i], memory,
-                                out={"out": self.d_out[i]}, sync=False)
-            self.d_flags[i].copy_(self.engine._flags[:B])   # before the next batch's stage
+            r = self.engine.run(self.d_rgb[i], self.d_mask[i], memory, sync=False,
+                                out={"out": self.d_out[i], "flags": self.d_flags[i]})
             self.ev_comp[i].record(self.comp)
+        slot = r["slot"]
+        self.own = {id(t) for t in (memory or ()) if id(t) in self.own} | {id(slot)}
+        self.own_refs = [t for t in (memory or ()) if id(t) in self.own] + [slot]
         with torch.cuda.stream(self.down):
             self.down.wait_event(self.ev_comp[i])
             out.copy_(self.d_out[i], non_blocking=True)
@@ -89,7 +95,7 @@ class BatchStreamer:
             self.ev_down[i].record(self.down)
         self.pending[i] = True
         self.k += 1
-        return r["slot"]
+        return slot
 
     def _complete(self, i: int) -> None:
         if self.pending[i]:
