@@ -155,9 +155,12 @@ def stage_flops(cfg, kv_bands=3):
 def stage_bytes(cfg):
     """Algorithmic HBM bytes per frame of the HBM-class stages (device path: f32 rgb in).
     Mask stage: m0 u8 + rgb f32 in; alpha f32, token validity u8 and the packed fp16
-    network input (4 channels per pixel) out."""
+    network input (4 channels per pixel) out.  Batch-1 decoder tail (decode.2 taps +
+    composite): rgb f32 and alpha in, composite f32 out (its fp16 tap planes, an artefact of
+    the unfused decomposition, are not counted)."""
     T, H, W = cfg.tokens, cfg.height, cfg.width
-    return {"mask_stage": H * W * (1 + 12 + 4 + 8) + T}
+    return {"mask_stage": H * W * (1 + 12 + 4 + 8) + T,
+            "decode2_composite": H * W * (12 + 4 + 12)}
 
 
 def stage_exps(cfg, kv_bands=3):
