@@ -30,11 +30,17 @@ class BatchStreamer:
     submit(rgb, mask, out, memory) enqueues one batch: rgb (B,H,W,3) u8 and mask (B,H,W)
     u8/bool in pinned host memory, out (B,H,W,3) u8 pinned host memory that receives the
     composite.  It returns the batch's new memory slot (device, (B,T,C)) for carried
-    memory.  Batch k's `out` is complete (and its redaction / non-finite flags checked) once
+    memory (with carry_memory=True the streamer keeps the 2-slot FIFO per stream itself,
+    `memory` stays None, and the returned slot is valid for the next two submits).  Batch
+    k's `out` is complete (and its redaction / non-finite flags checked) once
     submit() of batch k+2 has returned, or after finish(); a caller that reads the results
     rotates three `out` buffers (batch k+3 may reuse batch k's)."""
 
-    def __init__(self, engine, batch: int):
+    # carry_memory: steady-state forwards as CUDA graph replays, one per (buffer set,
+    # memory-ring phase): period lcm(2, 3) = 6, captured after GRAPH_WARM eager batches
+    GRAPH_WARM = 6
+
+    def __init__(self, engine, batch: int, carry_memory: bool = False, graphs: bool = True):
         torch = _lib.require_cuda()
         cfg = engine.config
         dev = engine.device
@@ -55,6 +61,14 @@ class BatchStreamer:
         self.k = 0
         self.own, self.own_refs = set(), []    # slots made on the compute stream (kept alive
                                                # so their ids stay unique)
+        # carry_memory: the streamer holds each stream's 2-slot FIFO itself (like the
+        # engine-held memory of dr_inpaint_u8_host): batch k reads the slots of batches k-2
+        # and k-1 (zero slots before), writes ring[k % 3]
+        self.carry = carry_memory
+        self.graphs = {} if (carry_memory and graphs) else None
+        if carry_memory:
+            self.ring = [torch.zeros((batch, cfg.tokens, cfg.channels), dtype=torch.float32,
+                                     device=dev) for _ in range(3)]
 
     def submit(self, rgb, mask, out, memory=None):
         torch = _lib.require_cuda()
@@ -66,6 +80,13 @@ class BatchStreamer:
         if tuple(out.shape) != tuple(self.d_out[0].shape) or out.dtype != torch.uint8:
             raise ConfigError(f"out must be u8 {tuple(self.d_out[0].shape)}")
         i = self.k & 1
+        if self.carry:
+            if memory is not None:
+                raise ConfigError("a carry_memory streamer holds the memory itself")
+            k = self.k
+            zero = self.engine.zero_memory().slots[0]
+            memory = (zero if k < 2 else self.ring[(k - 2) % 3],
+                      zero if k < 1 else self.ring[(k - 1) % 3])
         self._complete(i)                  # set i's last download done, its flags checked
         with torch.cuda.stream(self.up):
             self.d_rgb[i].copy_(rgb, non_blocking=True)
@@ -81,11 +102,27 @@ class BatchStreamer:
             self.comp.wait_stream(torch.cuda.current_stream(self.engine.device))
             for t in foreign:
                 t.record_stream(self.comp)
-        with torch.cuda.stream(self.comp):
-            r = self.engine.run(self.d_rgb[i], self.d_mask[i], memory, sync=False,
-                                out={"out": self.d_out[i], "flags": self.d_flags[i]})
-            self.ev_comp[i].record(self.comp)
-        slot = r["slot"]
+        outs = {"out": self.d_out[i], "flags": self.d_flags[i]}
+        if self.carry:
+            outs["slot"] = self.ring[self.k % 3]
+        if self.graphs is not None and self.k >= self.GRAPH_WARM:
+            # steady state: every launch decision (slot K/V cache entries included) repeats
+            # with period 6, so the captured forward of phase k % 6 is replayed
+            g = self.graphs.get(self.k % 6)
+            if g is None:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.comp):
+                    self.engine.run(self.d_rgb[i], self.d_mask[i], memory, sync=False, out=outs)
+                self.graphs[self.k % 6] = g
+            with torch.cuda.stream(self.comp):
+                g.replay()
+                self.ev_comp[i].record(self.comp)
+            slot = outs["slot"]
+        else:
+            with torch.cuda.stream(self.comp):
+                r = self.engine.run(self.d_rgb[i], self.d_mask[i], memory, sync=False, out=outs)
+                self.ev_comp[i].record(self.comp)
+            slot = r["slot"]
         self.own = {id(t) for t in (memory or ()) if id(t) in self.own} | {id(slot)}
         self.own_refs = [t for t in (memory or ()) if id(t) in self.own] + [slot]
         with torch.cuda.stream(self.down):

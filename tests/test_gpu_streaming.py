@@ -64,3 +64,32 @@ def test_streamer_reports_unredacted_batch():
         for rgb_k, m_k in data:
             bs.submit(rgb_k, m_k, out)
         bs.finish()
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_carried_streamer_graph_replays_equal_serial_run(B):
+    """carry_memory=True: the streamer's own 2-slot FIFO per stream and, after the warm-up,
+    CUDA-graph replays of the forward (one per buffer set x memory-ring phase, period 6)
+    over two full periods -- bit-equal to the serial engine with the same FIFO."""
+    cfg = DsttConfig.baseline(128, mask_dilate=3, mask_feather_sigma=1.5)
+    n = BatchStreamer.GRAPH_WARM + 13
+    data = _batches(np.random.default_rng(11), n, B, 128, 128)
+    eng, ref = DsttEngine(cfg, seed=0), DsttEngine(cfg, seed=0)
+    bs = BatchStreamer(eng, B, carry_memory=True)
+    outs = [torch.empty((B, 128, 128, 3), dtype=torch.uint8).pin_memory() for _ in range(n)]
+    zero = ref.zero_memory().slots[0]
+    hist, ref_out, slots = [], [], []
+    for k, (rgb, m) in enumerate(data):
+        slot = bs.submit(rgb, m, outs[k])
+        with torch.cuda.stream(bs.comp):                      # ring buffer: copy it in order
+            slots.append(slot.clone())
+        mem = (hist[-2] if k >= 2 else zero, hist[-1] if k >= 1 else zero)
+        r = ref.run(rgb, m, mem)
+        hist.append(r["slot"])
+        ref_out.append(r["out"].cpu())
+    bs.finish()
+    torch.cuda.synchronize()
+    assert len(bs.graphs) == 6
+    for k in range(n):
+        assert torch.equal(outs[k], ref_out[k]), f"frame {k} composite"
+        assert torch.equal(slots[k].cpu(), hist[k].cpu()), f"frame {k} new slot"
