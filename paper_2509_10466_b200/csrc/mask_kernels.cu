@@ -2,11 +2,13 @@
 // packed fp16 network input, fused in ONE kernel over TH x 64-pixel tiles.  HBM-bound
 // integer/byte work; no tensor cores.  Per tile (TH rows x 64 px, NT = 32 TH threads):
 //
-//  1. m0 bytes of the tile plus a halo of r + R pixels -> 32-pixel bit words in smem
-//     (warp ballots over coalesced byte loads; off-frame = 0)
+//  1. m0 bytes of the tile plus a halo of r + R pixels -> 32-pixel bit words in smem,
+//     straight from global memory (coalesced 16-byte pieces, SIMD byte compares; off-frame
+//     = 0) while the rgb tile lands by cp.async
 //  2. m1 = m0 (+) L1-ball(r) == the r-fold 3x3-cross dilation (masks.py:17, :193; SURVEY
-//     A2): r cross iterations on the bit words of the tile + halo (shift/or, ping-pong in
-//     smem) -- bit-exact by construction; kept on the tile plus a halo of R
+//     A2): horizontal dilations of the bit words by funnel shifts, then a vertical OR over
+//     the ball's rows (or r cross iterations in warp registers / smem for large r) --
+//     bit-exact by construction; kept on the tile plus a halo of R
 //  3. feather: alpha = max(m1, G_sigma(m1)), scipy.ndimage.gaussian_filter
 //     semantics (mode 'nearest', truncate 4): vertical then horizontal pass, each in
 //     float64 in scipy's symmetric-filter order (x[0]*w[0], then (x[-j]+x[+j])*w[j] from
@@ -18,7 +20,8 @@
 //     all-one window gives 0 / the precomputed all-ones sum
 //  4. token validity (any pixel of the patch outside m1) and the network input
 //     cat[rgb zeroed in m1, m1] in conv-weight (c, ky, kx) order (dstt.py:253, :314-316;
-//     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79)
+//     u8 -> f32 is an IEEE divide by 255), plus the u8 API's redaction check (base.py:76-79);
+//     the frame's last CTA writes the frame's flags word (no memset before the forward)
 #include <cstddef>
 #include <cstdlib>
 
