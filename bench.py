@@ -788,7 +788,8 @@ def measure_e2e(args, eng, cfg, B, imgs, masks, P, world, dev, barrier, lib, Bin
 STREAMED_API = ("BatchStreamer.submit (DsttEngine.run per batch) on u8 (B,H,W,3) pinned host "
                 "frames + masks, per-stream memory -> u8 composite in pinned host memory; "
                 "upload of batch k+1 and download of batch k-1 overlap the forward of batch k "
-                "(streaming.py)")
+                "(streaming.py); steps run back to back with no L2 flush between them, so "
+                "this figure can exceed the L2-flushed device value")
 
 
 def _streamed(args, eng, B, host_rgb, host_m, P, K, carried, barrier, dev):
