@@ -411,3 +411,25 @@ def test_c4_1024_mask_aware_warm_sequence_vs_oracle():
         ref_slots = (ref_slots[1], ref["slot"][0])
         assert np.array_equal(res["token_valid"].cpu().numpy().astype(bool), ref["token_valid"])
         assert_close_img(res["out"].cpu().numpy(), ref["out"], f"C4 frame {seed}")
+
+
+def test_mask_aware_fully_masked_frame_in_a_batch_vs_oracle(rng):
+    """Mask-aware attention with one frame of the batch entirely masked (no valid key: the
+    spatial block falls back to unmasked attention for that frame only) next to a partly
+    masked frame, with warm memory slots, both vs the oracle."""
+    cfg = DsttConfig.baseline(128, mask_dilate=2, mask_feather_sigma=1.5,
+                              mask_aware_attention=True)
+    eng = DsttEngine(cfg, seed=0)
+    w = seed_parameters(cfg, 0)
+    imgs = rng.random((2, 3, 128, 128)).astype(np.float32)
+    m0 = np.zeros((2, 128, 128), bool)
+    m0[0] = True
+    m0[1, 20:70, 30:90] = True
+    slots = [rng.normal(0, 1, (cfg.tokens, cfg.channels)).astype(np.float32) for _ in range(2)]
+    res = eng.run(cuda(imgs), cuda(m0), [cuda(s) for s in slots], want_masks=True)
+    for i in range(2):
+        ref = O.inpaint_path(cfg, w, imgs[i:i + 1], m0[i:i + 1], slots)
+        assert np.array_equal(res["token_valid"][i:i + 1].cpu().numpy().astype(bool),
+                              ref["token_valid"])
+        assert_close_img(res["out"][i:i + 1].cpu().numpy(), ref["out"], f"frame {i}")
+    assert not res["token_valid"][0].any()
