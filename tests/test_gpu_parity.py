@@ -86,6 +86,22 @@ def test_mask_stage_large_radius_borders(rng, mask_th):
         assert np.array_equal(got, O.dilate_mask(m0, r)), r
 
 
+@pytest.mark.parametrize("hw", [(37, 100), (61, 97), (5, 3)])
+def test_mask_stage_ragged_sizes_vs_oracle(rng, hw, mask_th):
+    """Widths that are not multiples of 16 (4-byte and byte load paths) and heights that
+    are not multiples of the tile: dilation bit-exact, feather within 1e-6, vs the oracle."""
+    H, W = hw
+    m0 = rng.random((2, H, W)) > 0.97
+    m0[1, :, W // 2] = True
+    for r in (0, 3):
+        got = dilate_mask(cuda(m0.astype(np.uint8)), r).cpu().numpy().astype(bool)
+        assert np.array_equal(got, O.dilate_mask(m0, r)), (hw, r)
+    m1 = O.dilate_mask(m0, 2)
+    a = feather_mask(cuda(m1.astype(np.uint8)), 1.5).cpu().numpy()
+    ref = np.stack([O.feather_mask(m1[i], 1.5) for i in range(2)])
+    assert np.max(np.abs(a - ref)) <= 1e-6, hw
+
+
 # ------------------------------------------------------------------ forward vs goldens
 def _engine_b64(g, **kw):
     cfg = cfg_from(g["cfg"], **kw)
