@@ -449,3 +449,22 @@ def test_mask_aware_fully_masked_frame_in_a_batch_vs_oracle(rng):
                               ref["token_valid"])
         assert_close_img(res["out"][i:i + 1].cpu().numpy(), ref["out"], f"frame {i}")
     assert not res["token_valid"][0].any()
+
+
+def test_composite_guarantee_many_frames_and_engine_reload(rng, tmp_path):
+    """The reference acceptance checks on the engine API (test_acceptance.py:129-144,
+    test_dstt.py:207-214): over 200 frames of one stream, every pixel outside the mask
+    keeps its input byte (r = 0, sigma = 0: the reference composite), and an engine
+    rebuilt from its saved DRWT weights reproduces the stream bit for bit."""
+    cfg = DsttConfig.baseline(64)
+    eng = DsttEngine(cfg, seed=5)
+    eng.save_weights(tmp_path / "w.drwt")
+    eng2 = DsttEngine(cfg, weights_path=tmp_path / "w.drwt")
+    m1, m2 = eng.zero_memory(), eng2.zero_memory()
+    for t in range(200):
+        rgb, bits = _redacted(rng, 64, 64, float(rng.uniform(0.0, 0.6)))
+        a = eng.inpaint(rgb, BinaryMask(bits), m1)
+        b = eng2.inpaint(rgb, BinaryMask(bits), m2)
+        m1, m2 = a.memory, b.memory
+        assert np.array_equal(a.rgb[~bits], rgb[~bits]), f"frame {t} leaked outside the mask"
+        assert np.array_equal(a.rgb, b.rgb), f"frame {t}: reloaded engine differs"
