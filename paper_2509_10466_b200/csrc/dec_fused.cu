@@ -849,7 +849,6 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
   const int PC = a.Cc + 2, PR = a.R + 2;
   pdl_wait();
   const __half* tokf = a.tok16 + (size_t)f * PR * PC * 64;
-  const int co = tid & 63, pg = tid >> 6;
   for (int kb = k_lo; kb <= k_hi; kb += 64) {
     const int cnt = min(64, k_hi - kb + 1);              // pixels of this pass
     __syncthreads();
@@ -864,46 +863,56 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
       sm.tok[j][2 * c2 + 1] = v.y;
     }
     __syncthreads();
-    // thread (co, pg) takes the pixels j = pg + 4i: 16 of them per pass, 4 when the pass
-    // has <= 16 (small batches: a quarter of the FMA chain per thread)
+    // thread (channel pair cp, pg) takes channels 2cp, 2cp+1 of the pixels j = pg + 8i: 8
+    // of them per pass, 2 when the pass has <= 16 (small batches).  Every broadcast token
+    // float4 feeds 8 FMAs (two channels), the weights come as float2 pairs.
+    const int cp = tid & 31, pg8 = tid >> 5;
     auto corr_pass = [&](auto ni_tag) {
       constexpr int NI = decltype(ni_tag)::value;
-      float acc[NI], pre[NI];
+      float2 acc[NI], pre[NI];
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
-        acc[i] = sm.eb[co];
+        acc[i] = *reinterpret_cast<const float2*>(&sm.eb[2 * cp]);
         // the pixels' stored pre-activations, loaded before the products
-        const int k = kb + pg + 4 * i, pos = r + 8 * k;
+        const int k = kb + pg8 + 8 * i, pos = r + 8 * k;
         const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
-        pre[i] = k <= k_hi ? __ldg(a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + co) : 0.f;
+        pre[i] = k <= k_hi ? __ldg(reinterpret_cast<const float2*>(
+                                 a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 2 * cp))
+                           : make_float2(0.f, 0.f);
       }
       for (int t = 0; t < nt; ++t) {
         const int o = 1 + (t == 0 ? 0 : dt1);            // token row of pixel j: j + o
 #pragma unroll 2
         for (int c4 = 0; c4 < 16; ++c4) {
-          const float w0 = sm.k[t][4 * c4][co], w1 = sm.k[t][4 * c4 + 1][co];
-          const float w2 = sm.k[t][4 * c4 + 2][co], w3 = sm.k[t][4 * c4 + 3][co];
+          const float2 w0 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4][2 * cp]);
+          const float2 w1 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 1][2 * cp]);
+          const float2 w2 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 2][2 * cp]);
+          const float2 w3 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 3][2 * cp]);
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
-            const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[pg + 4 * i + o][4 * c4]);
-            acc[i] = fmaf(tv.x, w0, fmaf(tv.y, w1, fmaf(tv.z, w2, fmaf(tv.w, w3, acc[i]))));
+            const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[pg8 + 8 * i + o][4 * c4]);
+            acc[i].x = fmaf(tv.x, w0.x, fmaf(tv.y, w1.x, fmaf(tv.z, w2.x, fmaf(tv.w, w3.x, acc[i].x))));
+            acc[i].y = fmaf(tv.x, w0.y, fmaf(tv.y, w1.y, fmaf(tv.z, w2.y, fmaf(tv.w, w3.y, acc[i].y))));
           }
         }
       }
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
-        const int j = pg + 4 * i, k = kb + j;
-        float d = 0.f;
+        const int j = pg8 + 8 * i, k = kb + j;
+        float2 d = make_float2(0.f, 0.f);
         if (k <= k_hi) {
-          d = pre[i] - acc[i];
-          d = d >= 0.f ? d : 0.2f * d;
-          d = __half2float(__float2half_rn(d));           // decode.0's output is fp16
+          d.x = pre[i].x - acc[i].x;
+          d.y = pre[i].y - acc[i].y;
+          d.x = d.x >= 0.f ? d.x : 0.2f * d.x;
+          d.y = d.y >= 0.f ? d.y : 0.2f * d.y;
+          d.x = __half2float(__float2half_rn(d.x));       // decode.0's output is fp16
+          d.y = __half2float(__float2half_rn(d.y));
         }
-        sm.d0[j][co] = d;
+        *reinterpret_cast<float2*>(&sm.d0[j][2 * cp]) = d;
       }
     };
-    if (cnt <= 16) corr_pass(std::integral_constant<int, 4>{});
-    else corr_pass(std::integral_constant<int, 16>{});
+    if (cnt <= 16) corr_pass(std::integral_constant<int, 2>{});
+    else corr_pass(std::integral_constant<int, 8>{});
     __syncthreads();
     for (int i = tid; i < cnt * 27; i += 256) {
       const int j = i / 27, u = i - 27 * j, k = kb + j, pos = r + 8 * k;
