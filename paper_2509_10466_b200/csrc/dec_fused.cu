@@ -863,56 +863,62 @@ __global__ void __launch_bounds__(256) dec_border_kernel(const __grid_constant__
       sm.tok[j][2 * c2 + 1] = v.y;
     }
     __syncthreads();
-    // thread (channel pair cp, pg) takes channels 2cp, 2cp+1 of the pixels j = pg + 8i: 8
-    // of them per pass, 2 when the pass has <= 16 (small batches).  Every broadcast token
-    // float4 feeds 8 FMAs (two channels), the weights come as float2 pairs.
-    const int cp = tid & 31, pg8 = tid >> 5;
+    // thread (channel quad cq, pg) takes channels 4cq .. 4cq+3 of the pixels j = pg + 16i:
+    // 4 of them per pass, 1 when the pass has <= 16 (small batches).  Every broadcast
+    // token float4 feeds 16 FMAs, the weights come as float4 quads.
+    const int cq = tid & 15, pg16 = tid >> 4;
     auto corr_pass = [&](auto ni_tag) {
       constexpr int NI = decltype(ni_tag)::value;
-      float2 acc[NI], pre[NI];
+      float4 acc[NI], pre[NI];
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
-        acc[i] = *reinterpret_cast<const float2*>(&sm.eb[2 * cp]);
+        acc[i] = *reinterpret_cast<const float4*>(&sm.eb[4 * cq]);
         // the pixels' stored pre-activations, loaded before the products
-        const int k = kb + pg8 + 8 * i, pos = r + 8 * k;
+        const int k = kb + pg16 + 16 * i, pos = r + 8 * k;
         const int y = along_x ? (ed == 0 ? 0 : H - 1) : pos, x = along_x ? pos : (ed == 2 ? 0 : W - 1);
-        pre[i] = k <= k_hi ? __ldg(reinterpret_cast<const float2*>(
-                                 a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 2 * cp))
-                           : make_float2(0.f, 0.f);
+        pre[i] = k <= k_hi ? __ldg(reinterpret_cast<const float4*>(
+                                 a.bd0 + ((size_t)f * NB + border_index(y, x, H, W)) * 64 + 4 * cq))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      auto fma4 = [](float4 t, float4 w0, float4 w1, float4 w2, float4 w3, float4 c) {
+        c.x = fmaf(t.x, w0.x, fmaf(t.y, w1.x, fmaf(t.z, w2.x, fmaf(t.w, w3.x, c.x))));
+        c.y = fmaf(t.x, w0.y, fmaf(t.y, w1.y, fmaf(t.z, w2.y, fmaf(t.w, w3.y, c.y))));
+        c.z = fmaf(t.x, w0.z, fmaf(t.y, w1.z, fmaf(t.z, w2.z, fmaf(t.w, w3.z, c.z))));
+        c.w = fmaf(t.x, w0.w, fmaf(t.y, w1.w, fmaf(t.z, w2.w, fmaf(t.w, w3.w, c.w))));
+        return c;
+      };
       for (int t = 0; t < nt; ++t) {
         const int o = 1 + (t == 0 ? 0 : dt1);            // token row of pixel j: j + o
 #pragma unroll 2
         for (int c4 = 0; c4 < 16; ++c4) {
-          const float2 w0 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4][2 * cp]);
-          const float2 w1 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 1][2 * cp]);
-          const float2 w2 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 2][2 * cp]);
-          const float2 w3 = *reinterpret_cast<const float2*>(&sm.k[t][4 * c4 + 3][2 * cp]);
+          const float4 w0 = *reinterpret_cast<const float4*>(&sm.k[t][4 * c4][4 * cq]);
+          const float4 w1 = *reinterpret_cast<const float4*>(&sm.k[t][4 * c4 + 1][4 * cq]);
+          const float4 w2 = *reinterpret_cast<const float4*>(&sm.k[t][4 * c4 + 2][4 * cq]);
+          const float4 w3 = *reinterpret_cast<const float4*>(&sm.k[t][4 * c4 + 3][4 * cq]);
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
-            const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[pg8 + 8 * i + o][4 * c4]);
-            acc[i].x = fmaf(tv.x, w0.x, fmaf(tv.y, w1.x, fmaf(tv.z, w2.x, fmaf(tv.w, w3.x, acc[i].x))));
-            acc[i].y = fmaf(tv.x, w0.y, fmaf(tv.y, w1.y, fmaf(tv.z, w2.y, fmaf(tv.w, w3.y, acc[i].y))));
+            const float4 tv = *reinterpret_cast<const float4*>(&sm.tok[pg16 + 16 * i + o][4 * c4]);
+            acc[i] = fma4(tv, w0, w1, w2, w3, acc[i]);
           }
         }
       }
+      auto tail = [](float p, float q) {
+        float d = p - q;
+        d = d >= 0.f ? d : 0.2f * d;
+        return __half2float(__float2half_rn(d));          // decode.0's output is fp16
+      };
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
-        const int j = pg8 + 8 * i, k = kb + j;
-        float2 d = make_float2(0.f, 0.f);
-        if (k <= k_hi) {
-          d.x = pre[i].x - acc[i].x;
-          d.y = pre[i].y - acc[i].y;
-          d.x = d.x >= 0.f ? d.x : 0.2f * d.x;
-          d.y = d.y >= 0.f ? d.y : 0.2f * d.y;
-          d.x = __half2float(__float2half_rn(d.x));       // decode.0's output is fp16
-          d.y = __half2float(__float2half_rn(d.y));
-        }
-        *reinterpret_cast<float2*>(&sm.d0[j][2 * cp]) = d;
+        const int j = pg16 + 16 * i, k = kb + j;
+        float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k <= k_hi)
+          d = make_float4(tail(pre[i].x, acc[i].x), tail(pre[i].y, acc[i].y),
+                          tail(pre[i].z, acc[i].z), tail(pre[i].w, acc[i].w));
+        *reinterpret_cast<float4*>(&sm.d0[j][4 * cq]) = d;
       }
     };
-    if (cnt <= 16) corr_pass(std::integral_constant<int, 2>{});
-    else corr_pass(std::integral_constant<int, 8>{});
+    if (cnt <= 16) corr_pass(std::integral_constant<int, 1>{});
+    else corr_pass(std::integral_constant<int, 4>{});
     __syncthreads();
     for (int i = tid; i < cnt * 27; i += 256) {
       const int j = i / 27, u = i - 27 * j, k = kb + j, pos = r + 8 * k;
