@@ -444,6 +444,25 @@ __global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
   const bool act = x0 < a.W;
   const size_t plane = (size_t)a.H * a.W;
   const __half* ep = a.e_planes + (size_t)f * 27 * plane;
+  // the composite's inputs first: their loads fly with the 27 plane loads below
+  const size_t pix0 = (size_t)y * a.W + x0;
+  float alr[PX], rgbf[3][PX];
+  uint8_t src[3 * PX];
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < PX; ++i) alr[i] = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix0 + i) : 1.f;
+    if (a.out_f32) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+        for (int i = 0; i < PX; ++i) rgbf[ch][i] = __ldg(a.rgb_f32 + ((size_t)f * 3 + ch) * plane + pix0 + i);
+    }
+    if (a.out_u8 || a.packed) {                   // 3*PX bytes, 2*PX-byte aligned
+      const uint16_t* s8 = reinterpret_cast<const uint16_t*>(a.rgb_u8 + ((size_t)f * plane + pix0) * 3);
+#pragma unroll
+      for (int k = 0; k < 3 * PX / 2; ++k) *reinterpret_cast<uint16_t*>(src + 2 * k) = __ldg(s8 + k);
+    }
+  }
   float o[3][PX];
 #pragma unroll
   for (int co = 0; co < 3; ++co)
@@ -487,18 +506,9 @@ __global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
     }
   }
   if (act) {
-    const size_t pix0 = (size_t)y * a.W + x0;
-    float alr[PX];
-#pragma unroll
-    for (int i = 0; i < PX; ++i) alr[i] = a.alpha ? __ldg(a.alpha + (size_t)f * plane + pix0 + i) : 1.f;
     int4 sp = make_int4(0, 0, 0, 0);
     if (a.packed) sp = __ldg(a.spans + y);
-    uint8_t src[3 * PX], dst[3 * PX];
-    if (a.out_u8 || a.packed) {                   // 3*PX bytes, 2*PX-byte aligned
-      const uint16_t* s8 = reinterpret_cast<const uint16_t*>(a.rgb_u8 + ((size_t)f * plane + pix0) * 3);
-#pragma unroll
-      for (int k = 0; k < 3 * PX / 2; ++k) *reinterpret_cast<uint16_t*>(src + 2 * k) = __ldg(s8 + k);
-    }
+    uint8_t dst[3 * PX];
     bool bad = false;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(TPB) dec2_gather_vec_kernel(ConvTcArgs a) {
         if (a.fill) a.fill[pl + i] = out01[i];
         if (a.out_f32)
           a.out_f32[pl + i] = __fadd_rn(__fmul_rn(alr[i], out01[i]),
-                                        __fmul_rn(__fsub_rn(1.0f, alr[i]), __ldg(a.rgb_f32 + pl + i)));
+                                        __fmul_rn(__fsub_rn(1.0f, alr[i]), rgbf[ch][i]));
       }
       if (a.out_u8 || a.packed) {
 #pragma unroll
