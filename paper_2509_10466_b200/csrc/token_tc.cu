@@ -778,6 +778,23 @@ __global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
     phase ^= 1u;
   };
 
+  // residual stream: warps 0-3 (slice 0) own it, 16 values per row and thread (loaded
+  // first: these register loads fly while the GEMM input below is staged)
+  float x[NH][16];
+  const bool xw = slice == 0;
+  if constexpr (MODE != TOK_EMBED) {
+    if (xw) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 v = vq[h] ? __ldg(reinterpret_cast<const float2*>(a.resid_in + (size_t)nq[h] * C + 8 * k + cl))
+                                 : make_float2(0.f, 0.f);
+          x[h][2 * k] = v.x;
+          x[h][2 * k + 1] = v.y;
+        }
+    }
+  }
   // ------------------------------------------------------------ first GEMM input
   // A rows of token row r of the tile: 32 * (r / RQ) + r % RQ
   if constexpr (MODE == TOK_EMBED) {
@@ -795,22 +812,6 @@ __global__ void __launch_bounds__(32 * QWARPS, 1) token_q_kernel(TokenArgs a) {
       const uint4 v = n < a.n_tok ? __ldg(reinterpret_cast<const uint4*>(a.attn + (size_t)n * C) + ch)
                                   : make_uint4(0, 0, 0, 0);
       *reinterpret_cast<uint4*>(sa + sw128(32 * (r / RQ) + r % RQ, ch)) = v;
-    }
-  }
-  // residual stream: warps 0-3 (slice 0) own it, 16 values per row and thread
-  float x[NH][16];
-  const bool xw = slice == 0;
-  if constexpr (MODE != TOK_EMBED) {
-    if (xw) {
-#pragma unroll
-      for (int h = 0; h < NH; ++h)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float2 v = vq[h] ? __ldg(reinterpret_cast<const float2*>(a.resid_in + (size_t)nq[h] * C + 8 * k + cl))
-                                 : make_float2(0.f, 0.f);
-          x[h][2 * k] = v.x;
-          x[h][2 * k + 1] = v.y;
-        }
     }
   }
   tc::mbar_wait(&ctl.w_bar, 0);                 // weights and params in smem
